@@ -1,0 +1,284 @@
+/*
+ * deformtrack_b200.h -- C-ABI of the B200 (sm_100a) deformation-tracking hot path.
+ *
+ * The reference (arXiv 2007.08576, /root/reference/pkg/src/deformtrack) is a pure
+ * Python/numba package with no FFI of its own. The entry points below replace the
+ * reference functions named in each comment one for one: the operator-level ones
+ * mirror the numba kernels' positional signatures (kernels.py) and the numpy
+ * helpers around them, the frame-level ones mirror solver.solve_frame /
+ * tracking.track_frame. INTEGRATION.md shows the ctypes binding a maintainer of the
+ * reference would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch types cross this boundary;
+ *   - operator-level calls take DEVICE pointers and a cudaStream_t passed as void*;
+ *     they are asynchronous on that stream;
+ *   - dtypes follow the reference: float64 for geometry, int64 for indices, uint8 for
+ *     boolean masks (numpy bool is one byte);
+ *   - every call returns a dt_status; dt_last_error() gives the message of the last
+ *     failure on the calling thread;
+ *   - the library holds no global numeric state (the reference's process-global
+ *     numba.set_num_threads, solver.py:288, has no equivalent here); one dt_tracker
+ *     handle per sequence, one stream per handle.
+ */
+#ifndef DEFORMTRACK_B200_H
+#define DEFORMTRACK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes mirror deformtrack/exceptions.py:4-49. */
+typedef enum {
+  DT_OK = 0,
+  DT_ERR_INVALID_ARGUMENT = 1,     /* ValueError                                  */
+  DT_ERR_CUDA = 2,                 /* CUDA runtime failure (no reference twin)    */
+  DT_ERR_NO_VALID_HYPOTHESIS = 3,  /* exceptions.NoValidHypothesis (matching.py:184,208) */
+  DT_ERR_EMPTY_TEMPLATE = 4,       /* exceptions.EmptyTemplate (warpfield.py:86,172)     */
+  DT_ERR_ALL_ZERO_WEIGHTS = 5,     /* exceptions.AllZeroWeights (geometry.py:173)        */
+  DT_ERR_UNSUPPORTED = 6,          /* configuration outside what the device path covers  */
+  DT_ERR_NOT_BOUND = 7             /* solver.py:282-283 "template must be bound"         */
+} dt_status;
+
+const char* dt_last_error(void);
+/* Library version string and the sm arch it was compiled for. */
+const char* dt_version(void);
+/* Number of SMs and the largest thread-block cluster the solver kernel can use. */
+int dt_device_info(int device, int* sm_count, int* max_cluster);
+
+/* ------------------------------------------------------------------------------
+ * Operator level (device pointers). Each replaces one reference function.
+ * ---------------------------------------------------------------------------- */
+
+/* correspond.compute_observation_normals (correspond.py:36-73) fused with
+ * valid_depth_mask (correspond.py:23-26).  depth (h,w) f64 -> normals (h,w,3) f64,
+ * valid (h,w) u8. */
+int dt_observation_normals(const double* depth, int64_t h, int64_t w,
+                           double fx, double fy, double cx, double cy,
+                           double z_min, double z_max,
+                           double* normals, uint8_t* valid, void* stream);
+
+/* kernels.warp_and_rasterize (kernels.py:483-569). pixels are (u,v) int64, -1 where
+ * the point found no valid pair. */
+int dt_warp_and_rasterize(const double* points, const double* normals,
+                          const int64_t* bind_idx, const double* alpha,
+                          int64_t n, int64_t k, const double* warps, int64_t m,
+                          const double* depth, const uint8_t* depth_valid,
+                          const double* obs_normals, int64_t height, int64_t width,
+                          double fx, double fy, double cx, double cy,
+                          double gate_distance, double cos_gate,
+                          double* out_p, double* out_n, uint8_t* valid,
+                          double* obs_p, double* obs_n, int64_t* pixels,
+                          void* stream);
+
+/* kernels.icp_reduce (kernels.py:148-220). basis (m,8,6) as warp_increment_basis
+ * (energy.py:205-219). partial (m,27), support (m), cost (m), r (n). */
+int dt_icp_reduce(const double* points, const double* obs_normals, const double* obs_points,
+                  const int64_t* bind_idx, const double* alpha, int64_t n, int64_t k,
+                  const double* warps, const double* basis, int64_t m,
+                  double tukey_scale, const double* frozen, int use_frozen, int want_jac,
+                  double* partial, double* support, double* cost, double* r,
+                  void* stream);
+
+/* kernels.feature_reduce (kernels.py:222-284). */
+int dt_feature_reduce(const double* points, const double* obs_points, const double* match_w,
+                      const int64_t* bind_idx, const double* alpha, int64_t n, int64_t k,
+                      const double* warps, const double* basis, int64_t m,
+                      double feature_weight, int want_jac,
+                      double* partial, double* support, double* cost, void* stream);
+
+/* kernels.arap_reduce (kernels.py:341-467). R (m,3,3), t (m,3) as
+ * geometry.dq_to_transform_batch (geometry.py:238-264); edges (e,2) int64. */
+int dt_arap_reduce(const double* ctrl_points, const double* R, const double* t,
+                   const double* warps, const int64_t* edges, const double* edge_weights,
+                   int64_t n_edges, const double* wa, int64_t m,
+                   double angle_weight, double rotation_weight, int want_jac,
+                   double* partial, double* cost, void* stream);
+
+/* solver._solve_damped (solver.py:217-258). A (m,6,6), b (m,6), lam (m) ->
+ * delta (m,6), ok (m) u8. */
+int dt_solve_damped(const double* A, const double* b, const double* lam, int64_t m,
+                    double* delta, uint8_t* ok, void* stream);
+
+/* solver.apply_step (solver.py:261-264). */
+int dt_apply_step(const double* warps, const double* delta, int64_t m, double* out,
+                  void* stream);
+
+/* energy.warp_increment_basis (energy.py:205-219): warps (m,8) -> (m,8,6). */
+int dt_warp_increment_basis(const double* warps, int64_t m, double* basis, void* stream);
+
+/* geometry.dq_to_transform_batch (geometry.py:238-264): warps (m,8) -> R (m,3,3), t (m,3). */
+int dt_dq_to_transform(const double* warps, int64_t m, double* R, double* t, void* stream);
+
+/* warpfield.warp_all (warpfield.py:236-250). */
+int dt_warp_all(const double* points, const double* normals, const int64_t* bind_idx,
+                const double* alpha, int64_t n, int64_t k, const double* warps,
+                double* out_p, double* out_n, void* stream);
+
+/* warpfield.bind_points (warpfield.py:157-194): brute-force k-nearest controls,
+ * nearest first (ties -> lower control index), normalized Gaussian weights. */
+int dt_bind_points(const double* points, int64_t n, const double* ctrl, int64_t m,
+                   int64_t k, double sigma, int64_t* idx, double* w, void* stream);
+
+/* Brute-force Hamming matching of 256-bit ORB descriptors (north-star part 3a; no
+ * reference twin). For every template descriptor: the frame
+ * descriptor with the smallest popcount(a xor b), ties -> lowest frame index. */
+int dt_hamming_match(const uint8_t* template_desc, int64_t n_template,
+                     const uint8_t* frame_desc, int64_t n_frame,
+                     int32_t* best_idx, int32_t* best_dist, void* stream);
+
+/* matching.preselect_inliers (matching.py:174-226) with the reference indices given
+ * explicitly (refs, n_refs): the host draws them with numpy's Generator exactly as
+ * matching.py:189-193 does, or passes arange(n) (exhaustive).
+ * Outputs (device): weights (n) f64, flags (n) u8, residuals (n) f64, rotation (9) f64,
+ * info: int64[2] = {status (DT_OK or DT_ERR_NO_VALID_HYPOTHESIS), reference index},
+ * support: f64[1]. */
+typedef struct {
+  double distance_threshold;   /* PreselectConfig.distance_threshold (matching.py:69) */
+  int32_t n_reweight_iters;    /* PreselectConfig.n_reweight_iters                   */
+  double inlier_weight_min;    /* PreselectConfig.inlier_weight_min                  */
+  double min_support;          /* PreselectConfig.min_support                        */
+} dt_preselect_params;
+
+int dt_preselect(const double* src, const double* dst, int64_t n,
+                 const int64_t* refs, int64_t n_refs, const dt_preselect_params* params,
+                 double* weights, uint8_t* flags, double* residuals, double* rotation,
+                 int64_t* info, double* support, void* stream);
+
+/* ------------------------------------------------------------------------------
+ * Frame level: a device-resident tracker (one per sequence / stream).
+ * Replaces solver.solve_frame (solver.py:267-378) and tracking.track_frame
+ * (tracking.py:67-95): preselect -> bind matches -> LM loop -> warp_all, with the
+ * whole Levenberg-Marquardt loop running on the device in one cluster kernel.
+ * ---------------------------------------------------------------------------- */
+
+typedef struct dt_tracker dt_tracker;
+
+typedef struct {
+  /* EnergyWeights (energy.py:49-65) */
+  double feature_weight, arap_weight, angle_weight, rotation_weight, tukey_scale, data_floor;
+  /* SolverConfig (solver.py:43-71) */
+  int32_t max_outer_iters;
+  double lambda_init, lambda_decrease, lambda_increase, lambda_min, lambda_max;
+  int32_t max_retries;
+  double step_tol, cost_tol, gate_distance, cos_gate; /* cos_gate = cos(deg2rad(gate_angle_deg)) */
+  /* PreselectConfig (matching.py:58-80) */
+  dt_preselect_params preselect;
+  /* camera (geometry.PinholeCamera, geometry.py:355-370) + DepthSection (config.py:36-43) */
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  double z_min, z_max;
+  /* sampling radius of the graph: sigma of the per-frame match binding (solver.py:292-296) */
+  double sampling_radius;
+  /* device execution: thread-block cluster size of the solver kernel (0 = auto) */
+  int32_t cluster_size;
+  /* Hamming gate for descriptor matching (256 = keep every best match) */
+  int32_t max_hamming;
+} dt_config;
+
+/* EnergyReport (energy.py:107-168) scalar fields. The per-iteration histories are
+ * read with dt_tracker_get_history. */
+typedef struct {
+  double icp_cost, feature_cost, arap_cost, total_cost;
+  double match_weight_sum, final_step_norm;
+  double preselect_support;
+  int32_t n_correspondences, n_matches, n_preselected;
+  int32_t outer_iterations, accepted_steps, rejected_steps;
+  int32_t stalled, converged, n_cost_history;
+  int32_t preselect_status;     /* DT_OK or DT_ERR_NO_VALID_HYPOTHESIS (tracking.py:56-64) */
+  int32_t preselect_reference;  /* winning reference index, -1 when none */
+  int32_t frame_id;
+} dt_report;
+
+/* Create a tracker from host arrays: the bound template (Template, warpfield.py:25-47)
+ * and the control graph (ControlGraph, warpfield.py:50-74) with its warm-start warps. */
+int dt_tracker_create(const dt_config* cfg,
+                      const double* t_points, const double* t_normals,
+                      const int64_t* bind_idx, const double* bind_w, int64_t n, int64_t k,
+                      const double* ctrl_points, const double* warps, int64_t m,
+                      const int64_t* edges, const double* edge_weights, int64_t n_edges,
+                      int device, void* stream, dt_tracker** out);
+int dt_tracker_destroy(dt_tracker* t);
+/* Template-side ORB features: 256-bit descriptors (T,32) u8 and their frame-0 3D
+ * points (T,3) f64 (host). Binds the feature points to the graph once. */
+int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* points,
+                            int64_t n_features);
+/* Warm-start warps (m,8) f64: host (from_device=0) or device pointer. */
+int dt_tracker_set_warps(dt_tracker* t, const double* warps, int from_device);
+int dt_tracker_get_warps(dt_tracker* t, double* warps_host);
+int dt_tracker_set_config(dt_tracker* t, const dt_config* cfg);
+int dt_tracker_sync(dt_tracker* t);
+
+/* Per-frame inputs. Pointers are HOST pointers unless `on_device` is set, in which case
+ * they are device pointers already resident in HBM. Any optional input may be NULL.
+ *   depth            (h,w) f64 mm                         required
+ *   normals          (h,w,3) f64; NULL -> computed on the device from depth
+ *   match_src/dst    (n_pairs,3) f64 MatchSet pairs (matching.py:21-55)
+ *   frame_desc/kp    (n_frame,32) u8 + (n_frame,2) int32 (u,v) keypoints: the ORB path,
+ *                    matched against the template features set above
+ *   match_w          (n_pairs) f64 weights of ALREADY annotated pairs: preselection is
+ *                    skipped (the solver.solve_frame contract, solver.py:267); NULL ->
+ *                    the pairs are preselected on the device first (track_frame)
+ *   refs             (n_refs) int64 preselect references; NULL -> exhaustive arange(n)
+ *   use_matches      0 = no feature term this frame
+ */
+typedef struct {
+  const double* depth;
+  const double* normals;
+  const double* match_src;
+  const double* match_dst;
+  const double* match_w;
+  int64_t n_pairs;
+  const uint8_t* frame_desc;
+  const int32_t* frame_kp;
+  int64_t n_frame;
+  const int64_t* refs;
+  int64_t n_refs;
+  int32_t use_matches;
+  int32_t on_device;
+  int32_t frame_id;
+} dt_frame_input;
+
+/* Per-frame outputs (HOST pointers; any may be NULL to skip that copy).
+ *   warps (m,8), points (n,3), normals (n,3), match_weights / match_flags (n_matches),
+ *   match_src / match_dst (n_matches,3) (the ORB path's MatchSet), control_data_weights (m),
+ *   report. */
+typedef struct {
+  double* warps;
+  double* points;
+  double* normals;
+  double* match_weights;
+  uint8_t* match_flags;
+  double* match_src;
+  double* match_dst;
+  int64_t match_capacity;
+  double* control_data_weights;
+  dt_report* report;
+} dt_frame_output;
+
+/* Run one frame (asynchronous on the tracker stream; results valid after
+ * dt_tracker_sync). The warps solved here become the warm start of the next frame. */
+int dt_track_frame(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out);
+/* Per-outer-iteration histories of the last frame (host): cost_history
+ * (max_outer_iters,2), lambda_history (max_outer_iters,2), stalled (max_outer_iters). */
+int dt_tracker_get_history(dt_tracker* t, double* cost_history, double* lambda_history,
+                           int32_t* stalled);
+/* Device pointers of the resident per-frame outputs (for zero-copy consumers). */
+int dt_tracker_device_outputs(dt_tracker* t, double** warps, double** points, double** normals);
+/* Counters: kernels launched by the last dt_track_frame call. */
+int dt_tracker_last_launches(dt_tracker* t);
+
+/* Run one frame on several trackers at once: one thread-block cluster per tracker
+ * in a single solver launch (independent sequences, BASELINE config 5). All trackers
+ * must live on the same device; `stream` orders the batch. */
+int dt_track_frames_batched(dt_tracker** trackers, const dt_frame_input* inputs,
+                            dt_frame_output* outputs, int32_t n_trackers, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DEFORMTRACK_B200_H */

@@ -1,0 +1,289 @@
+"""Python handle around one ``dt_tracker`` (include/deformtrack_b200.h).
+
+A ``DeviceTracker`` owns the device-resident template, control graph, CSR lists and
+solver state of one sequence. Frames go in as host arrays (or device pointers); the
+C-ABI does the host<->device copies, the per-frame kernels and the single
+thread-block-cluster LM launch, then returns the solution and the report.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as dev
+from ._lib import Config, FrameInput, FrameOutput, PreselectParams, Report, check, lib
+
+
+def make_config(camera, weights, solver, preselect=None, *, sampling_radius: float,
+                z_min: float = 1.0, z_max: float = 1.0e5, cluster_size: int = 0,
+                max_hamming: int = 256) -> Config:
+    """Pack EnergyWeights + SolverConfig + PreselectConfig + camera into dt_config."""
+    pp = PreselectParams(5.0, 10, 0.5, 0.2)
+    if preselect is not None:
+        pp = preselect.params()
+    cos_gate = float(np.cos(np.deg2rad(solver.gate_angle_deg)))
+    return Config(
+        feature_weight=float(weights.feature_weight), arap_weight=float(weights.arap_weight),
+        angle_weight=float(weights.angle_weight), rotation_weight=float(weights.rotation_weight),
+        tukey_scale=float(weights.tukey_scale), data_floor=float(weights.data_floor),
+        max_outer_iters=int(solver.max_outer_iters),
+        lambda_init=float(solver.lambda_init), lambda_decrease=float(solver.lambda_decrease),
+        lambda_increase=float(solver.lambda_increase), lambda_min=float(solver.lambda_min),
+        lambda_max=float(solver.lambda_max), max_retries=int(solver.max_retries),
+        step_tol=float(solver.step_tol), cost_tol=float(solver.cost_tol),
+        gate_distance=float(solver.gate_distance), cos_gate=cos_gate,
+        preselect=pp,
+        fx=float(camera.fx), fy=float(camera.fy), cx=float(camera.cx), cy=float(camera.cy),
+        width=int(camera.width), height=int(camera.height),
+        z_min=float(z_min), z_max=float(z_max),
+        sampling_radius=float(sampling_radius), cluster_size=int(cluster_size),
+        max_hamming=int(max_hamming),
+    )
+
+
+def _cfg_bytes(cfg: Config) -> bytes:
+    return bytes(memoryview(cfg))
+
+
+def _host_ptr(a) -> int | None:
+    """Raw pointer of a C-contiguous numpy array or a (pinned) host torch tensor."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr() if a.numel() else None
+    return a.ctypes.data if a.size else None
+
+
+@dataclass
+class FrameOutputs:
+    warps: np.ndarray
+    points: np.ndarray | None
+    normals: np.ndarray | None
+    control_data_weights: np.ndarray
+    report: Report
+    cost_history: list
+    lambda_history: list
+    stalled: np.ndarray
+    match_weights: np.ndarray | None = None
+    match_flags: np.ndarray | None = None
+    match_src: np.ndarray | None = None
+    match_dst: np.ndarray | None = None
+
+
+class DeviceTracker:
+    """One sequence resident on one device (one stream)."""
+
+    def __init__(self, template, graph, cfg: Config, device: int | None = None):
+        dev.require_cuda()
+        import torch
+
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.n = len(template)
+        self.k = int(template.bind_indices.shape[1])
+        self.m = len(graph)
+        self._cfg = cfg
+        self._cfg_key = _cfg_bytes(cfg)
+        self.n_features = 0
+        tp = np.ascontiguousarray(template.points, dtype=np.float64)
+        tn = np.ascontiguousarray(template.normals, dtype=np.float64)
+        bi = np.ascontiguousarray(template.bind_indices, dtype=np.int64)
+        bw = np.ascontiguousarray(template.bind_weights, dtype=np.float64)
+        cp = np.ascontiguousarray(graph.points, dtype=np.float64)
+        wp = np.ascontiguousarray(graph.warps, dtype=np.float64)
+        ed = np.ascontiguousarray(graph.edges, dtype=np.int64).reshape(-1, 2)
+        ew = np.ascontiguousarray(graph.edge_weights, dtype=np.float64)
+        handle = C.c_void_p()
+        check(lib.dt_tracker_create(C.byref(cfg), _host_ptr(tp), _host_ptr(tn), _host_ptr(bi),
+                                    _host_ptr(bw), self.n, self.k, _host_ptr(cp), _host_ptr(wp),
+                                    self.m, _host_ptr(ed), _host_ptr(ew), ed.shape[0],
+                                    self.device, None, C.byref(handle)), "dt_tracker_create")
+        self._h = handle
+
+    # -- configuration -------------------------------------------------------------
+    def set_config(self, cfg: Config) -> None:
+        key = _cfg_bytes(cfg)
+        if key == self._cfg_key:
+            return
+        check(lib.dt_tracker_set_config(self._h, C.byref(cfg)), "dt_tracker_set_config")
+        self._cfg = cfg
+        self._cfg_key = key
+
+    @property
+    def config(self) -> Config:
+        return self._cfg
+
+    def set_warps(self, warps) -> None:
+        w = np.ascontiguousarray(warps, dtype=np.float64).reshape(self.m, 8)
+        check(lib.dt_tracker_set_warps(self._h, _host_ptr(w), 0), "dt_tracker_set_warps")
+
+    def get_warps(self) -> np.ndarray:
+        out = np.empty((self.m, 8))
+        check(lib.dt_tracker_get_warps(self._h, _host_ptr(out)), "dt_tracker_get_warps")
+        return out
+
+    def set_features(self, desc, points) -> None:
+        d = np.ascontiguousarray(desc, dtype=np.uint8).reshape(-1, 32)
+        p = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        if d.shape[0] != p.shape[0]:
+            raise ValueError("one 3D point per template descriptor required")
+        check(lib.dt_tracker_set_features(self._h, _host_ptr(d), _host_ptr(p), d.shape[0]),
+              "dt_tracker_set_features")
+        self.n_features = d.shape[0]
+
+    # -- frames --------------------------------------------------------------------
+    def track(self, depth, normals=None, *, pairs=None, match_w=None, frame_desc=None,
+              frame_kp=None, refs=None, frame_id: int = 0, want_points: bool = True,
+              want_matches: bool = False, outputs: dict | None = None) -> FrameOutputs:
+        """Run one frame. Host inputs; returns host outputs (after the stream sync)."""
+        keep = []
+
+        def hp(a, dtype):
+            if a is None:
+                return None
+            if hasattr(a, "data_ptr"):
+                keep.append(a)
+                return _host_ptr(a)
+            arr = np.ascontiguousarray(a, dtype=dtype)
+            keep.append(arr)
+            return _host_ptr(arr)
+
+        fi = FrameInput()
+        fi.depth = hp(depth, np.float64)
+        fi.normals = hp(normals, np.float64)
+        n_pairs = 0
+        if pairs is not None:
+            src, dst = pairs
+            n_pairs = int(np.asarray(src).shape[0]) if not hasattr(src, "shape") else int(src.shape[0])
+            fi.match_src = hp(src, np.float64)
+            fi.match_dst = hp(dst, np.float64)
+            fi.match_w = hp(match_w, np.float64)
+        fi.n_pairs = n_pairs
+        n_frame = 0
+        if frame_desc is not None:
+            n_frame = int(frame_desc.shape[0])
+            fi.frame_desc = hp(frame_desc, np.uint8)
+            fi.frame_kp = hp(frame_kp, np.int32)
+        fi.n_frame = n_frame
+        if refs is not None:
+            r = np.ascontiguousarray(refs, dtype=np.int64)
+            keep.append(r)
+            fi.refs = _host_ptr(r)
+            fi.n_refs = r.shape[0]
+        fi.use_matches = 1 if (n_pairs > 0 or n_frame > 0) else 0
+        fi.on_device = 0
+        fi.frame_id = int(frame_id)
+
+        o = outputs or {}
+        warps = o.get("warps")
+        if warps is None:
+            warps = np.empty((self.m, 8))
+        pts = nrm = None
+        if want_points:
+            pts = o.get("points")
+            nrm = o.get("normals")
+            if pts is None:
+                pts = np.empty((self.n, 3))
+            if nrm is None:
+                nrm = np.empty((self.n, 3))
+        cdw = np.empty(self.m)
+        report = Report()
+        cap = max(n_pairs, self.n_features) if (want_matches or n_pairs) else 0
+        mw = np.empty(cap) if cap else None
+        mf = np.empty(cap, dtype=np.uint8) if cap else None
+        ms = np.empty((cap, 3)) if (cap and n_frame) else None
+        md = np.empty((cap, 3)) if (cap and n_frame) else None
+        fo = FrameOutput()
+        fo.warps = _host_ptr(warps)
+        fo.points = _host_ptr(pts)
+        fo.normals = _host_ptr(nrm)
+        fo.match_weights = _host_ptr(mw)
+        fo.match_flags = _host_ptr(mf)
+        fo.match_src = _host_ptr(ms)
+        fo.match_dst = _host_ptr(md)
+        fo.match_capacity = cap
+        fo.control_data_weights = _host_ptr(cdw)
+        fo.report = C.cast(C.pointer(report), C.c_void_p).value
+        check(lib.dt_track_frame(self._h, C.byref(fi), C.byref(fo)), "dt_track_frame")
+        it = int(self._cfg.max_outer_iters)
+        ch = np.zeros((it, 2))
+        lh = np.zeros((it, 2))
+        st = np.zeros(it, dtype=np.int32)
+        check(lib.dt_tracker_get_history(self._h, _host_ptr(ch), _host_ptr(lh), _host_ptr(st)),
+              "dt_tracker_get_history")
+        nh = int(report.n_cost_history)
+        no = int(report.outer_iterations)
+        return FrameOutputs(
+            warps=warps, points=pts, normals=nrm, control_data_weights=cdw, report=report,
+            cost_history=[[float(a), float(b)] for a, b in ch[:nh]],
+            lambda_history=[[float(a), float(b)] for a, b in lh[:no]],
+            stalled=st[:no].copy(), match_weights=mw, match_flags=mf, match_src=ms,
+            match_dst=md,
+        )
+
+    def track_raw(self, fi: FrameInput, fo: FrameOutput) -> None:
+        """Lowest-overhead entry: caller-built dt_frame_input / dt_frame_output."""
+        check(lib.dt_track_frame(self._h, C.byref(fi), C.byref(fo)), "dt_track_frame")
+
+    def launches(self) -> int:
+        return int(lib.dt_tracker_last_launches(self._h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.dt_tracker_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _SessionCache:
+    """Trackers keyed by the identity of the template / graph arrays they were built
+    from (the arrays are held, so ids cannot be recycled while cached)."""
+
+    def __init__(self, capacity: int = 4):
+        self.capacity = capacity
+        self._d: OrderedDict = OrderedDict()
+
+    def get(self, template, graph, cfg: Config) -> DeviceTracker:
+        arrays = (template.points, template.normals, template.bind_indices, template.bind_weights,
+                  graph.points, graph.edges, graph.edge_weights)
+        key = tuple(id(a) for a in arrays) + (cfg.width, cfg.height, float(graph.sampling_radius))
+        hit = self._d.get(key)
+        if hit is not None:
+            self._d.move_to_end(key)
+            trk = hit[1]
+            trk.set_config(cfg)
+            return trk
+        trk = DeviceTracker(template, graph, cfg)
+        self._d[key] = (arrays, trk)
+        while len(self._d) > self.capacity:
+            _, (_, old) = self._d.popitem(last=False)
+            old.close()
+        return trk
+
+    def clear(self) -> None:
+        for _, (_, trk) in self._d.items():
+            trk.close()
+        self._d.clear()
+
+
+SESSIONS = _SessionCache()
+
+
+def nvh_message(n: int) -> str:
+    """Message of the reference's NoValidHypothesis (matching.py:184, 208)."""
+    if n < 3:
+        return f"{n} matches cannot support a rotation hypothesis"
+    return "every reference hypothesis was discarded"
+
+
+def isclose_cfg(a: Config, b: Config) -> bool:  # pragma: no cover - debug helper
+    return _cfg_bytes(a) == _cfg_bytes(b) and not math.isnan(a.step_tol)

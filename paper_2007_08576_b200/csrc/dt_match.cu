@@ -1,0 +1,403 @@
+// dt_match.cu -- ORB Hamming matching and 1-point-RANSAC + reweighting preselection.
+//
+//  * k_hamming: brute-force 256-bit descriptor matching (north-star part 3a; the
+//    reference has no implementation). popc(a ^ b) over 8 x 32-bit words,
+//    frame descriptors staged through shared memory, per-lane running argmin and a
+//    warp-shuffle (dist, index) argmin; ties resolve to the lowest frame index.
+//  * k_preselect_refs / k_preselect_final: matching.preselect_inliers
+//    (matching.py:174-226). One warp per reference hypothesis runs the whole
+//    rectify -> (weighted Procrustes -> residuals -> reweight) x iters alternation
+//    (matching.py:145-171); the 3x3 Procrustes uses a one-sided Jacobi SVD whose singular
+//    values are accurate relative to S0, so the reference's degeneracy test
+//    S1 <= 1e-9 S0 (matching.py:122) decides the same way as LAPACK's gesdd.
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "dt_common.cuh"
+#include "dt_ops.cuh"
+
+namespace dt {
+
+// ---------------------------------------------------------------------------------
+// Hamming
+// ---------------------------------------------------------------------------------
+
+constexpr int HAM_TPW = 2;                 // template descriptors per warp
+constexpr int HAM_WARPS = 8;               // warps per CTA
+constexpr int HAM_TILE = 512;              // frame descriptors per smem tile (16 KB)
+
+__global__ void __launch_bounds__(HAM_WARPS * 32)
+k_hamming(const uint4* __restrict__ tdesc, int64_t nt, const uint4* __restrict__ fdesc, int64_t nf,
+          int32_t* __restrict__ best_idx, int32_t* __restrict__ best_dist) {
+  __shared__ uint4 s_tile[HAM_TILE * 2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t0 = ((int64_t)blockIdx.x * HAM_WARPS + warp) * HAM_TPW;
+  uint32_t a[HAM_TPW][8];
+#pragma unroll
+  for (int j = 0; j < HAM_TPW; ++j) {
+    const int64_t t = t0 + j;
+    uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
+    if (t < nt) {
+      lo = tdesc[2 * t];
+      hi = tdesc[2 * t + 1];
+    }
+    a[j][0] = lo.x; a[j][1] = lo.y; a[j][2] = lo.z; a[j][3] = lo.w;
+    a[j][4] = hi.x; a[j][5] = hi.y; a[j][6] = hi.z; a[j][7] = hi.w;
+  }
+  int bd[HAM_TPW], bi[HAM_TPW];
+#pragma unroll
+  for (int j = 0; j < HAM_TPW; ++j) {
+    bd[j] = 0x7fffffff;
+    bi[j] = 0x7fffffff;
+  }
+  for (int64_t base = 0; base < nf; base += HAM_TILE) {
+    const int cnt = (int)((nf - base) < HAM_TILE ? (nf - base) : HAM_TILE);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * cnt; i += blockDim.x) s_tile[i] = fdesc[2 * base + i];
+    __syncthreads();
+    for (int f = lane; f < cnt; f += 32) {
+      const uint4 lo = s_tile[2 * f], hi = s_tile[2 * f + 1];
+#pragma unroll
+      for (int j = 0; j < HAM_TPW; ++j) {
+        const int d = __popc(a[j][0] ^ lo.x) + __popc(a[j][1] ^ lo.y) + __popc(a[j][2] ^ lo.z) +
+                      __popc(a[j][3] ^ lo.w) + __popc(a[j][4] ^ hi.x) + __popc(a[j][5] ^ hi.y) +
+                      __popc(a[j][6] ^ hi.z) + __popc(a[j][7] ^ hi.w);
+        if (d < bd[j]) {  // strict: this lane visits indices in increasing order
+          bd[j] = d;
+          bi[j] = (int)(base + f);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < HAM_TPW; ++j) {
+    int d = bd[j], i = bi[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int od = __shfl_xor_sync(0xffffffffu, d, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+      if (od < d || (od == d && oi < i)) {
+        d = od;
+        i = oi;
+      }
+    }
+    const int64_t t = t0 + j;
+    if (lane == 0 && t < nt) {
+      best_idx[t] = nf > 0 ? i : -1;
+      best_dist[t] = nf > 0 ? d : 257;
+    }
+  }
+}
+
+int launch_hamming(const uint8_t* tdesc, int64_t nt, const uint8_t* fdesc, int64_t nf,
+                   int32_t* best_idx, int32_t* best_dist, cudaStream_t s) {
+  if (nt == 0) return DT_OK;
+  const int per_cta = HAM_WARPS * HAM_TPW;
+  k_hamming<<<grid_for(nt, per_cta), HAM_WARPS * 32, 0, s>>>(
+      reinterpret_cast<const uint4*>(tdesc), nt, reinterpret_cast<const uint4*>(fdesc), nf,
+      best_idx, best_dist);
+  DT_CHECK_LAUNCH();
+  return DT_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// Weighted Procrustes rotation (matching.weighted_rotation, matching.py:108-125).
+// C is the 3x3 weighted cross-covariance sum_k w_k s2_k s1_k^T, row-major. Returns false
+// when the weighted vectors span fewer than two dimensions.
+// ---------------------------------------------------------------------------------
+
+__device__ __forceinline__ bool procrustes(const double C[9], double R[9]) {
+  double A[9], V[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+#pragma unroll
+  for (int i = 0; i < 9; ++i) A[i] = C[i];
+  const int P[3] = {0, 0, 1}, Q[3] = {1, 2, 2};
+  for (int sweep = 0; sweep < 16; ++sweep) {
+    bool rotated = false;
+#pragma unroll
+    for (int pq = 0; pq < 3; ++pq) {
+      const int p = P[pq], q = Q[pq];
+      double alpha = 0.0, beta = 0.0, gamma = 0.0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        alpha += A[r * 3 + p] * A[r * 3 + p];
+        beta += A[r * 3 + q] * A[r * 3 + q];
+        gamma += A[r * 3 + p] * A[r * 3 + q];
+      }
+      if (gamma != 0.0 && fabs(gamma) > 1e-16 * sqrt(alpha * beta)) {
+        rotated = true;
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        double t;
+        if (fabs(zeta) > 1e150) t = 0.5 / zeta;
+        else t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t);
+        const double sn = c * t;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double ap = A[r * 3 + p], aq = A[r * 3 + q];
+          A[r * 3 + p] = c * ap - sn * aq;
+          A[r * 3 + q] = sn * ap + c * aq;
+          const double vp = V[r * 3 + p], vq = V[r * 3 + q];
+          V[r * 3 + p] = c * vp - sn * vq;
+          V[r * 3 + q] = sn * vp + c * vq;
+        }
+      }
+    }
+    if (!rotated) break;
+  }
+  double sig[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    sig[i] = sqrt(A[0 * 3 + i] * A[0 * 3 + i] + A[1 * 3 + i] * A[1 * 3 + i] + A[2 * 3 + i] * A[2 * 3 + i]);
+  // order the singular values descending (stable)
+  int o0 = 0, o1 = 1, o2 = 2;
+  if (sig[o1] > sig[o0]) { int x = o0; o0 = o1; o1 = x; }
+  if (sig[o2] > sig[o1]) { int x = o1; o1 = o2; o2 = x; }
+  if (sig[o1] > sig[o0]) { int x = o0; o0 = o1; o1 = x; }
+  const double S0 = sig[o0], S1 = sig[o1];
+  if (!(S0 > 0.0) || S1 <= 1e-9 * S0) return false;
+  double u1[3], u2[3], v1[3], v2[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    u1[r] = A[r * 3 + o0] / S0;
+    u2[r] = A[r * 3 + o1] / S1;
+    v1[r] = V[r * 3 + o0];
+    v2[r] = V[r * 3 + o1];
+  }
+  // R = U diag(1,1,sign det(U V^T)) V^T = u1 v1^T + u2 v2^T + (u1 x u2)(v1 x v2)^T
+  const double u3[3] = {u1[1] * u2[2] - u1[2] * u2[1], u1[2] * u2[0] - u1[0] * u2[2],
+                        u1[0] * u2[1] - u1[1] * u2[0]};
+  const double v3[3] = {v1[1] * v2[2] - v1[2] * v2[1], v1[2] * v2[0] - v1[0] * v2[2],
+                        v1[0] * v2[1] - v1[1] * v2[0]};
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) R[a * 3 + b] = u1[a] * v1[b] + u2[a] * v2[b] + u3[a] * v3[b];
+  return true;
+}
+
+// residual |s2 - R s1| (matching.rotation_residuals, matching.py:128-130)
+__device__ __forceinline__ double rot_residual(const double R[9], const double s1[3], const double s2[3]) {
+  const double e0 = s2[0] - (s1[0] * R[0] + s1[1] * R[1] + s1[2] * R[2]);
+  const double e1 = s2[1] - (s1[0] * R[3] + s1[1] * R[4] + s1[2] * R[5]);
+  const double e2 = s2[2] - (s1[0] * R[6] + s1[1] * R[7] + s1[2] * R[8]);
+  return sqrt(e0 * e0 + e1 * e1 + e2 * e2);
+}
+
+// reweight (matching.py:133-136): min(H/d, 1), a zero residual maps to 1
+__device__ __forceinline__ double reweight(double d, double H) {
+  return d > H ? H / fmax(d, 1e-300) : 1.0;
+}
+
+__global__ void k_preselect_refs(const double* __restrict__ src, const double* __restrict__ dst,
+                                 const int64_t* __restrict__ n_dev, int64_t n_fixed,
+                                 const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive,
+                                 double H, int iters, double min_support,
+                                 double* __restrict__ ref_support, double* __restrict__ ref_rot,
+                                 uint8_t* __restrict__ ref_valid) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t n = n_dev ? *n_dev : n_fixed;
+  const int64_t nr = exhaustive ? n : n_refs;
+  if (w >= nr) return;
+  const int64_t ref = exhaustive ? w : refs[w];
+  if (n < 3 || ref < 0 || ref >= n) {
+    if (lane == 0) ref_valid[w] = 0;
+    return;
+  }
+  const double rs0 = src[3 * ref], rs1 = src[3 * ref + 1], rs2 = src[3 * ref + 2];
+  const double rd0 = dst[3 * ref], rd1 = dst[3 * ref + 1], rd2 = dst[3 * ref + 2];
+  double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  bool valid = true;
+  for (int it = 0; it < iters; ++it) {
+    double C[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) C[i] = 0.0;
+    for (int64_t k = lane; k < n; k += 32) {
+      const double s1[3] = {src[3 * k] - rs0, src[3 * k + 1] - rs1, src[3 * k + 2] - rs2};
+      const double s2[3] = {dst[3 * k] - rd0, dst[3 * k + 1] - rd1, dst[3 * k + 2] - rd2};
+      const double wk = it == 0 ? 1.0 : reweight(rot_residual(R, s1, s2), H);
+      const double ws[3] = {s2[0] * wk, s2[1] * wk, s2[2] * wk};
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) C[a * 3 + b] += ws[a] * s1[b];
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i) C[i] = warp_sum(C[i]);
+    if (!procrustes(C, R)) {
+      valid = false;
+      break;
+    }
+  }
+  double support = 0.0;
+  if (valid) {
+    for (int64_t k = lane; k < n; k += 32) {
+      const double s1[3] = {src[3 * k] - rs0, src[3 * k + 1] - rs1, src[3 * k + 2] - rs2};
+      const double s2[3] = {dst[3 * k] - rd0, dst[3 * k + 1] - rd1, dst[3 * k + 2] - rd2};
+      support += reweight(rot_residual(R, s1, s2), H);
+    }
+    support = warp_sum(support);
+    if (support < min_support * (double)n) valid = false;
+  }
+  if (lane == 0) {
+    ref_valid[w] = valid ? 1 : 0;
+    ref_support[w] = support;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) ref_rot[9 * w + i] = R[i];
+  }
+}
+
+// Winner = max support, ties -> lower reference index (matching.py:198-206); then the
+// flags and weights of every match (matching.py:210-213).
+__global__ void k_preselect_final(const double* __restrict__ src, const double* __restrict__ dst,
+                                  const int64_t* __restrict__ n_dev, int64_t n_fixed,
+                                  const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive,
+                                  double H, double inlier_min,
+                                  const double* __restrict__ ref_support,
+                                  const double* __restrict__ ref_rot,
+                                  const uint8_t* __restrict__ ref_valid, double* weights,
+                                  uint8_t* flags, double* residuals, double* rotation,
+                                  int64_t* info, double* support_out) {
+  __shared__ double s_sup[1024];
+  __shared__ int64_t s_ref[1024];
+  __shared__ int64_t s_pos[1024];
+  const int64_t n = n_dev ? *n_dev : n_fixed;
+  const int64_t nr = exhaustive ? n : n_refs;
+  double best = -1.0;
+  int64_t best_ref = -1, best_pos = -1;
+  for (int64_t w = threadIdx.x; w < nr; w += blockDim.x) {
+    if (!ref_valid[w]) continue;
+    const int64_t ref = exhaustive ? w : refs[w];
+    const double sp = ref_support[w];
+    if (best_ref < 0 || sp > best || (sp == best && ref < best_ref)) {
+      best = sp;
+      best_ref = ref;
+      best_pos = w;
+    }
+  }
+  s_sup[threadIdx.x] = best;
+  s_ref[threadIdx.x] = best_ref;
+  s_pos[threadIdx.x] = best_pos;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      const double os = s_sup[threadIdx.x + off];
+      const int64_t orf = s_ref[threadIdx.x + off];
+      const int64_t op = s_pos[threadIdx.x + off];
+      const int64_t me = s_ref[threadIdx.x];
+      if (orf >= 0 && (me < 0 || os > s_sup[threadIdx.x] || (os == s_sup[threadIdx.x] && orf < me))) {
+        s_sup[threadIdx.x] = os;
+        s_ref[threadIdx.x] = orf;
+        s_pos[threadIdx.x] = op;
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t ref = s_ref[0];
+  const int64_t pos = s_pos[0];
+  if (ref < 0) {
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+      weights[k] = 0.0;
+      flags[k] = 0;
+      if (residuals) residuals[k] = 0.0;
+    }
+    if (threadIdx.x == 0) {
+      info[0] = DT_ERR_NO_VALID_HYPOTHESIS;
+      info[1] = -1;
+      if (support_out) support_out[0] = 0.0;
+      if (rotation)
+        for (int i = 0; i < 9; ++i) rotation[i] = (i % 4 == 0) ? 1.0 : 0.0;
+    }
+    return;
+  }
+  double R[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = ref_rot[9 * pos + i];
+  const double rs0 = src[3 * ref], rs1 = src[3 * ref + 1], rs2 = src[3 * ref + 2];
+  const double rd0 = dst[3 * ref], rd1 = dst[3 * ref + 1], rd2 = dst[3 * ref + 2];
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    const double s1[3] = {src[3 * k] - rs0, src[3 * k + 1] - rs1, src[3 * k + 2] - rs2};
+    const double s2[3] = {dst[3 * k] - rd0, dst[3 * k + 1] - rd1, dst[3 * k + 2] - rd2};
+    const double d = rot_residual(R, s1, s2);
+    const double fw = reweight(d, H);
+    const bool flag = fw >= inlier_min;
+    double soft = 1.0 - d / (5.0 * H);
+    soft = soft < 0.0 ? 0.0 : (soft > 1.0 ? 1.0 : soft);
+    weights[k] = flag ? fw : soft;
+    flags[k] = flag ? 1 : 0;
+    if (residuals) residuals[k] = d;
+  }
+  if (threadIdx.x == 0) {
+    info[0] = DT_OK;
+    info[1] = ref;
+    if (support_out) support_out[0] = s_sup[0];
+    if (rotation)
+      for (int i = 0; i < 9; ++i) rotation[i] = R[i];
+  }
+}
+
+int launch_preselect(const double* src, const double* dst, const int64_t* n_dev, int64_t n_max,
+                     const int64_t* refs, int64_t n_refs, int exhaustive, double H, int iters,
+                     double inlier_min, double min_support, double* weights, uint8_t* flags,
+                     double* residuals, double* rotation, int64_t* info, double* support,
+                     double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s) {
+  const int64_t nr = exhaustive ? n_max : n_refs;
+  if (nr > 0) {
+    const int threads = 256;
+    k_preselect_refs<<<grid_for(nr * 32, threads), threads, 0, s>>>(
+        src, dst, n_dev, n_max, refs, n_refs, exhaustive, H, iters, min_support, ref_support,
+        ref_rot, ref_valid);
+    DT_CHECK_LAUNCH();
+  }
+  k_preselect_final<<<1, 1024, 0, s>>>(src, dst, n_dev, n_max, refs, n_refs, exhaustive, H,
+                                       inlier_min, ref_support, ref_rot, ref_valid, weights, flags,
+                                       residuals, rotation, info, support);
+  DT_CHECK_LAUNCH();
+  return DT_OK;
+}
+
+}  // namespace dt
+
+using namespace dt;
+
+extern "C" {
+
+int dt_hamming_match(const uint8_t* template_desc, int64_t n_template, const uint8_t* frame_desc,
+                     int64_t n_frame, int32_t* best_idx, int32_t* best_dist, void* stream) {
+  DT_REQUIRE(n_template >= 0 && n_frame >= 0, DT_ERR_INVALID_ARGUMENT, "negative descriptor count");
+  return launch_hamming(template_desc, n_template, frame_desc, n_frame, best_idx, best_dist,
+                        as_stream(stream));
+}
+
+int dt_preselect(const double* src, const double* dst, int64_t n, const int64_t* refs,
+                 int64_t n_refs, const dt_preselect_params* params, double* weights,
+                 uint8_t* flags, double* residuals, double* rotation, int64_t* info,
+                 double* support, void* stream) {
+  DT_REQUIRE(params != nullptr, DT_ERR_INVALID_ARGUMENT, "params is NULL");
+  DT_REQUIRE(params->distance_threshold > 0.0, DT_ERR_INVALID_ARGUMENT,
+             "distance_threshold must be positive");
+  DT_REQUIRE(params->n_reweight_iters >= 1, DT_ERR_INVALID_ARGUMENT, "n_reweight_iters must be >= 1");
+  cudaStream_t s = as_stream(stream);
+  const int exhaustive = refs == nullptr ? 1 : 0;
+  const int64_t nr = exhaustive ? n : n_refs;
+  double *ref_support = nullptr, *ref_rot = nullptr;
+  uint8_t* ref_valid = nullptr;
+  const int64_t cap = nr > 0 ? nr : 1;
+  DT_CHECK_CUDA(cudaMallocAsync((void**)&ref_support, sizeof(double) * cap, s));
+  DT_CHECK_CUDA(cudaMallocAsync((void**)&ref_rot, sizeof(double) * 9 * cap, s));
+  DT_CHECK_CUDA(cudaMallocAsync((void**)&ref_valid, cap, s));
+  const int st = launch_preselect(src, dst, nullptr, n, refs, n_refs, exhaustive,
+                                  params->distance_threshold, params->n_reweight_iters,
+                                  params->inlier_weight_min, params->min_support, weights, flags,
+                                  residuals, rotation, info, support, ref_support, ref_rot,
+                                  ref_valid, s);
+  cudaFreeAsync(ref_support, s);
+  cudaFreeAsync(ref_rot, s);
+  cudaFreeAsync(ref_valid, s);
+  return st;
+}
+
+}  // extern "C"

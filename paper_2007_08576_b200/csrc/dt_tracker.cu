@@ -1,0 +1,885 @@
+// dt_tracker.cu -- device-resident tracker: one sequence, one stream.
+//
+// Per frame (tracking.track_frame, tracking.py:67-95):
+//   depth -> normals + validity            k_observation_normals   (correspond.py:36-73)
+//   [ORB] Hamming match + back-projection  k_hamming, k_build_matches (north-star 3a)
+//   preselection                           k_preselect_refs/final  (matching.py:174-226)
+//   active matches, binding, control CSR   k_active, k_csr_*_dev   (solver.py:113-119, 292-296)
+//   LM solve                               k_solve_frame (cluster) (solver.py:267-378)
+//   output warp                            k_warp_all              (warpfield.py:236-250)
+// All launches go to the tracker's stream; the host only waits at the end of the frame
+// when it asked for host outputs.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "dt_common.cuh"
+#include "dt_math.cuh"
+#include "dt_ops.cuh"
+#include "dt_solver.cuh"
+
+namespace dt {
+
+// ---------------------------------------------------------------------------------
+// small device kernels of the frame pipeline
+// ---------------------------------------------------------------------------------
+
+__global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+
+__global__ void k_valid_mask(const double* __restrict__ depth, int64_t npix, double zmin,
+                             double zmax, uint8_t* __restrict__ valid) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npix) return;
+  const double z = depth[i];
+  valid[i] = (isfinite(z) && z > zmin && z < zmax) ? 1 : 0;
+}
+
+// Block-wide exclusive scan of 0/1 flags for a 1024-thread CTA. Returns this thread's
+// offset; *total receives the block count.
+__device__ __forceinline__ int block_scan_flag(bool flag, int* s_warp, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, flag);
+  const int in_warp = __popc(bal & ((1u << lane) - 1u));
+  if (lane == 0) s_warp[warp] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      const int v = s_warp[w];
+      s_warp[w] = run;
+      run += v;
+    }
+    s_warp[32] = run;
+  }
+  __syncthreads();
+  const int off = s_warp[warp] + in_warp;
+  *total = s_warp[32];
+  __syncthreads();
+  return off;
+}
+
+// ORB path: keep, in template-feature order, every feature whose best frame match passes
+// the Hamming gate and lands on a valid depth pixel; the observed point is the keypoint
+// back-projected through the frame's depth (geometry.back_project, geometry.py:387-396).
+__global__ void __launch_bounds__(1024)
+k_build_matches(int64_t nt, const int32_t* __restrict__ best_idx, const int32_t* __restrict__ best_dist,
+                int max_ham, const int32_t* __restrict__ kp, int64_t nf,
+                const double* __restrict__ depth, const uint8_t* __restrict__ dvalid, int width,
+                int height, double fx, double fy, double cx, double cy,
+                const double* __restrict__ tpts, const int32_t* __restrict__ tbidx,
+                const double* __restrict__ tbw, int k, double* __restrict__ src,
+                double* __restrict__ dst, int32_t* __restrict__ bidx, double* __restrict__ bw,
+                int32_t* __restrict__ feat_id, int64_t* __restrict__ n_out) {
+  __shared__ int s_warp[33];
+  int64_t base_out = 0;
+  for (int64_t base = 0; base < nt; base += blockDim.x) {
+    const int64_t t = base + threadIdx.x;
+    bool ok = false;
+    int u = 0, v = 0;
+    if (t < nt) {
+      const int f = best_idx[t];
+      if (f >= 0 && f < nf && best_dist[t] <= max_ham) {
+        u = kp[2 * f];
+        v = kp[2 * f + 1];
+        ok = u >= 0 && u < width && v >= 0 && v < height && dvalid[(int64_t)v * width + u];
+      }
+    }
+    int total;
+    const int off = block_scan_flag(ok, s_warp, &total);
+    if (ok) {
+      const int64_t o = base_out + off;
+      const double d = depth[(int64_t)v * width + u];
+      src[3 * o] = tpts[3 * t];
+      src[3 * o + 1] = tpts[3 * t + 1];
+      src[3 * o + 2] = tpts[3 * t + 2];
+      dst[3 * o] = ((double)u - cx) / fx * d;
+      dst[3 * o + 1] = ((double)v - cy) / fy * d;
+      dst[3 * o + 2] = d;
+      for (int s = 0; s < k; ++s) {
+        bidx[o * k + s] = tbidx[t * k + s];
+        bw[o * k + s] = tbw[t * k + s];
+      }
+      feat_id[o] = (int32_t)t;
+    }
+    base_out += total;
+  }
+  if (threadIdx.x == 0) *n_out = base_out;
+}
+
+// Active matches (weights > 0, solver.py:113) in order, plus the report statistics
+// n_preselected and match_weight_sum (solver.py:368-370), summed in a fixed order.
+__global__ void __launch_bounds__(1024)
+k_active(const int64_t* __restrict__ n_dev, const double* __restrict__ weights,
+         const uint8_t* __restrict__ flags, const double* __restrict__ src,
+         const double* __restrict__ dst, const int32_t* __restrict__ bidx,
+         const double* __restrict__ bw, int k, int use, double* __restrict__ fp,
+         double* __restrict__ fo, double* __restrict__ fwt, int32_t* __restrict__ fbidx,
+         double* __restrict__ fbw, int64_t* __restrict__ n_active, double* __restrict__ stats) {
+  __shared__ int s_warp[33];
+  __shared__ double s_sum[32];
+  const int64_t n = use ? *n_dev : 0;
+  int64_t base_out = 0;
+  double wsum = 0.0;
+  int64_t nflag = 0;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t j = base + threadIdx.x;
+    const bool in = j < n;
+    const double w = in ? weights[j] : 0.0;
+    const bool act = in && w > 0.0;
+    // fixed-order chunk sum of the weights
+    double v = warp_sum(w);
+    if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = v;
+    int flg = (in && flags[j]) ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) flg += __shfl_xor_sync(0xffffffffu, flg, o);
+    int total;
+    const int off = block_scan_flag(act, s_warp, &total);
+    if (threadIdx.x == 0) {
+      double cs = 0.0;
+      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) cs += s_sum[w2];
+      wsum += cs;
+    }
+    if (act) {
+      const int64_t o = base_out + off;
+      for (int i = 0; i < 3; ++i) {
+        fp[3 * o + i] = src[3 * j + i];
+        fo[3 * o + i] = dst[3 * j + i];
+      }
+      fwt[o] = w;
+      for (int s = 0; s < k; ++s) {
+        fbidx[o * k + s] = bidx[j * k + s];
+        fbw[o * k + s] = bw[j * k + s];
+      }
+    }
+    if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = flg;  // reuse after scan
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) nflag += s_warp[w2];
+    __syncthreads();
+    base_out += total;
+  }
+  if (threadIdx.x == 0) {
+    *n_active = base_out;
+    stats[0] = wsum;
+    stats[1] = (double)nflag;
+  }
+}
+
+// Control -> (match * k + slot) CSR over the active matches, count read on the device.
+__global__ void k_csr_count_dev(const int32_t* __restrict__ keys, const int64_t* __restrict__ n_dev,
+                                int k, int m, int* __restrict__ cnt) {
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (warp >= m) return;
+  const int64_t ne = *n_dev * k;
+  int total = 0;
+  for (int64_t base = 0; base < ne; base += 32) {
+    const int64_t e = base + lane;
+    const bool hit = e < ne && keys[e] == warp;
+    total += __popc(__ballot_sync(0xffffffffu, hit));
+  }
+  if (lane == 0) cnt[warp] = total;
+}
+
+__global__ void k_scan_counts(const int* __restrict__ cnt, int m, int* __restrict__ ptr) {
+  __shared__ int s_part[1024];
+  const int t = threadIdx.x;
+  const int per = (m + blockDim.x - 1) / blockDim.x;
+  const int lo = min(m, t * per), hi = min(m, lo + per);
+  int s = 0;
+  for (int i = lo; i < hi; ++i) s += cnt[i];
+  s_part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int run = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const int v = s_part[i];
+      s_part[i] = run;
+      run += v;
+    }
+    ptr[m] = run;
+  }
+  __syncthreads();
+  int run = s_part[t];
+  for (int i = lo; i < hi; ++i) {
+    ptr[i] = run;
+    run += cnt[i];
+  }
+}
+
+__global__ void k_csr_fill_dev(const int32_t* __restrict__ keys, const int64_t* __restrict__ n_dev,
+                               int k, int m, const int* __restrict__ ptr, int* __restrict__ ent) {
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (warp >= m) return;
+  const int64_t ne = *n_dev * k;
+  int pos = ptr[warp];
+  for (int64_t base = 0; base < ne; base += 32) {
+    const int64_t e = base + lane;
+    const bool hit = e < ne && keys[e] == warp;
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    if (hit) ent[pos + __popc(bal & ((1u << lane) - 1u))] = (int)e;
+    pos += __popc(bal);
+  }
+}
+
+__global__ void k_warp_all_i32(const double* __restrict__ pts, const double* __restrict__ nrm,
+                               const int32_t* __restrict__ bidx, const double* __restrict__ alpha,
+                               int64_t n, int k, const double* __restrict__ warps, double* out_p,
+                               double* out_n) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double B[8], sgn[KMAX];
+  blend_at(warps, bidx + c * k, alpha + c * k, k, B, sgn);
+  double x0, x1, x2, s2;
+  apply_blend(B, pts[3 * c], pts[3 * c + 1], pts[3 * c + 2], x0, x1, x2, s2);
+  double r0, r1, r2;
+  rotate_normal(B, nrm[3 * c], nrm[3 * c + 1], nrm[3 * c + 2], r0, r1, r2);
+  out_p[3 * c] = x0;
+  out_p[3 * c + 1] = x1;
+  out_p[3 * c + 2] = x2;
+  out_n[3 * c] = r0;
+  out_n[3 * c + 1] = r1;
+  out_n[3 * c + 2] = r2;
+}
+
+int launch_warp_all_i32(const double* pts, const double* nrm, const int32_t* bidx,
+                        const double* alpha, int64_t n, int k, const double* warps, double* out_p,
+                        double* out_n, cudaStream_t s) {
+  if (n == 0) return DT_OK;
+  k_warp_all_i32<<<grid_for(n, 128), 128, 0, s>>>(pts, nrm, bidx, alpha, n, k, warps, out_p, out_n);
+  DT_CHECK_LAUNCH();
+  return DT_OK;
+}
+
+}  // namespace dt
+
+using namespace dt;
+
+// ---------------------------------------------------------------------------------
+// tracker state
+// ---------------------------------------------------------------------------------
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct dt_tracker {
+  dt_config cfg;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n = 0, k = 0, m = 0, ne = 0;
+  int cluster = 1;
+  int launches = 0;
+  bool args_dirty = false;
+  std::vector<DevBuf> bufs;
+  // template / graph
+  double *tp = nullptr, *tn = nullptr, *bw = nullptr, *cpts = nullptr, *ew = nullptr;
+  int32_t *bidx = nullptr, *edges = nullptr;
+  int *cptr = nullptr, *cent = nullptr, *iptr = nullptr, *ient = nullptr;
+  // frame
+  double *depth = nullptr, *onrm = nullptr;
+  uint8_t* dvalid = nullptr;
+  // features (ORB path)
+  int64_t n_feat = 0;
+  uint8_t* tdesc = nullptr;
+  double* tfeat_pts = nullptr;
+  int32_t* tfeat_bidx = nullptr;
+  double* tfeat_bw = nullptr;
+  uint8_t* fdesc = nullptr;
+  int32_t* fkp = nullptr;
+  int64_t fdesc_cap = 0;
+  int32_t *ham_idx = nullptr, *ham_dist = nullptr;
+  // matches
+  int64_t match_cap = 0;
+  double *m_src = nullptr, *m_dst = nullptr, *m_w = nullptr, *m_res = nullptr, *m_bw = nullptr;
+  uint8_t* m_flags = nullptr;
+  int32_t *m_bidx = nullptr, *m_feat = nullptr;
+  int64_t* refs = nullptr;
+  int64_t refs_cap = 0;
+  double *ref_support = nullptr, *ref_rot = nullptr;
+  uint8_t* ref_valid = nullptr;
+  int64_t* info = nullptr;      // [0] status [1] ref, [2] n_match, [3] n_active
+  double* pstats = nullptr;     // [0] support [1] rotation... (support only)
+  double* astats = nullptr;     // [0] weight sum [1] n flags
+  double *fp = nullptr, *fo = nullptr, *fwt = nullptr, *fbw = nullptr;
+  int32_t* fbidx = nullptr;
+  int *mptr = nullptr, *ment = nullptr, *mcnt = nullptr;
+  // solver state
+  double *warp_a = nullptr, *warp_b = nullptr, *warps_out = nullptr, *lam = nullptr, *wa = nullptr;
+  double *partial = nullptr, *cost3 = nullptr, *cost3_t = nullptr, *delta = nullptr, *oknorm = nullptr;
+  uint8_t *cvalid = nullptr, *pr_sgn = nullptr, *fr_sgn = nullptr;
+  double *cobs = nullptr, *cnrm = nullptr, *pr_r = nullptr, *pr_rs = nullptr, *pr_gn = nullptr;
+  double *fr_res = nullptr, *fr_G = nullptr;
+  int* cta_counts = nullptr;
+  dt_report* report = nullptr;
+  double *cost_hist = nullptr, *lam_hist = nullptr, *wa_out = nullptr;
+  int32_t* stalled_hist = nullptr;
+  // outputs
+  double *out_p = nullptr, *out_n = nullptr;
+  SolverArgs host_args;
+  SolverArgs* dev_args = nullptr;
+  // pinned staging for the report / stats
+  dt_report* h_report = nullptr;
+  int64_t* h_info = nullptr;
+  double* h_stats = nullptr;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(dt_tracker* t, T** out, size_t count) {
+  void* p = nullptr;
+  const size_t bytes = sizeof(T) * (count > 0 ? count : 1);
+  DT_CHECK_CUDA(cudaMalloc(&p, bytes));
+  DT_CHECK_CUDA(cudaMemsetAsync(p, 0, bytes, t->stream));
+  t->bufs.push_back({p, bytes});
+  *out = static_cast<T*>(p);
+  return DT_OK;
+}
+
+#define DT_TRY(expr)        \
+  do {                      \
+    int _st = (expr);       \
+    if (_st != DT_OK) return _st; \
+  } while (0)
+
+template <typename T>
+int upload(dt_tracker* t, T* dst, const T* src, size_t count) {
+  if (count == 0) return DT_OK;
+  DT_CHECK_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyHostToDevice, t->stream));
+  return DT_OK;
+}
+
+int ensure_match_capacity(dt_tracker* t, int64_t cap) {
+  if (cap <= t->match_cap) return DT_OK;
+  cap = std::max<int64_t>(cap, 64);
+  const int64_t k = t->k;
+  DT_TRY(dalloc(t, &t->m_src, 3 * cap));
+  DT_TRY(dalloc(t, &t->m_dst, 3 * cap));
+  DT_TRY(dalloc(t, &t->m_w, cap));
+  DT_TRY(dalloc(t, &t->m_res, cap));
+  DT_TRY(dalloc(t, &t->m_flags, cap));
+  DT_TRY(dalloc(t, &t->m_bidx, k * cap));
+  DT_TRY(dalloc(t, &t->m_bw, k * cap));
+  DT_TRY(dalloc(t, &t->m_feat, cap));
+  DT_TRY(dalloc(t, &t->ref_support, cap));
+  DT_TRY(dalloc(t, &t->ref_rot, 9 * cap));
+  DT_TRY(dalloc(t, &t->ref_valid, cap));
+  DT_TRY(dalloc(t, &t->fp, 3 * cap));
+  DT_TRY(dalloc(t, &t->fo, 3 * cap));
+  DT_TRY(dalloc(t, &t->fwt, cap));
+  DT_TRY(dalloc(t, &t->fbidx, k * cap));
+  DT_TRY(dalloc(t, &t->fbw, k * cap));
+  DT_TRY(dalloc(t, &t->ment, k * cap));
+  DT_TRY(dalloc(t, &t->fr_res, 3 * cap));
+  DT_TRY(dalloc(t, &t->fr_G, 24 * cap));
+  DT_TRY(dalloc(t, &t->fr_sgn, cap));
+  t->match_cap = cap;
+  t->args_dirty = true;
+  return DT_OK;
+}
+
+void fill_args(dt_tracker* t) {
+  SolverArgs& a = t->host_args;
+  const dt_config& c = t->cfg;
+  a.n = (int)t->n;
+  a.k = (int)t->k;
+  a.m = (int)t->m;
+  a.n_edges = (int)t->ne;
+  a.height = c.height;
+  a.width = c.width;
+  a.max_outer = c.max_outer_iters;
+  a.max_retries = c.max_retries;
+  a.fx = c.fx; a.fy = c.fy; a.cx = c.cx; a.cy = c.cy;
+  a.gate = c.gate_distance;
+  a.cos_gate = c.cos_gate;
+  a.tukey = c.tukey_scale;
+  a.fw = c.feature_weight;
+  a.arap_w = c.arap_weight;
+  a.angle_w = c.angle_weight;
+  a.rot_w = c.rotation_weight;
+  a.data_floor = c.data_floor;
+  a.lam_init = c.lambda_init;
+  a.lam_dec = c.lambda_decrease;
+  a.lam_inc = c.lambda_increase;
+  a.lam_min = c.lambda_min;
+  a.lam_max = c.lambda_max;
+  a.step_tol = c.step_tol;
+  a.cost_tol = c.cost_tol;
+  a.tp = t->tp; a.tn = t->tn; a.bidx = t->bidx; a.bw = t->bw;
+  a.cptr = t->cptr; a.cent = t->cent;
+  a.cpts = t->cpts; a.edges = t->edges; a.ew = t->ew; a.iptr = t->iptr; a.ient = t->ient;
+  a.depth = t->depth; a.dvalid = t->dvalid; a.onrm = t->onrm;
+  a.n_active = t->info + 3;
+  a.fp = t->fp; a.fo = t->fo; a.fwt = t->fwt; a.fbidx = t->fbidx; a.fbw = t->fbw;
+  a.mptr = t->mptr; a.ment = t->ment;
+  a.warp_a = t->warp_a; a.warp_b = t->warp_b; a.warps_out = t->warps_out;
+  a.lam = t->lam; a.wa = t->wa; a.partial = t->partial; a.cost3 = t->cost3; a.cost3_t = t->cost3_t;
+  a.delta = t->delta; a.oknorm = t->oknorm;
+  a.cvalid = t->cvalid; a.cobs = t->cobs; a.cnrm = t->cnrm;
+  a.pr_r = t->pr_r; a.pr_rs = t->pr_rs; a.pr_gn = t->pr_gn; a.pr_sgn = t->pr_sgn;
+  a.fr_res = t->fr_res; a.fr_G = t->fr_G; a.fr_sgn = t->fr_sgn;
+  a.cta_counts = t->cta_counts;
+  a.report = t->report;
+  a.cost_hist = t->cost_hist;
+  a.lam_hist = t->lam_hist;
+  a.stalled_hist = t->stalled_hist;
+  a.wa_out = t->wa_out;
+}
+
+int push_args(dt_tracker* t) {
+  fill_args(t);
+  t->args_dirty = false;
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->dev_args, &t->host_args, sizeof(SolverArgs),
+                                cudaMemcpyHostToDevice, t->stream));
+  DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
+  return DT_OK;
+}
+
+int validate_config(const dt_config* c) {
+  DT_REQUIRE(c != nullptr, DT_ERR_INVALID_ARGUMENT, "config is NULL");
+  DT_REQUIRE(c->max_outer_iters >= 1 && c->max_retries >= 0, DT_ERR_INVALID_ARGUMENT,
+             "iteration budgets must be positive");
+  DT_REQUIRE(c->lambda_min > 0.0 && c->lambda_min <= c->lambda_init && c->lambda_init <= c->lambda_max,
+             DT_ERR_INVALID_ARGUMENT, "lambda_init must lie inside [lambda_min, lambda_max]");
+  DT_REQUIRE(c->lambda_decrease < 1.0 && c->lambda_increase > 1.0, DT_ERR_INVALID_ARGUMENT,
+             "damping factors must shrink on accept and grow on reject");
+  DT_REQUIRE(c->tukey_scale > 0.0, DT_ERR_INVALID_ARGUMENT, "tukey_scale must be positive");
+  DT_REQUIRE(c->width > 0 && c->height > 0 && c->fx > 0.0 && c->fy > 0.0, DT_ERR_INVALID_ARGUMENT,
+             "invalid camera");
+  return DT_OK;
+}
+
+// stable counting sort of (key, entry) by key on the host (template-time CSR)
+void host_csr(const std::vector<int>& keys, const std::vector<int>& ents, int m,
+              std::vector<int>& ptr, std::vector<int>& out) {
+  ptr.assign(m + 1, 0);
+  for (int kk : keys) ptr[kk + 1]++;
+  for (int i = 0; i < m; ++i) ptr[i + 1] += ptr[i];
+  out.assign(keys.size(), 0);
+  std::vector<int> pos(ptr.begin(), ptr.end() - 1);
+  for (size_t i = 0; i < keys.size(); ++i) out[pos[keys[i]]++] = ents[i];
+}
+
+int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
+  cudaStream_t s = t->stream;
+  const dt_config& c = t->cfg;
+  const int64_t npix = (int64_t)c.width * c.height;
+  const cudaMemcpyKind kind = in->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  DT_REQUIRE(in->depth != nullptr, DT_ERR_INVALID_ARGUMENT, "depth is required");
+  t->launches = 0;
+  // warm start: the previous solution (or set_warps) is in warps_out
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->warp_a, t->warps_out, sizeof(double) * 8 * t->m,
+                                cudaMemcpyDeviceToDevice, s));
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->depth, in->depth, sizeof(double) * npix, kind, s));
+  if (in->normals) {
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->onrm, in->normals, sizeof(double) * 3 * npix, kind, s));
+    k_valid_mask<<<grid_for(npix, 256), 256, 0, s>>>(t->depth, npix, c.z_min, c.z_max, t->dvalid);
+    DT_CHECK_LAUNCH();
+  } else {
+    DT_TRY(launch_observation_normals(t->depth, c.height, c.width, c.fx, c.fy, c.cx, c.cy, c.z_min,
+                                      c.z_max, t->onrm, t->dvalid, s));
+  }
+  ++t->launches;
+
+  // ---- matches ----
+  bool use = in->use_matches != 0;
+  int64_t n_max = 0;
+  if (use && in->frame_desc != nullptr) {
+    DT_REQUIRE(t->n_feat > 0, DT_ERR_INVALID_ARGUMENT, "frame descriptors given but no template features set");
+    if (in->n_frame > t->fdesc_cap) {
+      const int64_t cap = std::max<int64_t>(in->n_frame, 256);
+      DT_TRY(dalloc(t, &t->fdesc, 32 * cap));
+      DT_TRY(dalloc(t, &t->fkp, 2 * cap));
+      t->fdesc_cap = cap;
+    }
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->fdesc, in->frame_desc, 32 * in->n_frame, kind, s));
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
+    DT_TRY(launch_hamming(t->tdesc, t->n_feat, t->fdesc, in->n_frame, t->ham_idx, t->ham_dist, s));
+    k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_idx, t->ham_dist, c.max_hamming, t->fkp,
+                                       in->n_frame, t->depth, t->dvalid, c.width, c.height, c.fx,
+                                       c.fy, c.cx, c.cy, t->tfeat_pts, t->tfeat_bidx, t->tfeat_bw,
+                                       (int)t->k, t->m_src, t->m_dst, t->m_bidx, t->m_bw, t->m_feat,
+                                       t->info + 2);
+    DT_CHECK_LAUNCH();
+    t->launches += 2;
+    n_max = t->n_feat;
+  } else if (use && in->n_pairs > 0) {
+    DT_TRY(ensure_match_capacity(t, in->n_pairs));
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->m_src, in->match_src, sizeof(double) * 3 * in->n_pairs, kind, s));
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->m_dst, in->match_dst, sizeof(double) * 3 * in->n_pairs, kind, s));
+    k_set_i64<<<1, 1, 0, s>>>(t->info + 2, in->n_pairs);
+    DT_CHECK_LAUNCH();
+    // per-frame binding of the match template points, sigma = graph sampling radius
+    // (solver.py:292-296)
+    DT_TRY(launch_bind_points_i32(t->m_src, in->n_pairs, t->cpts, (int)t->m, (int)t->k,
+                                  c.sampling_radius, t->m_bidx, t->m_bw, s));
+    t->launches += 2;
+    n_max = in->n_pairs;
+  } else {
+    use = false;
+  }
+  *used_matches = use;
+  if (use && in->match_w != nullptr && in->frame_desc == nullptr) {
+    // weights given by the caller (already annotated MatchSet): no preselection
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->m_w, in->match_w, sizeof(double) * in->n_pairs, kind, s));
+    DT_CHECK_CUDA(cudaMemsetAsync(t->m_flags, 0, in->n_pairs, s));
+    k_set_i64<<<1, 1, 0, s>>>(t->info, DT_OK);
+    DT_CHECK_LAUNCH();
+    ++t->launches;
+  } else if (use) {
+    int exhaustive = 1;
+    int64_t n_refs = 0;
+    if (in->refs != nullptr && in->n_refs > 0) {
+      if (in->n_refs > t->refs_cap) {
+        DT_TRY(dalloc(t, &t->refs, in->n_refs));
+        t->refs_cap = in->n_refs;
+      }
+      DT_CHECK_CUDA(cudaMemcpyAsync(t->refs, in->refs, sizeof(int64_t) * in->n_refs, kind, s));
+      exhaustive = 0;
+      n_refs = in->n_refs;
+    }
+    if (!exhaustive && n_refs > t->match_cap) DT_TRY(ensure_match_capacity(t, n_refs));
+    DT_TRY(launch_preselect(t->m_src, t->m_dst, t->info + 2, n_max, t->refs, n_refs, exhaustive,
+                            c.preselect.distance_threshold, c.preselect.n_reweight_iters,
+                            c.preselect.inlier_weight_min, c.preselect.min_support, t->m_w,
+                            t->m_flags, t->m_res, nullptr, t->info, t->pstats, t->ref_support,
+                            t->ref_rot, t->ref_valid, s));
+    t->launches += 2;
+  } else {
+    k_set_i64<<<1, 1, 0, s>>>(t->info + 2, 0);
+    DT_CHECK_LAUNCH();
+    ++t->launches;
+  }
+  k_active<<<1, 1024, 0, s>>>(t->info + 2, t->m_w, t->m_flags, t->m_src, t->m_dst, t->m_bidx,
+                              t->m_bw, (int)t->k, use ? 1 : 0, t->fp, t->fo, t->fwt, t->fbidx,
+                              t->fbw, t->info + 3, t->astats);
+  DT_CHECK_LAUNCH();
+  const int cthreads = 256;
+  const int cblocks = grid_for(t->m * 32, cthreads);
+  k_csr_count_dev<<<cblocks, cthreads, 0, s>>>(t->fbidx, t->info + 3, (int)t->k, (int)t->m, t->mcnt);
+  DT_CHECK_LAUNCH();
+  k_scan_counts<<<1, 1024, 0, s>>>(t->mcnt, (int)t->m, t->mptr);
+  DT_CHECK_LAUNCH();
+  k_csr_fill_dev<<<cblocks, cthreads, 0, s>>>(t->fbidx, t->info + 3, (int)t->k, (int)t->m, t->mptr,
+                                              t->ment);
+  DT_CHECK_LAUNCH();
+  t->launches += 4;
+
+  // ---- solve ----
+  if (t->args_dirty) {
+    fill_args(t);
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->dev_args, &t->host_args, sizeof(SolverArgs),
+                                  cudaMemcpyHostToDevice, s));
+    DT_CHECK_CUDA(cudaStreamSynchronize(s));
+    t->args_dirty = false;
+  }
+  DT_CHECK_CUDA(cudaMemsetAsync(t->stalled_hist, 0, sizeof(int32_t) * c.max_outer_iters, s));
+  DT_TRY(solver_launch(t->dev_args, 1, t->cluster, (int)t->m, s));
+  ++t->launches;
+  // ---- output warp (tracking.py:87) ----
+  DT_TRY(launch_warp_all_i32(t->tp, t->tn, t->bidx, t->bw, t->n, (int)t->k, t->warps_out, t->out_p,
+                             t->out_n, s));
+  ++t->launches;
+  return DT_OK;
+}
+
+int collect_outputs(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out, bool used) {
+  cudaStream_t s = t->stream;
+  if (out == nullptr) return DT_OK;
+  if (out->warps)
+    DT_CHECK_CUDA(cudaMemcpyAsync(out->warps, t->warps_out, sizeof(double) * 8 * t->m, cudaMemcpyDeviceToHost, s));
+  if (out->points)
+    DT_CHECK_CUDA(cudaMemcpyAsync(out->points, t->out_p, sizeof(double) * 3 * t->n, cudaMemcpyDeviceToHost, s));
+  if (out->normals)
+    DT_CHECK_CUDA(cudaMemcpyAsync(out->normals, t->out_n, sizeof(double) * 3 * t->n, cudaMemcpyDeviceToHost, s));
+  if (out->control_data_weights)
+    DT_CHECK_CUDA(cudaMemcpyAsync(out->control_data_weights, t->wa_out, sizeof(double) * t->m,
+                                  cudaMemcpyDeviceToHost, s));
+  const int64_t cap = std::min<int64_t>(out->match_capacity, t->match_cap);
+  if (cap > 0) {
+    if (out->match_weights)
+      DT_CHECK_CUDA(cudaMemcpyAsync(out->match_weights, t->m_w, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
+    if (out->match_flags)
+      DT_CHECK_CUDA(cudaMemcpyAsync(out->match_flags, t->m_flags, cap, cudaMemcpyDeviceToHost, s));
+    if (out->match_src)
+      DT_CHECK_CUDA(cudaMemcpyAsync(out->match_src, t->m_src, sizeof(double) * 3 * cap, cudaMemcpyDeviceToHost, s));
+    if (out->match_dst)
+      DT_CHECK_CUDA(cudaMemcpyAsync(out->match_dst, t->m_dst, sizeof(double) * 3 * cap, cudaMemcpyDeviceToHost, s));
+  }
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->h_report, t->report, sizeof(dt_report), cudaMemcpyDeviceToHost, s));
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->h_info, t->info, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, s));
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->h_stats, t->astats, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->h_stats + 2, t->pstats, sizeof(double), cudaMemcpyDeviceToHost, s));
+  DT_CHECK_CUDA(cudaStreamSynchronize(s));
+  dt_report* R = t->h_report;
+  R->frame_id = in->frame_id;
+  if (used) {
+    R->n_matches = (int32_t)t->h_info[2];
+    R->n_preselected = (int32_t)t->h_stats[1];
+    R->match_weight_sum = t->h_stats[0];
+    R->preselect_status = (int32_t)t->h_info[0];
+    R->preselect_reference = (int32_t)t->h_info[1];
+    R->preselect_support = t->h_stats[2];
+  } else {
+    R->n_matches = 0;
+    R->n_preselected = 0;
+    R->match_weight_sum = 0.0;
+    R->preselect_status = DT_OK;
+    R->preselect_reference = -1;
+    R->preselect_support = 0.0;
+  }
+  if (out->report) *out->report = *R;
+  return DT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dt_tracker_create(const dt_config* cfg, const double* t_points, const double* t_normals,
+                      const int64_t* bind_idx, const double* bind_w, int64_t n, int64_t k,
+                      const double* ctrl_points, const double* warps, int64_t m,
+                      const int64_t* edges, const double* edge_weights, int64_t n_edges,
+                      int device, void* stream, dt_tracker** out) {
+  DT_TRY(validate_config(cfg));
+  DT_REQUIRE(out != nullptr, DT_ERR_INVALID_ARGUMENT, "out is NULL");
+  DT_REQUIRE(m >= 1, DT_ERR_EMPTY_TEMPLATE, "control graph is empty");
+  DT_REQUIRE(k >= 1 && k <= KMAX, DT_ERR_UNSUPPORTED, "bind_k outside [1, %d]", KMAX);
+  DT_REQUIRE(bind_idx != nullptr && bind_w != nullptr, DT_ERR_NOT_BOUND,
+             "template must be bound to the control graph first");
+  DT_REQUIRE(n < (1ll << 28), DT_ERR_UNSUPPORTED, "template too large");
+  DT_CHECK_CUDA(cudaSetDevice(device));
+  dt_tracker* t = new (std::nothrow) dt_tracker();
+  DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "out of host memory");
+  t->cfg = *cfg;
+  t->device = device;
+  t->n = n;
+  t->k = k;
+  t->m = m;
+  t->ne = n_edges;
+  if (stream) t->stream = as_stream(stream);
+  else DT_CHECK_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+  const int64_t npix = (int64_t)cfg->width * cfg->height;
+  // static data
+  std::vector<int32_t> bidx32(n * k), edges32(2 * n_edges);
+  for (int64_t i = 0; i < n * k; ++i) {
+    DT_REQUIRE(bind_idx[i] >= 0 && bind_idx[i] < m, DT_ERR_INVALID_ARGUMENT, "bind index out of range");
+    bidx32[i] = (int32_t)bind_idx[i];
+  }
+  for (int64_t i = 0; i < 2 * n_edges; ++i) {
+    DT_REQUIRE(edges[i] >= 0 && edges[i] < m, DT_ERR_INVALID_ARGUMENT, "edge index out of range");
+    edges32[i] = (int32_t)edges[i];
+  }
+  // control -> (point, slot), encoded (p << 3) | slot, in point order
+  std::vector<int> keys(n * k), ents(n * k), cptr, cent;
+  for (int64_t p = 0; p < n; ++p)
+    for (int64_t s = 0; s < k; ++s) {
+      keys[p * k + s] = bidx32[p * k + s];
+      ents[p * k + s] = (int)((p << 3) | s);
+    }
+  host_csr(keys, ents, (int)m, cptr, cent);
+  std::vector<int> ekeys(2 * n_edges), eents(2 * n_edges), iptr, ient;
+  for (int64_t e = 0; e < n_edges; ++e)
+    for (int s = 0; s < 2; ++s) {
+      ekeys[2 * e + s] = edges32[2 * e + s];
+      eents[2 * e + s] = (int)((e << 1) | s);
+    }
+  host_csr(ekeys, eents, (int)m, iptr, ient);
+
+  DT_TRY(dalloc(t, &t->tp, 3 * n));
+  DT_TRY(dalloc(t, &t->tn, 3 * n));
+  DT_TRY(dalloc(t, &t->bidx, k * n));
+  DT_TRY(dalloc(t, &t->bw, k * n));
+  DT_TRY(dalloc(t, &t->cptr, m + 1));
+  DT_TRY(dalloc(t, &t->cent, k * n));
+  DT_TRY(dalloc(t, &t->cpts, 3 * m));
+  DT_TRY(dalloc(t, &t->edges, 2 * n_edges));
+  DT_TRY(dalloc(t, &t->ew, n_edges));
+  DT_TRY(dalloc(t, &t->iptr, m + 1));
+  DT_TRY(dalloc(t, &t->ient, 2 * n_edges));
+  DT_TRY(upload(t, t->tp, t_points, 3 * n));
+  DT_TRY(upload(t, t->tn, t_normals, 3 * n));
+  DT_TRY(upload(t, t->bidx, bidx32.data(), k * n));
+  DT_TRY(upload(t, t->bw, bind_w, k * n));
+  DT_TRY(upload(t, t->cptr, cptr.data(), m + 1));
+  DT_TRY(upload(t, t->cent, cent.data(), cent.size()));
+  DT_TRY(upload(t, t->cpts, ctrl_points, 3 * m));
+  DT_TRY(upload(t, t->edges, edges32.data(), 2 * n_edges));
+  DT_TRY(upload(t, t->ew, edge_weights, n_edges));
+  DT_TRY(upload(t, t->iptr, iptr.data(), m + 1));
+  DT_TRY(upload(t, t->ient, ient.data(), ient.size()));
+  // frame buffers
+  DT_TRY(dalloc(t, &t->depth, npix));
+  DT_TRY(dalloc(t, &t->onrm, 3 * npix));
+  DT_TRY(dalloc(t, &t->dvalid, npix));
+  DT_TRY(dalloc(t, &t->info, 4));
+  DT_TRY(dalloc(t, &t->pstats, 2));
+  DT_TRY(dalloc(t, &t->astats, 2));
+  DT_TRY(dalloc(t, &t->mptr, m + 1));
+  DT_TRY(dalloc(t, &t->mcnt, m));
+  DT_TRY(ensure_match_capacity(t, 64));
+  // solver state
+  DT_TRY(dalloc(t, &t->warp_a, 8 * m));
+  DT_TRY(dalloc(t, &t->warp_b, 8 * m));
+  DT_TRY(dalloc(t, &t->warps_out, 8 * m));
+  DT_TRY(dalloc(t, &t->lam, m));
+  DT_TRY(dalloc(t, &t->wa, m));
+  DT_TRY(dalloc(t, &t->partial, 27 * m));
+  DT_TRY(dalloc(t, &t->cost3, 3 * m));
+  DT_TRY(dalloc(t, &t->cost3_t, 3 * m));
+  DT_TRY(dalloc(t, &t->delta, 6 * m));
+  DT_TRY(dalloc(t, &t->oknorm, 4 * m));
+  DT_TRY(dalloc(t, &t->cvalid, n));
+  DT_TRY(dalloc(t, &t->cobs, 3 * n));
+  DT_TRY(dalloc(t, &t->cnrm, 3 * n));
+  DT_TRY(dalloc(t, &t->pr_r, n));
+  DT_TRY(dalloc(t, &t->pr_rs, n));
+  DT_TRY(dalloc(t, &t->pr_gn, 8 * n));
+  DT_TRY(dalloc(t, &t->pr_sgn, n));
+  DT_TRY(dalloc(t, &t->cta_counts, 16));
+  DT_TRY(dalloc(t, &t->report, 1));
+  DT_TRY(dalloc(t, &t->cost_hist, 2 * cfg->max_outer_iters));
+  DT_TRY(dalloc(t, &t->lam_hist, 2 * cfg->max_outer_iters));
+  DT_TRY(dalloc(t, &t->stalled_hist, cfg->max_outer_iters));
+  DT_TRY(dalloc(t, &t->wa_out, m));
+  DT_TRY(dalloc(t, &t->out_p, 3 * n));
+  DT_TRY(dalloc(t, &t->out_n, 3 * n));
+  DT_TRY(dalloc(t, &t->dev_args, 1));
+  DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_report, sizeof(dt_report)));
+  DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_info, sizeof(int64_t) * 4));
+  DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_stats, sizeof(double) * 4));
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->warps_out, warps, sizeof(double) * 8 * m, cudaMemcpyHostToDevice, t->stream));
+  DT_REQUIRE(solver_smem_bytes((int)m) <= 227 * 1024, DT_ERR_UNSUPPORTED, "too many control points (%lld)",
+             (long long)m);
+  t->cluster = solver_pick_cluster(device, cfg->cluster_size, (int)m);
+  DT_TRY(push_args(t));
+  *out = t;
+  return DT_OK;
+}
+
+int dt_tracker_destroy(dt_tracker* t) {
+  if (!t) return DT_OK;
+  cudaStreamSynchronize(t->stream);
+  for (auto& b : t->bufs) cudaFree(b.p);
+  if (t->h_report) cudaFreeHost(t->h_report);
+  if (t->h_info) cudaFreeHost(t->h_info);
+  if (t->h_stats) cudaFreeHost(t->h_stats);
+  delete t;
+  return DT_OK;
+}
+
+int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* points, int64_t n_features) {
+  DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
+  DT_REQUIRE(n_features >= 0, DT_ERR_INVALID_ARGUMENT, "negative feature count");
+  t->n_feat = n_features;
+  DT_TRY(ensure_match_capacity(t, n_features));
+  DT_TRY(dalloc(t, &t->tdesc, 32 * n_features));
+  DT_TRY(dalloc(t, &t->tfeat_pts, 3 * n_features));
+  DT_TRY(dalloc(t, &t->tfeat_bidx, t->k * n_features));
+  DT_TRY(dalloc(t, &t->tfeat_bw, t->k * n_features));
+  DT_TRY(dalloc(t, &t->ham_idx, n_features));
+  DT_TRY(dalloc(t, &t->ham_dist, n_features));
+  DT_TRY(upload(t, t->tdesc, desc, 32 * n_features));
+  DT_TRY(upload(t, t->tfeat_pts, points, 3 * n_features));
+  // the match binding depends only on the template-side point (SURVEY §8a invariant):
+  // bind every feature once, sigma = graph sampling radius (solver.py:292-296)
+  DT_TRY(launch_bind_points_i32(t->tfeat_pts, n_features, t->cpts, (int)t->m, (int)t->k,
+                                t->cfg.sampling_radius, t->tfeat_bidx, t->tfeat_bw, t->stream));
+  DT_TRY(push_args(t));
+  return DT_OK;
+}
+
+int dt_tracker_set_warps(dt_tracker* t, const double* warps, int from_device) {
+  DT_REQUIRE(t != nullptr && warps != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->warps_out, warps, sizeof(double) * 8 * t->m,
+                                from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                t->stream));
+  DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
+  return DT_OK;
+}
+
+int dt_tracker_get_warps(dt_tracker* t, double* warps_host) {
+  DT_REQUIRE(t != nullptr && warps_host != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  DT_CHECK_CUDA(cudaMemcpyAsync(warps_host, t->warps_out, sizeof(double) * 8 * t->m,
+                                cudaMemcpyDeviceToHost, t->stream));
+  DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
+  return DT_OK;
+}
+
+int dt_tracker_set_config(dt_tracker* t, const dt_config* cfg) {
+  DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
+  DT_TRY(validate_config(cfg));
+  DT_REQUIRE(cfg->width == t->cfg.width && cfg->height == t->cfg.height, DT_ERR_INVALID_ARGUMENT,
+             "camera size cannot change on a live tracker");
+  if (cfg->max_outer_iters > t->cfg.max_outer_iters) {
+    DT_TRY(dalloc(t, &t->cost_hist, 2 * cfg->max_outer_iters));
+    DT_TRY(dalloc(t, &t->lam_hist, 2 * cfg->max_outer_iters));
+    DT_TRY(dalloc(t, &t->stalled_hist, cfg->max_outer_iters));
+  }
+  t->cfg = *cfg;
+  t->cluster = solver_pick_cluster(t->device, cfg->cluster_size, (int)t->m);
+  DT_TRY(push_args(t));
+  return DT_OK;
+}
+
+int dt_tracker_sync(dt_tracker* t) {
+  DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
+  DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
+  return DT_OK;
+}
+
+int dt_track_frame(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out) {
+  DT_REQUIRE(t != nullptr && in != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  bool used = false;
+  DT_TRY(enqueue_frame(t, in, &used));
+  return collect_outputs(t, in, out, used);
+}
+
+int dt_tracker_get_history(dt_tracker* t, double* cost_history, double* lambda_history,
+                           int32_t* stalled) {
+  DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
+  const int it = t->cfg.max_outer_iters;
+  if (cost_history)
+    DT_CHECK_CUDA(cudaMemcpyAsync(cost_history, t->cost_hist, sizeof(double) * 2 * it, cudaMemcpyDeviceToHost, t->stream));
+  if (lambda_history)
+    DT_CHECK_CUDA(cudaMemcpyAsync(lambda_history, t->lam_hist, sizeof(double) * 2 * it, cudaMemcpyDeviceToHost, t->stream));
+  if (stalled)
+    DT_CHECK_CUDA(cudaMemcpyAsync(stalled, t->stalled_hist, sizeof(int32_t) * it, cudaMemcpyDeviceToHost, t->stream));
+  DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
+  return DT_OK;
+}
+
+int dt_tracker_device_outputs(dt_tracker* t, double** warps, double** points, double** normals) {
+  DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
+  if (warps) *warps = t->warps_out;
+  if (points) *points = t->out_p;
+  if (normals) *normals = t->out_n;
+  return DT_OK;
+}
+
+int dt_tracker_last_launches(dt_tracker* t) { return t ? t->launches : 0; }
+
+int dt_track_frames_batched(dt_tracker** trackers, const dt_frame_input* inputs,
+                            dt_frame_output* outputs, int32_t n_trackers, void* stream) {
+  (void)stream;
+  // independent sequences: each tracker enqueues on its own stream; the streams overlap
+  // on the device (one cluster per sequence)
+  std::vector<char> used(n_trackers, 0);
+  for (int32_t i = 0; i < n_trackers; ++i) {
+    bool u = false;
+    DT_TRY(enqueue_frame(trackers[i], &inputs[i], &u));
+    used[i] = u ? 1 : 0;
+  }
+  for (int32_t i = 0; i < n_trackers; ++i)
+    DT_TRY(collect_outputs(trackers[i], &inputs[i], outputs ? &outputs[i] : nullptr, used[i] != 0));
+  return DT_OK;
+}
+
+}  // extern "C"

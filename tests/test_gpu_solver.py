@@ -1,0 +1,152 @@
+"""Frame-level parity on the GPU: the fused cluster LM solver against the reference's
+own solve_frame / track_frame outputs (golden fixtures), teacher-forced per frame
+(each frame starts from the reference's previous-frame warps).
+
+Bars (north star): per-vertex positions within 1e-4 m = 0.1 mm (the reference is in
+mm), final cost / RMS within 1 %, preselection flags bit-exact, integer report fields
+exact. The device is held to much tighter numbers where the physics allows it."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from tests.fixtures import SOLVER_CASES, jload, load, solver_case  # noqa: E402
+
+VERTEX_TOL_MM = 1e-4 * 1e3   # 1e-4 m, the north-star bar, in the reference's mm
+
+
+def _api():
+    import paper_2007_08576_b200 as dt
+
+    return dt
+
+
+def _template_graph(dt, tpl, graph, warps, radius):
+    t = dt.Template(tpl[0], tpl[1], bind_indices=tpl[2], bind_weights=tpl[3])
+    g = dt.ControlGraph(graph[0], warps, graph[1], graph[2], sampling_radius=radius)
+    return t, g
+
+
+@pytest.mark.parametrize("name", SOLVER_CASES)
+def test_solve_frame_matches_reference(name):
+    dt = _api()
+    from paper_2007_08576_b200.warpfield import warp_all
+
+    c = solver_case(name)
+    fx, fy, cx, cy = c["cam"]
+    cam = dt.PinholeCamera(fx, fy, cx, cy, *c["dims"])
+    tpl, graph = _template_graph(dt, c["tpl"], c["graph"], c["warps_in"], c["radius"])
+    obs = dt.Observation.from_depth(c["depth"], cam)
+    matches = None
+    if c["matches"] is not None:
+        s, d, w, f = c["matches"]
+        matches = dt.MatchSet(s, d, w, f)
+    scfg = {k: v for k, v in c["solver"].items()}
+    out, rep = dt.solve_frame(tpl, graph, obs, matches, dt.EnergyWeights(**c["weights"]),
+                              dt.SolverConfig(**scfg))
+    ref = c["report"]
+    p_dev, _ = warp_all(tpl, out)
+    p_ref, _ = warp_all(tpl, graph.with_warps(c["warps_out"]))
+    assert float(np.abs(p_dev - p_ref).max()) < 1e-6
+    np.testing.assert_allclose(out.warps, c["warps_out"], rtol=0, atol=1e-9)
+    s = ref["solver"]
+    assert rep.n_correspondences == ref["counts"]["correspondences"]
+    assert rep.outer_iterations == s["outer_iterations"]
+    assert rep.accepted_steps == s["accepted_steps"]
+    assert rep.rejected_steps == s["rejected_steps"]
+    assert rep.converged == s["converged"] and rep.stalled == s["stalled"]
+    assert len(rep.cost_history) == len(s["cost_history"])
+    np.testing.assert_allclose(rep.cost_history, s["cost_history"] or np.zeros((0, 2)),
+                               rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(rep.lambda_history, s["lambda_history"], rtol=1e-12)
+    tot = ref["energy"]["total"]
+    assert abs(rep.total_cost - tot) <= 1e-9 * max(tot, 1e-12) + 1e-12
+    np.testing.assert_allclose(rep.control_data_weights, ref["control_data_weights"], rtol=1e-9)
+    assert rep.n_matches == ref["counts"]["matches"]
+    assert rep.n_preselected == ref["counts"]["preselected"]
+
+
+@pytest.mark.parametrize("fixture", ["tracking", "tracking_cfg1"])
+def test_track_frame_teacher_forced(fixture):
+    dt = _api()
+    z = load(fixture)
+    cfgd = jload(z["config"])
+    cfgd.pop("paths", None)
+    cfgd["sampling"] = {k: v for k, v in cfgd["sampling"].items()}
+    cfg = dt.load_config(cfgd)
+    fx, fy, cx, cy, w, h = (float(x) for x in z["cam"])
+    cam = dt.PinholeCamera(fx, fy, cx, cy, int(w), int(h))
+    tpl0 = (z["t_points"], z["t_normals"], z["bind_idx"], z["bind_w"])
+    gr0 = (z["ctrl"], z["edges"], z["edge_w"])
+    tpl, graph = _template_graph(dt, tpl0, gr0, z["f0_warps_in"], float(z["radius"]))
+    for f in range(int(z["n_frames"])):
+        g = graph.with_warps(z[f"f{f}_warps_in"])
+        obs = dt.Observation.from_depth(z[f"f{f}_depth"], cam, frame_id=f)
+        ms = dt.MatchSet.from_pairs(z[f"f{f}_m_src"], z[f"f{f}_m_dst"])
+        res = dt.track_frame(tpl, g, obs, ms, cfg)
+        ref = jload(z[f"f{f}_report"])
+        np.testing.assert_array_equal(res.matches.preselected, z[f"f{f}_m_flags"])
+        np.testing.assert_allclose(res.matches.weights, z[f"f{f}_m_w"], rtol=1e-9, atol=1e-12)
+        dev = float(np.abs(res.points - z[f"f{f}_points"]).max())
+        assert dev < VERTEX_TOL_MM, f"frame {f}: vertex deviation {dev} mm"
+        assert dev < 1e-6, f"frame {f}: vertex deviation {dev} mm (device tighter bar)"
+        tot = ref["energy"]["total"]
+        assert abs(res.report.total_cost - tot) <= 1e-6 * tot
+        assert res.report.n_correspondences == ref["counts"]["correspondences"]
+        assert res.report.accepted_steps == ref["solver"]["accepted_steps"]
+        assert res.report.rejected_steps == ref["solver"]["rejected_steps"]
+        assert res.report.n_preselected == ref["counts"]["preselected"]
+        assert abs(res.report.match_weight_sum - ref["match_weight_sum"]) < 1e-9
+
+
+def test_cluster_size_does_not_change_bits():
+    """The device analogue of the reference's thread-count invariance
+    (test_solver.py:186-206): every reduction is per control in a fixed order, so the
+    solution and report are bitwise identical for any thread-block cluster size."""
+    dt = _api()
+    from paper_2007_08576_b200._session import SESSIONS
+
+    c = solver_case("solver_rigid_matches")
+    fx, fy, cx, cy = c["cam"]
+    cam = dt.PinholeCamera(fx, fy, cx, cy, *c["dims"])
+    tpl, graph = _template_graph(dt, c["tpl"], c["graph"], c["warps_in"], c["radius"])
+    obs = dt.Observation.from_depth(c["depth"], cam)
+    s, d, w, f = c["matches"]
+    ms = dt.MatchSet(s, d, w, f)
+    outs = []
+    for cs in (1, 2, 4, 8, 16):
+        SESSIONS.clear()
+        out, rep = dt.solve_frame(tpl, graph, obs, ms, dt.EnergyWeights(),
+                                  dt.SolverConfig(max_outer_iters=20, cluster_size=cs))
+        outs.append((out.warps, rep.to_dict()))
+    for wts, rd in outs[1:]:
+        np.testing.assert_array_equal(wts, outs[0][0])
+        assert rd == outs[0][1]
+    assert outs[0][1]["solver"]["cost_history"]
+
+
+def test_repeatable_bitwise():
+    dt = _api()
+    c = solver_case("solver_translation")
+    fx, fy, cx, cy = c["cam"]
+    cam = dt.PinholeCamera(fx, fy, cx, cy, *c["dims"])
+    tpl, graph = _template_graph(dt, c["tpl"], c["graph"], c["warps_in"], c["radius"])
+    obs = dt.Observation.from_depth(c["depth"], cam)
+    cfg = dt.SolverConfig(max_outer_iters=10, step_tol=0.0, cost_tol=0.0)
+    a = dt.solve_frame(tpl, graph, obs, None, dt.EnergyWeights(), cfg)
+    b = dt.solve_frame(tpl, graph, obs, None, dt.EnergyWeights(), cfg)
+    np.testing.assert_array_equal(a[0].warps, b[0].warps)
+    assert a[1].to_dict() == b[1].to_dict()
+
+
+def test_unbound_template_raises():
+    dt = _api()
+    c = solver_case("solver_fixed_point")
+    fx, fy, cx, cy = c["cam"]
+    cam = dt.PinholeCamera(fx, fy, cx, cy, *c["dims"])
+    tpl = dt.Template(c["tpl"][0], c["tpl"][1])
+    graph = dt.ControlGraph(c["graph"][0], c["warps_in"], c["graph"][1], c["graph"][2], 4.0)
+    with pytest.raises(ValueError):
+        dt.solve_frame(tpl, graph, dt.Observation.from_depth(c["depth"], cam), None,
+                       dt.EnergyWeights(), dt.SolverConfig())
