@@ -203,9 +203,12 @@ int dt_tracker_create(const dt_config* cfg,
                       int device, void* stream, dt_tracker** out);
 int dt_tracker_destroy(dt_tracker* t);
 /* Template-side ORB features: 256-bit descriptors (T,32) u8 and their frame-0 3D
- * points (T,3) f64 (host). Binds the feature points to the graph once. */
+ * points (T,3) f64 (host). The features' control binding (solver.py:292-296: k nearest
+ * controls, sigma = graph sampling radius) depends only on these fixed points, so it is
+ * computed once here: taken from bind_idx (T,k) int64 / bind_w (T,k) f64 when given
+ * (e.g. the reference's kd-tree order), else on the device (ties -> lower index). */
 int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* points,
-                            int64_t n_features);
+                            int64_t n_features, const int64_t* bind_idx, const double* bind_w);
 /* Warm-start warps (m,8) f64: host (from_device=0) or device pointer. */
 int dt_tracker_set_warps(dt_tracker* t, const double* warps, int from_device);
 int dt_tracker_get_warps(dt_tracker* t, double* warps_host);
@@ -222,6 +225,8 @@ int dt_tracker_sync(dt_tracker* t);
  *   match_w          (n_pairs) f64 weights of ALREADY annotated pairs: preselection is
  *                    skipped (the solver.solve_frame contract, solver.py:267); NULL ->
  *                    the pairs are preselected on the device first (track_frame)
+ *   match_bidx/bw    (n_pairs,k) int64 / f64 binding of the pairs' template points;
+ *                    NULL -> bound on the device per frame (k nearest, ties -> lower index)
  *   refs             (n_refs) int64 preselect references; NULL -> exhaustive arange(n)
  *   use_matches      0 = no feature term this frame
  */
@@ -231,6 +236,8 @@ typedef struct {
   const double* match_src;
   const double* match_dst;
   const double* match_w;
+  const int64_t* match_bidx;
+  const double* match_bw;
   int64_t n_pairs;
   const uint8_t* frame_desc;
   const int32_t* frame_kp;

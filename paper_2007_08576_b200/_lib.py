@@ -74,7 +74,7 @@ class Report(C.Structure):
 class FrameInput(C.Structure):
     _fields_ = [
         ("depth", P), ("normals", P), ("match_src", P), ("match_dst", P), ("match_w", P),
-        ("n_pairs", I64),
+        ("match_bidx", P), ("match_bw", P), ("n_pairs", I64),
         ("frame_desc", P), ("frame_kp", P), ("n_frame", I64), ("refs", P), ("n_refs", I64),
         ("use_matches", I32), ("on_device", I32), ("frame_id", I32),
     ]
@@ -108,7 +108,7 @@ _SIGNATURES: dict[str, list] = {
     "dt_tracker_create": [C.POINTER(Config), P, P, P, P, I64, I64, P, P, I64, P, P, I64, C.c_int,
                           P, C.POINTER(P)],
     "dt_tracker_destroy": [P],
-    "dt_tracker_set_features": [P, P, P, I64],
+    "dt_tracker_set_features": [P, P, P, I64, P, P],
     "dt_tracker_set_warps": [P, P, C.c_int],
     "dt_tracker_get_warps": [P, P],
     "dt_tracker_set_config": [P, C.POINTER(Config)],

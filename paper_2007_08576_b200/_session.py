@@ -9,7 +9,6 @@ thread-block-cluster LM launch, then returns the solution and the report.
 from __future__ import annotations
 
 import ctypes as C
-import math
 from collections import OrderedDict
 from dataclasses import dataclass
 
@@ -126,18 +125,24 @@ class DeviceTracker:
         check(lib.dt_tracker_get_warps(self._h, _host_ptr(out)), "dt_tracker_get_warps")
         return out
 
-    def set_features(self, desc, points) -> None:
+    def set_features(self, desc, points, binding=None) -> None:
         d = np.ascontiguousarray(desc, dtype=np.uint8).reshape(-1, 32)
         p = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
         if d.shape[0] != p.shape[0]:
             raise ValueError("one 3D point per template descriptor required")
-        check(lib.dt_tracker_set_features(self._h, _host_ptr(d), _host_ptr(p), d.shape[0]),
+        bi = bw = None
+        if binding is not None:
+            bi = np.ascontiguousarray(binding[0], dtype=np.int64).reshape(d.shape[0], self.k)
+            bw = np.ascontiguousarray(binding[1], dtype=np.float64).reshape(d.shape[0], self.k)
+        check(lib.dt_tracker_set_features(self._h, _host_ptr(d), _host_ptr(p), d.shape[0],
+                                          _host_ptr(bi), _host_ptr(bw)),
               "dt_tracker_set_features")
         self.n_features = d.shape[0]
 
     # -- frames --------------------------------------------------------------------
-    def track(self, depth, normals=None, *, pairs=None, match_w=None, frame_desc=None,
-              frame_kp=None, refs=None, frame_id: int = 0, want_points: bool = True,
+    def track(self, depth, normals=None, *, pairs=None, match_w=None, match_binding=None,
+              frame_desc=None, frame_kp=None, refs=None, frame_id: int = 0,
+              want_points: bool = True,
               want_matches: bool = False, outputs: dict | None = None) -> FrameOutputs:
         """Run one frame. Host inputs; returns host outputs (after the stream sync)."""
         keep = []
@@ -162,6 +167,9 @@ class DeviceTracker:
             fi.match_src = hp(src, np.float64)
             fi.match_dst = hp(dst, np.float64)
             fi.match_w = hp(match_w, np.float64)
+            if match_binding is not None:
+                fi.match_bidx = hp(match_binding[0], np.int64)
+                fi.match_bw = hp(match_binding[1], np.float64)
         fi.n_pairs = n_pairs
         n_frame = 0
         if frame_desc is not None:
@@ -284,6 +292,3 @@ def nvh_message(n: int) -> str:
         return f"{n} matches cannot support a rotation hypothesis"
     return "every reference hypothesis was discarded"
 
-
-def isclose_cfg(a: Config, b: Config) -> bool:  # pragma: no cover - debug helper
-    return _cfg_bytes(a) == _cfg_bytes(b) and not math.isnan(a.step_tol)

@@ -261,9 +261,9 @@ __global__ void k_preselect_final(const double* __restrict__ src, const double* 
                                   const uint8_t* __restrict__ ref_valid, double* weights,
                                   uint8_t* flags, double* residuals, double* rotation,
                                   int64_t* info, double* support_out) {
-  __shared__ double s_sup[1024];
-  __shared__ int64_t s_ref[1024];
-  __shared__ int64_t s_pos[1024];
+  __shared__ double s_sup[512];
+  __shared__ int64_t s_ref[512];
+  __shared__ int64_t s_pos[512];
   const int64_t n = n_dev ? *n_dev : n_fixed;
   const int64_t nr = exhaustive ? n : n_refs;
   double best = -1.0;
@@ -352,7 +352,7 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
         ref_rot, ref_valid);
     DT_CHECK_LAUNCH();
   }
-  k_preselect_final<<<1, 1024, 0, s>>>(src, dst, n_dev, n_max, refs, n_refs, exhaustive, H,
+  k_preselect_final<<<1, 512, 0, s>>>(src, dst, n_dev, n_max, refs, n_refs, exhaustive, H,
                                        inlier_min, ref_support, ref_rot, ref_valid, weights, flags,
                                        residuals, rotation, info, support);
   DT_CHECK_LAUNCH();

@@ -107,21 +107,31 @@ __device__ __forceinline__ bool rasterize_one(double x0, double x1, double x2, d
                                               int width, double fx, double fy, double cx,
                                               double cy, double gate, double cos_gate,
                                               double obs[3], double g[3], int& ui, int& vi) {
-  if (!(x2 > 0.0)) return false;
+#ifdef DT_DEBUG_RASTER
+#define DBG(...) printf(__VA_ARGS__)
+#else
+#define DBG(...)
+#endif
+  if (!(x2 > 0.0)) { DBG("x2 %g\n", x2); return false; }
   const double uf = rint(fx * x0 / x2 + cx);
   const double vf = rint(fy * x1 / x2 + cy);
+  DBG("uf %.17g vf %.17g w %d h %d\n", uf, vf, width, height);
   if (!(uf >= 0.0 && uf < (double)width && vf >= 0.0 && vf < (double)height)) return false;
   ui = (int)uf;
   vi = (int)vf;
   const int64_t pix = (int64_t)vi * width + ui;
+  DBG("ui %d vi %d pix %lld valid %d\n", ui, vi, (long long)pix, (int)dvalid[pix]);
   if (!dvalid[pix]) return false;
   const double d = depth[pix];
   const double ox = ((double)ui - cx) / fx * d;
   const double oy = ((double)vi - cy) / fy * d;
   const double gx = onrm[3 * pix + 0], gy = onrm[3 * pix + 1], gz = onrm[3 * pix + 2];
+  DBG("d %.17g g %.17g %.17g %.17g\n", d, gx, gy, gz);
   if (gx * gx + gy * gy + gz * gz <= 0.25) return false;
   const double dx = ox - x0, dy = oy - x1, dz = d - x2;
+  DBG("dist %.17g gate %g\n", sqrt(dx * dx + dy * dy + dz * dz), gate);
   if (sqrt(dx * dx + dy * dy + dz * dz) >= gate) return false;
+  DBG("cos %.17g cg %.17g\n", gx * r0 + gy * r1 + gz * r2, cos_gate);
   if (gx * r0 + gy * r1 + gz * r2 <= cos_gate) return false;
   obs[0] = ox;
   obs[1] = oy;
@@ -192,7 +202,7 @@ __global__ void k_csr_count(const KeyT* __restrict__ keys, int64_t ne, int m, in
   if (lane == 0) cnt[warp] = total;
 }
 
-__global__ void k_exclusive_scan(const int* __restrict__ cnt, int m, int* __restrict__ ptr) {
+__global__ void __launch_bounds__(1024) k_exclusive_scan(const int* __restrict__ cnt, int m, int* __restrict__ ptr) {
   // single block; m is at most a few thousand controls
   __shared__ int s_part[1024];
   const int t = threadIdx.x;

@@ -185,7 +185,7 @@ __global__ void k_csr_count_dev(const int32_t* __restrict__ keys, const int64_t*
   if (lane == 0) cnt[warp] = total;
 }
 
-__global__ void k_scan_counts(const int* __restrict__ cnt, int m, int* __restrict__ ptr) {
+__global__ void __launch_bounds__(1024) k_scan_counts(const int* __restrict__ cnt, int m, int* __restrict__ ptr) {
   __shared__ int s_part[1024];
   const int t = threadIdx.x;
   const int per = (m + blockDim.x - 1) / blockDim.x;
@@ -320,6 +320,7 @@ struct dt_tracker {
   dt_report* report = nullptr;
   double *cost_hist = nullptr, *lam_hist = nullptr, *wa_out = nullptr;
   int32_t* stalled_hist = nullptr;
+  int* bad_flag = nullptr;
   // outputs
   double *out_p = nullptr, *out_n = nullptr;
   SolverArgs host_args;
@@ -467,6 +468,38 @@ void host_csr(const std::vector<int>& keys, const std::vector<int>& ents, int m,
   for (size_t i = 0; i < keys.size(); ++i) out[pos[keys[i]]++] = ents[i];
 }
 
+__global__ void k_i64_to_i32(const int64_t* __restrict__ a, int64_t n, int m, int32_t* __restrict__ b,
+                             int* __restrict__ bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t v = a[i];
+  if (v < 0 || v >= m) *bad = 1;
+  b[i] = (int32_t)(v < 0 ? 0 : (v >= m ? m - 1 : v));
+}
+
+// binding (n, k) int64 + f64 from the caller -> the tracker's int32 / f64 buffers
+int upload_binding(dt_tracker* t, const int64_t* bidx, const double* bw, int64_t n, bool on_dev,
+                   int32_t* dst_idx, double* dst_w) {
+  cudaStream_t s = t->stream;
+  const int64_t cnt = n * t->k;
+  if (cnt == 0) return DT_OK;
+  if (on_dev) {
+    k_i64_to_i32<<<grid_for(cnt, 256), 256, 0, s>>>(bidx, cnt, (int)t->m, dst_idx, t->bad_flag);
+    DT_CHECK_LAUNCH();
+  } else {
+    std::vector<int32_t> tmp(cnt);
+    for (int64_t i = 0; i < cnt; ++i) {
+      DT_REQUIRE(bidx[i] >= 0 && bidx[i] < t->m, DT_ERR_INVALID_ARGUMENT, "binding index out of range");
+      tmp[i] = (int32_t)bidx[i];
+    }
+    DT_CHECK_CUDA(cudaMemcpyAsync(dst_idx, tmp.data(), sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, s));
+    DT_CHECK_CUDA(cudaStreamSynchronize(s));  // tmp is stack-owned
+  }
+  DT_CHECK_CUDA(cudaMemcpyAsync(dst_w, bw, sizeof(double) * cnt,
+                                on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  return DT_OK;
+}
+
 int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   cudaStream_t s = t->stream;
   const dt_config& c = t->cfg;
@@ -516,10 +549,16 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     DT_CHECK_CUDA(cudaMemcpyAsync(t->m_dst, in->match_dst, sizeof(double) * 3 * in->n_pairs, kind, s));
     k_set_i64<<<1, 1, 0, s>>>(t->info + 2, in->n_pairs);
     DT_CHECK_LAUNCH();
-    // per-frame binding of the match template points, sigma = graph sampling radius
-    // (solver.py:292-296)
-    DT_TRY(launch_bind_points_i32(t->m_src, in->n_pairs, t->cpts, (int)t->m, (int)t->k,
-                                  c.sampling_radius, t->m_bidx, t->m_bw, s));
+    if (in->match_bidx != nullptr && in->match_bw != nullptr) {
+      // caller-supplied binding (e.g. the reference's kd-tree tie order)
+      DT_TRY(upload_binding(t, in->match_bidx, in->match_bw, in->n_pairs, in->on_device != 0,
+                            t->m_bidx, t->m_bw));
+    } else {
+      // per-frame binding of the match template points, sigma = graph sampling radius
+      // (solver.py:292-296)
+      DT_TRY(launch_bind_points_i32(t->m_src, in->n_pairs, t->cpts, (int)t->m, (int)t->k,
+                                    c.sampling_radius, t->m_bidx, t->m_bw, s));
+    }
     t->launches += 2;
     n_max = in->n_pairs;
   } else {
@@ -744,6 +783,7 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_TRY(dalloc(t, &t->pr_gn, 8 * n));
   DT_TRY(dalloc(t, &t->pr_sgn, n));
   DT_TRY(dalloc(t, &t->cta_counts, 16));
+  DT_TRY(dalloc(t, &t->bad_flag, 1));
   DT_TRY(dalloc(t, &t->report, 1));
   DT_TRY(dalloc(t, &t->cost_hist, 2 * cfg->max_outer_iters));
   DT_TRY(dalloc(t, &t->lam_hist, 2 * cfg->max_outer_iters));
@@ -775,7 +815,8 @@ int dt_tracker_destroy(dt_tracker* t) {
   return DT_OK;
 }
 
-int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* points, int64_t n_features) {
+int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* points, int64_t n_features,
+                            const int64_t* bind_idx, const double* bind_w) {
   DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
   DT_REQUIRE(n_features >= 0, DT_ERR_INVALID_ARGUMENT, "negative feature count");
   t->n_feat = n_features;
@@ -790,8 +831,12 @@ int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* po
   DT_TRY(upload(t, t->tfeat_pts, points, 3 * n_features));
   // the match binding depends only on the template-side point (SURVEY §8a invariant):
   // bind every feature once, sigma = graph sampling radius (solver.py:292-296)
-  DT_TRY(launch_bind_points_i32(t->tfeat_pts, n_features, t->cpts, (int)t->m, (int)t->k,
-                                t->cfg.sampling_radius, t->tfeat_bidx, t->tfeat_bw, t->stream));
+  if (bind_idx != nullptr && bind_w != nullptr) {
+    DT_TRY(upload_binding(t, bind_idx, bind_w, n_features, false, t->tfeat_bidx, t->tfeat_bw));
+  } else {
+    DT_TRY(launch_bind_points_i32(t->tfeat_pts, n_features, t->cpts, (int)t->m, (int)t->k,
+                                  t->cfg.sampling_radius, t->tfeat_bidx, t->tfeat_bw, t->stream));
+  }
   DT_TRY(push_args(t));
   return DT_OK;
 }

@@ -42,7 +42,7 @@ def warp_and_rasterize(points, normals, bind_idx, alpha, warps, depth, depth_val
     obs_n = dev.empty((n, 3))
     pixels = dev.empty((n, 2), np.int64)
     ins = [_d(pts), _d(normals), _d(bidx, np.int64), _d(alpha), _d(W), _d(depth),
-           _d(np.asarray(depth_valid, dtype=np.uint8)), _d(obs_normals)]
+           _d(depth_valid, np.uint8), _d(obs_normals)]
     check(lib.dt_warp_and_rasterize(
         dev.ptr(ins[0]), dev.ptr(ins[1]), dev.ptr(ins[2]), dev.ptr(ins[3]), n, k,
         dev.ptr(ins[4]), W.shape[0], dev.ptr(ins[5]), dev.ptr(ins[6]), dev.ptr(ins[7]), h, w,

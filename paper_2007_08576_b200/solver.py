@@ -127,9 +127,13 @@ def report_from_outputs(out, frame_id: int, matches: MatchSet | None) -> EnergyR
 
 def solve_frame(template: Template, graph: ControlGraph, observation: Observation,
                 matches: MatchSet | None, weights: EnergyWeights, config: SolverConfig,
-                frame_id: int = 0) -> tuple[ControlGraph, EnergyReport]:
+                frame_id: int = 0, *, match_binding=None) -> tuple[ControlGraph, EnergyReport]:
     """Track one frame from the warm start in ``graph`` (solver.py:267-378). The input
-    graph is not modified; returns the solved graph and the frame's report."""
+    graph is not modified; returns the solved graph and the frame's report.
+
+    ``match_binding`` (optional, not in the reference signature): (idx, w) of the
+    matches' template points; by default they are bound on the device each frame
+    (k nearest controls, exact distance ties to the lower control index)."""
     t0 = time.perf_counter()
     if not template.is_bound:
         raise ValueError("template must be bound to the control graph first")
@@ -144,6 +148,7 @@ def solve_frame(template: Template, graph: ControlGraph, observation: Observatio
         None if observation.normals_on_device else observation.normals,
         pairs=(matches.template_points, matches.observed_points) if use else None,
         match_w=matches.weights if use else None,
+        match_binding=match_binding if use else None,
         frame_id=frame_id,
         want_points=False,
     )

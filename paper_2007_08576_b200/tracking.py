@@ -74,9 +74,11 @@ def _frame_config(graph: ControlGraph, observation: Observation, config: RunConf
 
 
 def track_frame(template: Template, graph: ControlGraph, observation: Observation,
-                matches: MatchSet | None, config: RunConfig) -> FrameResult:
+                matches: MatchSet | None, config: RunConfig, *,
+                match_binding=None) -> FrameResult:
     """Preselect + solve + output warp from the warm start in ``graph``
-    (tracking.py:67-95), in one device call."""
+    (tracking.py:67-95), in one device call. ``match_binding``: optional (idx, w)
+    binding of the matches' template points (default: bound on the device)."""
     t0 = time.perf_counter()
     if not template.is_bound:
         raise ValueError("template must be bound to the control graph first")
@@ -89,6 +91,7 @@ def track_frame(template: Template, graph: ControlGraph, observation: Observatio
         observation.depth,
         None if observation.normals_on_device else observation.normals,
         pairs=(matches.template_points, matches.observed_points) if have else None,
+        match_binding=match_binding if have else None,
         refs=refs,
         frame_id=observation.frame_id,
         want_points=True,
@@ -160,8 +163,14 @@ class Tracker:
 
     def set_features(self, descriptors, points) -> None:
         """Template-side ORB features: (T, 32) uint8 descriptors and their frame-0 3D
-        points (T, 3)."""
-        self.device.set_features(descriptors, points)
+        points (T, 3). Their control binding is fixed for the sequence, so it is computed
+        once here with the reference's kd-tree (solver.py:292-296, sigma = sampling
+        radius) and kept on the device."""
+        from .warpfield import bind_points
+
+        k = int(self.template.bind_indices.shape[1])
+        binding = bind_points(points, self.graph.points, k, self.graph.sampling_radius)
+        self.device.set_features(descriptors, points, binding)
 
     def set_exhaustive(self, flag: bool = True) -> None:
         """Evaluate every match as a preselection hypothesis (the paper's exhaustive

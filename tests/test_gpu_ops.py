@@ -120,18 +120,21 @@ def test_solve_damped(kz):
 
 
 def test_bind_points(kz):
-    from paper_2007_08576_b200.warpfield import bind_points
+    from paper_2007_08576_b200.warpfield import bind_points, bind_points_device
 
+    idx, w = bind_points_device(kz["bind_pts"], kz["bind_ctrl"], 4, 7.0)
+    np.testing.assert_array_equal(idx, kz["bind_idx_ref"])
+    np.testing.assert_allclose(w, kz["bind_w_ref"], rtol=1e-14, atol=1e-16)
     idx, w = bind_points(kz["bind_pts"], kz["bind_ctrl"], 4, 7.0)
     np.testing.assert_array_equal(idx, kz["bind_idx_ref"])
     np.testing.assert_allclose(w, kz["bind_w_ref"], rtol=1e-14, atol=1e-16)
 
 
 def test_bind_points_pads_small_graphs():
-    from paper_2007_08576_b200.warpfield import bind_points
+    from paper_2007_08576_b200.warpfield import bind_points_device
 
     pts = np.random.default_rng(0).normal(size=(10, 3))
-    idx, w = bind_points(pts, np.array([[0.0, 0, 0], [1.0, 0, 0]]), 4, 1.0)
+    idx, w = bind_points_device(pts, np.array([[0.0, 0, 0], [1.0, 0, 0]]), 4, 1.0)
     assert idx.shape == (10, 4)
     np.testing.assert_array_equal(idx[:, 2], idx[:, 0])
     np.testing.assert_array_equal(w[:, 2:], 0.0)
