@@ -1,0 +1,489 @@
+#!/usr/bin/env python
+"""Benchmark: per-frame deformation tracking on B200 (BASELINE.json metric, config 2).
+
+Workload (config 2): synthetic ex-vivo-like sphere patch, 640x480 depth, 141x141 = 19,881
+template points, ~389 densely connected control points (radius 5.3), 2,000 template ORB
+features (+500 distractors, 10 % outliers), exhaustive 1-point-RANSAC + reweighting
+preselection, 10 Levenberg-Marquardt outer iterations per frame (step_tol = cost_tol = 0,
+so every frame runs exactly 10). One step = one frame of the whole hot path:
+raw depth -> normals -> Hamming ORB matching -> preselection -> LM solve -> output warp.
+
+  value  frames/s with the frame inputs already resident in HBM, device-timed with CUDA
+         events on the tracker stream around each frame (L2 flushed between frames by a
+         256 MiB write, outside the timed events); summed over K frames.
+  e2e    frames/s through the C-ABI call dt_track_frame with pinned HOST buffers: depth +
+         descriptors + keypoints copied in, warps + warped points + normals copied out,
+         wall clock around each synchronous call.
+  --impl reference   the reference algorithm on the host cores: the oracle port
+         (oracle/, C kernels bit-identical to the reference's numba kernels + numpy),
+         same workload, one frame per step.
+
+Multi-GPU: frames of one sequence are sequentially dependent (warm start), so the path
+does not shard: each rank tracks its own independent sequence (replicas only,
+SURVEY.md §8e); value = all ranks' frames / max-over-ranks device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "tracking frames/sec (Hz) at 640x480, 400 ctrl pts, 10 GN iters; ms/GN iteration"
+UNIT = "frames/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--frames", type=int, default=20, help="distinct frames generated (cycled)")
+    ap.add_argument("--cluster", type=int, default=0, help="solver cluster size (0 = max)")
+    ap.add_argument("--cpu-frames", type=int, default=3, help="CPU-baseline sample (frames)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------------
+
+
+def make_workload(config_id: int, n_frames: int, seed: int):
+    from dataclasses import replace
+
+    from paper_2007_08576_b200 import synth
+    from paper_2007_08576_b200.config import load_config
+    from paper_2007_08576_b200.tracking import prepare_template
+
+    spec = synth.CONFIGS[config_id]
+    scene = replace(spec["scene"], seed=seed)
+    cfg = load_config({
+        "sampling": {"radius": spec["radius"]},
+        "solver": {"max_outer_iters": spec["iters"], "step_tol": 0.0, "cost_tol": 0.0},
+    })
+    cam = synth.camera_for(scene)
+    tpl0 = synth.make_template(scene)
+    feats = synth.make_features(scene, tpl0)
+    frames = [synth.make_frame(scene, cam, tpl0, feats, f) for f in range(1, n_frames + 1)]
+    tpl, graph = prepare_template(tpl0, cfg)
+    return dict(scene=scene, cfg=cfg, cam=cam, tpl=tpl, graph=graph, feats=feats, frames=frames,
+                iters=spec["iters"], radius=spec["radius"])
+
+
+def workload_config(wl, n_gpus, rank_frames_desc):
+    tpl, graph, sc = wl["tpl"], wl["graph"], wl["scene"]
+    return {
+        "workload": f"config 2: synthetic sphere patch {sc.width}x{sc.height}, "
+                    f"{len(tpl)} template points, {len(graph)} control points, "
+                    f"{graph.edges.shape[0]} dense connections, {sc.n_features} ORB features "
+                    f"(+{sc.n_distractors} distractors, {int(sc.outlier_fraction * 100)}% outliers), "
+                    f"exhaustive preselection, {wl['iters']} LM iterations/frame",
+        "template_points": len(tpl),
+        "control_points": len(graph),
+        "edges": int(graph.edges.shape[0]),
+        "orb_features": sc.n_features,
+        "image": [sc.width, sc.height],
+        "lm_iterations": wl["iters"],
+        "preselection": "exhaustive",
+        "frames": rank_frames_desc,
+        "l2": "flushed between timed frames (256 MiB write outside the timed events)",
+        "parallelism": f"replicas x{n_gpus} (independent sequences, no collective)",
+    }
+
+
+# ---------------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------------
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------
+# algorithmic bytes for the roofline of the LM solver kernel
+# ---------------------------------------------------------------------------------
+
+
+def solver_algorithmic_bytes(n, m, e, k, n_valid, n_active, report):
+    """Bytes one k_solve_frame launch must touch at minimum, by the §8d per-unit table:
+    relink 100 B/point (p, n, binding, depth + obs-normal gather, writes); linearization
+    68 B/valid correspondence + 60 B/match + 232 B/control; rigidity pass 16 B/edge +
+    312 B/control; damped solve 328 B/control/attempt; tentative value pass
+    64 B/valid correspondence + 60 B/match + 16 B/edge + 96 B/control."""
+    it = int(report.outer_iterations)
+    attempts = int(report.accepted_steps) + int(report.rejected_steps) + int(report.converged)
+    relinks = it + 1
+    lin = it * (n_valid * 68 + n_active * 60 + m * 29 * 8)
+    arap = it * (e * 16 + m * 88 + m * 28 * 8)
+    solves = attempts * m * (27 * 8 + 64 + 48)
+    value = (attempts + 1) * (n_valid * 64 + n_active * 60 + e * 16 + m * 96)
+    return relinks * n * 100 + lin + arap + solves + value
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------------
+# the B200 arm
+# ---------------------------------------------------------------------------------
+
+
+def run_b200(args, rank, world, local_rank):
+    import ctypes as C
+
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    if not (ROOT / "paper_2007_08576_b200" / "libdeformtrack_b200.so").exists():
+        import __graft_entry__
+
+        __graft_entry__.build()
+    from paper_2007_08576_b200._lib import FrameInput, FrameOutput, Report
+    from paper_2007_08576_b200._session import DeviceTracker, make_config
+
+    wl = make_workload(args.config, args.frames, seed=rank)
+    cfg = wl["cfg"]
+    stream = torch.cuda.Stream()
+    dcfg = make_config(wl["cam"], cfg.energy, cfg.make_solver_config(), cfg.make_preselect_config(),
+                       sampling_radius=wl["graph"].sampling_radius, cluster_size=args.cluster)
+    trk = DeviceTracker(wl["tpl"], wl["graph"], dcfg, stream=stream.cuda_stream)
+    from paper_2007_08576_b200.warpfield import bind_points
+
+    feats = wl["feats"]
+    binding = bind_points(feats.points, wl["graph"].points, 4, wl["graph"].sampling_radius)
+    trk.set_features(feats.descriptors, feats.points, binding)
+
+    dev = torch.device("cuda", local_rank)
+    frames = wl["frames"]
+    F = len(frames)
+    d_depth = [torch.from_numpy(f.depth).to(dev) for f in frames]
+    d_desc = [torch.from_numpy(f.descriptors).to(dev) for f in frames]
+    d_kp = [torch.from_numpy(f.keypoints).to(dev) for f in frames]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def dev_input(i, fid):
+        fi = FrameInput()
+        fi.depth = d_depth[i].data_ptr()
+        fi.frame_desc = d_desc[i].data_ptr()
+        fi.frame_kp = d_kp[i].data_ptr()
+        fi.n_frame = int(d_desc[i].shape[0])
+        fi.use_matches = 1
+        fi.on_device = 1
+        fi.frame_id = fid
+        return fi
+
+    # ---- warm-up ----
+    trk.set_warps(wl["graph"].warps)
+    with torch.cuda.stream(stream):
+        for w in range(args.warmup):
+            trk.enqueue(dev_input(w % F, w))
+    stream.synchronize()
+
+    # ---- timed: device-resident inputs ----
+    K = args.steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    with ClockSampler(local_rank) as clocks:
+        with torch.cuda.stream(stream):
+            for i in range(K):
+                fi_idx = (args.warmup + i) % F
+                flush.zero_()
+                starts[i].record(stream)
+                trk.enqueue(dev_input(fi_idx, args.warmup + i))
+                ends[i].record(stream)
+                launches += trk.launches()
+        stream.synchronize()
+    torch.cuda.synchronize()
+    per_frame_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(per_frame_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # report of the last timed frame (outputs resident on the device)
+    rep = Report()
+    fo = FrameOutput()
+    fo.report = C.cast(C.pointer(rep), C.c_void_p).value
+    trk.collect(dev_input((args.warmup + K - 1) % F, 0), fo)
+
+    # ---- per-phase device time (CUDA events between the pipeline stages) ----
+    trk.set_profiling(True)
+    phases = []
+    with torch.cuda.stream(stream):
+        for i in range(min(10, K)):
+            flush.zero_()
+            trk.enqueue(dev_input((args.warmup + K + i) % F, 0))
+            phases.append(trk.phase_ms())
+    trk.set_profiling(False)
+    phase_avg = {k: float(np.mean([p[k] for p in phases])) for k in phases[0]}
+
+    # ---- e2e: host buffers through the C-ABI ----
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        h_depth = [pin(f.depth) for f in frames]
+        h_desc = [pin(f.descriptors) for f in frames]
+        h_kp = [pin(f.keypoints) for f in frames]
+        out_w = torch.empty((len(wl["graph"]), 8), dtype=torch.float64).pin_memory()
+        out_p = torch.empty((len(wl["tpl"]), 3), dtype=torch.float64).pin_memory()
+        out_n = torch.empty((len(wl["tpl"]), 3), dtype=torch.float64).pin_memory()
+        erep = Report()
+        fo = FrameOutput()
+        fo.warps = out_w.data_ptr()
+        fo.points = out_p.data_ptr()
+        fo.normals = out_n.data_ptr()
+        fo.report = C.cast(C.pointer(erep), C.c_void_p).value
+        trk.set_warps(wl["graph"].warps)
+
+        def host_input(i, fid):
+            fi = FrameInput()
+            fi.depth = h_depth[i].data_ptr()
+            fi.frame_desc = h_desc[i].data_ptr()
+            fi.frame_kp = h_kp[i].data_ptr()
+            fi.n_frame = int(h_desc[i].shape[0])
+            fi.use_matches = 1
+            fi.on_device = 0
+            fi.frame_id = fid
+            return fi
+
+        for w in range(args.warmup):
+            trk.track_raw(host_input(w % F, w), fo)
+        if world > 1:
+            torch.distributed.barrier()
+        wall = 0.0
+        for i in range(K):
+            fi = host_input((args.warmup + i) % F, args.warmup + i)
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            trk.track_raw(fi, fo)
+            wall += time.perf_counter() - t0
+        wall_ms = wall * 1e3
+        if world > 1:
+            t = torch.tensor([wall_ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            wall_ms = float(t.item())
+        h2d = frames[0].depth.nbytes + frames[0].descriptors.nbytes + frames[0].keypoints.nbytes
+        d2h = out_w.numel() * 8 + out_p.numel() * 8 + out_n.numel() * 8 + C.sizeof(Report)
+        e2e = {"value": world * K / (wall_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": wall_ms / K,
+               "api": "dt_track_frame (C-ABI) via paper_2007_08576_b200._session.DeviceTracker.track_raw"}
+
+    # ---- roofline of the dominant kernel ----
+    n, m = len(wl["tpl"]), len(wl["graph"])
+    e = int(wl["graph"].edges.shape[0])
+    dominant = max(phase_avg, key=phase_avg.get)
+    peak, peak_src = measured_peaks()
+    solver_bytes = solver_algorithmic_bytes(n, m, e, 4, int(rep.n_correspondences),
+                                            int(rep.n_preselected), rep)
+    solver_ms = phase_avg["lm_solver"]
+    achieved = solver_bytes / (solver_ms * 1e-3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "solver_dram_bytes.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    roofline = {"kernel": "k_solve_frame (LM solver, one cluster launch per frame)",
+                "bound": "hbm", "achieved": round(achieved, 3), "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "algorithmic_bytes_per_launch": int(solver_bytes),
+                "launch_ms": solver_ms, "peak_source": peak_src,
+                "dominant_phase": dominant,
+                "note": "latency-bound: ~70 dependent phases/frame; see DESIGN.md §roofline"}
+
+    value = world * K / (total_ms / 1e3)
+    ms_per_step = total_ms / K
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "ms_per_gn_iteration": ms_per_step / wl["iters"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (builder sphere-patch generator, seeded; random 256-bit descriptors)",
+        "config": workload_config(wl, world, f"{F} distinct frames cycled (period 20)"),
+        "e2e": e2e, "roofline": roofline, "gpu_launches": launches,
+        "phase_ms": phase_avg, "clocks": clocks.summary(),
+        "frame_report": {"n_correspondences": int(rep.n_correspondences),
+                         "n_matches": int(rep.n_matches), "n_preselected": int(rep.n_preselected),
+                         "outer_iterations": int(rep.outer_iterations),
+                         "accepted_steps": int(rep.accepted_steps),
+                         "rejected_steps": int(rep.rejected_steps),
+                         "total_cost": float(rep.total_cost)},
+        "solver_cluster": int(dcfg.cluster_size) or "auto",
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(wl, args.cpu_frames)
+    trk.close()
+    return result
+
+
+# ---------------------------------------------------------------------------------
+# CPU: the reference algorithm (oracle port) on the host cores
+# ---------------------------------------------------------------------------------
+
+
+def oracle_frame_runner(wl):
+    from oracle import kernels as OK
+    from oracle import pipeline as OP
+
+    tpl, graph, cam = wl["tpl"], wl["graph"], wl["cam"]
+    feats = wl["feats"]
+    tplt = (tpl.points, tpl.normals, tpl.bind_indices, tpl.bind_weights)
+    grt = (graph.points, graph.edges, graph.edge_weights)
+    camt = (cam.fx, cam.fy, cam.cx, cam.cy)
+    sch = OP.Schedule(max_outer_iters=wl["iters"], step_tol=0.0, cost_tol=0.0)
+    state = {"warps": graph.warps.copy()}
+
+    def step(fr):
+        normals = OP.observation_normals(fr.depth, *camt)
+        src, dst, _ = OP.matches_from_descriptors(feats.descriptors, feats.points,
+                                                  fr.descriptors, fr.keypoints, fr.depth, camt)
+        res, _, _, _ = OP.track(tplt, grt, state["warps"], fr.depth, normals, camt, (src, dst),
+                                OP.Weights(), sch, graph.sampling_radius, refs=None)
+        state["warps"] = res.warps
+        return res
+
+    return step, OK
+
+
+def cpu_baseline(wl, n_frames):
+    step, OK = oracle_frame_runner(wl)
+    cores = os.cpu_count() or 1
+    OK.set_threads(cores)
+    step(wl["frames"][0])  # warm caches / page in
+    t0 = time.perf_counter()
+    for f in wl["frames"][1:1 + n_frames]:
+        step(f)
+    dt = time.perf_counter() - t0
+    return {"value": n_frames / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{n_frames} consecutive config-2 frames (full path: normals, Hamming, "
+                      f"exhaustive preselection, 10 LM iterations, output warp) through the "
+                      f"oracle port (C kernels bit-identical to the reference's numba "
+                      f"kernels, OpenMP over the reference's 8 chunks, + numpy)",
+            "ms_per_frame": dt * 1e3 / n_frames}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    wl = make_workload(args.config, args.frames, seed=0)
+    step, OK = oracle_frame_runner(wl)
+    cores = os.cpu_count() or 1
+    OK.set_threads(cores)
+    frames = wl["frames"]
+    for w in range(args.warmup):
+        step(frames[w % len(frames)])
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(frames[(args.warmup + i) % len(frames)])
+    dt = time.perf_counter() - t0
+    value = args.steps / dt
+    sample = (f"{args.steps} consecutive config-2 frames, one full frame per step (normals, "
+              f"Hamming, exhaustive preselection, 10 LM iterations, warp), oracle port of the "
+              f"reference on {cores} host threads")
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+        "ms_per_gn_iteration": dt * 1e3 / args.steps / wl["iters"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(wl, 1, f"{len(frames)} distinct frames cycled"),
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl")
+    res = run_b200(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch
+
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -269,6 +269,19 @@ typedef struct {
 /* Run one frame (asynchronous on the tracker stream; results valid after
  * dt_tracker_sync). The warps solved here become the warm start of the next frame. */
 int dt_track_frame(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out);
+/* Enqueue one frame without any host output or synchronization (inputs may be host or
+ * device pointers as flagged); results stay resident (dt_tracker_device_outputs) and
+ * dt_tracker_collect copies them out later. */
+int dt_track_frame_async(dt_tracker* t, const dt_frame_input* in);
+int dt_tracker_collect(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out);
+/* The tracker's CUDA stream (cudaStream_t). */
+void* dt_tracker_stream(dt_tracker* t);
+/* Per-phase device timing of each frame (CUDA events between the pipeline stages):
+ * ms[0] depth normals, [1] ORB Hamming + match build, [2] preselection,
+ * [3] active matches + control CSR, [4] LM solver kernel, [5] output warp. */
+#define DT_N_PHASES 6
+int dt_tracker_set_profiling(dt_tracker* t, int on);
+int dt_tracker_get_phase_ms(dt_tracker* t, float* ms);
 /* Per-outer-iteration histories of the last frame (host): cost_history
  * (max_outer_iters,2), lambda_history (max_outer_iters,2), stalled (max_outer_iters). */
 int dt_tracker_get_history(dt_tracker* t, double* cost_history, double* lambda_history,

@@ -28,9 +28,13 @@ I = C.c_int
 
 def _load():
     if not _LIB_PATH.exists():
-        from paper_2007_08576_b200._build import build_oracle
+        import importlib.util
 
-        build_oracle()
+        spec = importlib.util.spec_from_file_location(
+            "_dt_build", Path(__file__).resolve().parent.parent / "paper_2007_08576_b200" / "_build.py")
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        mod.build_oracle()
     lib = C.CDLL(str(_LIB_PATH))
     lib.or_icp_reduce.argtypes = [P, P, P, P, P, I64, I, P, P, F64, P, I, I, I, I64, P, P, P, P]
     lib.or_feature_reduce.argtypes = [P, P, P, P, P, I64, I, P, P, F64, I, I, I64, P, P, P]

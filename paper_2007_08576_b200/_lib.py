@@ -119,9 +119,16 @@ _SIGNATURES: dict[str, list] = {
     "dt_tracker_last_launches": [P],
     "dt_track_frames_batched": [C.POINTER(P), C.POINTER(FrameInput), C.POINTER(FrameOutput),
                                 I32, P],
+    "dt_track_frame_async": [P, C.POINTER(FrameInput)],
+    "dt_tracker_collect": [P, C.POINTER(FrameInput), C.POINTER(FrameOutput)],
+    "dt_tracker_set_profiling": [P, C.c_int],
+    "dt_tracker_get_phase_ms": [P, P],
 }
 
-EXPORTED = ["dt_last_error", "dt_version", *_SIGNATURES]
+N_PHASES = 6
+PHASES = ("normals", "orb_match", "preselect", "match_prep", "lm_solver", "warp_out")
+
+EXPORTED = ["dt_last_error", "dt_version", "dt_tracker_stream", *_SIGNATURES]
 
 
 def _load() -> C.CDLL:
@@ -139,6 +146,8 @@ def _load() -> C.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = argtypes
         fn.restype = C.c_int
+    lib.dt_tracker_stream.argtypes = [P]
+    lib.dt_tracker_stream.restype = P
     return lib
 
 

@@ -77,7 +77,8 @@ class FrameOutputs:
 class DeviceTracker:
     """One sequence resident on one device (one stream)."""
 
-    def __init__(self, template, graph, cfg: Config, device: int | None = None):
+    def __init__(self, template, graph, cfg: Config, device: int | None = None,
+                 stream: int | None = None):
         dev.require_cuda()
         import torch
 
@@ -100,7 +101,7 @@ class DeviceTracker:
         check(lib.dt_tracker_create(C.byref(cfg), _host_ptr(tp), _host_ptr(tn), _host_ptr(bi),
                                     _host_ptr(bw), self.n, self.k, _host_ptr(cp), _host_ptr(wp),
                                     self.m, _host_ptr(ed), _host_ptr(ew), ed.shape[0],
-                                    self.device, None, C.byref(handle)), "dt_tracker_create")
+                                    self.device, stream, C.byref(handle)), "dt_tracker_create")
         self._h = handle
 
     # -- configuration -------------------------------------------------------------
@@ -236,6 +237,33 @@ class DeviceTracker:
     def track_raw(self, fi: FrameInput, fo: FrameOutput) -> None:
         """Lowest-overhead entry: caller-built dt_frame_input / dt_frame_output."""
         check(lib.dt_track_frame(self._h, C.byref(fi), C.byref(fo)), "dt_track_frame")
+
+    def enqueue(self, fi: FrameInput) -> None:
+        """Enqueue one frame on the tracker stream; no host outputs, no synchronization."""
+        check(lib.dt_track_frame_async(self._h, C.byref(fi)), "dt_track_frame_async")
+
+    def collect(self, fi: FrameInput, fo: FrameOutput) -> None:
+        check(lib.dt_tracker_collect(self._h, C.byref(fi), C.byref(fo)), "dt_tracker_collect")
+
+    @property
+    def stream(self) -> int:
+        return int(lib.dt_tracker_stream(self._h) or 0)
+
+    def set_profiling(self, on: bool) -> None:
+        check(lib.dt_tracker_set_profiling(self._h, int(bool(on))), "dt_tracker_set_profiling")
+
+    def phase_ms(self) -> dict:
+        from ._lib import N_PHASES, PHASES
+
+        buf = (C.c_float * N_PHASES)()
+        check(lib.dt_tracker_get_phase_ms(self._h, C.cast(buf, C.c_void_p)), "dt_tracker_get_phase_ms")
+        return {name: float(buf[i]) for i, name in enumerate(PHASES)}
+
+    def device_outputs(self):
+        w, p, n = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib.dt_tracker_device_outputs(self._h, C.byref(w), C.byref(p), C.byref(n)),
+              "dt_tracker_device_outputs")
+        return w.value, p.value, n.value
 
     def launches(self) -> int:
         return int(lib.dt_tracker_last_launches(self._h))

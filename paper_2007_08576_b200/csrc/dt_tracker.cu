@@ -277,6 +277,9 @@ struct dt_tracker {
   int cluster = 1;
   int launches = 0;
   bool args_dirty = false;
+  bool profiling = false;
+  bool last_used = false;
+  cudaEvent_t ev[DT_N_PHASES + 1] = {};
   std::vector<DevBuf> bufs;
   // template / graph
   double *tp = nullptr, *tn = nullptr, *bw = nullptr, *cpts = nullptr, *ew = nullptr;
@@ -500,6 +503,10 @@ int upload_binding(dt_tracker* t, const int64_t* bidx, const double* bw, int64_t
   return DT_OK;
 }
 
+void mark(dt_tracker* t, int i) {
+  if (t->profiling) cudaEventRecord(t->ev[i], t->stream);
+}
+
 int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   cudaStream_t s = t->stream;
   const dt_config& c = t->cfg;
@@ -507,6 +514,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   const cudaMemcpyKind kind = in->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   DT_REQUIRE(in->depth != nullptr, DT_ERR_INVALID_ARGUMENT, "depth is required");
   t->launches = 0;
+  mark(t, 0);
   // warm start: the previous solution (or set_warps) is in warps_out
   DT_CHECK_CUDA(cudaMemcpyAsync(t->warp_a, t->warps_out, sizeof(double) * 8 * t->m,
                                 cudaMemcpyDeviceToDevice, s));
@@ -520,6 +528,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
                                       c.z_max, t->onrm, t->dvalid, s));
   }
   ++t->launches;
+  mark(t, 1);
 
   // ---- matches ----
   bool use = in->use_matches != 0;
@@ -565,6 +574,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     use = false;
   }
   *used_matches = use;
+  mark(t, 2);
   if (use && in->match_w != nullptr && in->frame_desc == nullptr) {
     // weights given by the caller (already annotated MatchSet): no preselection
     DT_CHECK_CUDA(cudaMemcpyAsync(t->m_w, in->match_w, sizeof(double) * in->n_pairs, kind, s));
@@ -596,6 +606,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     DT_CHECK_LAUNCH();
     ++t->launches;
   }
+  mark(t, 3);
   k_active<<<1, 1024, 0, s>>>(t->info + 2, t->m_w, t->m_flags, t->m_src, t->m_dst, t->m_bidx,
                               t->m_bw, (int)t->k, use ? 1 : 0, t->fp, t->fo, t->fwt, t->fbidx,
                               t->fbw, t->info + 3, t->astats);
@@ -610,6 +621,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
                                               t->ment);
   DT_CHECK_LAUNCH();
   t->launches += 4;
+  mark(t, 4);
 
   // ---- solve ----
   if (t->args_dirty) {
@@ -622,10 +634,12 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   DT_CHECK_CUDA(cudaMemsetAsync(t->stalled_hist, 0, sizeof(int32_t) * c.max_outer_iters, s));
   DT_TRY(solver_launch(t->dev_args, 1, t->cluster, (int)t->m, s));
   ++t->launches;
+  mark(t, 5);
   // ---- output warp (tracking.py:87) ----
   DT_TRY(launch_warp_all_i32(t->tp, t->tn, t->bidx, t->bw, t->n, (int)t->k, t->warps_out, t->out_p,
                              t->out_n, s));
   ++t->launches;
+  mark(t, 6);
   return DT_OK;
 }
 
@@ -807,6 +821,8 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
 int dt_tracker_destroy(dt_tracker* t) {
   if (!t) return DT_OK;
   cudaStreamSynchronize(t->stream);
+  for (auto& e : t->ev)
+    if (e) cudaEventDestroy(e);
   for (auto& b : t->bufs) cudaFree(b.p);
   if (t->h_report) cudaFreeHost(t->h_report);
   if (t->h_info) cudaFreeHost(t->h_info);
@@ -884,6 +900,7 @@ int dt_track_frame(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out
   DT_REQUIRE(t != nullptr && in != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
   bool used = false;
   DT_TRY(enqueue_frame(t, in, &used));
+  t->last_used = used;
   return collect_outputs(t, in, out, used);
 }
 
@@ -910,6 +927,37 @@ int dt_tracker_device_outputs(dt_tracker* t, double** warps, double** points, do
 }
 
 int dt_tracker_last_launches(dt_tracker* t) { return t ? t->launches : 0; }
+
+int dt_track_frame_async(dt_tracker* t, const dt_frame_input* in) {
+  DT_REQUIRE(t != nullptr && in != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  bool used = false;
+  DT_TRY(enqueue_frame(t, in, &used));
+  t->last_used = used;
+  return DT_OK;
+}
+
+int dt_tracker_collect(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out) {
+  DT_REQUIRE(t != nullptr && in != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  return collect_outputs(t, in, out, t->last_used);
+}
+
+void* dt_tracker_stream(dt_tracker* t) { return t ? (void*)t->stream : nullptr; }
+
+int dt_tracker_set_profiling(dt_tracker* t, int on) {
+  DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
+  if (on && !t->ev[0])
+    for (auto& e : t->ev) DT_CHECK_CUDA(cudaEventCreate(&e));
+  t->profiling = on != 0;
+  return DT_OK;
+}
+
+int dt_tracker_get_phase_ms(dt_tracker* t, float* ms) {
+  DT_REQUIRE(t != nullptr && ms != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  DT_REQUIRE(t->profiling, DT_ERR_INVALID_ARGUMENT, "profiling is off");
+  DT_CHECK_CUDA(cudaEventSynchronize(t->ev[DT_N_PHASES]));
+  for (int i = 0; i < DT_N_PHASES; ++i) DT_CHECK_CUDA(cudaEventElapsedTime(&ms[i], t->ev[i], t->ev[i + 1]));
+  return DT_OK;
+}
 
 int dt_track_frames_batched(dt_tracker** trackers, const dt_frame_input* inputs,
                             dt_frame_output* outputs, int32_t n_trackers, void* stream) {

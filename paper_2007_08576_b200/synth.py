@@ -155,15 +155,20 @@ def render_depth(scene: Scene, camera: PinholeCamera, frame: int, newton_iters: 
     s = np.full(u.shape, PATCH_DISTANCE)
     half = scene.extent / 2.0
     for _ in range(newton_iters):
-        x = np.clip(s * rd[..., 0] + off[0], -half * 1.2, half * 1.2)
-        y = np.clip(s * rd[..., 1] + off[1], -half * 1.2, half * 1.2)
+        xr = s * rd[..., 0] + off[0]
+        yr = s * rd[..., 1] + off[1]
+        x = np.clip(xr, -half * 1.2, half * 1.2)
+        y = np.clip(yr, -half * 1.2, half * 1.2)
         z = s * rd[..., 2] + off[2]
         g, gx, gy = surf(x, y)
         f = z - PATCH_DISTANCE - g
         df = rd[..., 2] - gx * rd[..., 0] - gy * rd[..., 1]
         step = f / df
         s = s - step
-        if np.max(np.abs(step)) < 1e-12:
+        # converged once every ray that can hit the patch has settled (rays far outside
+        # the patch are clipped and never do; they are invalid anyway)
+        on_patch = (np.abs(xr) <= half * 1.05) & (np.abs(yr) <= half * 1.05)
+        if not np.any(on_patch) or np.max(np.abs(step[on_patch])) < 1e-11:
             break
     x = s * rd[..., 0] + off[0]
     y = s * rd[..., 1] + off[1]
