@@ -282,6 +282,9 @@ void* dt_tracker_stream(dt_tracker* t);
 #define DT_N_PHASES 6
 int dt_tracker_set_profiling(dt_tracker* t, int on);
 int dt_tracker_get_phase_ms(dt_tracker* t, float* ms);
+/* With profiling on, the solver kernel stamps (phase code, globaltimer ns) pairs at every
+ * cluster barrier of the last frame; returns the number of pairs copied into buf. */
+int dt_tracker_get_trace(dt_tracker* t, long long* buf, int cap);
 /* Per-outer-iteration histories of the last frame (host): cost_history
  * (max_outer_iters,2), lambda_history (max_outer_iters,2), stalled (max_outer_iters). */
 int dt_tracker_get_history(dt_tracker* t, double* cost_history, double* lambda_history,

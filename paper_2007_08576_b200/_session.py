@@ -259,6 +259,15 @@ class DeviceTracker:
         check(lib.dt_tracker_get_phase_ms(self._h, C.cast(buf, C.c_void_p)), "dt_tracker_get_phase_ms")
         return {name: float(buf[i]) for i, name in enumerate(PHASES)}
 
+    def trace(self, cap: int = 4096) -> np.ndarray:
+        """(code, ns) pairs stamped by the solver kernel at its cluster barriers (last
+        frame, profiling on)."""
+        buf = np.zeros((cap, 2), dtype=np.int64)
+        n = lib.dt_tracker_get_trace(self._h, _host_ptr(buf), cap)
+        if n < 0:
+            check(n, "dt_tracker_get_trace")
+        return buf[:n].copy()
+
     def device_outputs(self):
         w, p, n = C.c_void_p(), C.c_void_p(), C.c_void_p()
         check(lib.dt_tracker_device_outputs(self._h, C.byref(w), C.byref(p), C.byref(n)),

@@ -1,19 +1,28 @@
 // dt_solver.cu -- one frame of the deformation solve (solver.solve_frame,
-// solver.py:267-378) as ONE kernel launch per frame: a thread-block cluster owns a
-// sequence, keeps the control warps in shared memory and runs the whole
-// Levenberg-Marquardt loop (relink -> linearize -> per-control 6x6 damped solves ->
-// tentative value pass -> accept / reject -> damping ladder) on the device, with
-// cluster barriers (barrier.cluster, ~0.2 us) between phases instead of kernel
-// boundaries or host round trips.
+// solver.py:267-378) as ONE persistent kernel launch: the whole Levenberg-Marquardt loop
+// (relink -> linearize -> per-control normal equations -> damped 6x6 solves -> tentative
+// value pass -> accept / reject -> damping ladder) runs on the device with barriers
+// between phases instead of kernel boundaries or host round trips.
 //
-// Work split inside a cluster of C CTAs x 256 threads:
-//   per-point phases (warp + rasterize + linearize) stride over the template points,
-//   per-control phases give each control to one warp, which gathers that control's
-//   rows through static CSR lists (template binding, incident edges) and a per-frame
-//   CSR (feature matches) and folds them in a fixed order, so every reduction is
-//   deterministic and independent of C; totals over controls are summed in a fixed
-//   order by every CTA redundantly, so all CTAs take identical control decisions.
-// Several sequences (BASELINE config 5) run as several clusters of the same launch.
+// Two sync domains from one kernel body:
+//   * cluster mode: a thread-block cluster (<= 16 CTAs, barrier.cluster) owns one
+//     sequence; many sequences run as many clusters of one launch (BASELINE config 5);
+//   * grid mode: a cooperative grid over every SM owns one sequence (lowest latency).
+//
+// Phases of one outer iteration (each ends at a domain barrier):
+//   P1  points & matches: warp + project + gate + residual + Tukey + blend gradient
+//       (kernels.py:483-569, 173-197, 239-250); icp / feature cost of the iterate
+//   P2  controls: data rows -> normal equations (FP64 tensor-core Gram products,
+//       mma.sync m8n8k4 f64), support -> rigidity weight wa (energy.py:394-402)
+//   P3  controls: rigidity rows (kernels.py:341-467) -> normal equations, first damped
+//       6x6 Cholesky (solver.py:217-258); edges: rigidity cost of the iterate
+//   P5  controls: exp(delta) * W, renormalize (solver.py:261-264)
+//   P6  points / matches / edges: cost at the tentative warps with frozen robust and
+//       rigidity weights (solver.py:333-335); accept iff strictly lower (solver.py:336)
+// Every reduction is deterministic and independent of the launch shape: normal equations
+// are per control in CSR order, costs are per fixed 256-item chunk then summed in chunk
+// order, and every CTA evaluates the totals identically, so all CTAs take the same
+// control-flow decisions.
 
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
@@ -31,53 +40,130 @@ namespace cg = cooperative_groups;
 namespace dt {
 
 constexpr int NWARPS = SOLVER_THREADS / 32;
-constexpr int SCR_COLS = 30;  // 27 partial + support + icp cost + feature cost
+constexpr int STAGE = 32 * 9;  // per-warp row staging (32 rows x 8 cols, padded to 9)
+constexpr int GOUT = 64;       // per-warp 8x8 Gram readout
+constexpr int M_MAX_SMEM = 1100;
 
 size_t solver_smem_bytes(int m) {
-  return sizeof(double) * ((size_t)8 * m + (size_t)NWARPS * 32 * SCR_COLS);
+  return sizeof(double) * ((size_t)20 * m + (size_t)NWARPS * (STAGE + GOUT));
 }
 
-// L2-coherent loads for data produced by other CTAs of the cluster.
+// 27 normal-equation columns from the 8x8 Gram of rows [J0..J5, wv, 0]:
+// triu(J^T J) in kernels.py:41-44 order, then J^T wv.
+__constant__ unsigned char kColRow[27] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3,
+                                          4, 4, 5, 0, 1, 2, 3, 4, 5};
+__constant__ unsigned char kColCol[27] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5,
+                                          4, 5, 5, 6, 6, 6, 6, 6, 6};
+
+// L2-coherent loads for data produced by other CTAs.
 __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ uint8_t ldu8(const uint8_t* p) {
   return (uint8_t)__ldcg(reinterpret_cast<const unsigned char*>(p));
 }
 __device__ __forceinline__ int ldi(const int* p) { return __ldcg(p); }
 
-struct Ctx {
-  int C, r, tid, warp, lane, gw, GW, gt, GT;
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------------------------
+// FP64 tensor-core Gram accumulation: every lane contributes one 8-column row per push;
+// C += R^T R over the 32 rows as 8 DMMA.8x8x4 steps (fragment: lane = 4 g + t holds
+// R[4q + t][g] as both the A and the B element; C[g][2t..2t+1] per lane).
+// ---------------------------------------------------------------------------------
+
+struct Gram {
+  double c0 = 0.0, c1 = 0.0;
 };
 
-__device__ __forceinline__ void load_warps(const SolverArgs& A, const double* src, double* s_w) {
-  const int n = 8 * A.m;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) s_w[i] = ld(src + i);
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
 }
 
-// Blend of template point p at the warps in shared memory.
-__device__ __forceinline__ void blend_point(const SolverArgs& A, const double* s_w, int64_t p,
-                                            double B[8], double sgn[KMAX]) {
-  int idx[KMAX];
-  double w[KMAX];
+__device__ __forceinline__ void gram_push(Gram& G, double* stage, const double row[8]) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int s = 0; s < KMAX; ++s)
-    if (s < A.k) {
-      idx[s] = A.bidx[p * A.k + s];
-      w[s] = A.bw[p * A.k + s];
-    }
-  blend_at(s_w, idx, w, A.k, B, sgn);
+  for (int c = 0; c < 8; ++c) stage[lane * 9 + c] = row[c];
+  __syncwarp();
+  const int t = lane & 3, g = lane >> 2;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const double v = stage[(4 * q + t) * 9 + g];
+    dmma884(G.c0, G.c1, v, v);
+  }
+  __syncwarp();
 }
 
-__device__ __forceinline__ void blend_match(const SolverArgs& A, const double* s_w, int64_t j,
-                                            double B[8], double sgn[KMAX]) {
+__device__ __forceinline__ void gram_store(const Gram& G, double* out) {
+  const int lane = threadIdx.x & 31;
+  const int t = lane & 3, g = lane >> 2;
+  out[g * 8 + 2 * t] = G.c0;
+  out[g * 8 + 2 * t + 1] = G.c1;
+  __syncwarp();
+}
+
+__device__ __forceinline__ double gram_col(const double* out, int col) {
+  return out[kColRow[col] * 8 + kColCol[col]];
+}
+
+// ---------------------------------------------------------------------------------
+// sync domains
+// ---------------------------------------------------------------------------------
+
+template <bool GRID>
+struct Dom;
+
+template <>
+struct Dom<false> {
+  cg::cluster_group g;
+  __device__ Dom() : g(cg::this_cluster()) {}
+  __device__ int rank() const { return (int)g.block_rank(); }
+  __device__ int size() const { return (int)g.num_blocks(); }
+  __device__ int seq() const { return (int)(blockIdx.x / g.num_blocks()); }
+  __device__ void sync() { g.sync(); }
+};
+
+template <>
+struct Dom<true> {
+  cg::grid_group g;
+  __device__ Dom() : g(cg::this_grid()) {}
+  __device__ int rank() const { return (int)blockIdx.x; }
+  __device__ int size() const { return (int)gridDim.x; }
+  __device__ int seq() const { return 0; }
+  __device__ void sync() { g.sync(); }
+};
+
+// ---------------------------------------------------------------------------------
+// state in shared memory: warps and their rigid transforms
+// ---------------------------------------------------------------------------------
+
+__device__ __forceinline__ void load_state(const SolverArgs& A, const double* src, double* s_w,
+                                           double* s_T) {
+  const int n8 = 8 * A.m;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n8; i += blockDim.x) s_w[i] = ld(src + i);
+  __syncthreads();
+  for (int c = threadIdx.x; c < A.m; c += blockDim.x)
+    dq_to_transform(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
+  __syncthreads();
+}
+
+template <typename IdxT>
+__device__ __forceinline__ void blend_rows(const double* s_w, const IdxT* bidx, const double* bw,
+                                           int64_t i, int k, double B[8], double sgn[KMAX],
+                                           double a[KMAX]) {
   int idx[KMAX];
-  double w[KMAX];
 #pragma unroll
   for (int s = 0; s < KMAX; ++s)
-    if (s < A.k) {
-      idx[s] = A.fbidx[j * A.k + s];
-      w[s] = A.fbw[j * A.k + s];
+    if (s < k) {
+      idx[s] = bidx[i * k + s];
+      a[s] = bw[i * k + s];
     }
-  blend_at(s_w, idx, w, A.k, B, sgn);
+  blend_at(s_w, idx, a, k, B, sgn);
 }
 
 __device__ __forceinline__ unsigned sign_bits(const double sgn[KMAX], int k) {
@@ -88,325 +174,597 @@ __device__ __forceinline__ unsigned sign_bits(const double sgn[KMAX], int k) {
   return bits;
 }
 
-// Phase A, one template point: warp, project, gate (kernels.py:483-569), then the
-// point-to-plane residual, its Tukey weight and (jac) its blend gradient
-// (kernels.py:173-197). Returns whether the point has a valid correspondence.
-__device__ __forceinline__ bool point_relink(const SolverArgs& A, const double* s_w, int64_t p, bool jac) {
-  double B[8], sgn[KMAX];
-  blend_point(A, s_w, p, B, sgn);
+// d(action)/dB with one reciprocal of |q|^2 (the Jacobian does not need the
+// reference's per-entry division; values agree to the last ulp or two)
+__device__ __forceinline__ void blend_gradient_fast(const double B[8], double px, double py,
+                                                    double pz, double x0, double x1, double x2,
+                                                    double s2, double* G) {
+  const double is = 1.0 / s2;
+  const double qw = B[0], qx = B[1], qy = B[2], qz = B[3];
+  const double dw = B[4], dx = B[5], dy = B[6], dz = B[7];
+  const double qup = qx * px + qy * py + qz * pz;
+  G[0] = (2.0 * qw * px + 2.0 * (qy * pz - qz * py) + 2.0 * dx - 2.0 * x0 * qw) * is;
+  G[8] = (2.0 * qw * py + 2.0 * (qz * px - qx * pz) + 2.0 * dy - 2.0 * x1 * qw) * is;
+  G[16] = (2.0 * qw * pz + 2.0 * (qx * py - qy * px) + 2.0 * dz - 2.0 * x2 * qw) * is;
+  G[1] = (2.0 * qup - 2.0 * dw - 2.0 * x0 * qx) * is;
+  G[9] = (-2.0 * py * qx + 2.0 * qy * px - 2.0 * qw * pz - 2.0 * dz - 2.0 * x1 * qx) * is;
+  G[17] = (-2.0 * pz * qx + 2.0 * qz * px + 2.0 * qw * py + 2.0 * dy - 2.0 * x2 * qx) * is;
+  G[2] = (-2.0 * px * qy + 2.0 * qx * py + 2.0 * qw * pz + 2.0 * dz - 2.0 * x0 * qy) * is;
+  G[10] = (2.0 * qup - 2.0 * dw - 2.0 * x1 * qy) * is;
+  G[18] = (-2.0 * pz * qy + 2.0 * qz * py - 2.0 * qw * px - 2.0 * dx - 2.0 * x2 * qy) * is;
+  G[3] = (-2.0 * px * qz + 2.0 * qx * pz - 2.0 * qw * py - 2.0 * dy - 2.0 * x0 * qz) * is;
+  G[11] = (-2.0 * py * qz + 2.0 * qy * pz + 2.0 * qw * px + 2.0 * dx - 2.0 * x1 * qz) * is;
+  G[19] = (2.0 * qup - 2.0 * dw - 2.0 * x2 * qz) * is;
+  G[4] = -2.0 * qx * is;
+  G[12] = -2.0 * qy * is;
+  G[20] = -2.0 * qz * is;
+  G[5] = 2.0 * qw * is;
+  G[13] = 2.0 * qz * is;
+  G[21] = -2.0 * qy * is;
+  G[6] = -2.0 * qz * is;
+  G[14] = 2.0 * qw * is;
+  G[22] = 2.0 * qx * is;
+  G[7] = 2.0 * qy * is;
+  G[15] = -2.0 * qx * is;
+  G[23] = 2.0 * qw * is;
+}
+
+// ---------------------------------------------------------------------------------
+// P1 / final relink: one template point. Returns its icp cost sum_s (rs sqrt(a_s) r)^2
+// (0 without a valid correspondence); *valid_out receives the gate outcome.
+// ---------------------------------------------------------------------------------
+
+__device__ __forceinline__ double point_relink(const SolverArgs& A, const double* s_w, int64_t p,
+                                               bool jac, int* valid_out) {
+  double B[8], sgn[KMAX], a[KMAX];
+  blend_rows(s_w, A.bidx, A.bw, p, A.k, B, sgn, a);
   const double px = A.tp[3 * p], py = A.tp[3 * p + 1], pz = A.tp[3 * p + 2];
   double x0, x1, x2, s2;
   apply_blend(B, px, py, pz, x0, x1, x2, s2);
   double r0, r1, r2;
   rotate_normal(B, A.tn[3 * p], A.tn[3 * p + 1], A.tn[3 * p + 2], r0, r1, r2);
-  double o[3], g[3];
-  int ui, vi;
-  // projection and gates (identical to rasterize_one in dt_ops.cu)
   bool ok = false;
+  double o0 = 0, o1 = 0, o2 = 0, g0 = 0, g1 = 0, g2 = 0;
+  // projection and gates, in the reference's IEEE order (kernels.py:537-568)
   if (x2 > 0.0) {
     const double uf = rint(A.fx * x0 / x2 + A.cx);
     const double vf = rint(A.fy * x1 / x2 + A.cy);
     if (uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height) {
-      ui = (int)uf;
-      vi = (int)vf;
+      const int ui = (int)uf, vi = (int)vf;
       const int64_t pix = (int64_t)vi * A.width + ui;
       if (A.dvalid[pix]) {
         const double d = A.depth[pix];
-        o[0] = ((double)ui - A.cx) / A.fx * d;
-        o[1] = ((double)vi - A.cy) / A.fy * d;
-        o[2] = d;
-        g[0] = A.onrm[3 * pix];
-        g[1] = A.onrm[3 * pix + 1];
-        g[2] = A.onrm[3 * pix + 2];
-        if (g[0] * g[0] + g[1] * g[1] + g[2] * g[2] > 0.25) {
-          const double dx = o[0] - x0, dy = o[1] - x1, dz = d - x2;
-          if (sqrt(dx * dx + dy * dy + dz * dz) < A.gate &&
-              g[0] * r0 + g[1] * r1 + g[2] * r2 > A.cos_gate)
-            ok = true;
+        o0 = ((double)ui - A.cx) / A.fx * d;
+        o1 = ((double)vi - A.cy) / A.fy * d;
+        o2 = d;
+        g0 = A.onrm[3 * pix];
+        g1 = A.onrm[3 * pix + 1];
+        g2 = A.onrm[3 * pix + 2];
+        if (g0 * g0 + g1 * g1 + g2 * g2 > 0.25) {
+          const double dx = o0 - x0, dy = o1 - x1, dz = d - x2;
+          ok = sqrt(dx * dx + dy * dy + dz * dz) < A.gate &&
+               g0 * r0 + g1 * r1 + g2 * r2 > A.cos_gate;
         }
       }
     }
   }
   A.cvalid[p] = ok ? 1 : 0;
-  if (!ok) return false;
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    A.cobs[3 * p + i] = o[i];
-    A.cnrm[3 * p + i] = g[i];
-  }
-  const double r = g[0] * (x0 - o[0]) + g[1] * (x1 - o[1]) + g[2] * (x2 - o[2]);
+  *valid_out = ok ? 1 : 0;
+  if (!ok) return 0.0;
+  A.cobs[3 * p] = o0;
+  A.cobs[3 * p + 1] = o1;
+  A.cobs[3 * p + 2] = o2;
+  A.cnrm[3 * p] = g0;
+  A.cnrm[3 * p + 1] = g1;
+  A.cnrm[3 * p + 2] = g2;
+  const double r = g0 * (x0 - o0) + g1 * (x1 - o1) + g2 * (x2 - o2);
+  const double rs = tukey_sqrt(r, A.tukey);
   A.pr_r[p] = r;
-  A.pr_rs[p] = tukey_sqrt(r, A.tukey);
+  A.pr_rs[p] = rs;
   A.pr_sgn[p] = (uint8_t)sign_bits(sgn, A.k);
   if (jac) {
     double G[24];
-    blend_gradient(B, px, py, pz, x0, x1, x2, s2, G);
+    blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, G);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) A.pr_gn[8 * p + e] = g[0] * G[e] + g[1] * G[8 + e] + g[2] * G[16 + e];
+    for (int e = 0; e < 8; ++e) A.pr_gn[8 * p + e] = g0 * G[e] + g1 * G[8 + e] + g2 * G[16 + e];
+  }
+  double cost = 0.0;
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s)
+    if (s < A.k) {
+      const double wv = rs * sqrt(a[s]) * r;
+      cost += wv * wv;
+    }
+  return cost;
+}
+
+// icp cost of point p at the warps in smem with the frozen correspondence and robust weight
+__device__ __forceinline__ double point_value(const SolverArgs& A, const double* s_w, int64_t p) {
+  if (!ldu8(A.cvalid + p)) return 0.0;
+  double B[8], sgn[KMAX], a[KMAX];
+  blend_rows(s_w, A.bidx, A.bw, p, A.k, B, sgn, a);
+  double x0, x1, x2, s2;
+  apply_blend(B, A.tp[3 * p], A.tp[3 * p + 1], A.tp[3 * p + 2], x0, x1, x2, s2);
+  const double r = ld(A.cnrm + 3 * p) * (x0 - ld(A.cobs + 3 * p)) +
+                   ld(A.cnrm + 3 * p + 1) * (x1 - ld(A.cobs + 3 * p + 1)) +
+                   ld(A.cnrm + 3 * p + 2) * (x2 - ld(A.cobs + 3 * p + 2));
+  const double rs = ld(A.pr_rs + p);
+  double cost = 0.0;
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s)
+    if (s < A.k) {
+      const double wv = rs * sqrt(a[s]) * r;
+      cost += wv * wv;
+    }
+  return cost;
+}
+
+// one active match: residual (and its blend gradient); returns its feature cost
+__device__ __forceinline__ double match_eval(const SolverArgs& A, const double* s_w, int64_t j,
+                                             bool store, bool jac) {
+  double B[8], sgn[KMAX], a[KMAX];
+  blend_rows(s_w, A.fbidx, A.fbw, j, A.k, B, sgn, a);
+  const double px = A.fp[3 * j], py = A.fp[3 * j + 1], pz = A.fp[3 * j + 2];
+  double x0, x1, x2, s2;
+  apply_blend(B, px, py, pz, x0, x1, x2, s2);
+  const double e0 = x0 - A.fo[3 * j], e1 = x1 - A.fo[3 * j + 1], e2 = x2 - A.fo[3 * j + 2];
+  if (store) {
+    A.fr_res[3 * j] = e0;
+    A.fr_res[3 * j + 1] = e1;
+    A.fr_res[3 * j + 2] = e2;
+    A.fr_sgn[j] = (uint8_t)sign_bits(sgn, A.k);
+    if (jac) blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, A.fr_G + 24 * j);
+  }
+  const double w = A.fwt[j];
+  double cost = 0.0;
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s)
+    if (s < A.k) {
+      const double sw = sqrt(A.fw * w * a[s]);
+      const double v0 = sw * e0, v1 = sw * e1, v2 = sw * e2;
+      cost += v0 * v0 + v1 * v1 + v2 * v2;
+    }
+  return cost;
+}
+
+// rigidity cost of one connection (both endpoint bins): 2 x (length + angle 0->1 +
+// angle 1->0 + rotation) with the transforms / quaternions in smem
+__device__ __forceinline__ double edge_value(const SolverArgs& A, const double* s_w,
+                                             const double* s_T, const double* wa, int e) {
+  const int i0 = A.edges[2 * e], i1 = A.edges[2 * e + 1];
+  double dummy[1] = {0.0};
+  double cost = 0.0;
+  arap_edge_bin(A.cpts + 3 * i0, A.cpts + 3 * i1, s_T + 12 * i0, s_T + 12 * i0 + 9, s_T + 12 * i1,
+                s_T + 12 * i1 + 9, s_w + 8 * i0, s_w + 8 * i1, A.ew[e], ld(wa + i0), ld(wa + i1),
+                A.angle_w, A.rot_w, 0, false, dummy, &cost);
+  return 2.0 * cost;
+}
+
+// ---------------------------------------------------------------------------------
+// rigidity rows of one (edge, bin) for the Gram accumulation (kernels.py:341-467)
+// ---------------------------------------------------------------------------------
+
+struct EdgeBin {
+  double p0t[3], p1t[3], c01[3], c10[3];
+  double base;
+  int i0, i1, side;
+};
+
+__device__ __forceinline__ void edge_setup(const SolverArgs& A, const double* s_T, const double* wa,
+                                           int e2, EdgeBin& eb) {
+  const int e = e2 >> 1;
+  eb.side = e2 & 1;
+  eb.i0 = A.edges[2 * e];
+  eb.i1 = A.edges[2 * e + 1];
+  const double* p0 = A.cpts + 3 * eb.i0;
+  const double* p1 = A.cpts + 3 * eb.i1;
+  const double* T0 = s_T + 12 * eb.i0;
+  const double* T1 = s_T + 12 * eb.i1;
+  eb.base = A.ew[e] * 0.5 * (ld(wa + eb.i0) + ld(wa + eb.i1));
+  xform(T0, T0 + 9, p0[0], p0[1], p0[2], eb.p0t);
+  xform(T1, T1 + 9, p1[0], p1[1], p1[2], eb.p1t);
+  xform(T0, T0 + 9, p1[0], p1[1], p1[2], eb.c01);
+  xform(T1, T1 + 9, p0[0], p0[1], p0[2], eb.c10);
+}
+
+__device__ __forceinline__ void length_row(const SolverArgs& A, const EdgeBin& eb, double row[8]) {
+  const double* p0 = A.cpts + 3 * eb.i0;
+  const double* p1 = A.cpts + 3 * eb.i1;
+  const double rx = p1[0] - p0[0], ry = p1[1] - p0[1], rz = p1[2] - p0[2];
+  const double rest = sqrt(rx * rx + ry * ry + rz * rz);
+  const double bx = eb.p1t[0] - eb.p0t[0], by = eb.p1t[1] - eb.p0t[1], bz = eb.p1t[2] - eb.p0t[2];
+  const double ln = sqrt(bx * bx + by * by + bz * bz);
+  const double sw = sqrt(0.5 * eb.base);
+  double bhx = 0.0, bhy = 0.0, bhz = 0.0;
+  if (ln > 1e-9) {
+    const double il = 1.0 / ln;
+    bhx = bx * il;
+    bhy = by * il;
+    bhz = bz * il;
+  }
+  if (eb.side == 0) {
+    row[0] = sw * (eb.p0t[1] * (-bhz) - eb.p0t[2] * (-bhy));
+    row[1] = sw * (eb.p0t[2] * (-bhx) - eb.p0t[0] * (-bhz));
+    row[2] = sw * (eb.p0t[0] * (-bhy) - eb.p0t[1] * (-bhx));
+    row[3] = sw * (-bhx);
+    row[4] = sw * (-bhy);
+    row[5] = sw * (-bhz);
+  } else {
+    row[0] = sw * (eb.p1t[1] * bhz - eb.p1t[2] * bhy);
+    row[1] = sw * (eb.p1t[2] * bhx - eb.p1t[0] * bhz);
+    row[2] = sw * (eb.p1t[0] * bhy - eb.p1t[1] * bhx);
+    row[3] = sw * bhx;
+    row[4] = sw * bhy;
+    row[5] = sw * bhz;
+  }
+  row[6] = sw * (ln - rest);
+  row[7] = 0.0;
+}
+
+// angle row of direction dir (0: 0->1, 1: 1->0) for this bin
+__device__ __forceinline__ void angle_row_bin(const SolverArgs& A, const EdgeBin& eb, int dir,
+                                              double row[8]) {
+  const double sw = sqrt(0.5 * eb.base * A.angle_w);
+  double J[6];
+  double wv;
+  if (dir == 0)
+    wv = angle_row(eb.c01[0] - eb.p0t[0], eb.c01[1] - eb.p0t[1], eb.c01[2] - eb.p0t[2],
+                   eb.p1t[0] - eb.p0t[0], eb.p1t[1] - eb.p0t[1], eb.p1t[2] - eb.p0t[2], eb.p0t[0],
+                   eb.p0t[1], eb.p0t[2], eb.p1t[0], eb.p1t[1], eb.p1t[2], sw,
+                   eb.side == 0 ? 0 : 1, true, J);
+  else
+    wv = angle_row(eb.c10[0] - eb.p1t[0], eb.c10[1] - eb.p1t[1], eb.c10[2] - eb.p1t[2],
+                   eb.p0t[0] - eb.p1t[0], eb.p0t[1] - eb.p1t[1], eb.p0t[2] - eb.p1t[2], eb.p1t[0],
+                   eb.p1t[1], eb.p1t[2], eb.p0t[0], eb.p0t[1], eb.p0t[2], sw,
+                   eb.side == 0 ? 1 : 0, true, J);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) row[i] = J[i];
+  row[6] = wv;
+  row[7] = 0.0;
+}
+
+// rotation row r (0..3) for this bin: sw_r * (J4[r] | 0 0 0 | d_r) (kernels.py:419-461)
+__device__ __forceinline__ void rotation_row(const SolverArgs& A, const EdgeBin& eb,
+                                             const double* s_w, int r, double row[8]) {
+  const double sw = sqrt(0.5 * eb.base * A.rot_w);
+  const double* q0 = s_w + 8 * eb.i0;
+  const double* q1 = s_w + 8 * eb.i1;
+  const double dq = q0[0] * q1[0] + q0[1] * q1[1] + q0[2] * q1[2] + q0[3] * q1[3];
+  const double sg = dq < 0.0 ? -1.0 : 1.0;
+  const double d = q0[r] - sg * q1[r];
+  double P[12];
+  if (eb.side == 0) {
+    half_left_mul(q0[0], q0[1], q0[2], q0[3], P);
+  } else {
+    const double h = -sg * 0.5;
+    P[0] = h * q1[1] * -1.0; P[1] = h * q1[2] * -1.0; P[2] = h * q1[3] * -1.0;
+    P[3] = h * q1[0];        P[4] = h * q1[3];        P[5] = h * -q1[2];
+    P[6] = h * -q1[3];       P[7] = h * q1[0];        P[8] = h * q1[1];
+    P[9] = h * q1[2];        P[10] = h * -q1[1];      P[11] = h * q1[0];
+  }
+  row[0] = sw * P[3 * r];
+  row[1] = sw * P[3 * r + 1];
+  row[2] = sw * P[3 * r + 2];
+  row[3] = row[4] = row[5] = 0.0;
+  row[6] = sw * d;
+  row[7] = 0.0;
+}
+
+// Cholesky of the damped 6x6 system on a packed lower triangle (solver.py:217-258):
+// M = A + lam diag(max(diag A, 1e-12)); forward / backward substitution in the
+// reference's order. false (delta = 0) on a non-positive pivot.
+__device__ __forceinline__ bool solve6(const double* part, double lam, double delta[6]) {
+  double L[21];  // row-major packed lower triangle: L[i(i+1)/2 + j]
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) L[i * (i + 1) / 2 + j] = part[triu_col(j, i)];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const double a = L[i * (i + 1) / 2 + i];
+    L[i * (i + 1) / 2 + i] = a + lam * fmax(a, 1e-12);
+  }
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    double s = L[j * (j + 1) / 2 + j];
+#pragma unroll
+    for (int q = 0; q < j; ++q) s -= L[j * (j + 1) / 2 + q] * L[j * (j + 1) / 2 + q];
+    ok = ok && (s > 0.0);
+    const double ljj = sqrt(s);
+    L[j * (j + 1) / 2 + j] = ljj;
+#pragma unroll
+    for (int i = j + 1; i < 6; ++i) {
+      double v = L[i * (i + 1) / 2 + j];
+#pragma unroll
+      for (int q = 0; q < j; ++q) v -= L[i * (i + 1) / 2 + q] * L[j * (j + 1) / 2 + q];
+      L[i * (i + 1) / 2 + j] = v / ljj;
+    }
+  }
+  if (!ok) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) delta[i] = 0.0;
+    return false;
+  }
+  double y[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    double acc = -part[21 + i];
+#pragma unroll
+    for (int j = 0; j < i; ++j) acc -= L[i * (i + 1) / 2 + j] * y[j];
+    y[i] = acc / L[i * (i + 1) / 2 + i];
+  }
+#pragma unroll
+  for (int i = 5; i >= 0; --i) {
+    double acc = y[i];
+#pragma unroll
+    for (int j = i + 1; j < 6; ++j) acc -= L[j * (j + 1) / 2 + i] * delta[j];
+    delta[i] = acc / L[i * (i + 1) / 2 + i];
   }
   return true;
 }
 
-// Phase A, one active feature match (kernels.py:239-250).
-__device__ __forceinline__ void match_lin(const SolverArgs& A, const double* s_w, int64_t j, bool jac) {
-  double B[8], sgn[KMAX];
-  blend_match(A, s_w, j, B, sgn);
-  const double px = A.fp[3 * j], py = A.fp[3 * j + 1], pz = A.fp[3 * j + 2];
-  double x0, x1, x2, s2;
-  apply_blend(B, px, py, pz, x0, x1, x2, s2);
-  A.fr_res[3 * j] = x0 - A.fo[3 * j];
-  A.fr_res[3 * j + 1] = x1 - A.fo[3 * j + 1];
-  A.fr_res[3 * j + 2] = x2 - A.fo[3 * j + 2];
-  A.fr_sgn[j] = (uint8_t)sign_bits(sgn, A.k);
-  if (jac) blend_gradient(B, px, py, pz, x0, x1, x2, s2, A.fr_G + 24 * j);
-}
-
-// Per-control gather of the data rows (icp + feature) in jac or value mode. In
-// tentative mode (`tent`) the residuals are re-evaluated at the warps in shared memory
-// with the frozen robust weights and the linearization's correspondences
-// (solver.py:333-335); otherwise the stored per-point records are used.
-__device__ __forceinline__ void control_data(const SolverArgs& A, const double* s_w, int c, int64_t n_act,
-                             bool jac, bool tent, double* acc /*30*/) {
+// Fixed-order sum of a chunk-sum array by one warp (lane-strided, then xor tree).
+__device__ __forceinline__ double sum_fixed(const double* a, int n) {
   const int lane = threadIdx.x & 31;
-  Basis K;
-  if (jac) make_basis(s_w + 8 * c, K);
-  double* sup = &acc[27];
-  double* cicp = &acc[28];
-  double* cfeat = &acc[29];
-  const int k = A.k;
-  const int q1 = ldi(A.cptr + c + 1);
-  for (int q = ldi(A.cptr + c) + lane; q < q1; q += 32) {
-    const int e = ldi(A.cent + q);
-    const int64_t p = e >> 3;
-    const int s = e & 7;
-    if (!ldu8(A.cvalid + p)) continue;
-    const double a = A.bw[p * k + s];
-    const double rs = ld(A.pr_rs + p);
-    double r;
-    unsigned sbits;
-    if (tent) {
-      double B[8], sgn[KMAX];
-      blend_point(A, s_w, p, B, sgn);
-      double x0, x1, x2, s2;
-      apply_blend(B, A.tp[3 * p], A.tp[3 * p + 1], A.tp[3 * p + 2], x0, x1, x2, s2);
-      r = ld(A.cnrm + 3 * p) * (x0 - ld(A.cobs + 3 * p)) +
-          ld(A.cnrm + 3 * p + 1) * (x1 - ld(A.cobs + 3 * p + 1)) +
-          ld(A.cnrm + 3 * p + 2) * (x2 - ld(A.cobs + 3 * p + 2));
-      sbits = 0;
-    } else {
-      r = ld(A.pr_r + p);
-      sbits = ldu8(A.pr_sgn + p);
-    }
-    *sup += rs * rs * a;
-    const double sw = rs * sqrt(a);
-    const double wv = sw * r;
-    *cicp += wv * wv;
-    if (jac) {
-      double gn[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) gn[i] = ld(A.pr_gn + 8 * p + i);
-      const double sg = ((sbits >> s) & 1u) ? -1.0 : 1.0;
-      const double coef = sw * a * sg;
-      double pr[6], J[6];
-      basis_project(gn, K.Kr, K.Kd, pr);
-#pragma unroll
-      for (int d = 0; d < 6; ++d) J[d] = coef * pr[d];
-      fold_row(acc, J, wv);
-    }
-  }
-  if (A.mptr != nullptr && n_act > 0) {
-    const int m1 = ldi(A.mptr + c + 1);
-    for (int q = ldi(A.mptr + c) + lane; q < m1; q += 32) {
-      const int e = ldi(A.ment + q);
-      const int64_t j = e / k;
-      const int s = e - (int)j * k;
-      const double a = A.fbw[e];
-      double res[3];
-      unsigned sbits;
-      if (tent) {
-        double B[8], sgn[KMAX];
-        blend_match(A, s_w, j, B, sgn);
-        double x0, x1, x2, s2;
-        apply_blend(B, A.fp[3 * j], A.fp[3 * j + 1], A.fp[3 * j + 2], x0, x1, x2, s2);
-        res[0] = x0 - A.fo[3 * j];
-        res[1] = x1 - A.fo[3 * j + 1];
-        res[2] = x2 - A.fo[3 * j + 2];
-        sbits = 0;
-      } else {
-        res[0] = ld(A.fr_res + 3 * j);
-        res[1] = ld(A.fr_res + 3 * j + 1);
-        res[2] = ld(A.fr_res + 3 * j + 2);
-        sbits = ldu8(A.fr_sgn + j);
-      }
-      const double w_pair = A.fw * A.fwt[j] * a;
-      *sup += w_pair;
-      const double sw = sqrt(w_pair);
-      const double wv0 = sw * res[0], wv1 = sw * res[1], wv2 = sw * res[2];
-      *cfeat += wv0 * wv0 + wv1 * wv1 + wv2 * wv2;
-      if (jac) {
-        const double sg = ((sbits >> s) & 1u) ? -1.0 : 1.0;
-        const double coef = sw * a * sg;
-        double GK[18];
-#pragma unroll
-        for (int comp = 0; comp < 3; ++comp) {
-          double g[8], pr[6];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) g[i] = ld(A.fr_G + 24 * j + 8 * comp + i);
-          basis_project(g, K.Kr, K.Kd, pr);
-#pragma unroll
-          for (int d = 0; d < 6; ++d) GK[comp * 6 + d] = coef * pr[d];
-        }
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-#pragma unroll
-          for (int jj = i; jj < 6; ++jj)
-            acc[triu_col(i, jj)] += GK[i] * GK[jj] + GK[6 + i] * GK[6 + jj] + GK[12 + i] * GK[12 + jj];
-          acc[21 + i] += GK[i] * wv0 + GK[6 + i] * wv1 + GK[12 + i] * wv2;
-        }
-      }
-    }
-  }
+  double s = 0.0;
+  for (int i = lane; i < n; i += 32) s += ld(a + i);
+  return warp_sum(s);
 }
 
-// Per-control gather of the rigidity rows over the control's incident edges.
-__device__ __forceinline__ void control_arap(const SolverArgs& A, const double* s_w, int c, const double* wa,
-                             bool jac, double* acc /*27*/, double* cost) {
-  const int lane = threadIdx.x & 31;
-  const int q1 = ldi(A.iptr + c + 1);
-  for (int q = ldi(A.iptr + c) + lane; q < q1; q += 32) {
-    const int e2 = ldi(A.ient + q);
-    const int e = e2 >> 1, side = e2 & 1;
-    const int i0 = A.edges[2 * e], i1 = A.edges[2 * e + 1];
-    double R0[9], t0[3], R1[9], t1[3];
-    dq_to_transform(s_w + 8 * i0, R0, t0);
-    dq_to_transform(s_w + 8 * i1, R1, t1);
-    arap_edge_bin(A.cpts + 3 * i0, A.cpts + 3 * i1, R0, t0, R1, t1, s_w + 8 * i0, s_w + 8 * i1,
-                  A.ew[e], ld(wa + i0), ld(wa + i1), A.angle_w, A.rot_w, side, jac, acc, cost);
-  }
-}
+#define TRACE(code)                                                \
+  do {                                                             \
+    if (tr && rank == 0 && threadIdx.x == 0 && tn < A.trace_cap) { \
+      tr[1 + 2 * tn] = (code);                                     \
+      tr[2 + 2 * tn] = gtimer();                                   \
+      ++tn;                                                        \
+    }                                                              \
+  } while (0)
+#define DSYNC(phase)         \
+  do {                       \
+    TRACE(10 * (phase));     \
+    dom.sync();              \
+    TRACE(10 * (phase) + 1); \
+  } while (0)
 
-// Sum three per-control cost columns over all controls in a fixed order (warp 0,
-// lane-strided then xor tree); every CTA evaluates it identically. Result broadcast
-// through s_out[0..2]. Must be called by the whole CTA.
-__device__ void total3(const double* c3, int m, double* s_out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (warp == 0) {
-    double a = 0.0, b = 0.0, d = 0.0;
-    for (int i = lane; i < m; i += 32) {
-      a += ld(c3 + 3 * i);
-      b += ld(c3 + 3 * i + 1);
-      d += ld(c3 + 3 * i + 2);
-    }
-    a = warp_sum(a);
-    b = warp_sum(b);
-    d = warp_sum(d);
-    if (lane == 0) {
-      s_out[0] = a;
-      s_out[1] = b;
-      s_out[2] = d;
-    }
-  }
-  __syncthreads();
-}
-
+template <bool GRID>
 __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverArgs* __restrict__ all) {
-  cg::cluster_group cluster = cg::this_cluster();
-  const int C = (int)cluster.num_blocks();
-  const int rank = (int)cluster.block_rank();
+  Dom<GRID> dom;
+  const int C = dom.size();
+  const int rank = dom.rank();
   __shared__ SolverArgs A;
-  __shared__ double s_tot[8];
-  __shared__ double s_misc[8];
+  __shared__ double s_red[8];
   __shared__ int s_cnt[NWARPS];
   extern __shared__ double smem[];
-  if (threadIdx.x == 0) A = all[blockIdx.x / C];
+  if (threadIdx.x == 0) A = all[dom.seq()];
   __syncthreads();
-  double* s_w = smem;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* s_scr = smem + 8 * A.m + warp * 32 * SCR_COLS;
-  const int gw = rank * NWARPS + warp, GW = C * NWARPS;
-  const int64_t gt = (int64_t)rank * blockDim.x + threadIdx.x, GT = (int64_t)C * blockDim.x;
   const int m = A.m;
   const int64_t n = A.n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* s_w = smem;
+  double* s_T = smem + 8 * m;
+  double* stage = smem + 20 * m + warp * (STAGE + GOUT);
+  double* gout = stage + STAGE;
+  const int gw = rank * NWARPS + warp, GW = C * NWARPS;
+  const int gt = rank * (int)blockDim.x + (int)threadIdx.x, GT = C * (int)blockDim.x;
   const int64_t n_act = A.n_active ? *A.n_active : 0;
+  const int nch_p = (int)((n + CHUNK - 1) / CHUNK);
+  const int nch_m = (int)((n_act + CHUNK - 1) / CHUNK);
+  const int nch_e = (A.n_edges + CHUNK - 1) / CHUNK;
+  double* cs_p = A.csum;
+  double* cs_m = A.csum + A.nch_p;
+  double* cs_e = cs_m + A.nch_m;
+  long long* tr = A.trace;
+  int tn = 0;
+  TRACE(0);
 
-  for (int c = gw; c < m; c += GW)
-    if (lane == 0) A.lam[c] = A.lam_init;
+  for (int c = gt; c < m; c += GT) A.lam[c] = A.lam_init;
 
   double* cur = A.warp_a;
   double* tent = A.warp_b;
-  int accepted_steps = 0, rejected_steps = 0, n_hist = 0;
+  int accepted_steps = 0, rejected_steps = 0, n_hist = 0, outer_done = 0, lam_pending = -1;
   bool converged = false, stalled = false;
   double final_step_norm = 0.0;
-  int outer_done = 0;
-  int lam_pending = -1;
   int parity = 0;
+
+  // totals of the three chunk-sum segments, identical in every CTA
+  auto totals = [&](double& t, double* parts) {
+    __syncthreads();
+    if (warp == 0) {
+      const double a = sum_fixed(cs_p, nch_p);
+      const double b = sum_fixed(cs_m, nch_m);
+      const double e = sum_fixed(cs_e, nch_e);
+      if (lane == 0) {
+        s_red[0] = a;
+        s_red[1] = b;
+        s_red[2] = e;
+      }
+    }
+    __syncthreads();
+    t = s_red[0] + s_red[1] + s_red[2];
+    if (parts) {
+      parts[0] = s_red[0];
+      parts[1] = s_red[1];
+      parts[2] = s_red[2];
+    }
+  };
+  auto lam_history = [&](int it) {
+    if (rank == 0 && warp == 0) {
+      double lo = INFINITY, hi = -INFINITY;
+      for (int i = lane; i < m; i += 32) {
+        const double v = ld(A.lam + i);
+        lo = fmin(lo, v);
+        hi = fmax(hi, v);
+      }
+      lo = warp_min(lo);
+      hi = warp_max(hi);
+      if (lane == 0) {
+        A.lam_hist[2 * it] = lo;
+        A.lam_hist[2 * it + 1] = hi;
+      }
+    }
+  };
 
   for (int outer = 0; outer < A.max_outer; ++outer) {
     outer_done = outer + 1;
-    // ---- Phase A: relink + linearize every point and match at `cur` ----
-    load_warps(A, cur, s_w);
-    __syncthreads();
-    for (int64_t p = gt; p < n; p += GT) point_relink(A, s_w, p, true);
-    for (int64_t j = gt; j < n_act; j += GT) match_lin(A, s_w, j, true);
-    cluster.sync();
-    if (lam_pending >= 0 && rank == 0) {
-      // lambda_history of the previous outer iteration (solver.py:345); lam is not
-      // touched again before the next cluster barrier
-      if (warp == 0) {
-        double lo = INFINITY, hi = -INFINITY;
-        for (int i = lane; i < m; i += 32) {
-          const double v = ld(A.lam + i);
-          lo = fmin(lo, v);
-          hi = fmax(hi, v);
+    // ---- P1: relink + linearize at `cur`; icp / feature cost of the iterate ----
+    load_state(A, cur, s_w, s_T);
+    for (int ch = gw; ch < nch_p; ch += GW) {
+      double acc = 0.0;
+      int vdummy;
+      for (int i = 0; i < CHUNK / 32; ++i) {
+        const int64_t p = (int64_t)ch * CHUNK + i * 32 + lane;
+        if (p < n) acc += point_relink(A, s_w, p, true, &vdummy);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) cs_p[ch] = acc;
+    }
+    for (int ch = gw; ch < nch_m; ch += GW) {
+      double acc = 0.0;
+      for (int i = 0; i < CHUNK / 32; ++i) {
+        const int64_t j = (int64_t)ch * CHUNK + i * 32 + lane;
+        if (j < n_act) acc += match_eval(A, s_w, j, true, true);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) cs_m[ch] = acc;
+    }
+    DSYNC(1);
+    if (lam_pending >= 0) lam_history(lam_pending);
+    lam_pending = -1;
+
+    // ---- P2: data rows -> normal equations (Gram on the FP64 tensor cores) ----
+    for (int c = gw; c < m; c += GW) {
+      Basis K;
+      make_basis(s_w + 8 * c, K);
+      Gram G;
+      double sup = 0.0;
+      const int q0 = ldi(A.cptr + c), q1 = ldi(A.cptr + c + 1);
+      for (int base = q0; base < q1; base += 32) {
+        const int q = base + lane;
+        double row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (q < q1) {
+          const int e = ldi(A.cent + q);
+          const int64_t p = e >> 3;
+          const int s = e & 7;
+          if (ldu8(A.cvalid + p)) {
+            const double a = A.bw[p * A.k + s];
+            const double rs = ld(A.pr_rs + p);
+            sup += rs * rs * a;
+            const double sw = rs * sqrt(a);
+            const double sg = ((ldu8(A.pr_sgn + p) >> s) & 1u) ? -1.0 : 1.0;
+            const double coef = sw * a * sg;
+            double gn[8], pr[6];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) gn[i] = ld(A.pr_gn + 8 * p + i);
+            basis_project(gn, K.Kr, K.Kd, pr);
+#pragma unroll
+            for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
+            row[6] = sw * ld(A.pr_r + p);
+          }
         }
-        lo = warp_min(lo);
-        hi = warp_max(hi);
-        if (lane == 0) {
-          A.lam_hist[2 * lam_pending] = lo;
-          A.lam_hist[2 * lam_pending + 1] = hi;
+        gram_push(G, stage, row);
+      }
+      if (n_act > 0) {
+        const int m0 = ldi(A.mptr + c), m1 = ldi(A.mptr + c + 1);
+        for (int base = m0; base < m1; base += 32) {
+          const int q = base + lane;
+          const bool live = q < m1;
+          int64_t j = 0;
+          double coef = 0.0, sw = 0.0;
+          if (live) {
+            const int e = ldi(A.ment + q);
+            j = e / A.k;
+            const int s = e - (int)j * A.k;
+            const double a = A.fbw[e];
+            const double w_pair = A.fw * A.fwt[j] * a;
+            sup += w_pair;
+            sw = sqrt(w_pair);
+            const double sg = ((ldu8(A.fr_sgn + j) >> s) & 1u) ? -1.0 : 1.0;
+            coef = sw * a * sg;
+          }
+#pragma unroll 1
+          for (int comp = 0; comp < 3; ++comp) {
+            double row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (live) {
+              double g[8], pr[6];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) g[i] = ld(A.fr_G + 24 * j + 8 * comp + i);
+              basis_project(g, K.Kr, K.Kd, pr);
+#pragma unroll
+              for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
+              row[6] = sw * ld(A.fr_res + 3 * j + comp);
+            }
+            gram_push(G, stage, row);
+          }
         }
       }
-      lam_pending = -1;
+      gram_store(G, gout);
+      sup = warp_sum(sup);
+      if (lane < 27) A.partial[27 * c + lane] = gram_col(gout, lane);
+      if (lane == 27) A.wa[c] = A.arap_w * fmax(sup, A.data_floor);
+      __syncwarp();
     }
-    lam_pending = -1;
-    // ---- Phase B: per-control data rows -> partial, support, wa ----
+    DSYNC(2);
+
+    // ---- P3: rigidity rows -> normal equations + first damped solve; rigidity cost ----
+    double* okn = A.oknorm + (size_t)parity * 2 * m;
     for (int c = gw; c < m; c += GW) {
-      double acc[SCR_COLS];
+      Gram G;
+      const int q0 = ldi(A.iptr + c), q1 = ldi(A.iptr + c + 1);
+      for (int base = q0; base < q1; base += 32) {
+        const int q = base + lane;
+        const bool live = q < q1;
+        EdgeBin eb;
+        if (live) edge_setup(A, s_T, A.wa, ldi(A.ient + q), eb);
+        double row[8];
+#pragma unroll 1
+        for (int r = 0; r < 7; ++r) {
+          if (live) {
+            if (r == 0) length_row(A, eb, row);
+            else if (r < 3) angle_row_bin(A, eb, r - 1, row);
+            else rotation_row(A, eb, s_w, r - 3, row);
+          } else {
 #pragma unroll
-      for (int i = 0; i < SCR_COLS; ++i) acc[i] = 0.0;
-      control_data(A, s_w, c, n_act, true, false, acc);
-      double out[SCR_COLS];
-      warp_column_sum<SCR_COLS>(acc, s_scr, out);
-      if (lane < 27) A.partial[27 * c + lane] = out[lane];
-      if (lane == 27) A.wa[c] = A.arap_w * fmax(out[27], A.data_floor);
-      if (lane == 28) A.cost3[3 * c] = out[28];
-      if (lane == 29) A.cost3[3 * c + 1] = out[29];
+            for (int i = 0; i < 8; ++i) row[i] = 0.0;
+          }
+          gram_push(G, stage, row);
+        }
+      }
+      gram_store(G, gout);
+      if (lane < 27) A.partial[27 * c + lane] = A.partial[27 * c + lane] + gram_col(gout, lane);
+      __syncwarp();
+      if (lane == 0) {
+        double part[27], d[6];
+        for (int i = 0; i < 27; ++i) part[i] = A.partial[27 * c + i];
+        const bool good = solve6(part, ld(A.lam + c), d);
+        double nn = 0.0;
+        for (int i = 0; i < 6; ++i) {
+          A.delta[6 * c + i] = d[i];
+          nn += d[i] * d[i];
+        }
+        okn[2 * c] = good ? 1.0 : 0.0;
+        okn[2 * c + 1] = sqrt(nn);
+      }
+      __syncwarp();
     }
-    cluster.sync();
-    // ---- Phase C: per-control rigidity rows, then the first damped solve ----
-    for (int c = gw; c < m; c += GW) {
-      double acc[28];
-#pragma unroll
-      for (int i = 0; i < 28; ++i) acc[i] = 0.0;
-      control_arap(A, s_w, c, A.wa, true, acc, &acc[27]);
-      double out[28];
-      warp_column_sum<28>(acc, s_scr, out);
-      if (lane < 27) A.partial[27 * c + lane] = A.partial[27 * c + lane] + out[lane];
-      if (lane == 27) A.cost3[3 * c + 2] = out[27];
+    for (int ch = gw; ch < nch_e; ch += GW) {
+      double acc = 0.0;
+      for (int i = 0; i < CHUNK / 32; ++i) {
+        const int e = ch * CHUNK + i * 32 + lane;
+        if (e < A.n_edges) acc += edge_value(A, s_w, s_T, A.wa, e);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) cs_e[ch] = acc;
     }
     bool accepted = false;
     double cost_before = 0.0, cost_after = 0.0;
-    bool have_before = false;
     for (int attempt = 0; attempt <= A.max_retries; ++attempt) {
-      // damped solve per owned control (solver.py:217-258)
-      double* okn = A.oknorm + (size_t)parity * 2 * m;
-      for (int c = gw; c < m; c += GW) {
-        __syncwarp();
-        if (lane == 0) {
+      if (attempt > 0) {
+        okn = A.oknorm + (size_t)parity * 2 * m;
+        for (int c = gt; c < m; c += GT) {
           double part[27], d[6];
           for (int i = 0; i < 27; ++i) part[i] = ld(A.partial + 27 * c + i);
-          const bool good = damped_solve6(part, ld(A.lam + c), d);
+          const bool good = solve6(part, A.lam[c], d);
           double nn = 0.0;
           for (int i = 0; i < 6; ++i) {
             A.delta[6 * c + i] = d[i];
@@ -416,13 +774,9 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
           okn[2 * c + 1] = sqrt(nn);
         }
       }
-      cluster.sync();
-      if (!have_before) {
-        total3(A.cost3, m, s_tot);
-        cost_before = s_tot[0] + s_tot[1] + s_tot[2];
-        have_before = true;
-      }
-      // all ok? max step norm (identical in every CTA)
+      DSYNC(attempt == 0 ? 3 : 4);
+      if (attempt == 0) totals(cost_before, nullptr);
+      // all solves ok? largest step norm (identical in every CTA)
       __syncthreads();
       if (warp == 0) {
         double allok = 1.0, mx = 0.0;
@@ -433,61 +787,71 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         allok = warp_min(allok);
         mx = warp_max(mx);
         if (lane == 0) {
-          s_misc[0] = allok;
-          s_misc[1] = mx;
+          s_red[4] = allok;
+          s_red[5] = mx;
         }
       }
       __syncthreads();
-      const bool all_ok = s_misc[0] > 0.5;
-      const double step_norm = s_misc[1];
+      const bool all_ok = s_red[4] > 0.5;
+      const double step_norm = s_red[5];
       parity ^= 1;
       if (!all_ok) {
         // raise the damping of the failed controls only, retry (solver.py:321-326)
-        for (int c = gw; c < m; c += GW)
-          if (lane == 0 && ld(okn + 2 * c) < 0.5) A.lam[c] = fmin(A.lam[c] * A.lam_inc, A.lam_max);
+        for (int c = gt; c < m; c += GT)
+          if (ld(okn + 2 * c) < 0.5) A.lam[c] = fmin(ld(A.lam + c) * A.lam_inc, A.lam_max);
         ++rejected_steps;
         continue;
       }
       final_step_norm = step_norm;
-      if (step_norm < A.step_tol) {
+      if (step_norm < A.step_tol) {  // checked before the step (solver.py:327-331)
         converged = true;
         break;
       }
-      // tentative warps (solver.py:332)
-      for (int c = gw; c < m; c += GW)
-        if (lane < 8) {
-          double out8[8];
-          apply_step_one(cur + 8 * c, A.delta + 6 * c, out8);
-          // every lane evaluates the same step; lane l stores component l
-          tent[8 * c + lane] = out8[lane];
-        }
-      cluster.sync();
-      // value pass at the tentative warps with frozen robust and rigidity weights
-      load_warps(A, tent, s_w);
-      __syncthreads();
-      for (int c = gw; c < m; c += GW) {
-        double acc[SCR_COLS];
-#pragma unroll
-        for (int i = 0; i < SCR_COLS; ++i) acc[i] = 0.0;
-        control_data(A, s_w, c, n_act, false, true, acc);
-        double ca = 0.0;
-        control_arap(A, s_w, c, A.wa, false, acc, &ca);
-        acc[27] = ca;  // reuse the support slot for the rigidity cost
-        double out[SCR_COLS];
-        warp_column_sum<SCR_COLS>(acc, s_scr, out);
-        if (lane == 28) A.cost3_t[3 * c] = out[28];
-        if (lane == 29) A.cost3_t[3 * c + 1] = out[29];
-        if (lane == 27) A.cost3_t[3 * c + 2] = out[27];
+      // ---- P5: tentative warps ----
+      for (int c = gt; c < m; c += GT) {
+        double W[8], d[6], o[8];
+        for (int i = 0; i < 8; ++i) W[i] = ld(cur + 8 * c + i);
+        for (int i = 0; i < 6; ++i) d[i] = ld(A.delta + 6 * c + i);
+        apply_step_one(W, d, o);
+        for (int i = 0; i < 8; ++i) tent[8 * c + i] = o[i];
       }
-      cluster.sync();
-      total3(A.cost3_t, m, s_tot);
-      cost_after = s_tot[0] + s_tot[1] + s_tot[2];
+      DSYNC(5);
+      // ---- P6: cost at the tentative warps, frozen weights and correspondences ----
+      load_state(A, tent, s_w, s_T);
+      for (int ch = gw; ch < nch_p; ch += GW) {
+        double acc = 0.0;
+        for (int i = 0; i < CHUNK / 32; ++i) {
+          const int64_t p = (int64_t)ch * CHUNK + i * 32 + lane;
+          if (p < n) acc += point_value(A, s_w, p);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) cs_p[ch] = acc;
+      }
+      for (int ch = gw; ch < nch_m; ch += GW) {
+        double acc = 0.0;
+        for (int i = 0; i < CHUNK / 32; ++i) {
+          const int64_t j = (int64_t)ch * CHUNK + i * 32 + lane;
+          if (j < n_act) acc += match_eval(A, s_w, j, false, false);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) cs_m[ch] = acc;
+      }
+      for (int ch = gw; ch < nch_e; ch += GW) {
+        double acc = 0.0;
+        for (int i = 0; i < CHUNK / 32; ++i) {
+          const int e = ch * CHUNK + i * 32 + lane;
+          if (e < A.n_edges) acc += edge_value(A, s_w, s_T, A.wa, e);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) cs_e[ch] = acc;
+      }
+      DSYNC(6);
+      totals(cost_after, nullptr);
       if (cost_after < cost_before) {
         double* tmp = cur;
         cur = tent;
         tent = tmp;
-        for (int c = gw; c < m; c += GW)
-          if (lane == 0) A.lam[c] = fmax(A.lam[c] * A.lam_dec, A.lam_min);
+        for (int c = gt; c < m; c += GT) A.lam[c] = fmax(ld(A.lam + c) * A.lam_dec, A.lam_min);
         ++accepted_steps;
         if (rank == 0 && threadIdx.x == 0) {
           A.cost_hist[2 * n_hist] = cost_before;
@@ -497,8 +861,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         accepted = true;
         break;
       }
-      for (int c = gw; c < m; c += GW)
-        if (lane == 0) A.lam[c] = fmin(A.lam[c] * A.lam_inc, A.lam_max);
+      for (int c = gt; c < m; c += GT) A.lam[c] = fmin(ld(A.lam + c) * A.lam_inc, A.lam_max);
       ++rejected_steps;
     }
     lam_pending = outer;
@@ -516,73 +879,86 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
 
   // ---- final report: relink at the solution, recompute robust and rigidity weights
   // (solver.py:360-376) ----
-  load_warps(A, cur, s_w);
-  __syncthreads();
+  load_state(A, cur, s_w, s_T);
   int my_valid = 0;
-  for (int64_t p = gt; p < n; p += GT) my_valid += point_relink(A, s_w, p, false) ? 1 : 0;
-  for (int64_t j = gt; j < n_act; j += GT) match_lin(A, s_w, j, false);
-  // per-CTA count of correspondences
+  for (int ch = gw; ch < nch_p; ch += GW) {
+    double acc = 0.0;
+    for (int i = 0; i < CHUNK / 32; ++i) {
+      const int64_t p = (int64_t)ch * CHUNK + i * 32 + lane;
+      int v = 0;
+      if (p < n) acc += point_relink(A, s_w, p, false, &v);
+      my_valid += v;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) cs_p[ch] = acc;
+  }
+  for (int ch = gw; ch < nch_m; ch += GW) {
+    double acc = 0.0;
+    for (int i = 0; i < CHUNK / 32; ++i) {
+      const int64_t j = (int64_t)ch * CHUNK + i * 32 + lane;
+      if (j < n_act) acc += match_eval(A, s_w, j, true, false);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) cs_m[ch] = acc;
+  }
   for (int o = 16; o > 0; o >>= 1) my_valid += __shfl_xor_sync(0xffffffffu, my_valid, o);
   if (lane == 0) s_cnt[warp] = my_valid;
   __syncthreads();
   if (threadIdx.x == 0) {
     int t = 0;
     for (int w = 0; w < NWARPS; ++w) t += s_cnt[w];
-    A.cta_counts[rank] = t;
+    A.counts[rank] = t;
   }
-  // final warps out
-  for (int c = gw; c < m; c += GW)
-    if (lane < 8) A.warps_out[8 * c + lane] = ld(cur + 8 * c + lane);
-  cluster.sync();
-  if (lam_pending >= 0 && rank == 0 && warp == 0) {
-    double lo = INFINITY, hi = -INFINITY;
-    for (int i = lane; i < m; i += 32) {
-      const double v = ld(A.lam + i);
-      lo = fmin(lo, v);
-      hi = fmax(hi, v);
+  for (int c = gt; c < m; c += GT)
+    for (int i = 0; i < 8; ++i) A.warps_out[8 * c + i] = s_w[8 * c + i];
+  DSYNC(7);
+  if (lam_pending >= 0) lam_history(lam_pending);
+  // support per control with the recomputed robust weights -> wa
+  for (int c = gw; c < m; c += GW) {
+    double sup = 0.0;
+    const int q0 = ldi(A.cptr + c), q1 = ldi(A.cptr + c + 1);
+    for (int q = q0 + lane; q < q1; q += 32) {
+      const int e = ldi(A.cent + q);
+      const int64_t p = e >> 3;
+      if (!ldu8(A.cvalid + p)) continue;
+      const double rs = ld(A.pr_rs + p);
+      sup += rs * rs * A.bw[p * A.k + (e & 7)];
     }
-    lo = warp_min(lo);
-    hi = warp_max(hi);
+    if (n_act > 0) {
+      const int m0 = ldi(A.mptr + c), m1 = ldi(A.mptr + c + 1);
+      for (int q = m0 + lane; q < m1; q += 32) {
+        const int e = ldi(A.ment + q);
+        sup += A.fw * A.fwt[e / A.k] * A.fbw[e];
+      }
+    }
+    sup = warp_sum(sup);
     if (lane == 0) {
-      A.lam_hist[2 * lam_pending] = lo;
-      A.lam_hist[2 * lam_pending + 1] = hi;
+      const double w = A.arap_w * fmax(sup, A.data_floor);
+      A.wa[c] = w;
+      A.wa_out[c] = w;
     }
   }
-  for (int c = gw; c < m; c += GW) {
-    double acc[SCR_COLS];
-#pragma unroll
-    for (int i = 0; i < SCR_COLS; ++i) acc[i] = 0.0;
-    control_data(A, s_w, c, n_act, false, false, acc);
-    double out[SCR_COLS];
-    warp_column_sum<SCR_COLS>(acc, s_scr, out);
-    if (lane == 27) {
-      const double wv = A.arap_w * fmax(out[27], A.data_floor);
-      A.wa[c] = wv;
-      A.wa_out[c] = wv;
+  DSYNC(8);
+  for (int ch = gw; ch < nch_e; ch += GW) {
+    double acc = 0.0;
+    for (int i = 0; i < CHUNK / 32; ++i) {
+      const int e = ch * CHUNK + i * 32 + lane;
+      if (e < A.n_edges) acc += edge_value(A, s_w, s_T, A.wa, e);
     }
-    if (lane == 28) A.cost3[3 * c] = out[28];
-    if (lane == 29) A.cost3[3 * c + 1] = out[29];
+    acc = warp_sum(acc);
+    if (lane == 0) cs_e[ch] = acc;
   }
-  cluster.sync();
-  for (int c = gw; c < m; c += GW) {
-    double acc[28];
-#pragma unroll
-    for (int i = 0; i < 28; ++i) acc[i] = 0.0;
-    control_arap(A, s_w, c, A.wa, false, acc, &acc[27]);
-    double out[28];
-    warp_column_sum<28>(acc, s_scr, out);
-    if (lane == 27) A.cost3[3 * c + 2] = out[27];
-  }
-  cluster.sync();
-  total3(A.cost3, m, s_tot);
+  DSYNC(9);
+  double tot = 0.0, parts[3];
+  totals(tot, parts);
   if (rank == 0 && threadIdx.x == 0) {
     dt_report* R = A.report;
-    R->icp_cost = s_tot[0];
-    R->feature_cost = s_tot[1];
-    R->arap_cost = s_tot[2];
-    R->total_cost = s_tot[0] + s_tot[1] + s_tot[2];
+    R->icp_cost = parts[0];
+    R->feature_cost = parts[1];
+    R->arap_cost = parts[2];
+    R->total_cost = tot;
     int nc = 0;
-    for (int i = 0; i < C; ++i) nc += __ldcg(A.cta_counts + i);
+    for (int i = 0; i < C; ++i) nc += __ldcg(A.counts + i);
     R->n_correspondences = nc;
     R->outer_iterations = outer_done;
     R->accepted_steps = accepted_steps;
@@ -592,7 +968,12 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     R->final_step_norm = final_step_norm;
     R->n_cost_history = n_hist;
   }
+  TRACE(99);
+  if (tr && rank == 0 && threadIdx.x == 0) tr[0] = tn;
 }
+
+template __global__ void k_solve_frame<false>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true>(const SolverArgs* __restrict__);
 
 static int g_max_cluster[16] = {0};
 
@@ -600,9 +981,10 @@ int solver_max_cluster(int device) {
   if (device < 0 || device >= 16) return 8;
   if (g_max_cluster[device] > 0) return g_max_cluster[device];
   int best = 1;
-  cudaFuncSetAttribute(k_solve_frame, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  auto* fn = k_solve_frame<false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const size_t smem = solver_smem_bytes(1024);
-  cudaFuncSetAttribute(k_solve_frame, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int c = 16; c >= 1; c >>= 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c, 1, 1);
@@ -616,7 +998,7 @@ int solver_max_cluster(int device) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, k_solve_frame, &cfg) == cudaSuccess && nclusters > 0) {
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) == cudaSuccess && nclusters > 0) {
       best = c;
       break;
     }
@@ -635,12 +1017,38 @@ int solver_pick_cluster(int device, int requested, int m_max) {
   return c;
 }
 
-int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, cudaStream_t s) {
+int solver_grid_blocks(int device, int m_max) {
+  auto* fn = k_solve_frame<true>;
   const size_t smem = solver_smem_bytes(m_max);
-  DT_REQUIRE(smem <= 227 * 1024, DT_ERR_UNSUPPORTED,
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SOLVER_THREADS, smem) != cudaSuccess)
+    per_sm = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return per_sm >= 1 ? sms : 0;  // one CTA per SM
+}
+
+int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, int grid_mode,
+                  cudaStream_t s) {
+  const size_t smem = solver_smem_bytes(m_max);
+  DT_REQUIRE(m_max <= M_MAX_SMEM && smem <= 227 * 1024, DT_ERR_UNSUPPORTED,
              "control graph too large for the shared-memory warp table (m=%d)", m_max);
-  DT_CHECK_CUDA(cudaFuncSetAttribute(k_solve_frame, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  DT_CHECK_CUDA(cudaFuncSetAttribute(k_solve_frame, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (grid_mode) {
+    DT_REQUIRE(n_seq == 1, DT_ERR_UNSUPPORTED, "grid mode runs one sequence per launch");
+    auto* fn = k_solve_frame<true>;
+    DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0;
+    DT_CHECK_CUDA(cudaGetDevice(&dev));
+    const int blocks = solver_grid_blocks(dev, m_max);
+    DT_REQUIRE(blocks > 0, DT_ERR_UNSUPPORTED, "solver kernel cannot be co-resident for a grid launch");
+    void* params[] = {(void*)&d_args};
+    DT_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(blocks), dim3(SOLVER_THREADS),
+                                              params, smem, s));
+    return DT_OK;
+  }
+  auto* fn = k_solve_frame<false>;
+  DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(n_seq * cluster), 1, 1);
   cfg.blockDim = dim3(SOLVER_THREADS, 1, 1);
@@ -653,7 +1061,7 @@ int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, c
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  DT_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_solve_frame, d_args));
+  DT_CHECK_CUDA(cudaLaunchKernelEx(&cfg, fn, d_args));
   return DT_OK;
 }
 

@@ -1,5 +1,7 @@
 // dt_solver.cuh -- the fused per-frame Levenberg-Marquardt solver (solver.solve_frame,
-// solver.py:267-378) as one thread-block-cluster kernel per sequence.
+// solver.py:267-378) as one persistent kernel per frame: either one thread-block
+// cluster per sequence (batched sequences) or one cooperative grid over every SM
+// (lowest single-sequence latency).
 #pragma once
 
 #include <cstdint>
@@ -8,9 +10,13 @@
 
 namespace dt {
 
+constexpr int SOLVER_THREADS = 512;
+constexpr int CHUNK = 256;  // items per deterministic partial sum of the value passes
+
 struct SolverArgs {
   // sizes
   int n, k, m, n_edges, height, width, max_outer, max_retries;
+  int nch_p, nch_m, nch_e;  // value-pass chunk counts (points, matches, edges)
   // camera, gates and energy weights
   double fx, fy, cx, cy, gate, cos_gate;
   double tukey, fw, arap_w, angle_w, rot_w, data_floor;
@@ -48,9 +54,8 @@ struct SolverArgs {
   double* warps_out; // solution
   double* lam;
   double* wa;
-  double* partial;   // m x 27
-  double* cost3;     // m x 3 (icp, feature, arap) of the linearization pass
-  double* cost3_t;   // m x 3 of the tentative (value) pass
+  double* partial;   // m x 27 normal-equation columns
+  double* csum;      // nch_p + nch_m + nch_e deterministic chunk sums
   double* delta;     // m x 6
   double* oknorm;    // 2 parities x m x 2 (ok, step norm)
   uint8_t* cvalid;   // per template point: correspondence valid
@@ -63,19 +68,25 @@ struct SolverArgs {
   double* fr_res;    // Ma x 3
   double* fr_G;      // Ma x 24
   uint8_t* fr_sgn;   // Ma
-  int* cta_counts;   // cluster-size scratch
+  int* counts;       // per-CTA correspondence counts (<= 1024 CTAs)
   // outputs
   dt_report* report;
   double* cost_hist;  // max_outer x 2
   double* lam_hist;   // max_outer x 2
   int32_t* stalled_hist;
   double* wa_out;     // m control_data_weights
+  // optional in-kernel phase trace (CTA 0, thread 0): trace[0] = count, then
+  // (code, globaltimer ns) pairs
+  long long* trace;
+  int trace_cap;
 };
 
-constexpr int SOLVER_THREADS = 256;
-
 size_t solver_smem_bytes(int m);
-int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, cudaStream_t s);
+// mode: 0 = one cluster of `cluster` CTAs per sequence; 1 = one cooperative grid over
+// every SM for a single sequence
+int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, int grid_mode,
+                  cudaStream_t s);
 int solver_pick_cluster(int device, int requested, int m_max);
+int solver_grid_blocks(int device, int m_max);
 
 }  // namespace dt

@@ -275,9 +275,12 @@ struct dt_tracker {
   cudaStream_t stream = nullptr;
   int64_t n = 0, k = 0, m = 0, ne = 0;
   int cluster = 1;
+  int grid_mode = 0;
   int launches = 0;
   bool args_dirty = false;
   bool profiling = false;
+  long long* trace = nullptr;
+  int trace_cap = 0;
   bool last_used = false;
   cudaEvent_t ev[DT_N_PHASES + 1] = {};
   std::vector<DevBuf> bufs;
@@ -315,11 +318,11 @@ struct dt_tracker {
   int *mptr = nullptr, *ment = nullptr, *mcnt = nullptr;
   // solver state
   double *warp_a = nullptr, *warp_b = nullptr, *warps_out = nullptr, *lam = nullptr, *wa = nullptr;
-  double *partial = nullptr, *cost3 = nullptr, *cost3_t = nullptr, *delta = nullptr, *oknorm = nullptr;
+  double *partial = nullptr, *csum = nullptr, *delta = nullptr, *oknorm = nullptr;
   uint8_t *cvalid = nullptr, *pr_sgn = nullptr, *fr_sgn = nullptr;
   double *cobs = nullptr, *cnrm = nullptr, *pr_r = nullptr, *pr_rs = nullptr, *pr_gn = nullptr;
   double *fr_res = nullptr, *fr_G = nullptr;
-  int* cta_counts = nullptr;
+  int* counts = nullptr;
   dt_report* report = nullptr;
   double *cost_hist = nullptr, *lam_hist = nullptr, *wa_out = nullptr;
   int32_t* stalled_hist = nullptr;
@@ -385,6 +388,11 @@ int ensure_match_capacity(dt_tracker* t, int64_t cap) {
   DT_TRY(dalloc(t, &t->fr_G, 24 * cap));
   DT_TRY(dalloc(t, &t->fr_sgn, cap));
   t->match_cap = cap;
+  {
+    const int64_t nch = (t->n + CHUNK - 1) / CHUNK + (cap + CHUNK - 1) / CHUNK +
+                        (t->ne + CHUNK - 1) / CHUNK;
+    DT_TRY(dalloc(t, &t->csum, nch));
+  }
   t->args_dirty = true;
   return DT_OK;
 }
@@ -424,17 +432,22 @@ void fill_args(dt_tracker* t) {
   a.fp = t->fp; a.fo = t->fo; a.fwt = t->fwt; a.fbidx = t->fbidx; a.fbw = t->fbw;
   a.mptr = t->mptr; a.ment = t->ment;
   a.warp_a = t->warp_a; a.warp_b = t->warp_b; a.warps_out = t->warps_out;
-  a.lam = t->lam; a.wa = t->wa; a.partial = t->partial; a.cost3 = t->cost3; a.cost3_t = t->cost3_t;
+  a.lam = t->lam; a.wa = t->wa; a.partial = t->partial; a.csum = t->csum;
+  a.nch_p = (int)((t->n + CHUNK - 1) / CHUNK);
+  a.nch_m = (int)((t->match_cap + CHUNK - 1) / CHUNK);
+  a.nch_e = (int)((t->ne + CHUNK - 1) / CHUNK);
   a.delta = t->delta; a.oknorm = t->oknorm;
   a.cvalid = t->cvalid; a.cobs = t->cobs; a.cnrm = t->cnrm;
   a.pr_r = t->pr_r; a.pr_rs = t->pr_rs; a.pr_gn = t->pr_gn; a.pr_sgn = t->pr_sgn;
   a.fr_res = t->fr_res; a.fr_G = t->fr_G; a.fr_sgn = t->fr_sgn;
-  a.cta_counts = t->cta_counts;
+  a.counts = t->counts;
   a.report = t->report;
   a.cost_hist = t->cost_hist;
   a.lam_hist = t->lam_hist;
   a.stalled_hist = t->stalled_hist;
   a.wa_out = t->wa_out;
+  a.trace = t->profiling ? t->trace : nullptr;
+  a.trace_cap = t->trace_cap;
 }
 
 int push_args(dt_tracker* t) {
@@ -444,6 +457,15 @@ int push_args(dt_tracker* t) {
                                 cudaMemcpyHostToDevice, t->stream));
   DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
   return DT_OK;
+}
+
+// cluster_size <= 0: one cooperative grid over every SM (lowest latency for one
+// sequence), falling back to the largest cluster; > 0: cluster of that size
+void pick_mode(dt_tracker* t) {
+  t->grid_mode = 0;
+  t->cluster = solver_pick_cluster(t->device, t->cfg.cluster_size > 0 ? t->cfg.cluster_size : 0,
+                                   (int)t->m);
+  if (t->cfg.cluster_size <= 0 && solver_grid_blocks(t->device, (int)t->m) > 0) t->grid_mode = 1;
 }
 
 int validate_config(const dt_config* c) {
@@ -632,7 +654,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     t->args_dirty = false;
   }
   DT_CHECK_CUDA(cudaMemsetAsync(t->stalled_hist, 0, sizeof(int32_t) * c.max_outer_iters, s));
-  DT_TRY(solver_launch(t->dev_args, 1, t->cluster, (int)t->m, s));
+  DT_TRY(solver_launch(t->dev_args, 1, t->cluster, (int)t->m, t->grid_mode, s));
   ++t->launches;
   mark(t, 5);
   // ---- output warp (tracking.py:87) ----
@@ -785,8 +807,6 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_TRY(dalloc(t, &t->lam, m));
   DT_TRY(dalloc(t, &t->wa, m));
   DT_TRY(dalloc(t, &t->partial, 27 * m));
-  DT_TRY(dalloc(t, &t->cost3, 3 * m));
-  DT_TRY(dalloc(t, &t->cost3_t, 3 * m));
   DT_TRY(dalloc(t, &t->delta, 6 * m));
   DT_TRY(dalloc(t, &t->oknorm, 4 * m));
   DT_TRY(dalloc(t, &t->cvalid, n));
@@ -796,7 +816,7 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_TRY(dalloc(t, &t->pr_rs, n));
   DT_TRY(dalloc(t, &t->pr_gn, 8 * n));
   DT_TRY(dalloc(t, &t->pr_sgn, n));
-  DT_TRY(dalloc(t, &t->cta_counts, 16));
+  DT_TRY(dalloc(t, &t->counts, 1024));
   DT_TRY(dalloc(t, &t->bad_flag, 1));
   DT_TRY(dalloc(t, &t->report, 1));
   DT_TRY(dalloc(t, &t->cost_hist, 2 * cfg->max_outer_iters));
@@ -812,7 +832,7 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_CHECK_CUDA(cudaMemcpyAsync(t->warps_out, warps, sizeof(double) * 8 * m, cudaMemcpyHostToDevice, t->stream));
   DT_REQUIRE(solver_smem_bytes((int)m) <= 227 * 1024, DT_ERR_UNSUPPORTED, "too many control points (%lld)",
              (long long)m);
-  t->cluster = solver_pick_cluster(device, cfg->cluster_size, (int)m);
+  pick_mode(t);
   DT_TRY(push_args(t));
   *out = t;
   return DT_OK;
@@ -885,7 +905,7 @@ int dt_tracker_set_config(dt_tracker* t, const dt_config* cfg) {
     DT_TRY(dalloc(t, &t->stalled_hist, cfg->max_outer_iters));
   }
   t->cfg = *cfg;
-  t->cluster = solver_pick_cluster(t->device, cfg->cluster_size, (int)t->m);
+  pick_mode(t);
   DT_TRY(push_args(t));
   return DT_OK;
 }
@@ -941,13 +961,32 @@ int dt_tracker_collect(dt_tracker* t, const dt_frame_input* in, dt_frame_output*
   return collect_outputs(t, in, out, t->last_used);
 }
 
+int dt_tracker_get_trace(dt_tracker* t, long long* buf, int cap) {
+  DT_REQUIRE(t != nullptr && buf != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!t->trace) return 0;
+  long long n = 0;
+  DT_CHECK_CUDA(cudaMemcpyAsync(&n, t->trace, sizeof(long long), cudaMemcpyDeviceToHost, t->stream));
+  DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
+  const long long cnt = std::min<long long>(n, cap);
+  if (cnt > 0)
+    DT_CHECK_CUDA(cudaMemcpyAsync(buf, t->trace + 1, sizeof(long long) * 2 * cnt,
+                                  cudaMemcpyDeviceToHost, t->stream));
+  DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
+  return (int)cnt;
+}
+
 void* dt_tracker_stream(dt_tracker* t) { return t ? (void*)t->stream : nullptr; }
 
 int dt_tracker_set_profiling(dt_tracker* t, int on) {
   DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
   if (on && !t->ev[0])
     for (auto& e : t->ev) DT_CHECK_CUDA(cudaEventCreate(&e));
+  if (on && !t->trace) {
+    t->trace_cap = 4096;
+    DT_TRY(dalloc(t, &t->trace, 1 + 2 * (size_t)t->trace_cap));
+  }
   t->profiling = on != 0;
+  DT_TRY(push_args(t));
   return DT_OK;
 }
 

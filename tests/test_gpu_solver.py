@@ -123,7 +123,7 @@ def test_cluster_size_does_not_change_bits():
     s, d, w, f = c["matches"]
     ms = dt.MatchSet(s, d, w, f)
     outs = []
-    for cs in (1, 2, 4, 8, 16):
+    for cs in (0, 1, 2, 4, 8, 16):  # 0 = cooperative grid over every SM
         SESSIONS.clear()
         out, rep = dt.solve_frame(tpl, graph, obs, ms, dt.EnergyWeights(),
                                   dt.SolverConfig(max_outer_iters=20, cluster_size=cs))

@@ -1,0 +1,98 @@
+"""Per-phase latency budget of one config-2 frame on the device.
+
+Runs a few frames with profiling on and prints (a) the pipeline stages timed with CUDA
+events between kernels and (b) the solver kernel's internal phases from its
+globaltimer trace (work time per phase = previous barrier release -> this barrier
+arrival of CTA 0; barrier = arrival -> release).
+
+    python tools/profile_phases.py [--config 2] [--frames 4] [--cluster 0]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from collections import defaultdict
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+NAMES = {0: "start", 1: "relink+linearize", 2: "data gather", 3: "rigidity+solve",
+         5: "apply step", 6: "value pass", 7: "final relink", 8: "final data",
+         9: "final rigidity", 99: "end"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--frames", type=int, default=4)
+    ap.add_argument("--cluster", type=int, default=0)
+    ap.add_argument("--json", default=None)
+    args = ap.parse_args()
+    import torch
+
+    import bench
+    from paper_2007_08576_b200._lib import FrameInput
+    from paper_2007_08576_b200._session import DeviceTracker, make_config
+    from paper_2007_08576_b200.warpfield import bind_points
+
+    wl = bench.make_workload(args.config, args.frames, seed=0)
+    cfg = wl["cfg"]
+    dcfg = make_config(wl["cam"], cfg.energy, cfg.make_solver_config(), cfg.make_preselect_config(),
+                       sampling_radius=wl["graph"].sampling_radius, cluster_size=args.cluster)
+    trk = DeviceTracker(wl["tpl"], wl["graph"], dcfg)
+    feats = wl["feats"]
+    trk.set_features(feats.descriptors, feats.points,
+                     bind_points(feats.points, wl["graph"].points, 4, wl["graph"].sampling_radius))
+    dev = torch.device("cuda")
+    trk.set_profiling(True)
+    stages = []
+    work = defaultdict(float)
+    wait = defaultdict(float)
+    for i, fr in enumerate(wl["frames"]):
+        d = torch.from_numpy(fr.depth).to(dev)
+        de = torch.from_numpy(fr.descriptors).to(dev)
+        kp = torch.from_numpy(fr.keypoints).to(dev)
+        fi = FrameInput()
+        fi.depth, fi.frame_desc, fi.frame_kp = d.data_ptr(), de.data_ptr(), kp.data_ptr()
+        fi.n_frame, fi.use_matches, fi.on_device, fi.frame_id = de.shape[0], 1, 1, i
+        trk.enqueue(fi)
+        stages.append(trk.phase_ms())
+        tr = trk.trace()
+        if i == 0:
+            continue  # first frame: cold caches
+        prev_t = tr[0, 1]
+        for code, t in tr[1:]:
+            ph, kind = divmod(int(code), 10)
+            if code == 99:
+                continue
+            if kind == 0:
+                work[ph] += (t - prev_t) / 1e3
+            else:
+                wait[ph] += (t - prev_t) / 1e3
+            prev_t = t
+    nf = len(wl["frames"]) - 1
+    st = {k: float(np.mean([s[k] for s in stages[1:]])) for k in stages[0]}
+    print("pipeline stages (ms/frame):", json.dumps({k: round(v, 4) for k, v in st.items()}))
+    print(f"{'solver phase':22s} {'work us/frame':>14s} {'barrier us/frame':>17s}")
+    tot_w = tot_b = 0.0
+    for ph in sorted(set(work) | set(wait)):
+        w, b = work[ph] / nf, wait[ph] / nf
+        tot_w += w
+        tot_b += b
+        print(f"{NAMES.get(ph, ph):22s} {w:14.1f} {b:17.1f}")
+    print(f"{'total':22s} {tot_w:14.1f} {tot_b:17.1f}")
+    if args.json:
+        Path(args.json).write_text(json.dumps({"stages_ms": st,
+                                               "solver_work_us": {NAMES.get(k, k): v / nf for k, v in work.items()},
+                                               "solver_barrier_us": {NAMES.get(k, k): v / nf for k, v in wait.items()}},
+                                              indent=1))
+    trk.close()
+
+
+if __name__ == "__main__":
+    main()
