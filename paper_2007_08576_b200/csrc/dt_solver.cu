@@ -20,7 +20,7 @@
 //   P6  points / matches / edges: cost at the tentative warps with frozen robust and
 //       rigidity weights (solver.py:333-335); accept iff strictly lower (solver.py:336)
 // Every reduction is deterministic and independent of the launch shape: normal equations
-// are per control in CSR order, costs are per fixed 256-item chunk then summed in chunk
+// are per control in CSR order, costs are per fixed 32-item chunk then summed in chunk
 // order, and every CTA evaluates the totals identically, so all CTAs take the same
 // control-flow decisions.
 
@@ -527,450 +527,7 @@ __device__ __forceinline__ double sum_fixed(const double* a, int n) {
     TRACE(10 * (phase) + 1); \
   } while (0)
 
-template <bool GRID>
-__global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverArgs* __restrict__ all) {
-  Dom<GRID> dom;
-  const int C = dom.size();
-  const int rank = dom.rank();
-  __shared__ SolverArgs A;
-  __shared__ double s_red[8];
-  __shared__ int s_cnt[NWARPS];
-  extern __shared__ double smem[];
-  if (threadIdx.x == 0) A = all[dom.seq()];
-  __syncthreads();
-  const int m = A.m;
-  const int64_t n = A.n;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* s_w = smem;
-  double* s_T = smem + 8 * m;
-  double* stage = smem + 20 * m + warp * (STAGE + GOUT);
-  double* gout = stage + STAGE;
-  const int gw = rank * NWARPS + warp, GW = C * NWARPS;
-  const int gt = rank * (int)blockDim.x + (int)threadIdx.x, GT = C * (int)blockDim.x;
-  const int64_t n_act = A.n_active ? *A.n_active : 0;
-  const int nch_p = (int)((n + CHUNK - 1) / CHUNK);
-  const int nch_m = (int)((n_act + CHUNK - 1) / CHUNK);
-  const int nch_e = (A.n_edges + CHUNK - 1) / CHUNK;
-  double* cs_p = A.csum;
-  double* cs_m = A.csum + A.nch_p;
-  double* cs_e = cs_m + A.nch_m;
-  long long* tr = A.trace;
-  int tn = 0;
-  TRACE(0);
-
-  for (int c = gt; c < m; c += GT) A.lam[c] = A.lam_init;
-
-  double* cur = A.warp_a;
-  double* tent = A.warp_b;
-  int accepted_steps = 0, rejected_steps = 0, n_hist = 0, outer_done = 0, lam_pending = -1;
-  bool converged = false, stalled = false;
-  double final_step_norm = 0.0;
-  int parity = 0;
-
-  // totals of the three chunk-sum segments, identical in every CTA
-  auto totals = [&](double& t, double* parts) {
-    __syncthreads();
-    if (warp == 0) {
-      const double a = sum_fixed(cs_p, nch_p);
-      const double b = sum_fixed(cs_m, nch_m);
-      const double e = sum_fixed(cs_e, nch_e);
-      if (lane == 0) {
-        s_red[0] = a;
-        s_red[1] = b;
-        s_red[2] = e;
-      }
-    }
-    __syncthreads();
-    t = s_red[0] + s_red[1] + s_red[2];
-    if (parts) {
-      parts[0] = s_red[0];
-      parts[1] = s_red[1];
-      parts[2] = s_red[2];
-    }
-  };
-  auto lam_history = [&](int it) {
-    if (rank == 0 && warp == 0) {
-      double lo = INFINITY, hi = -INFINITY;
-      for (int i = lane; i < m; i += 32) {
-        const double v = ld(A.lam + i);
-        lo = fmin(lo, v);
-        hi = fmax(hi, v);
-      }
-      lo = warp_min(lo);
-      hi = warp_max(hi);
-      if (lane == 0) {
-        A.lam_hist[2 * it] = lo;
-        A.lam_hist[2 * it + 1] = hi;
-      }
-    }
-  };
-
-  for (int outer = 0; outer < A.max_outer; ++outer) {
-    outer_done = outer + 1;
-    // ---- P1: relink + linearize at `cur`; icp / feature cost of the iterate ----
-    load_state(A, cur, s_w, s_T);
-    for (int ch = gw; ch < nch_p; ch += GW) {
-      double acc = 0.0;
-      int vdummy;
-      for (int i = 0; i < CHUNK / 32; ++i) {
-        const int64_t p = (int64_t)ch * CHUNK + i * 32 + lane;
-        if (p < n) acc += point_relink(A, s_w, p, true, &vdummy);
-      }
-      acc = warp_sum(acc);
-      if (lane == 0) cs_p[ch] = acc;
-    }
-    for (int ch = gw; ch < nch_m; ch += GW) {
-      double acc = 0.0;
-      for (int i = 0; i < CHUNK / 32; ++i) {
-        const int64_t j = (int64_t)ch * CHUNK + i * 32 + lane;
-        if (j < n_act) acc += match_eval(A, s_w, j, true, true);
-      }
-      acc = warp_sum(acc);
-      if (lane == 0) cs_m[ch] = acc;
-    }
-    DSYNC(1);
-    if (lam_pending >= 0) lam_history(lam_pending);
-    lam_pending = -1;
-
-    // ---- P2: data rows -> normal equations (Gram on the FP64 tensor cores) ----
-    for (int c = gw; c < m; c += GW) {
-      Basis K;
-      make_basis(s_w + 8 * c, K);
-      Gram G;
-      double sup = 0.0;
-      const int q0 = ldi(A.cptr + c), q1 = ldi(A.cptr + c + 1);
-      for (int base = q0; base < q1; base += 32) {
-        const int q = base + lane;
-        double row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (q < q1) {
-          const int e = ldi(A.cent + q);
-          const int64_t p = e >> 3;
-          const int s = e & 7;
-          if (ldu8(A.cvalid + p)) {
-            const double a = A.bw[p * A.k + s];
-            const double rs = ld(A.pr_rs + p);
-            sup += rs * rs * a;
-            const double sw = rs * sqrt(a);
-            const double sg = ((ldu8(A.pr_sgn + p) >> s) & 1u) ? -1.0 : 1.0;
-            const double coef = sw * a * sg;
-            double gn[8], pr[6];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) gn[i] = ld(A.pr_gn + 8 * p + i);
-            basis_project(gn, K.Kr, K.Kd, pr);
-#pragma unroll
-            for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
-            row[6] = sw * ld(A.pr_r + p);
-          }
-        }
-        gram_push(G, stage, row);
-      }
-      if (n_act > 0) {
-        const int m0 = ldi(A.mptr + c), m1 = ldi(A.mptr + c + 1);
-        for (int base = m0; base < m1; base += 32) {
-          const int q = base + lane;
-          const bool live = q < m1;
-          int64_t j = 0;
-          double coef = 0.0, sw = 0.0;
-          if (live) {
-            const int e = ldi(A.ment + q);
-            j = e / A.k;
-            const int s = e - (int)j * A.k;
-            const double a = A.fbw[e];
-            const double w_pair = A.fw * A.fwt[j] * a;
-            sup += w_pair;
-            sw = sqrt(w_pair);
-            const double sg = ((ldu8(A.fr_sgn + j) >> s) & 1u) ? -1.0 : 1.0;
-            coef = sw * a * sg;
-          }
-#pragma unroll 1
-          for (int comp = 0; comp < 3; ++comp) {
-            double row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            if (live) {
-              double g[8], pr[6];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) g[i] = ld(A.fr_G + 24 * j + 8 * comp + i);
-              basis_project(g, K.Kr, K.Kd, pr);
-#pragma unroll
-              for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
-              row[6] = sw * ld(A.fr_res + 3 * j + comp);
-            }
-            gram_push(G, stage, row);
-          }
-        }
-      }
-      gram_store(G, gout);
-      sup = warp_sum(sup);
-      if (lane < 27) A.partial[27 * c + lane] = gram_col(gout, lane);
-      if (lane == 27) A.wa[c] = A.arap_w * fmax(sup, A.data_floor);
-      __syncwarp();
-    }
-    DSYNC(2);
-
-    // ---- P3: rigidity rows -> normal equations + first damped solve; rigidity cost ----
-    double* okn = A.oknorm + (size_t)parity * 2 * m;
-    for (int c = gw; c < m; c += GW) {
-      Gram G;
-      const int q0 = ldi(A.iptr + c), q1 = ldi(A.iptr + c + 1);
-      for (int base = q0; base < q1; base += 32) {
-        const int q = base + lane;
-        const bool live = q < q1;
-        EdgeBin eb;
-        if (live) edge_setup(A, s_T, A.wa, ldi(A.ient + q), eb);
-        double row[8];
-#pragma unroll 1
-        for (int r = 0; r < 7; ++r) {
-          if (live) {
-            if (r == 0) length_row(A, eb, row);
-            else if (r < 3) angle_row_bin(A, eb, r - 1, row);
-            else rotation_row(A, eb, s_w, r - 3, row);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) row[i] = 0.0;
-          }
-          gram_push(G, stage, row);
-        }
-      }
-      gram_store(G, gout);
-      if (lane < 27) A.partial[27 * c + lane] = A.partial[27 * c + lane] + gram_col(gout, lane);
-      __syncwarp();
-      if (lane == 0) {
-        double part[27], d[6];
-        for (int i = 0; i < 27; ++i) part[i] = A.partial[27 * c + i];
-        const bool good = solve6(part, ld(A.lam + c), d);
-        double nn = 0.0;
-        for (int i = 0; i < 6; ++i) {
-          A.delta[6 * c + i] = d[i];
-          nn += d[i] * d[i];
-        }
-        okn[2 * c] = good ? 1.0 : 0.0;
-        okn[2 * c + 1] = sqrt(nn);
-      }
-      __syncwarp();
-    }
-    for (int ch = gw; ch < nch_e; ch += GW) {
-      double acc = 0.0;
-      for (int i = 0; i < CHUNK / 32; ++i) {
-        const int e = ch * CHUNK + i * 32 + lane;
-        if (e < A.n_edges) acc += edge_value(A, s_w, s_T, A.wa, e);
-      }
-      acc = warp_sum(acc);
-      if (lane == 0) cs_e[ch] = acc;
-    }
-    bool accepted = false;
-    double cost_before = 0.0, cost_after = 0.0;
-    for (int attempt = 0; attempt <= A.max_retries; ++attempt) {
-      if (attempt > 0) {
-        okn = A.oknorm + (size_t)parity * 2 * m;
-        for (int c = gt; c < m; c += GT) {
-          double part[27], d[6];
-          for (int i = 0; i < 27; ++i) part[i] = ld(A.partial + 27 * c + i);
-          const bool good = solve6(part, A.lam[c], d);
-          double nn = 0.0;
-          for (int i = 0; i < 6; ++i) {
-            A.delta[6 * c + i] = d[i];
-            nn += d[i] * d[i];
-          }
-          okn[2 * c] = good ? 1.0 : 0.0;
-          okn[2 * c + 1] = sqrt(nn);
-        }
-      }
-      DSYNC(attempt == 0 ? 3 : 4);
-      if (attempt == 0) totals(cost_before, nullptr);
-      // all solves ok? largest step norm (identical in every CTA)
-      __syncthreads();
-      if (warp == 0) {
-        double allok = 1.0, mx = 0.0;
-        for (int i = lane; i < m; i += 32) {
-          allok = fmin(allok, ld(okn + 2 * i));
-          mx = fmax(mx, ld(okn + 2 * i + 1));
-        }
-        allok = warp_min(allok);
-        mx = warp_max(mx);
-        if (lane == 0) {
-          s_red[4] = allok;
-          s_red[5] = mx;
-        }
-      }
-      __syncthreads();
-      const bool all_ok = s_red[4] > 0.5;
-      const double step_norm = s_red[5];
-      parity ^= 1;
-      if (!all_ok) {
-        // raise the damping of the failed controls only, retry (solver.py:321-326)
-        for (int c = gt; c < m; c += GT)
-          if (ld(okn + 2 * c) < 0.5) A.lam[c] = fmin(ld(A.lam + c) * A.lam_inc, A.lam_max);
-        ++rejected_steps;
-        continue;
-      }
-      final_step_norm = step_norm;
-      if (step_norm < A.step_tol) {  // checked before the step (solver.py:327-331)
-        converged = true;
-        break;
-      }
-      // ---- P5: tentative warps ----
-      for (int c = gt; c < m; c += GT) {
-        double W[8], d[6], o[8];
-        for (int i = 0; i < 8; ++i) W[i] = ld(cur + 8 * c + i);
-        for (int i = 0; i < 6; ++i) d[i] = ld(A.delta + 6 * c + i);
-        apply_step_one(W, d, o);
-        for (int i = 0; i < 8; ++i) tent[8 * c + i] = o[i];
-      }
-      DSYNC(5);
-      // ---- P6: cost at the tentative warps, frozen weights and correspondences ----
-      load_state(A, tent, s_w, s_T);
-      for (int ch = gw; ch < nch_p; ch += GW) {
-        double acc = 0.0;
-        for (int i = 0; i < CHUNK / 32; ++i) {
-          const int64_t p = (int64_t)ch * CHUNK + i * 32 + lane;
-          if (p < n) acc += point_value(A, s_w, p);
-        }
-        acc = warp_sum(acc);
-        if (lane == 0) cs_p[ch] = acc;
-      }
-      for (int ch = gw; ch < nch_m; ch += GW) {
-        double acc = 0.0;
-        for (int i = 0; i < CHUNK / 32; ++i) {
-          const int64_t j = (int64_t)ch * CHUNK + i * 32 + lane;
-          if (j < n_act) acc += match_eval(A, s_w, j, false, false);
-        }
-        acc = warp_sum(acc);
-        if (lane == 0) cs_m[ch] = acc;
-      }
-      for (int ch = gw; ch < nch_e; ch += GW) {
-        double acc = 0.0;
-        for (int i = 0; i < CHUNK / 32; ++i) {
-          const int e = ch * CHUNK + i * 32 + lane;
-          if (e < A.n_edges) acc += edge_value(A, s_w, s_T, A.wa, e);
-        }
-        acc = warp_sum(acc);
-        if (lane == 0) cs_e[ch] = acc;
-      }
-      DSYNC(6);
-      totals(cost_after, nullptr);
-      if (cost_after < cost_before) {
-        double* tmp = cur;
-        cur = tent;
-        tent = tmp;
-        for (int c = gt; c < m; c += GT) A.lam[c] = fmax(ld(A.lam + c) * A.lam_dec, A.lam_min);
-        ++accepted_steps;
-        if (rank == 0 && threadIdx.x == 0) {
-          A.cost_hist[2 * n_hist] = cost_before;
-          A.cost_hist[2 * n_hist + 1] = cost_after;
-        }
-        ++n_hist;
-        accepted = true;
-        break;
-      }
-      for (int c = gt; c < m; c += GT) A.lam[c] = fmin(ld(A.lam + c) * A.lam_inc, A.lam_max);
-      ++rejected_steps;
-    }
-    lam_pending = outer;
-    if (converged) break;
-    if (!accepted) {
-      stalled = true;
-      if (rank == 0 && threadIdx.x == 0) A.stalled_hist[outer] = 1;
-      continue;
-    }
-    if (cost_before - cost_after <= A.cost_tol * fmax(cost_before, 1e-30)) {
-      converged = true;
-      break;
-    }
-  }
-
-  // ---- final report: relink at the solution, recompute robust and rigidity weights
-  // (solver.py:360-376) ----
-  load_state(A, cur, s_w, s_T);
-  int my_valid = 0;
-  for (int ch = gw; ch < nch_p; ch += GW) {
-    double acc = 0.0;
-    for (int i = 0; i < CHUNK / 32; ++i) {
-      const int64_t p = (int64_t)ch * CHUNK + i * 32 + lane;
-      int v = 0;
-      if (p < n) acc += point_relink(A, s_w, p, false, &v);
-      my_valid += v;
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) cs_p[ch] = acc;
-  }
-  for (int ch = gw; ch < nch_m; ch += GW) {
-    double acc = 0.0;
-    for (int i = 0; i < CHUNK / 32; ++i) {
-      const int64_t j = (int64_t)ch * CHUNK + i * 32 + lane;
-      if (j < n_act) acc += match_eval(A, s_w, j, true, false);
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) cs_m[ch] = acc;
-  }
-  for (int o = 16; o > 0; o >>= 1) my_valid += __shfl_xor_sync(0xffffffffu, my_valid, o);
-  if (lane == 0) s_cnt[warp] = my_valid;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < NWARPS; ++w) t += s_cnt[w];
-    A.counts[rank] = t;
-  }
-  for (int c = gt; c < m; c += GT)
-    for (int i = 0; i < 8; ++i) A.warps_out[8 * c + i] = s_w[8 * c + i];
-  DSYNC(7);
-  if (lam_pending >= 0) lam_history(lam_pending);
-  // support per control with the recomputed robust weights -> wa
-  for (int c = gw; c < m; c += GW) {
-    double sup = 0.0;
-    const int q0 = ldi(A.cptr + c), q1 = ldi(A.cptr + c + 1);
-    for (int q = q0 + lane; q < q1; q += 32) {
-      const int e = ldi(A.cent + q);
-      const int64_t p = e >> 3;
-      if (!ldu8(A.cvalid + p)) continue;
-      const double rs = ld(A.pr_rs + p);
-      sup += rs * rs * A.bw[p * A.k + (e & 7)];
-    }
-    if (n_act > 0) {
-      const int m0 = ldi(A.mptr + c), m1 = ldi(A.mptr + c + 1);
-      for (int q = m0 + lane; q < m1; q += 32) {
-        const int e = ldi(A.ment + q);
-        sup += A.fw * A.fwt[e / A.k] * A.fbw[e];
-      }
-    }
-    sup = warp_sum(sup);
-    if (lane == 0) {
-      const double w = A.arap_w * fmax(sup, A.data_floor);
-      A.wa[c] = w;
-      A.wa_out[c] = w;
-    }
-  }
-  DSYNC(8);
-  for (int ch = gw; ch < nch_e; ch += GW) {
-    double acc = 0.0;
-    for (int i = 0; i < CHUNK / 32; ++i) {
-      const int e = ch * CHUNK + i * 32 + lane;
-      if (e < A.n_edges) acc += edge_value(A, s_w, s_T, A.wa, e);
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) cs_e[ch] = acc;
-  }
-  DSYNC(9);
-  double tot = 0.0, parts[3];
-  totals(tot, parts);
-  if (rank == 0 && threadIdx.x == 0) {
-    dt_report* R = A.report;
-    R->icp_cost = parts[0];
-    R->feature_cost = parts[1];
-    R->arap_cost = parts[2];
-    R->total_cost = tot;
-    int nc = 0;
-    for (int i = 0; i < C; ++i) nc += __ldcg(A.counts + i);
-    R->n_correspondences = nc;
-    R->outer_iterations = outer_done;
-    R->accepted_steps = accepted_steps;
-    R->rejected_steps = rejected_steps;
-    R->stalled = stalled ? 1 : 0;
-    R->converged = converged ? 1 : 0;
-    R->final_step_norm = final_step_norm;
-    R->n_cost_history = n_hist;
-  }
-  TRACE(99);
-  if (tr && rank == 0 && threadIdx.x == 0) tr[0] = tn;
-}
+#include "dt_solver_kernel.cuh"
 
 template __global__ void k_solve_frame<false>(const SolverArgs* __restrict__);
 template __global__ void k_solve_frame<true>(const SolverArgs* __restrict__);

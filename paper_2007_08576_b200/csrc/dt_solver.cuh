@@ -11,7 +11,7 @@
 namespace dt {
 
 constexpr int SOLVER_THREADS = 512;
-constexpr int CHUNK = 256;  // items per deterministic partial sum of the value passes
+constexpr int CHUNK = 32;  // items per deterministic partial sum (one per lane)
 
 struct SolverArgs {
   // sizes
