@@ -288,6 +288,49 @@ __device__ __forceinline__ double angle_row(double ax, double ay, double az, dou
   return wv;
 }
 
+// Unit-weight bending-angle row of one direction with BOTH bins' Jacobians
+// (kernels.py:287-338 with sw = 1): Ja for the rotating side a, Jb for side b; returns
+// the angle value. angle_row(...) with weight sw equals sw * (these rows, this value).
+__device__ __forceinline__ double angle_unit(double ax, double ay, double az, double bx, double by,
+                                             double bz, double patx, double paty, double patz,
+                                             double pbtx, double pbty, double pbtz, double Ja[6],
+                                             double Jb[6]) {
+  const double na = sqrt(ax * ax + ay * ay + az * az);
+  const double nb = sqrt(bx * bx + by * by + bz * bz);
+  const bool ok = na > ANGLE_MIN_NORM && nb > ANGLE_MIN_NORM;
+  const double na_s = ok ? na : 1.0;
+  const double nb_s = ok ? nb : 1.0;
+  const double ahx = ax / na_s, ahy = ay / na_s, ahz = az / na_s;
+  const double bhx = bx / nb_s, bhy = by / nb_s, bhz = bz / nb_s;
+  double cth = ahx * bhx + ahy * bhy + ahz * bhz;
+  if (cth > 1.0) cth = 1.0;
+  else if (cth < -1.0) cth = -1.0;
+  const bool near_zero = (1.0 - cth) < ANGLE_COLLINEAR_EPS;
+  const bool near_pi = (1.0 + cth) < ANGLE_COLLINEAR_EPS;
+  const double val = (ok && !near_zero) ? acos(cth) : 0.0;
+  const bool grad_ok = ok && !near_zero && !near_pi;
+  const double inv_sin = grad_ok ? -1.0 / sqrt(fmax(1.0 - cth * cth, 1e-300)) : 0.0;
+  const double gax = inv_sin * (bhx - cth * ahx) / na_s;
+  const double gay = inv_sin * (bhy - cth * ahy) / na_s;
+  const double gaz = inv_sin * (bhz - cth * ahz) / na_s;
+  const double gbx = inv_sin * (ahx - cth * bhx) / nb_s;
+  const double gby = inv_sin * (ahy - cth * bhy) / nb_s;
+  const double gbz = inv_sin * (ahz - cth * bhz) / nb_s;
+  Ja[0] = (ay * gaz - az * gay) - (paty * gbz - patz * gby);
+  Ja[1] = (az * gax - ax * gaz) - (patz * gbx - patx * gbz);
+  Ja[2] = (ax * gay - ay * gax) - (patx * gby - paty * gbx);
+  Ja[3] = -gbx;
+  Ja[4] = -gby;
+  Ja[5] = -gbz;
+  Jb[0] = pbty * gbz - pbtz * gby;
+  Jb[1] = pbtz * gbx - pbtx * gbz;
+  Jb[2] = pbtx * gby - pbty * gbx;
+  Jb[3] = gbx;
+  Jb[4] = gby;
+  Jb[5] = gbz;
+  return val;
+}
+
 // Four quaternion-component rotation rows sharing one bin, rotation columns only
 // (kernels.py:470-480).
 __device__ __forceinline__ void fold_quad(double* acc, const double J4[12], double d0, double d1,

@@ -341,99 +341,86 @@ __device__ __forceinline__ double edge_value(const SolverArgs& A, const double* 
 }
 
 // ---------------------------------------------------------------------------------
-// rigidity rows of one (edge, bin) for the Gram accumulation (kernels.py:341-467)
+// rigidity rows, evaluated once per connection (kernels.py:341-467)
 // ---------------------------------------------------------------------------------
+// The rigidity weight of a connection only scales its rows (sqrt(0.5 base w_term)), so
+// the unit-weight rows of BOTH endpoint bins are evaluated once per edge in P2 -- in
+// parallel with the data gather, before the weights wa exist -- and P3 gathers them.
+// Layout per edge (ER doubles):
+//   [0,6) length J bin 0, [6,12) length J bin 1, [12] length value,
+//   [13,19) angle 0->1 J of bin 0 (side a), [19,25) of bin 1 (side b), [25] angle 0->1,
+//   [26,32) angle 1->0 J of bin 1 (side a), [32,38) of bin 0 (side b), [38] angle 1->0.
+// The rotation rows need only the two quaternions and are rebuilt from smem.
 
-struct EdgeBin {
+constexpr int ER = 40;
+
+__device__ __forceinline__ void edge_unit_rows(const SolverArgs& A, const double* s_T, int e,
+                                               double* out) {
+  const int i0 = A.edges[2 * e], i1 = A.edges[2 * e + 1];
+  const double* p0 = A.cpts + 3 * i0;
+  const double* p1 = A.cpts + 3 * i1;
+  const double* T0 = s_T + 12 * i0;
+  const double* T1 = s_T + 12 * i1;
   double p0t[3], p1t[3], c01[3], c10[3];
-  double base;
-  int i0, i1, side;
-};
-
-__device__ __forceinline__ void edge_setup(const SolverArgs& A, const double* s_T, const double* wa,
-                                           int e2, EdgeBin& eb) {
-  const int e = e2 >> 1;
-  eb.side = e2 & 1;
-  eb.i0 = A.edges[2 * e];
-  eb.i1 = A.edges[2 * e + 1];
-  const double* p0 = A.cpts + 3 * eb.i0;
-  const double* p1 = A.cpts + 3 * eb.i1;
-  const double* T0 = s_T + 12 * eb.i0;
-  const double* T1 = s_T + 12 * eb.i1;
-  eb.base = A.ew[e] * 0.5 * (ld(wa + eb.i0) + ld(wa + eb.i1));
-  xform(T0, T0 + 9, p0[0], p0[1], p0[2], eb.p0t);
-  xform(T1, T1 + 9, p1[0], p1[1], p1[2], eb.p1t);
-  xform(T0, T0 + 9, p1[0], p1[1], p1[2], eb.c01);
-  xform(T1, T1 + 9, p0[0], p0[1], p0[2], eb.c10);
-}
-
-__device__ __forceinline__ void length_row(const SolverArgs& A, const EdgeBin& eb, double row[8]) {
-  const double* p0 = A.cpts + 3 * eb.i0;
-  const double* p1 = A.cpts + 3 * eb.i1;
+  xform(T0, T0 + 9, p0[0], p0[1], p0[2], p0t);
+  xform(T1, T1 + 9, p1[0], p1[1], p1[2], p1t);
+  xform(T0, T0 + 9, p1[0], p1[1], p1[2], c01);
+  xform(T1, T1 + 9, p0[0], p0[1], p0[2], c10);
+  // length (kernels.py:366-398)
   const double rx = p1[0] - p0[0], ry = p1[1] - p0[1], rz = p1[2] - p0[2];
   const double rest = sqrt(rx * rx + ry * ry + rz * rz);
-  const double bx = eb.p1t[0] - eb.p0t[0], by = eb.p1t[1] - eb.p0t[1], bz = eb.p1t[2] - eb.p0t[2];
+  const double bx = p1t[0] - p0t[0], by = p1t[1] - p0t[1], bz = p1t[2] - p0t[2];
   const double ln = sqrt(bx * bx + by * by + bz * bz);
-  const double sw = sqrt(0.5 * eb.base);
   double bhx = 0.0, bhy = 0.0, bhz = 0.0;
   if (ln > 1e-9) {
-    const double il = 1.0 / ln;
-    bhx = bx * il;
-    bhy = by * il;
-    bhz = bz * il;
+    bhx = bx / ln;
+    bhy = by / ln;
+    bhz = bz / ln;
   }
-  if (eb.side == 0) {
-    row[0] = sw * (eb.p0t[1] * (-bhz) - eb.p0t[2] * (-bhy));
-    row[1] = sw * (eb.p0t[2] * (-bhx) - eb.p0t[0] * (-bhz));
-    row[2] = sw * (eb.p0t[0] * (-bhy) - eb.p0t[1] * (-bhx));
-    row[3] = sw * (-bhx);
-    row[4] = sw * (-bhy);
-    row[5] = sw * (-bhz);
-  } else {
-    row[0] = sw * (eb.p1t[1] * bhz - eb.p1t[2] * bhy);
-    row[1] = sw * (eb.p1t[2] * bhx - eb.p1t[0] * bhz);
-    row[2] = sw * (eb.p1t[0] * bhy - eb.p1t[1] * bhx);
-    row[3] = sw * bhx;
-    row[4] = sw * bhy;
-    row[5] = sw * bhz;
-  }
-  row[6] = sw * (ln - rest);
-  row[7] = 0.0;
-}
-
-// angle row of direction dir (0: 0->1, 1: 1->0) for this bin
-__device__ __forceinline__ void angle_row_bin(const SolverArgs& A, const EdgeBin& eb, int dir,
-                                              double row[8]) {
-  const double sw = sqrt(0.5 * eb.base * A.angle_w);
-  double J[6];
-  double wv;
-  if (dir == 0)
-    wv = angle_row(eb.c01[0] - eb.p0t[0], eb.c01[1] - eb.p0t[1], eb.c01[2] - eb.p0t[2],
-                   eb.p1t[0] - eb.p0t[0], eb.p1t[1] - eb.p0t[1], eb.p1t[2] - eb.p0t[2], eb.p0t[0],
-                   eb.p0t[1], eb.p0t[2], eb.p1t[0], eb.p1t[1], eb.p1t[2], sw,
-                   eb.side == 0 ? 0 : 1, true, J);
-  else
-    wv = angle_row(eb.c10[0] - eb.p1t[0], eb.c10[1] - eb.p1t[1], eb.c10[2] - eb.p1t[2],
-                   eb.p0t[0] - eb.p1t[0], eb.p0t[1] - eb.p1t[1], eb.p0t[2] - eb.p1t[2], eb.p1t[0],
-                   eb.p1t[1], eb.p1t[2], eb.p0t[0], eb.p0t[1], eb.p0t[2], sw,
-                   eb.side == 0 ? 1 : 0, true, J);
+  out[0] = p0t[1] * (-bhz) - p0t[2] * (-bhy);
+  out[1] = p0t[2] * (-bhx) - p0t[0] * (-bhz);
+  out[2] = p0t[0] * (-bhy) - p0t[1] * (-bhx);
+  out[3] = -bhx;
+  out[4] = -bhy;
+  out[5] = -bhz;
+  out[6] = p1t[1] * bhz - p1t[2] * bhy;
+  out[7] = p1t[2] * bhx - p1t[0] * bhz;
+  out[8] = p1t[0] * bhy - p1t[1] * bhx;
+  out[9] = bhx;
+  out[10] = bhy;
+  out[11] = bhz;
+  out[12] = ln - rest;
+  // bending angle, both directions (kernels.py:400-417)
+  double Ja[6], Jb[6];
+  out[25] = angle_unit(c01[0] - p0t[0], c01[1] - p0t[1], c01[2] - p0t[2], p1t[0] - p0t[0],
+                       p1t[1] - p0t[1], p1t[2] - p0t[2], p0t[0], p0t[1], p0t[2], p1t[0], p1t[1],
+                       p1t[2], Ja, Jb);
 #pragma unroll
-  for (int i = 0; i < 6; ++i) row[i] = J[i];
-  row[6] = wv;
-  row[7] = 0.0;
+  for (int i = 0; i < 6; ++i) {
+    out[13 + i] = Ja[i];
+    out[19 + i] = Jb[i];
+  }
+  out[38] = angle_unit(c10[0] - p1t[0], c10[1] - p1t[1], c10[2] - p1t[2], p0t[0] - p1t[0],
+                       p0t[1] - p1t[1], p0t[2] - p1t[2], p1t[0], p1t[1], p1t[2], p0t[0], p0t[1],
+                       p0t[2], Ja, Jb);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    out[26 + i] = Ja[i];
+    out[32 + i] = Jb[i];
+  }
 }
 
-// rotation row r (0..3) for this bin: sw_r * (J4[r] | 0 0 0 | d_r) (kernels.py:419-461)
-__device__ __forceinline__ void rotation_row(const SolverArgs& A, const EdgeBin& eb,
-                                             const double* s_w, int r, double row[8]) {
-  const double sw = sqrt(0.5 * eb.base * A.rot_w);
-  const double* q0 = s_w + 8 * eb.i0;
-  const double* q1 = s_w + 8 * eb.i1;
+// rotation row r (0..3) of the bin `side` of edge (i0, i1) with weight sw: the 0.5 left
+// product of the bin's quaternion, rotation columns only (kernels.py:419-461)
+__device__ __forceinline__ void rotation_row(const double* s_w, int i0, int i1, int side, double sw,
+                                             int r, double row[8]) {
+  const double* q0 = s_w + 8 * i0;
+  const double* q1 = s_w + 8 * i1;
   const double dq = q0[0] * q1[0] + q0[1] * q1[1] + q0[2] * q1[2] + q0[3] * q1[3];
   const double sg = dq < 0.0 ? -1.0 : 1.0;
   const double d = q0[r] - sg * q1[r];
   double P[12];
-  if (eb.side == 0) {
+  if (side == 0) {
     half_left_mul(q0[0], q0[1], q0[2], q0[3], P);
   } else {
     const double h = -sg * 0.5;
@@ -450,6 +437,32 @@ __device__ __forceinline__ void rotation_row(const SolverArgs& A, const EdgeBin&
   row[7] = 0.0;
 }
 
+// rigidity cost of one connection at the iterate from its stored values: 2 x the bin
+// cost, accumulated in arap_edge_bin's order (length, angle 0->1, angle 1->0, rotation)
+__device__ __forceinline__ double edge_cost_rows(const SolverArgs& A, const double* s_w,
+                                                 const double* wa, const double* er, int e) {
+  const int i0 = A.edges[2 * e], i1 = A.edges[2 * e + 1];
+  const double base = A.ew[e] * 0.5 * (ld(wa + i0) + ld(wa + i1));
+  const double sw = sqrt(0.5 * base);
+  const double swa = sqrt(0.5 * base * A.angle_w);
+  const double swr = sqrt(0.5 * base * A.rot_w);
+  const double wl = sw * ld(er + 12);
+  const double w01 = swa * ld(er + 25);
+  const double w10 = swa * ld(er + 38);
+  const double* q0 = s_w + 8 * i0;
+  const double* q1 = s_w + 8 * i1;
+  const double dq = q0[0] * q1[0] + q0[1] * q1[1] + q0[2] * q1[2] + q0[3] * q1[3];
+  const double sg = dq < 0.0 ? -1.0 : 1.0;
+  const double d0 = q0[0] - sg * q1[0], d1 = q0[1] - sg * q1[1], d2 = q0[2] - sg * q1[2],
+               d3 = q0[3] - sg * q1[3];
+  double c = wl * wl;
+  c += w01 * w01;
+  c += w10 * w10;
+  c += swr * swr * (d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3);
+  return 2.0 * c;
+}
+
+// ---------------------------------------------------------------------------------
 // Cholesky of the damped 6x6 system on a packed lower triangle (solver.py:217-258):
 // M = A + lam diag(max(diag A, 1e-12)); forward / backward substitution in the
 // reference's order. false (delta = 0) on a non-positive pivot.

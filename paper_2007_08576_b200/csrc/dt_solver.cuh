@@ -56,6 +56,7 @@ struct SolverArgs {
   double* wa;
   double* partial;   // m x 27 normal-equation columns
   double* csum;      // nch_p + nch_m + nch_e deterministic chunk sums
+  double* erows;     // n_edges x 40 unit rigidity rows of both bins
   double* delta;     // m x 6
   double* oknorm;    // 2 parities x m x 2 (ok, step norm)
   uint8_t* cvalid;   // per template point: correspondence valid

@@ -69,9 +69,12 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   double* s_T = smem + 8 * m;
   double* stage = smem + 20 * m + warp * (STAGE + GOUT);
   double* gout = stage + STAGE;
-  const int gw = rank * NWARPS + warp, GW = C * NWARPS;
+  // work items are dealt round-robin over the CTAs first (item i -> CTA i % C), so
+  // every SM of the domain gets a share of each phase
+  const int gw = warp * C + rank, GW = C * NWARPS;
+  const int gw_rev = (NWARPS - 1 - warp) * C + rank;
   const int gt = rank * (int)blockDim.x + (int)threadIdx.x, GT = C * (int)blockDim.x;
-  const int gteam = rank * TEAMS_PER_CTA + team, GTEAM = C * TEAMS_PER_CTA;
+  const int gteam = team * C + rank, GTEAM = C * TEAMS_PER_CTA;
   const int team_rounds = (m + GTEAM - 1) / GTEAM;
   const int64_t n_act = A.n_active ? *A.n_active : 0;
   const int nch_p = (int)((n + CHUNK - 1) / CHUNK);
@@ -102,6 +105,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     outer_done = outer + 1;
     // ---- P1: relink + linearize at `cur`; icp / feature cost of the iterate ----
     load_state(A, cur, s_w, s_T);
+    TRACE(12);
     for (int ch = gw; ch < nch_p + nch_m; ch += GW) {
       double acc = 0.0;
       if (ch < nch_p) {
@@ -119,7 +123,14 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     }
     DSYNC(1);
 
-    // ---- P2: data rows -> normal equations (Gram on the FP64 tensor cores) ----
+    // ---- P2: unit rigidity rows of every connection (no wa needed), on the warps at
+    // the end of the domain; data rows -> normal equations (Gram on the FP64 tensor
+    // cores) on the teams ----
+    for (int ch = gw_rev; ch < nch_e; ch += GW) {
+      const int e = ch * CHUNK + lane;
+      if (e < A.n_edges) edge_unit_rows(A, s_T, e, A.erows + (size_t)ER * e);
+    }
+    TRACE(22);
     for (int r = 0; r < team_rounds; ++r) {
       const int c = r * GTEAM + gteam;
       Gram G;
@@ -219,15 +230,42 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         for (int base = q0 + 32 * tw; base < q1; base += 32 * TEAM) {
           const int q = base + lane;
           const bool live = q < q1;
-          EdgeBin eb;
-          if (live) edge_setup(A, s_T, A.wa, ldi(A.ient + q), eb);
+          int i0 = 0, i1 = 0, side = 0;
+          double sw = 0.0, swa = 0.0, swr = 0.0;
+          const double* er = A.erows;
+          if (live) {
+            const int e2 = ldi(A.ient + q);
+            const int e = e2 >> 1;
+            side = e2 & 1;
+            i0 = A.edges[2 * e];
+            i1 = A.edges[2 * e + 1];
+            const double base_w = A.ew[e] * 0.5 * (ld(A.wa + i0) + ld(A.wa + i1));
+            sw = sqrt(0.5 * base_w);
+            swa = sqrt(0.5 * base_w * A.angle_w);
+            swr = sqrt(0.5 * base_w * A.rot_w);
+            er = A.erows + (size_t)ER * e;
+          }
           double row[8];
+          // length row of this bin
+#pragma unroll
+          for (int i = 0; i < 6; ++i) row[i] = live ? sw * ld(er + 6 * side + i) : 0.0;
+          row[6] = live ? sw * ld(er + 12) : 0.0;
+          row[7] = 0.0;
+          gram_push(G, stage, row);
+          // angle 0->1: bin 0 is side a ([13,19)), bin 1 side b ([19,25))
+#pragma unroll
+          for (int i = 0; i < 6; ++i) row[i] = live ? swa * ld(er + 13 + 6 * side + i) : 0.0;
+          row[6] = live ? swa * ld(er + 25) : 0.0;
+          gram_push(G, stage, row);
+          // angle 1->0: bin 1 is side a ([26,32)), bin 0 side b ([32,38))
+#pragma unroll
+          for (int i = 0; i < 6; ++i) row[i] = live ? swa * ld(er + 32 - 6 * side + i) : 0.0;
+          row[6] = live ? swa * ld(er + 38) : 0.0;
+          gram_push(G, stage, row);
 #pragma unroll 1
-          for (int rr = 0; rr < 7; ++rr) {
+          for (int rr = 0; rr < 4; ++rr) {
             if (live) {
-              if (rr == 0) length_row(A, eb, row);
-              else if (rr < 3) angle_row_bin(A, eb, rr - 1, row);
-              else rotation_row(A, eb, s_w, rr - 3, row);
+              rotation_row(s_w, i0, i1, side, swr, rr, row);
             } else {
 #pragma unroll
               for (int i = 0; i < 8; ++i) row[i] = 0.0;
@@ -237,6 +275,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         }
       }
       gram_store(G, gout);
+      TRACE(32);
       __syncthreads();
       if (tw == 0 && c < m) {
         if (lane < 27) {
@@ -260,11 +299,12 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         }
       }
       __syncthreads();
+      TRACE(34);
     }
-    for (int ch = gw; ch < nch_e; ch += GW) {
+    for (int ch = gw_rev; ch < nch_e; ch += GW) {
       double acc = 0.0;
       const int e = ch * CHUNK + lane;
-      if (e < A.n_edges) acc = edge_value(A, s_w, s_T, A.wa, e);
+      if (e < A.n_edges) acc = edge_cost_rows(A, s_w, A.wa, A.erows + (size_t)ER * e, e);
       acc = warp_sum(acc);
       if (lane == 0) cs_e[ch] = acc;
     }
@@ -287,11 +327,21 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         }
       }
       DSYNC(attempt == 0 ? 3 : 4);
+      // prefetch this thread's step inputs (one control per thread when m <= 512)
+      double pW[8], pD[6];
+      const int pc = threadIdx.x;
+      if (pc < m) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pW[i] = ld(cur + 8 * pc + i);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) pD[i] = ld(A.delta + 6 * pc + i);
+      }
       if (attempt == 0) {
         double t3[3];
         block_totals(cs_p, nch_p, cs_m, nch_m, cs_e, nch_e, s_part, t3);
         cost_before = t3[0] + t3[1] + t3[2];
       }
+      TRACE(53);
       // all solves ok? largest step norm (identical in every CTA)
       {
         double allok = 1.0, mx = 0.0;
@@ -328,20 +378,24 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
           break;
         }
       }
+      TRACE(54);
       // ---- tentative warps, applied redundantly by every CTA (no barrier) ----
       __syncthreads();
-      for (int c = threadIdx.x; c < m; c += blockDim.x) {
+      if (pc < m) apply_step_one(pW, pD, s_w + 8 * pc);
+      for (int c = threadIdx.x + blockDim.x; c < m; c += blockDim.x) {
         double W[8], d[6];
         for (int i = 0; i < 8; ++i) W[i] = ld(cur + 8 * c + i);
         for (int i = 0; i < 6; ++i) d[i] = ld(A.delta + 6 * c + i);
         apply_step_one(W, d, s_w + 8 * c);
       }
       __syncthreads();
+      TRACE(55);
       for (int c = threadIdx.x; c < m; c += blockDim.x)
         dq_to_transform(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
       for (int c = gt; c < m; c += GT)
         for (int i = 0; i < 8; ++i) tent[8 * c + i] = s_w[8 * c + i];
       __syncthreads();
+      TRACE(52);
       // ---- P6: cost at the tentative warps, frozen weights and correspondences ----
       for (int ch = gw; ch < nch_p + nch_m + nch_e; ch += GW) {
         double acc = 0.0;
@@ -387,10 +441,19 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     }
     // lambda_history (solver.py:345): min / max of the final per-control damping of this
     // outer iteration, folded by the owners with order-independent integer atomics
-    for (int c = gt; c < m; c += GT) {
-      const unsigned long long b = dbits(A.lam[c]);
-      atomicMin(lam_hist + 2 * outer, b);
-      atomicMax(lam_hist + 2 * outer + 1, b);
+    for (int c0 = gt - lane; c0 < m; c0 += GT) {
+      const int c = c0 + lane;
+      unsigned long long lo = ~0ull, hi = 0ull;
+      if (c < m) lo = hi = dbits(A.lam[c]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      if (lane == 0) {
+        atomicMin(lam_hist + 2 * outer, lo);
+        atomicMax(lam_hist + 2 * outer + 1, hi);
+      }
     }
     if (converged) break;
     if (!accepted) {

@@ -318,7 +318,7 @@ struct dt_tracker {
   int *mptr = nullptr, *ment = nullptr, *mcnt = nullptr;
   // solver state
   double *warp_a = nullptr, *warp_b = nullptr, *warps_out = nullptr, *lam = nullptr, *wa = nullptr;
-  double *partial = nullptr, *csum = nullptr, *delta = nullptr, *oknorm = nullptr;
+  double *partial = nullptr, *csum = nullptr, *erows = nullptr, *delta = nullptr, *oknorm = nullptr;
   uint8_t *cvalid = nullptr, *pr_sgn = nullptr, *fr_sgn = nullptr;
   double *cobs = nullptr, *cnrm = nullptr, *pr_r = nullptr, *pr_rs = nullptr, *pr_gn = nullptr;
   double *fr_res = nullptr, *fr_G = nullptr;
@@ -432,7 +432,7 @@ void fill_args(dt_tracker* t) {
   a.fp = t->fp; a.fo = t->fo; a.fwt = t->fwt; a.fbidx = t->fbidx; a.fbw = t->fbw;
   a.mptr = t->mptr; a.ment = t->ment;
   a.warp_a = t->warp_a; a.warp_b = t->warp_b; a.warps_out = t->warps_out;
-  a.lam = t->lam; a.wa = t->wa; a.partial = t->partial; a.csum = t->csum;
+  a.lam = t->lam; a.wa = t->wa; a.partial = t->partial; a.csum = t->csum; a.erows = t->erows;
   a.nch_p = (int)((t->n + CHUNK - 1) / CHUNK);
   a.nch_m = (int)((t->match_cap + CHUNK - 1) / CHUNK);
   a.nch_e = (int)((t->ne + CHUNK - 1) / CHUNK);
@@ -817,6 +817,7 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_TRY(dalloc(t, &t->pr_gn, 8 * n));
   DT_TRY(dalloc(t, &t->pr_sgn, n));
   DT_TRY(dalloc(t, &t->counts, 1024));
+  DT_TRY(dalloc(t, &t->erows, 40 * (n_edges > 0 ? n_edges : 1)));
   DT_TRY(dalloc(t, &t->bad_flag, 1));
   DT_TRY(dalloc(t, &t->report, 1));
   DT_TRY(dalloc(t, &t->cost_hist, 2 * cfg->max_outer_iters));

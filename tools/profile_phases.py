@@ -21,9 +21,12 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-NAMES = {0: "start", 1: "relink+linearize", 2: "data gather", 3: "rigidity+solve",
-         5: "apply step", 6: "value pass", 7: "final relink", 8: "final data",
-         9: "final rigidity", 99: "end"}
+NAMES = {0: "start", 1: "relink+linearize", 1.2: "  load warps+transforms",
+         2: "data gather", 3: "rigidity: edge costs", 3.2: "  rigidity gather",
+         3.4: "  team combine+solve", 5: "apply step", 5.2: "  transforms+tent store",
+         5.3: "  cost_before totals", 5.4: "  ok/step-norm reduce", 5.5: "  apply_step x m",
+         2.2: "  edge unit rows",
+         6: "value pass", 7: "final relink", 8: "final data", 9: "final rigidity", 99: "end"}
 
 
 def main():
@@ -70,10 +73,12 @@ def main():
             ph, kind = divmod(int(code), 10)
             if code == 99:
                 continue
-            if kind == 0:
-                work[ph] += (t - prev_t) / 1e3
-            else:
+            if kind == 1:
                 wait[ph] += (t - prev_t) / 1e3
+            else:
+                # sub-phase stamps (kind 2, 4) split the work of phase ph
+                key = ph if kind == 0 else ph + kind / 10.0
+                work[key] += (t - prev_t) / 1e3
             prev_t = t
     nf = len(wl["frames"]) - 1
     st = {k: float(np.mean([s[k] for s in stages[1:]])) for k in stages[0]}
