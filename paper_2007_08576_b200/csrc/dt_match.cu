@@ -191,65 +191,189 @@ __device__ __forceinline__ double reweight(double d, double H) {
   return d > H ? H / fmax(d, 1e-300) : 1.0;
 }
 
-__global__ void k_preselect_refs(const double* __restrict__ src, const double* __restrict__ dst,
-                                 const int64_t* __restrict__ n_dev, int64_t n_fixed,
-                                 const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive,
-                                 double H, int iters, double min_support,
-                                 double* __restrict__ ref_support, double* __restrict__ ref_rot,
-                                 uint8_t* __restrict__ ref_valid) {
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// Warm-started one-sided Jacobi on the columns of A = C V0 (V0 from the previous IRLS
+// iteration, so one or two sweeps usually suffice); V (in/out) accumulates the rotations.
+__device__ __forceinline__ bool procrustes_warm(const double C[9], double V[9], double R[9]) {
+  double A[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      A[r * 3 + c] = C[r * 3 + 0] * V[0 * 3 + c] + C[r * 3 + 1] * V[1 * 3 + c] + C[r * 3 + 2] * V[2 * 3 + c];
+  const int P[3] = {0, 0, 1}, Q[3] = {1, 2, 2};
+  for (int sweep = 0; sweep < 16; ++sweep) {
+    bool rotated = false;
+#pragma unroll
+    for (int pq = 0; pq < 3; ++pq) {
+      const int p = P[pq], q = Q[pq];
+      double alpha = 0.0, beta = 0.0, gamma = 0.0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        alpha += A[r * 3 + p] * A[r * 3 + p];
+        beta += A[r * 3 + q] * A[r * 3 + q];
+        gamma += A[r * 3 + p] * A[r * 3 + q];
+      }
+      if (gamma != 0.0 && fabs(gamma) > 1e-15 * sqrt(alpha * beta)) {
+        rotated = true;
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        double t;
+        if (fabs(zeta) > 1e150) t = 0.5 / zeta;
+        else t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t);
+        const double sn = c * t;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double ap = A[r * 3 + p], aq = A[r * 3 + q];
+          A[r * 3 + p] = c * ap - sn * aq;
+          A[r * 3 + q] = sn * ap + c * aq;
+          const double vp = V[r * 3 + p], vq = V[r * 3 + q];
+          V[r * 3 + p] = c * vp - sn * vq;
+          V[r * 3 + q] = sn * vp + c * vq;
+        }
+      }
+    }
+    if (!rotated) break;
+  }
+  double sig[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    sig[i] = sqrt(A[0 * 3 + i] * A[0 * 3 + i] + A[1 * 3 + i] * A[1 * 3 + i] + A[2 * 3 + i] * A[2 * 3 + i]);
+  int o0 = 0, o1 = 1, o2 = 2;
+  if (sig[o1] > sig[o0]) { int x = o0; o0 = o1; o1 = x; }
+  if (sig[o2] > sig[o1]) { int x = o1; o1 = o2; o2 = x; }
+  if (sig[o1] > sig[o0]) { int x = o0; o0 = o1; o1 = x; }
+  const double S0 = sig[o0], S1 = sig[o1];
+  if (!(S0 > 0.0) || S1 <= 1e-9 * S0) return false;
+  double u1[3], u2[3], v1[3], v2[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    u1[r] = A[r * 3 + o0] / S0;
+    u2[r] = A[r * 3 + o1] / S1;
+    v1[r] = V[r * 3 + o0];
+    v2[r] = V[r * 3 + o1];
+  }
+  const double u3[3] = {u1[1] * u2[2] - u1[2] * u2[1], u1[2] * u2[0] - u1[0] * u2[2],
+                        u1[0] * u2[1] - u1[1] * u2[0]};
+  const double v3[3] = {v1[1] * v2[2] - v1[2] * v2[1], v1[2] * v2[0] - v1[0] * v2[2],
+                        v1[0] * v2[1] - v1[1] * v2[0]};
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) R[a * 3 + b] = u1[a] * v1[b] + u2[a] * v2[b] + u3[a] * v3[b];
+  return true;
+}
+
+// IRLS weight of one rectified match under R: reweight(|s2 - R s1|) = min(H/d, 1)
+// (matching.py:128-136), branch-free so the match loop stays unrolled: the residual is
+// accumulated with FMA and H/d is H * rsqrt(d^2) (<= 1 ulp from the reference's H/d; the
+// final flags are recomputed with the reference's exact arithmetic in k_preselect_final).
+__device__ __forceinline__ double irls_weight(const double R[9], double a0, double a1, double a2,
+                                              double b0, double b1, double b2, double H,
+                                              double Hsq) {
+  const double e0 = b0 - __fma_rn(a2, R[2], __fma_rn(a1, R[1], a0 * R[0]));
+  const double e1 = b1 - __fma_rn(a2, R[5], __fma_rn(a1, R[4], a0 * R[3]));
+  const double e2 = b2 - __fma_rn(a2, R[8], __fma_rn(a1, R[7], a0 * R[6]));
+  const double s = __fma_rn(e2, e2, __fma_rn(e1, e1, e0 * e0));
+  const double w = H * rsqrt(fmax(s, 1e-300));
+  return s > Hsq ? w : 1.0;
+}
+
+constexpr int RPW = 2;          // reference hypotheses per warp (share the match loads)
+constexpr int PRE_WARPS = 4;    // warps per CTA
+
+__global__ void __launch_bounds__(PRE_WARPS * 32)
+k_preselect_refs(const double* __restrict__ src, const double* __restrict__ dst,
+                 const int64_t* __restrict__ n_dev, int64_t n_fixed,
+                 const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive, double H,
+                 int iters, double min_support, double* __restrict__ ref_support,
+                 double* __restrict__ ref_rot, uint8_t* __restrict__ ref_valid) {
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t n = n_dev ? *n_dev : n_fixed;
   const int64_t nr = exhaustive ? n : n_refs;
-  if (w >= nr) return;
-  const int64_t ref = exhaustive ? w : refs[w];
-  if (n < 3 || ref < 0 || ref >= n) {
-    if (lane == 0) ref_valid[w] = 0;
-    return;
+  const int64_t w0 = wg * RPW;
+  if (w0 >= nr) return;
+  const double Hsq = H * H;
+  double rs[RPW][3], rd[RPW][3], R[RPW][9], V[RPW][9];
+  bool live[RPW];
+#pragma unroll
+  for (int j = 0; j < RPW; ++j) {
+    const int64_t w = w0 + j;
+    int64_t ref = -1;
+    if (w < nr) ref = exhaustive ? w : refs[w];
+    live[j] = n >= 3 && ref >= 0 && ref < n;
+    const int64_t rr = live[j] ? ref : 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      rs[j][i] = n > 0 ? __ldg(src + 3 * rr + i) : 0.0;
+      rd[j][i] = n > 0 ? __ldg(dst + 3 * rr + i) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      R[j][i] = (i % 4 == 0) ? 1.0 : 0.0;
+      V[j][i] = R[j][i];
+    }
   }
-  const double rs0 = src[3 * ref], rs1 = src[3 * ref + 1], rs2 = src[3 * ref + 2];
-  const double rd0 = dst[3 * ref], rd1 = dst[3 * ref + 1], rd2 = dst[3 * ref + 2];
-  double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-  bool valid = true;
   for (int it = 0; it < iters; ++it) {
-    double C[9];
+    double Cv[RPW][9];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) C[i] = 0.0;
+    for (int j = 0; j < RPW; ++j)
+#pragma unroll
+      for (int i = 0; i < 9; ++i) Cv[j][i] = 0.0;
+#pragma unroll 2
     for (int64_t k = lane; k < n; k += 32) {
-      const double s1[3] = {src[3 * k] - rs0, src[3 * k + 1] - rs1, src[3 * k + 2] - rs2};
-      const double s2[3] = {dst[3 * k] - rd0, dst[3 * k + 1] - rd1, dst[3 * k + 2] - rd2};
-      const double wk = it == 0 ? 1.0 : reweight(rot_residual(R, s1, s2), H);
-      const double ws[3] = {s2[0] * wk, s2[1] * wk, s2[2] * wk};
+      const double x0 = __ldg(src + 3 * k), x1 = __ldg(src + 3 * k + 1), x2 = __ldg(src + 3 * k + 2);
+      const double y0 = __ldg(dst + 3 * k), y1 = __ldg(dst + 3 * k + 1), y2 = __ldg(dst + 3 * k + 2);
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) C[a * 3 + b] += ws[a] * s1[b];
+      for (int j = 0; j < RPW; ++j) {
+        const double a0 = x0 - rs[j][0], a1 = x1 - rs[j][1], a2 = x2 - rs[j][2];
+        const double b0 = y0 - rd[j][0], b1 = y1 - rd[j][1], b2 = y2 - rd[j][2];
+        const double wk = it == 0 ? 1.0 : irls_weight(R[j], a0, a1, a2, b0, b1, b2, H, Hsq);
+        const double c0 = b0 * wk, c1 = b1 * wk, c2 = b2 * wk;
+        Cv[j][0] = __fma_rn(c0, a0, Cv[j][0]);
+        Cv[j][1] = __fma_rn(c0, a1, Cv[j][1]);
+        Cv[j][2] = __fma_rn(c0, a2, Cv[j][2]);
+        Cv[j][3] = __fma_rn(c1, a0, Cv[j][3]);
+        Cv[j][4] = __fma_rn(c1, a1, Cv[j][4]);
+        Cv[j][5] = __fma_rn(c1, a2, Cv[j][5]);
+        Cv[j][6] = __fma_rn(c2, a0, Cv[j][6]);
+        Cv[j][7] = __fma_rn(c2, a1, Cv[j][7]);
+        Cv[j][8] = __fma_rn(c2, a2, Cv[j][8]);
+      }
     }
 #pragma unroll
-    for (int i = 0; i < 9; ++i) C[i] = warp_sum(C[i]);
-    if (!procrustes(C, R)) {
-      valid = false;
-      break;
+    for (int j = 0; j < RPW; ++j) {
+#pragma unroll
+      for (int i = 0; i < 9; ++i) Cv[j][i] = warp_sum(Cv[j][i]);
+      if (live[j] && !procrustes_warm(Cv[j], V[j], R[j])) live[j] = false;
     }
   }
-  double support = 0.0;
-  if (valid) {
-    for (int64_t k = lane; k < n; k += 32) {
-      const double s1[3] = {src[3 * k] - rs0, src[3 * k + 1] - rs1, src[3 * k + 2] - rs2};
-      const double s2[3] = {dst[3 * k] - rd0, dst[3 * k + 1] - rd1, dst[3 * k + 2] - rd2};
-      support += reweight(rot_residual(R, s1, s2), H);
-    }
-    support = warp_sum(support);
-    if (support < min_support * (double)n) valid = false;
-  }
-  if (lane == 0) {
-    ref_valid[w] = valid ? 1 : 0;
-    ref_support[w] = support;
+  double sup[RPW];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) ref_rot[9 * w + i] = R[i];
+  for (int j = 0; j < RPW; ++j) sup[j] = 0.0;
+  for (int64_t k = lane; k < n; k += 32) {
+    const double x0 = __ldg(src + 3 * k), x1 = __ldg(src + 3 * k + 1), x2 = __ldg(src + 3 * k + 2);
+    const double y0 = __ldg(dst + 3 * k), y1 = __ldg(dst + 3 * k + 1), y2 = __ldg(dst + 3 * k + 2);
+#pragma unroll
+    for (int j = 0; j < RPW; ++j)
+      sup[j] += irls_weight(R[j], x0 - rs[j][0], x1 - rs[j][1], x2 - rs[j][2], y0 - rd[j][0],
+                            y1 - rd[j][1], y2 - rd[j][2], H, Hsq);
+  }
+#pragma unroll
+  for (int j = 0; j < RPW; ++j) {
+    const int64_t w = w0 + j;
+    if (w >= nr) continue;
+    double s = warp_sum(sup[j]);
+    bool ok = live[j];
+    if (ok && s < min_support * (double)n) ok = false;
+    if (lane == 0) {
+      ref_valid[w] = ok ? 1 : 0;
+      ref_support[w] = ok ? s : 0.0;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) ref_rot[9 * w + i] = R[j][i];
+    }
   }
 }
-
 // Winner = max support, ties -> lower reference index (matching.py:198-206); then the
 // flags and weights of every match (matching.py:210-213).
 __global__ void k_preselect_final(const double* __restrict__ src, const double* __restrict__ dst,
@@ -346,8 +470,8 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
                      double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s) {
   const int64_t nr = exhaustive ? n_max : n_refs;
   if (nr > 0) {
-    const int threads = 256;
-    k_preselect_refs<<<grid_for(nr * 32, threads), threads, 0, s>>>(
+    const int threads = PRE_WARPS * 32;
+    k_preselect_refs<<<grid_for((nr + RPW - 1) / RPW * 32, threads), threads, 0, s>>>(
         src, dst, n_dev, n_max, refs, n_refs, exhaustive, H, iters, min_support, ref_support,
         ref_rot, ref_valid);
     DT_CHECK_LAUNCH();
