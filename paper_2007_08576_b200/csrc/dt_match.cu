@@ -192,34 +192,34 @@ __device__ __forceinline__ double reweight(double d, double H) {
 }
 
 // Warm-started one-sided Jacobi on the columns of A = C V0 (V0 from the previous IRLS
-// iteration, so one or two sweeps usually suffice); V (in/out) accumulates the rotations.
-__device__ __forceinline__ bool procrustes_warm(const double C[9], double V[9], double R[9]) {
+// iteration, so one or two rotating sweeps usually suffice); V (in/out) accumulates the
+// rotations. Every lane may hold a different C (two hypotheses per warp run their SVDs in
+// the two half-warps at once); the sweep loop is warp-uniform. Singular values come from
+// the orthogonalized columns, accurate relative to S0, so the reference's degeneracy test
+// S1 <= 1e-9 S0 (matching.py:122) decides as LAPACK's gesdd does.
+__device__ __forceinline__ bool procrustes_lane(const double C[9], double V[9], double R[9]) {
   double A[9];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int c = 0; c < 3; ++c)
       A[r * 3 + c] = C[r * 3 + 0] * V[0 * 3 + c] + C[r * 3 + 1] * V[1 * 3 + c] + C[r * 3 + 2] * V[2 * 3 + c];
-  const int P[3] = {0, 0, 1}, Q[3] = {1, 2, 2};
   for (int sweep = 0; sweep < 16; ++sweep) {
     bool rotated = false;
 #pragma unroll
     for (int pq = 0; pq < 3; ++pq) {
-      const int p = P[pq], q = Q[pq];
-      double alpha = 0.0, beta = 0.0, gamma = 0.0;
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        alpha += A[r * 3 + p] * A[r * 3 + p];
-        beta += A[r * 3 + q] * A[r * 3 + q];
-        gamma += A[r * 3 + p] * A[r * 3 + q];
-      }
-      if (gamma != 0.0 && fabs(gamma) > 1e-15 * sqrt(alpha * beta)) {
+      const int p = pq == 2 ? 1 : 0, q = pq == 0 ? 1 : 2;
+      const double alpha = A[p] * A[p] + A[3 + p] * A[3 + p] + A[6 + p] * A[6 + p];
+      const double beta = A[q] * A[q] + A[3 + q] * A[3 + q] + A[6 + q] * A[6 + q];
+      const double gamma = A[p] * A[q] + A[3 + p] * A[3 + q] + A[6 + p] * A[6 + q];
+      // rotate while |gamma| > 1e-15 sqrt(alpha beta)
+      if (gamma != 0.0 && gamma * gamma > 1e-30 * (alpha * beta)) {
         rotated = true;
         const double zeta = (beta - alpha) / (2.0 * gamma);
         double t;
         if (fabs(zeta) > 1e150) t = 0.5 / zeta;
-        else t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t);
+        else t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = rsqrt(1.0 + t * t);
         const double sn = c * t;
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
@@ -232,26 +232,31 @@ __device__ __forceinline__ bool procrustes_warm(const double C[9], double V[9], 
         }
       }
     }
-    if (!rotated) break;
+    if (!__any_sync(0xffffffffu, rotated)) break;
   }
-  double sig[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-    sig[i] = sqrt(A[0 * 3 + i] * A[0 * 3 + i] + A[1 * 3 + i] * A[1 * 3 + i] + A[2 * 3 + i] * A[2 * 3 + i]);
-  int o0 = 0, o1 = 1, o2 = 2;
-  if (sig[o1] > sig[o0]) { int x = o0; o0 = o1; o1 = x; }
-  if (sig[o2] > sig[o1]) { int x = o1; o1 = o2; o2 = x; }
-  if (sig[o1] > sig[o0]) { int x = o0; o0 = o1; o1 = x; }
-  const double S0 = sig[o0], S1 = sig[o1];
+  double s0 = sqrt(A[0] * A[0] + A[3] * A[3] + A[6] * A[6]);
+  double s1 = sqrt(A[1] * A[1] + A[4] * A[4] + A[7] * A[7]);
+  double s2 = sqrt(A[2] * A[2] + A[5] * A[5] + A[8] * A[8]);
+  // order the columns by singular value (descending, stable)
+  int o0 = 0, o1 = 1;
+  double S0 = s0, S1 = s1;
+  if (s1 > s0) { o0 = 1; o1 = 0; S0 = s1; S1 = s0; }
+  if (s2 > S1) {
+    if (s2 > S0) { o1 = o0; S1 = S0; o0 = 2; S0 = s2; }
+    else { o1 = 2; S1 = s2; }
+  }
   if (!(S0 > 0.0) || S1 <= 1e-9 * S0) return false;
   double u1[3], u2[3], v1[3], v2[3];
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
-    u1[r] = A[r * 3 + o0] / S0;
-    u2[r] = A[r * 3 + o1] / S1;
-    v1[r] = V[r * 3 + o0];
-    v2[r] = V[r * 3 + o1];
+    const double a0 = o0 == 0 ? A[r * 3] : (o0 == 1 ? A[r * 3 + 1] : A[r * 3 + 2]);
+    const double a1 = o1 == 0 ? A[r * 3] : (o1 == 1 ? A[r * 3 + 1] : A[r * 3 + 2]);
+    u1[r] = a0 / S0;
+    u2[r] = a1 / S1;
+    v1[r] = o0 == 0 ? V[r * 3] : (o0 == 1 ? V[r * 3 + 1] : V[r * 3 + 2]);
+    v2[r] = o1 == 0 ? V[r * 3] : (o1 == 1 ? V[r * 3 + 1] : V[r * 3 + 2]);
   }
+  // R = U diag(1,1,sign det(U V^T)) V^T = u1 v1^T + u2 v2^T + (u1 x u2)(v1 x v2)^T
   const double u3[3] = {u1[1] * u2[2] - u1[2] * u2[1], u1[2] * u2[0] - u1[0] * u2[2],
                         u1[0] * u2[1] - u1[1] * u2[0]};
   const double v3[3] = {v1[1] * v2[2] - v1[2] * v2[1], v1[2] * v2[0] - v1[0] * v2[2],
@@ -278,102 +283,111 @@ __device__ __forceinline__ double irls_weight(const double R[9], double a0, doub
   return s > Hsq ? w : 1.0;
 }
 
-constexpr int RPW = 2;          // reference hypotheses per warp (share the match loads)
-constexpr int PRE_WARPS = 4;    // warps per CTA
+// Layout: a CTA of PS_SEGS x PS_REFS threads evaluates PS_REFS hypotheses; thread
+// (seg, r) owns hypothesis r and the matches k = seg (mod PS_SEGS). Each thread keeps its
+// hypothesis' rotation in registers and runs an independent, unrolled match loop; the
+// per-segment covariances are combined in a fixed order through shared memory and the
+// PS_REFS SVDs run at once on the lanes of warp 0.
+constexpr int PS_REFS = 8;
+constexpr int PS_SEGS = 32;
+constexpr int PS_THREADS = PS_REFS * PS_SEGS;
 
-__global__ void __launch_bounds__(PRE_WARPS * 32)
+__global__ void __launch_bounds__(PS_THREADS, 2)
 k_preselect_refs(const double* __restrict__ src, const double* __restrict__ dst,
                  const int64_t* __restrict__ n_dev, int64_t n_fixed,
                  const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive, double H,
                  int iters, double min_support, double* __restrict__ ref_support,
                  double* __restrict__ ref_rot, uint8_t* __restrict__ ref_valid) {
-  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  __shared__ double s_C[PS_SEGS][PS_REFS][9];
+  __shared__ double s_R[PS_REFS][9];
+  __shared__ int s_live[PS_REFS];
+  const int tid = threadIdx.x;
+  const int r = tid & (PS_REFS - 1);
+  const int seg = tid / PS_REFS;
   const int64_t n = n_dev ? *n_dev : n_fixed;
   const int64_t nr = exhaustive ? n : n_refs;
-  const int64_t w0 = wg * RPW;
-  if (w0 >= nr) return;
-  const double Hsq = H * H;
-  double rs[RPW][3], rd[RPW][3], R[RPW][9], V[RPW][9];
-  bool live[RPW];
-#pragma unroll
-  for (int j = 0; j < RPW; ++j) {
-    const int64_t w = w0 + j;
-    int64_t ref = -1;
-    if (w < nr) ref = exhaustive ? w : refs[w];
-    live[j] = n >= 3 && ref >= 0 && ref < n;
-    const int64_t rr = live[j] ? ref : 0;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      rs[j][i] = n > 0 ? __ldg(src + 3 * rr + i) : 0.0;
-      rd[j][i] = n > 0 ? __ldg(dst + 3 * rr + i) : 0.0;
-    }
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      R[j][i] = (i % 4 == 0) ? 1.0 : 0.0;
-      V[j][i] = R[j][i];
-    }
+  const int64_t w = (int64_t)blockIdx.x * PS_REFS + r;
+  if ((int64_t)blockIdx.x * PS_REFS >= nr) return;  // CTA-uniform
+  int64_t ref = -1;
+  if (w < nr) ref = exhaustive ? w : refs[w];
+  bool live = n >= 3 && ref >= 0 && ref < n;
+  const int64_t rr = live ? ref : 0;
+  double rs0 = 0, rs1 = 0, rs2 = 0, rd0 = 0, rd1 = 0, rd2 = 0;
+  if (n > 0) {
+    rs0 = __ldg(src + 3 * rr); rs1 = __ldg(src + 3 * rr + 1); rs2 = __ldg(src + 3 * rr + 2);
+    rd0 = __ldg(dst + 3 * rr); rd1 = __ldg(dst + 3 * rr + 1); rd2 = __ldg(dst + 3 * rr + 2);
   }
+  const double Hsq = H * H;
+  double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  double Vm[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};  // used by warp 0 only
   for (int it = 0; it < iters; ++it) {
-    double Cv[RPW][9];
+    double C[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+    for (int64_t k = seg; k < n; k += PS_SEGS) {
+      const double a0 = __ldg(src + 3 * k) - rs0, a1 = __ldg(src + 3 * k + 1) - rs1,
+                   a2 = __ldg(src + 3 * k + 2) - rs2;
+      const double b0 = __ldg(dst + 3 * k) - rd0, b1 = __ldg(dst + 3 * k + 1) - rd1,
+                   b2 = __ldg(dst + 3 * k + 2) - rd2;
+      const double wk = it == 0 ? 1.0 : irls_weight(R, a0, a1, a2, b0, b1, b2, H, Hsq);
+      const double c0 = b0 * wk, c1 = b1 * wk, c2 = b2 * wk;
+      C[0] = __fma_rn(c0, a0, C[0]);
+      C[1] = __fma_rn(c0, a1, C[1]);
+      C[2] = __fma_rn(c0, a2, C[2]);
+      C[3] = __fma_rn(c1, a0, C[3]);
+      C[4] = __fma_rn(c1, a1, C[4]);
+      C[5] = __fma_rn(c1, a2, C[5]);
+      C[6] = __fma_rn(c2, a0, C[6]);
+      C[7] = __fma_rn(c2, a1, C[7]);
+      C[8] = __fma_rn(c2, a2, C[8]);
+    }
 #pragma unroll
-    for (int j = 0; j < RPW; ++j)
+    for (int i = 0; i < 9; ++i) s_C[seg][r][i] = C[i];
+    __syncthreads();
+    if (tid < 32) {
+      // lane r (and its duplicates r + 8, r + 16, r + 24) combines hypothesis r in
+      // segment order
+      double Cr[9];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) Cv[j][i] = 0.0;
-#pragma unroll 2
-    for (int64_t k = lane; k < n; k += 32) {
-      const double x0 = __ldg(src + 3 * k), x1 = __ldg(src + 3 * k + 1), x2 = __ldg(src + 3 * k + 2);
-      const double y0 = __ldg(dst + 3 * k), y1 = __ldg(dst + 3 * k + 1), y2 = __ldg(dst + 3 * k + 2);
+      for (int i = 0; i < 9; ++i) {
+        double acc = 0.0;
+        for (int g = 0; g < PS_SEGS; ++g) acc += s_C[g][r][i];
+        Cr[i] = acc;
+      }
+      double Rm[9];
+      const bool ok = procrustes_lane(Cr, Vm, Rm);
+      if (tid < PS_REFS) {
 #pragma unroll
-      for (int j = 0; j < RPW; ++j) {
-        const double a0 = x0 - rs[j][0], a1 = x1 - rs[j][1], a2 = x2 - rs[j][2];
-        const double b0 = y0 - rd[j][0], b1 = y1 - rd[j][1], b2 = y2 - rd[j][2];
-        const double wk = it == 0 ? 1.0 : irls_weight(R[j], a0, a1, a2, b0, b1, b2, H, Hsq);
-        const double c0 = b0 * wk, c1 = b1 * wk, c2 = b2 * wk;
-        Cv[j][0] = __fma_rn(c0, a0, Cv[j][0]);
-        Cv[j][1] = __fma_rn(c0, a1, Cv[j][1]);
-        Cv[j][2] = __fma_rn(c0, a2, Cv[j][2]);
-        Cv[j][3] = __fma_rn(c1, a0, Cv[j][3]);
-        Cv[j][4] = __fma_rn(c1, a1, Cv[j][4]);
-        Cv[j][5] = __fma_rn(c1, a2, Cv[j][5]);
-        Cv[j][6] = __fma_rn(c2, a0, Cv[j][6]);
-        Cv[j][7] = __fma_rn(c2, a1, Cv[j][7]);
-        Cv[j][8] = __fma_rn(c2, a2, Cv[j][8]);
+        for (int i = 0; i < 9; ++i) s_R[r][i] = Rm[i];
+        s_live[r] = ok ? 1 : 0;
       }
     }
+    __syncthreads();
+    if (!s_live[r]) live = false;
+    if (live) {
 #pragma unroll
-    for (int j = 0; j < RPW; ++j) {
-#pragma unroll
-      for (int i = 0; i < 9; ++i) Cv[j][i] = warp_sum(Cv[j][i]);
-      if (live[j] && !procrustes_warm(Cv[j], V[j], R[j])) live[j] = false;
+      for (int i = 0; i < 9; ++i) R[i] = s_R[r][i];
     }
+    __syncthreads();
   }
-  double sup[RPW];
+  double sup = 0.0;
+#pragma unroll 4
+  for (int64_t k = seg; k < n; k += PS_SEGS)
+    sup += irls_weight(R, __ldg(src + 3 * k) - rs0, __ldg(src + 3 * k + 1) - rs1,
+                       __ldg(src + 3 * k + 2) - rs2, __ldg(dst + 3 * k) - rd0,
+                       __ldg(dst + 3 * k + 1) - rd1, __ldg(dst + 3 * k + 2) - rd2, H, Hsq);
+  s_C[seg][r][0] = sup;
+  __syncthreads();
+  if (tid < PS_REFS && w < nr) {
+    double s = 0.0;
+    for (int g = 0; g < PS_SEGS; ++g) s += s_C[g][r][0];
+    const bool ok = live && !(s < min_support * (double)n);
+    ref_valid[w] = ok ? 1 : 0;
+    ref_support[w] = ok ? s : 0.0;
 #pragma unroll
-  for (int j = 0; j < RPW; ++j) sup[j] = 0.0;
-  for (int64_t k = lane; k < n; k += 32) {
-    const double x0 = __ldg(src + 3 * k), x1 = __ldg(src + 3 * k + 1), x2 = __ldg(src + 3 * k + 2);
-    const double y0 = __ldg(dst + 3 * k), y1 = __ldg(dst + 3 * k + 1), y2 = __ldg(dst + 3 * k + 2);
-#pragma unroll
-    for (int j = 0; j < RPW; ++j)
-      sup[j] += irls_weight(R[j], x0 - rs[j][0], x1 - rs[j][1], x2 - rs[j][2], y0 - rd[j][0],
-                            y1 - rd[j][1], y2 - rd[j][2], H, Hsq);
-  }
-#pragma unroll
-  for (int j = 0; j < RPW; ++j) {
-    const int64_t w = w0 + j;
-    if (w >= nr) continue;
-    double s = warp_sum(sup[j]);
-    bool ok = live[j];
-    if (ok && s < min_support * (double)n) ok = false;
-    if (lane == 0) {
-      ref_valid[w] = ok ? 1 : 0;
-      ref_support[w] = ok ? s : 0.0;
-#pragma unroll
-      for (int i = 0; i < 9; ++i) ref_rot[9 * w + i] = R[j][i];
-    }
+    for (int i = 0; i < 9; ++i) ref_rot[9 * w + i] = R[i];
   }
 }
+
 // Winner = max support, ties -> lower reference index (matching.py:198-206); then the
 // flags and weights of every match (matching.py:210-213).
 __global__ void k_preselect_final(const double* __restrict__ src, const double* __restrict__ dst,
@@ -470,8 +484,7 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
                      double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s) {
   const int64_t nr = exhaustive ? n_max : n_refs;
   if (nr > 0) {
-    const int threads = PRE_WARPS * 32;
-    k_preselect_refs<<<grid_for((nr + RPW - 1) / RPW * 32, threads), threads, 0, s>>>(
+    k_preselect_refs<<<(unsigned)((nr + PS_REFS - 1) / PS_REFS), PS_THREADS, 0, s>>>(
         src, dst, n_dev, n_max, refs, n_refs, exhaustive, H, iters, min_support, ref_support,
         ref_rot, ref_valid);
     DT_CHECK_LAUNCH();
