@@ -209,124 +209,6 @@ __device__ __forceinline__ void blend_gradient_fast(const double B[8], double px
   G[23] = 2.0 * qw * is;
 }
 
-// ---------------------------------------------------------------------------------
-// P1 / final relink: one template point. Returns its icp cost sum_s (rs sqrt(a_s) r)^2
-// (0 without a valid correspondence); *valid_out receives the gate outcome.
-// ---------------------------------------------------------------------------------
-
-__device__ __forceinline__ double point_relink(const SolverArgs& A, const double* s_w, int64_t p,
-                                               bool jac, int* valid_out) {
-  double B[8], sgn[KMAX], a[KMAX];
-  blend_rows(s_w, A.bidx, A.bw, p, A.k, B, sgn, a);
-  const double px = A.tp[3 * p], py = A.tp[3 * p + 1], pz = A.tp[3 * p + 2];
-  double x0, x1, x2, s2;
-  apply_blend(B, px, py, pz, x0, x1, x2, s2);
-  double r0, r1, r2;
-  rotate_normal(B, A.tn[3 * p], A.tn[3 * p + 1], A.tn[3 * p + 2], r0, r1, r2);
-  bool ok = false;
-  double o0 = 0, o1 = 0, o2 = 0, g0 = 0, g1 = 0, g2 = 0;
-  // projection and gates, in the reference's IEEE order (kernels.py:537-568)
-  if (x2 > 0.0) {
-    const double uf = rint(A.fx * x0 / x2 + A.cx);
-    const double vf = rint(A.fy * x1 / x2 + A.cy);
-    if (uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height) {
-      const int ui = (int)uf, vi = (int)vf;
-      const int64_t pix = (int64_t)vi * A.width + ui;
-      if (A.dvalid[pix]) {
-        const double d = A.depth[pix];
-        o0 = ((double)ui - A.cx) / A.fx * d;
-        o1 = ((double)vi - A.cy) / A.fy * d;
-        o2 = d;
-        g0 = A.onrm[3 * pix];
-        g1 = A.onrm[3 * pix + 1];
-        g2 = A.onrm[3 * pix + 2];
-        if (g0 * g0 + g1 * g1 + g2 * g2 > 0.25) {
-          const double dx = o0 - x0, dy = o1 - x1, dz = d - x2;
-          ok = sqrt(dx * dx + dy * dy + dz * dz) < A.gate &&
-               g0 * r0 + g1 * r1 + g2 * r2 > A.cos_gate;
-        }
-      }
-    }
-  }
-  A.cvalid[p] = ok ? 1 : 0;
-  *valid_out = ok ? 1 : 0;
-  if (!ok) return 0.0;
-  A.cobs[3 * p] = o0;
-  A.cobs[3 * p + 1] = o1;
-  A.cobs[3 * p + 2] = o2;
-  A.cnrm[3 * p] = g0;
-  A.cnrm[3 * p + 1] = g1;
-  A.cnrm[3 * p + 2] = g2;
-  const double r = g0 * (x0 - o0) + g1 * (x1 - o1) + g2 * (x2 - o2);
-  const double rs = tukey_sqrt(r, A.tukey);
-  A.pr_r[p] = r;
-  A.pr_rs[p] = rs;
-  A.pr_sgn[p] = (uint8_t)sign_bits(sgn, A.k);
-  if (jac) {
-    double G[24];
-    blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, G);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) A.pr_gn[8 * p + e] = g0 * G[e] + g1 * G[8 + e] + g2 * G[16 + e];
-  }
-  double cost = 0.0;
-#pragma unroll
-  for (int s = 0; s < KMAX; ++s)
-    if (s < A.k) {
-      const double wv = rs * sqrt(a[s]) * r;
-      cost += wv * wv;
-    }
-  return cost;
-}
-
-// icp cost of point p at the warps in smem with the frozen correspondence and robust weight
-__device__ __forceinline__ double point_value(const SolverArgs& A, const double* s_w, int64_t p) {
-  if (!ldu8(A.cvalid + p)) return 0.0;
-  double B[8], sgn[KMAX], a[KMAX];
-  blend_rows(s_w, A.bidx, A.bw, p, A.k, B, sgn, a);
-  double x0, x1, x2, s2;
-  apply_blend(B, A.tp[3 * p], A.tp[3 * p + 1], A.tp[3 * p + 2], x0, x1, x2, s2);
-  const double r = ld(A.cnrm + 3 * p) * (x0 - ld(A.cobs + 3 * p)) +
-                   ld(A.cnrm + 3 * p + 1) * (x1 - ld(A.cobs + 3 * p + 1)) +
-                   ld(A.cnrm + 3 * p + 2) * (x2 - ld(A.cobs + 3 * p + 2));
-  const double rs = ld(A.pr_rs + p);
-  double cost = 0.0;
-#pragma unroll
-  for (int s = 0; s < KMAX; ++s)
-    if (s < A.k) {
-      const double wv = rs * sqrt(a[s]) * r;
-      cost += wv * wv;
-    }
-  return cost;
-}
-
-// one active match: residual (and its blend gradient); returns its feature cost
-__device__ __forceinline__ double match_eval(const SolverArgs& A, const double* s_w, int64_t j,
-                                             bool store, bool jac) {
-  double B[8], sgn[KMAX], a[KMAX];
-  blend_rows(s_w, A.fbidx, A.fbw, j, A.k, B, sgn, a);
-  const double px = A.fp[3 * j], py = A.fp[3 * j + 1], pz = A.fp[3 * j + 2];
-  double x0, x1, x2, s2;
-  apply_blend(B, px, py, pz, x0, x1, x2, s2);
-  const double e0 = x0 - A.fo[3 * j], e1 = x1 - A.fo[3 * j + 1], e2 = x2 - A.fo[3 * j + 2];
-  if (store) {
-    A.fr_res[3 * j] = e0;
-    A.fr_res[3 * j + 1] = e1;
-    A.fr_res[3 * j + 2] = e2;
-    A.fr_sgn[j] = (uint8_t)sign_bits(sgn, A.k);
-    if (jac) blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, A.fr_G + 24 * j);
-  }
-  const double w = A.fwt[j];
-  double cost = 0.0;
-#pragma unroll
-  for (int s = 0; s < KMAX; ++s)
-    if (s < A.k) {
-      const double sw = sqrt(A.fw * w * a[s]);
-      const double v0 = sw * e0, v1 = sw * e1, v2 = sw * e2;
-      cost += v0 * v0 + v1 * v1 + v2 * v2;
-    }
-  return cost;
-}
-
 // rigidity cost of one connection (both endpoint bins): 2 x (length + angle 0->1 +
 // angle 1->0 + rotation) with the transforms / quaternions in smem
 __device__ __forceinline__ double edge_value(const SolverArgs& A, const double* s_w,
@@ -478,6 +360,7 @@ __device__ __forceinline__ bool solve6(const double* part, double lam, double de
     L[i * (i + 1) / 2 + i] = a + lam * fmax(a, 1e-12);
   }
   bool ok = true;
+  double inv[6];  // one reciprocal per pivot instead of a division per entry
 #pragma unroll
   for (int j = 0; j < 6; ++j) {
     double s = L[j * (j + 1) / 2 + j];
@@ -485,13 +368,14 @@ __device__ __forceinline__ bool solve6(const double* part, double lam, double de
     for (int q = 0; q < j; ++q) s -= L[j * (j + 1) / 2 + q] * L[j * (j + 1) / 2 + q];
     ok = ok && (s > 0.0);
     const double ljj = sqrt(s);
+    inv[j] = 1.0 / ljj;
     L[j * (j + 1) / 2 + j] = ljj;
 #pragma unroll
     for (int i = j + 1; i < 6; ++i) {
       double v = L[i * (i + 1) / 2 + j];
 #pragma unroll
       for (int q = 0; q < j; ++q) v -= L[i * (i + 1) / 2 + q] * L[j * (j + 1) / 2 + q];
-      L[i * (i + 1) / 2 + j] = v / ljj;
+      L[i * (i + 1) / 2 + j] = v * inv[j];
     }
   }
   if (!ok) {
@@ -505,24 +389,16 @@ __device__ __forceinline__ bool solve6(const double* part, double lam, double de
     double acc = -part[21 + i];
 #pragma unroll
     for (int j = 0; j < i; ++j) acc -= L[i * (i + 1) / 2 + j] * y[j];
-    y[i] = acc / L[i * (i + 1) / 2 + i];
+    y[i] = acc * inv[i];
   }
 #pragma unroll
   for (int i = 5; i >= 0; --i) {
     double acc = y[i];
 #pragma unroll
     for (int j = i + 1; j < 6; ++j) acc -= L[j * (j + 1) / 2 + i] * delta[j];
-    delta[i] = acc / L[i * (i + 1) / 2 + i];
+    delta[i] = acc * inv[i];
   }
   return true;
-}
-
-// Fixed-order sum of a chunk-sum array by one warp (lane-strided, then xor tree).
-__device__ __forceinline__ double sum_fixed(const double* a, int n) {
-  const int lane = threadIdx.x & 31;
-  double s = 0.0;
-  for (int i = lane; i < n; i += 32) s += ld(a + i);
-  return warp_sum(s);
 }
 
 #define TRACE(code)                                                \

@@ -55,20 +55,24 @@ struct SolverArgs {
   double* lam;
   double* wa;
   double* partial;   // m x 27 normal-equation columns
-  double* csum;      // nch_p + nch_m + nch_e deterministic chunk sums
+  double* csum;      // 2 sets x (nch_p + nch_m + nch_e) deterministic chunk sums
   double* erows;     // n_edges x 40 unit rigidity rows of both bins
   double* delta;     // m x 6
   double* oknorm;    // 2 parities x m x 2 (ok, step norm)
-  uint8_t* cvalid;   // per template point: correspondence valid
-  double* cobs;      // n x 3 observed point
-  double* cnrm;      // n x 3 observed normal
-  double* pr_r;      // n raw residual
-  double* pr_rs;     // n robust sqrt weight (frozen for the tentative passes)
-  double* pr_gn;     // n x 8 gradient of r w.r.t. the blend
-  uint8_t* pr_sgn;   // n blend signs (bit per slot)
-  double* fr_res;    // Ma x 3
-  double* fr_G;      // Ma x 24
-  uint8_t* fr_sgn;   // Ma
+  // per-point / per-match linearization records, double-buffered (2 x n, 2 x Ma): the
+  // value pass at a tentative iterate relinearizes there speculatively into the other
+  // buffer, which becomes current when the step is accepted
+  uint8_t* cvalid;   // correspondence valid
+  double* cobs;      // x 3 observed point
+  double* cnrm;      // x 3 observed normal
+  double* pr_r;      // raw residual
+  double* pr_rs;     // robust sqrt weight (frozen for the tentative passes)
+  double* pr_gn;     // x 8 gradient of r w.r.t. the blend
+  uint8_t* pr_sgn;   // blend signs (bit per slot)
+  double* fr_res;    // x 3
+  double* fr_G;      // x 24
+  uint8_t* fr_sgn;
+  int ma_cap;        // match capacity (stride between the two match buffers)
   int* counts;       // per-CTA correspondence counts (<= 1024 CTAs)
   // outputs
   dt_report* report;

@@ -1,51 +1,200 @@
 // dt_solver_kernel.cuh -- body of the persistent LM kernel (included by dt_solver.cu).
 //
-// Work units inside the sync domain (C CTAs x 16 warps):
+// Work units inside the sync domain (C CTAs x 16 warps), dealt round-robin over the CTAs:
 //   * points / matches / edges: one item per lane, fixed 32-item chunks whose partial
 //     sums land in csum (deterministic, independent of C);
 //   * controls: a team of TEAM warps of one CTA per control; each warp folds every
 //     TEAM-th block of 32 rows into its own FP64 tensor-core Gram, the team combines the
 //     Grams in warp order (deterministic, independent of C).
-// Barriers per outer iteration: P1 | P2 | P3 (+ first solve) | value pass -- the
-// tentative step is applied redundantly by every CTA into its own shared memory, so it
-// costs no barrier.
+// Barriers per accepted outer iteration: P2 | P3 (+ first solve) | value pass. The
+// tentative step is applied redundantly by every CTA into its own shared memory (no
+// barrier), and the value pass also relinearizes at the tentative warps into the second
+// record buffer ("speculative relink"), so an accepted step starts the next iteration
+// directly at P2; a stalled iteration keeps its linearization -- the reference recomputes
+// it at the same warps, bit for bit the same -- and only re-solves.
 
 constexpr int TEAM = 4;
 constexpr int TEAMS_PER_CTA = NWARPS / TEAM;
 
-// Sum of the three chunk-sum segments in a fixed order (thread-strided, warp xor tree,
-// warps in order), identical in every CTA. Must be called by the whole CTA.
-__device__ __forceinline__ void block_totals(const double* cs_p, int np, const double* cs_m, int nm,
-                                             const double* cs_e, int ne, double* s_part,
-                                             double out[3]) {
+// one of the two per-point record buffers (correspondence + linearization)
+struct PBuf {
+  uint8_t* valid;
+  double* obs;
+  double* nrm;
+  double* r;
+  double* rs;
+  double* gn;
+  uint8_t* sgn;
+};
+
+// one of the two per-match record buffers
+struct MBuf {
+  double* res;
+  double* G;
+  uint8_t* sgn;
+};
+
+__device__ __forceinline__ PBuf pbuf(const SolverArgs& A, int b) {
+  const int64_t n = A.n;
+  return {A.cvalid + b * n, A.cobs + 3 * b * n, A.cnrm + 3 * b * n, A.pr_r + b * n,
+          A.pr_rs + b * n,  A.pr_gn + 8 * b * n, A.pr_sgn + b * n};
+}
+
+__device__ __forceinline__ MBuf mbuf(const SolverArgs& A, int b) {
+  const int64_t c = A.ma_cap;
+  return {A.fr_res + 3 * b * c, A.fr_G + 24 * b * c, A.fr_sgn + b * c};
+}
+
+// Relink point p at the warps in smem (kernels.py:483-569) and linearize it into `nb`
+// (kernels.py:173-197); returns the point's icp cost under the Tukey weight of the new
+// residual. With `ob`, *cost_old receives the point's cost at these warps under the
+// frozen correspondence and robust weight of record `ob` (the value pass,
+// solver.py:333-335).
+__device__ __forceinline__ double point_step(const SolverArgs& A, const double* s_w, int64_t p,
+                                             const PBuf* ob, const PBuf& nb, double* cost_old,
+                                             int* valid_out) {
+  double B[8], sgn[KMAX], a[KMAX];
+  blend_rows(s_w, A.bidx, A.bw, p, A.k, B, sgn, a);
+  const double px = A.tp[3 * p], py = A.tp[3 * p + 1], pz = A.tp[3 * p + 2];
+  double x0, x1, x2, s2;
+  apply_blend(B, px, py, pz, x0, x1, x2, s2);
+  if (ob) {
+    double co = 0.0;
+    if (ldu8(ob->valid + p)) {
+      const double r = ld(ob->nrm + 3 * p) * (x0 - ld(ob->obs + 3 * p)) +
+                       ld(ob->nrm + 3 * p + 1) * (x1 - ld(ob->obs + 3 * p + 1)) +
+                       ld(ob->nrm + 3 * p + 2) * (x2 - ld(ob->obs + 3 * p + 2));
+      const double rs = ld(ob->rs + p);
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s)
+        if (s < A.k) {
+          const double wv = rs * sqrt(a[s]) * r;
+          co += wv * wv;
+        }
+    }
+    *cost_old = co;
+  }
+  double r0, r1, r2;
+  rotate_normal(B, A.tn[3 * p], A.tn[3 * p + 1], A.tn[3 * p + 2], r0, r1, r2);
+  bool ok = false;
+  double o0 = 0, o1 = 0, o2 = 0, g0 = 0, g1 = 0, g2 = 0;
+  // projection and gates, in the reference's IEEE order (kernels.py:537-568)
+  if (x2 > 0.0) {
+    const double uf = rint(A.fx * x0 / x2 + A.cx);
+    const double vf = rint(A.fy * x1 / x2 + A.cy);
+    if (uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height) {
+      const int ui = (int)uf, vi = (int)vf;
+      const int64_t pix = (int64_t)vi * A.width + ui;
+      if (A.dvalid[pix]) {
+        const double d = A.depth[pix];
+        o0 = ((double)ui - A.cx) / A.fx * d;
+        o1 = ((double)vi - A.cy) / A.fy * d;
+        o2 = d;
+        g0 = A.onrm[3 * pix];
+        g1 = A.onrm[3 * pix + 1];
+        g2 = A.onrm[3 * pix + 2];
+        if (g0 * g0 + g1 * g1 + g2 * g2 > 0.25) {
+          const double dx = o0 - x0, dy = o1 - x1, dz = d - x2;
+          ok = sqrt(dx * dx + dy * dy + dz * dz) < A.gate &&
+               g0 * r0 + g1 * r1 + g2 * r2 > A.cos_gate;
+        }
+      }
+    }
+  }
+  nb.valid[p] = ok ? 1 : 0;
+  *valid_out = ok ? 1 : 0;
+  if (!ok) return 0.0;
+  nb.obs[3 * p] = o0;
+  nb.obs[3 * p + 1] = o1;
+  nb.obs[3 * p + 2] = o2;
+  nb.nrm[3 * p] = g0;
+  nb.nrm[3 * p + 1] = g1;
+  nb.nrm[3 * p + 2] = g2;
+  const double r = g0 * (x0 - o0) + g1 * (x1 - o1) + g2 * (x2 - o2);
+  const double rs = tukey_sqrt(r, A.tukey);
+  nb.r[p] = r;
+  nb.rs[p] = rs;
+  nb.sgn[p] = (uint8_t)sign_bits(sgn, A.k);
+  double G[24];
+  blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, G);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) nb.gn[8 * p + e] = g0 * G[e] + g1 * G[8 + e] + g2 * G[16 + e];
+  double cost = 0.0;
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s)
+    if (s < A.k) {
+      const double wv = rs * sqrt(a[s]) * r;
+      cost += wv * wv;
+    }
+  return cost;
+}
+
+// One active match at the warps in smem: residual + blend gradient into `nb`
+// (kernels.py:239-250); returns its feature cost (no robust weight, so the same value
+// serves the value pass and the relinearization).
+__device__ __forceinline__ double match_step(const SolverArgs& A, const double* s_w, int64_t j,
+                                             const MBuf& nb) {
+  double B[8], sgn[KMAX], a[KMAX];
+  blend_rows(s_w, A.fbidx, A.fbw, j, A.k, B, sgn, a);
+  const double px = A.fp[3 * j], py = A.fp[3 * j + 1], pz = A.fp[3 * j + 2];
+  double x0, x1, x2, s2;
+  apply_blend(B, px, py, pz, x0, x1, x2, s2);
+  const double e0 = x0 - A.fo[3 * j], e1 = x1 - A.fo[3 * j + 1], e2 = x2 - A.fo[3 * j + 2];
+  nb.res[3 * j] = e0;
+  nb.res[3 * j + 1] = e1;
+  nb.res[3 * j + 2] = e2;
+  nb.sgn[j] = (uint8_t)sign_bits(sgn, A.k);
+  blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, nb.G + 24 * j);
+  const double w = A.fwt[j];
+  double cost = 0.0;
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s)
+    if (s < A.k) {
+      const double sw = sqrt(A.fw * w * a[s]);
+      const double v0 = sw * e0, v1 = sw * e1, v2 = sw * e2;
+      cost += v0 * v0 + v1 * v1 + v2 * v2;
+    }
+  return cost;
+}
+
+// Fixed-order sum of one chunk-sum segment (4 loads in flight per thread, thread order,
+// warp xor tree, warps in order); identical in every CTA. Whole CTA; s_part >= NWARPS.
+__device__ __forceinline__ double seg_total(const double* a, int n, double* s_part) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double a = 0.0, b = 0.0, e = 0.0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) a += ld(cs_p + i);
-  for (int i = threadIdx.x; i < nm; i += blockDim.x) b += ld(cs_m + i);
-  for (int i = threadIdx.x; i < ne; i += blockDim.x) e += ld(cs_e + i);
-  a = warp_sum(a);
-  b = warp_sum(b);
-  e = warp_sum(e);
-  __syncthreads();
-  if (lane == 0) {
-    s_part[3 * warp] = a;
-    s_part[3 * warp + 1] = b;
-    s_part[3 * warp + 2] = e;
+  const int bd = (int)blockDim.x;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += 4 * bd) {
+    const double v0 = ld(a + i);
+    const double v1 = i + bd < n ? ld(a + i + bd) : 0.0;
+    const double v2 = i + 2 * bd < n ? ld(a + i + 2 * bd) : 0.0;
+    const double v3 = i + 3 * bd < n ? ld(a + i + 3 * bd) : 0.0;
+    acc += (v0 + v1) + (v2 + v3);
   }
+  acc = warp_sum(acc);
   __syncthreads();
-  double ta = 0.0, tb = 0.0, te = 0.0;
-  for (int w = 0; w < NWARPS; ++w) {
-    ta += s_part[3 * w];
-    tb += s_part[3 * w + 1];
-    te += s_part[3 * w + 2];
-  }
-  out[0] = ta;
-  out[1] = tb;
-  out[2] = te;
+  if (lane == 0) s_part[warp] = acc;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < NWARPS; ++w) t += s_part[w];
+  return t;
 }
 
 __device__ __forceinline__ unsigned long long dbits(double x) {
   return (unsigned long long)__double_as_longlong(x);
+}
+
+// damped solve of control c from the stored normal equations -> delta, (ok, |delta|)
+__device__ __forceinline__ void resolve_control(const SolverArgs& A, int c, double* okn) {
+  double part[27], d[6];
+  for (int i = 0; i < 27; ++i) part[i] = ld(A.partial + 27 * c + i);
+  const bool good = solve6(part, A.lam[c], d);
+  double nn = 0.0;
+  for (int i = 0; i < 6; ++i) {
+    A.delta[6 * c + i] = d[i];
+    nn += d[i] * d[i];
+  }
+  okn[2 * c] = good ? 1.0 : 0.0;
+  okn[2 * c + 1] = sqrt(nn);
 }
 
 template <bool GRID>
@@ -80,9 +229,14 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   const int nch_p = (int)((n + CHUNK - 1) / CHUNK);
   const int nch_m = (int)((n_act + CHUNK - 1) / CHUNK);
   const int nch_e = (A.n_edges + CHUNK - 1) / CHUNK;
-  double* cs_p = A.csum;
-  double* cs_m = A.csum + A.nch_p;
-  double* cs_e = cs_m + A.nch_m;
+  const int nch_tot = A.nch_p + A.nch_m + A.nch_e;
+  // chunk-sum set 0: value pass (points, matches, edges) and the rigidity cost of the
+  // iterate; set 1: icp / feature cost of each (speculative) relinearization
+  double* cs_p0 = A.csum;
+  double* cs_m0 = cs_p0 + A.nch_p;
+  double* cs_e0 = cs_m0 + A.nch_m;
+  double* cs_p1 = A.csum + nch_tot;
+  double* cs_m1 = cs_p1 + A.nch_p;
   unsigned long long* lam_hist = reinterpret_cast<unsigned long long*>(A.lam_hist);
   long long* tr = A.trace;
   int tn = 0;
@@ -96,235 +250,243 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
 
   double* cur = A.warp_a;
   double* tent = A.warp_b;
+  int pb = 0;               // record buffer holding the linearization at `cur`
+  bool smem_is_cur = true;  // s_w / s_T hold `cur`
+  bool need_lin = true;     // P2 / P3 must be evaluated at `cur`
   int accepted_steps = 0, rejected_steps = 0, n_hist = 0, outer_done = 0;
   bool converged = false, stalled = false;
   double final_step_norm = 0.0;
   int parity = 0;
+  double cb_icp = 0.0, cb_feat = 0.0, cb_arap = 0.0;
 
-  for (int outer = 0; outer < A.max_outer; ++outer) {
-    outer_done = outer + 1;
-    // ---- P1: relink + linearize at `cur`; icp / feature cost of the iterate ----
-    load_state(A, cur, s_w, s_T);
-    TRACE(12);
+  // ---- P1: relink + linearize at the warm start (record buffer 0) ----
+  load_state(A, cur, s_w, s_T);
+  TRACE(12);
+  {
+    const PBuf nb = pbuf(A, 0);
+    const MBuf nm = mbuf(A, 0);
     for (int ch = gw; ch < nch_p + nch_m; ch += GW) {
       double acc = 0.0;
       if (ch < nch_p) {
         const int64_t p = (int64_t)ch * CHUNK + lane;
-        int vdummy;
-        if (p < n) acc = point_relink(A, s_w, p, true, &vdummy);
+        int vd;
+        if (p < n) acc = point_step(A, s_w, p, nullptr, nb, nullptr, &vd);
         acc = warp_sum(acc);
-        if (lane == 0) cs_p[ch] = acc;
+        if (lane == 0) cs_p1[ch] = acc;
       } else {
         const int64_t j = (int64_t)(ch - nch_p) * CHUNK + lane;
-        if (j < n_act) acc = match_eval(A, s_w, j, true, true);
+        if (j < n_act) acc = match_step(A, s_w, j, nm);
         acc = warp_sum(acc);
-        if (lane == 0) cs_m[ch - nch_p] = acc;
+        if (lane == 0) cs_m1[ch - nch_p] = acc;
       }
     }
-    DSYNC(1);
+  }
+  DSYNC(1);
+  cb_icp = seg_total(cs_p1, nch_p, s_part);
+  cb_feat = seg_total(cs_m1, nch_m, s_part);
 
-    // ---- P2: unit rigidity rows of every connection (no wa needed), on the warps at
-    // the end of the domain; data rows -> normal equations (Gram on the FP64 tensor
-    // cores) on the teams ----
-    for (int ch = gw_rev; ch < nch_e; ch += GW) {
-      const int e = ch * CHUNK + lane;
-      if (e < A.n_edges) edge_unit_rows(A, s_T, e, A.erows + (size_t)ER * e);
-    }
-    TRACE(22);
-    for (int r = 0; r < team_rounds; ++r) {
-      const int c = r * GTEAM + gteam;
-      Gram G;
-      double sup = 0.0;
-      if (c < m) {
-        Basis K;
-        make_basis(s_w + 8 * c, K);
-        const int q0 = ldi(A.cptr + c), q1 = ldi(A.cptr + c + 1);
-        for (int base = q0 + 32 * tw; base < q1; base += 32 * TEAM) {
-          const int q = base + lane;
-          double row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          if (q < q1) {
-            const int e = ldi(A.cent + q);
-            const int64_t p = e >> 3;
-            const int s = e & 7;
-            if (ldu8(A.cvalid + p)) {
-              const double a = A.bw[p * A.k + s];
-              const double rs = ld(A.pr_rs + p);
-              sup += rs * rs * a;
-              const double sw = rs * sqrt(a);
-              const double sg = ((ldu8(A.pr_sgn + p) >> s) & 1u) ? -1.0 : 1.0;
-              const double coef = sw * a * sg;
-              double gn[8], pr[6];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) gn[i] = ld(A.pr_gn + 8 * p + i);
-              basis_project(gn, K.Kr, K.Kd, pr);
-#pragma unroll
-              for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
-              row[6] = sw * ld(A.pr_r + p);
-            }
-          }
-          gram_push(G, stage, row);
-        }
-        if (n_act > 0) {
-          const int m0 = ldi(A.mptr + c), m1 = ldi(A.mptr + c + 1);
-          for (int base = m0 + 32 * tw; base < m1; base += 32 * TEAM) {
+  for (int outer = 0; outer < A.max_outer; ++outer) {
+    outer_done = outer + 1;
+    double* okn = A.oknorm + (size_t)parity * 2 * m;
+    if (need_lin) {
+      const PBuf cb = pbuf(A, pb);
+      const MBuf cm = mbuf(A, pb);
+      // ---- P2: unit rigidity rows of every connection (no wa needed) on the warps at
+      // the end of each CTA; data rows -> normal equations (FP64 tensor-core Gram) on
+      // the teams ----
+      for (int ch = gw_rev; ch < nch_e; ch += GW) {
+        const int e = ch * CHUNK + lane;
+        if (e < A.n_edges) edge_unit_rows(A, s_T, e, A.erows + (size_t)ER * e);
+      }
+      TRACE(22);
+      for (int r = 0; r < team_rounds; ++r) {
+        const int c = r * GTEAM + gteam;
+        Gram G;
+        double sup = 0.0;
+        if (c < m) {
+          Basis K;
+          make_basis(s_w + 8 * c, K);
+          const int q0 = ldi(A.cptr + c), q1 = ldi(A.cptr + c + 1);
+          for (int base = q0 + 32 * tw; base < q1; base += 32 * TEAM) {
             const int q = base + lane;
-            const bool live = q < m1;
-            int64_t j = 0;
-            double coef = 0.0, sw = 0.0;
-            if (live) {
-              const int e = ldi(A.ment + q);
-              j = e / A.k;
-              const int s = e - (int)j * A.k;
-              const double a = A.fbw[e];
-              const double w_pair = A.fw * A.fwt[j] * a;
-              sup += w_pair;
-              sw = sqrt(w_pair);
-              const double sg = ((ldu8(A.fr_sgn + j) >> s) & 1u) ? -1.0 : 1.0;
-              coef = sw * a * sg;
-            }
-#pragma unroll 1
-            for (int comp = 0; comp < 3; ++comp) {
-              double row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-              if (live) {
-                double g[8], pr[6];
+            double row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (q < q1) {
+              const int e = ldi(A.cent + q);
+              const int64_t p = e >> 3;
+              const int s = e & 7;
+              if (ldu8(cb.valid + p)) {
+                const double a = A.bw[p * A.k + s];
+                const double rs = ld(cb.rs + p);
+                sup += rs * rs * a;
+                const double sw = rs * sqrt(a);
+                const double sg = ((ldu8(cb.sgn + p) >> s) & 1u) ? -1.0 : 1.0;
+                const double coef = sw * a * sg;
+                double gn[8], pr[6];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) g[i] = ld(A.fr_G + 24 * j + 8 * comp + i);
-                basis_project(g, K.Kr, K.Kd, pr);
+                for (int i = 0; i < 8; ++i) gn[i] = ld(cb.gn + 8 * p + i);
+                basis_project(gn, K.Kr, K.Kd, pr);
 #pragma unroll
                 for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
-                row[6] = sw * ld(A.fr_res + 3 * j + comp);
+                row[6] = sw * ld(cb.r + p);
+              }
+            }
+            gram_push(G, stage, row);
+          }
+          if (n_act > 0) {
+            const int m0 = ldi(A.mptr + c), m1 = ldi(A.mptr + c + 1);
+            for (int base = m0 + 32 * tw; base < m1; base += 32 * TEAM) {
+              const int q = base + lane;
+              const bool live = q < m1;
+              int64_t j = 0;
+              double coef = 0.0, sw = 0.0;
+              if (live) {
+                const int e = ldi(A.ment + q);
+                j = e / A.k;
+                const int s = e - (int)j * A.k;
+                const double a = A.fbw[e];
+                const double w_pair = A.fw * A.fwt[j] * a;
+                sup += w_pair;
+                sw = sqrt(w_pair);
+                const double sg = ((ldu8(cm.sgn + j) >> s) & 1u) ? -1.0 : 1.0;
+                coef = sw * a * sg;
+              }
+#pragma unroll 1
+              for (int comp = 0; comp < 3; ++comp) {
+                double row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                if (live) {
+                  double g[8], pr[6];
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) g[i] = ld(cm.G + 24 * j + 8 * comp + i);
+                  basis_project(g, K.Kr, K.Kd, pr);
+#pragma unroll
+                  for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
+                  row[6] = sw * ld(cm.res + 3 * j + comp);
+                }
+                gram_push(G, stage, row);
+              }
+            }
+          }
+        }
+        gram_store(G, gout);
+        sup = warp_sum(sup);
+        if (lane == 0) s_sup[warp] = sup;
+        __syncthreads();
+        if (tw == 0 && c < m) {
+          // combine the team's Grams in warp order
+          if (lane < 27) {
+            double v = 0.0;
+            for (int w = 0; w < TEAM; ++w) v += gram_col(gout + w * (STAGE + GOUT), lane);
+            A.partial[27 * c + lane] = v;
+          }
+          if (lane == 27) {
+            double su = 0.0;
+            for (int w = 0; w < TEAM; ++w) su += s_sup[warp + w];
+            A.wa[c] = A.arap_w * fmax(su, A.data_floor);
+          }
+        }
+        __syncthreads();
+      }
+      DSYNC(2);
+
+      // ---- P3: rigidity rows -> normal equations + first damped solve; rigidity cost
+      // of the iterate from the stored rows ----
+      for (int r = 0; r < team_rounds; ++r) {
+        const int c = r * GTEAM + gteam;
+        Gram G;
+        if (c < m) {
+          const int q0 = ldi(A.iptr + c), q1 = ldi(A.iptr + c + 1);
+          for (int base = q0 + 32 * tw; base < q1; base += 32 * TEAM) {
+            const int q = base + lane;
+            const bool live = q < q1;
+            int i0 = 0, i1 = 0, side = 0;
+            double sw = 0.0, swa = 0.0, swr = 0.0;
+            const double* er = A.erows;
+            if (live) {
+              const int e2 = ldi(A.ient + q);
+              const int e = e2 >> 1;
+              side = e2 & 1;
+              i0 = A.edges[2 * e];
+              i1 = A.edges[2 * e + 1];
+              const double base_w = A.ew[e] * 0.5 * (ld(A.wa + i0) + ld(A.wa + i1));
+              sw = sqrt(0.5 * base_w);
+              swa = sqrt(0.5 * base_w * A.angle_w);
+              swr = sqrt(0.5 * base_w * A.rot_w);
+              er = A.erows + (size_t)ER * e;
+            }
+            double row[8];
+            // length row of this bin
+#pragma unroll
+            for (int i = 0; i < 6; ++i) row[i] = live ? sw * ld(er + 6 * side + i) : 0.0;
+            row[6] = live ? sw * ld(er + 12) : 0.0;
+            row[7] = 0.0;
+            gram_push(G, stage, row);
+            // angle 0->1: bin 0 is side a ([13,19)), bin 1 side b ([19,25))
+#pragma unroll
+            for (int i = 0; i < 6; ++i) row[i] = live ? swa * ld(er + 13 + 6 * side + i) : 0.0;
+            row[6] = live ? swa * ld(er + 25) : 0.0;
+            gram_push(G, stage, row);
+            // angle 1->0: bin 1 is side a ([26,32)), bin 0 side b ([32,38))
+#pragma unroll
+            for (int i = 0; i < 6; ++i) row[i] = live ? swa * ld(er + 32 - 6 * side + i) : 0.0;
+            row[6] = live ? swa * ld(er + 38) : 0.0;
+            gram_push(G, stage, row);
+#pragma unroll 1
+            for (int rr = 0; rr < 4; ++rr) {
+              if (live) {
+                rotation_row(s_w, i0, i1, side, swr, rr, row);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) row[i] = 0.0;
               }
               gram_push(G, stage, row);
             }
           }
         }
-      }
-      gram_store(G, gout);
-      sup = warp_sum(sup);
-      if (lane == 0) s_sup[warp] = sup;
-      __syncthreads();
-      if (tw == 0 && c < m) {
-        // combine the team's Grams in warp order
-        if (lane < 27) {
-          double v = 0.0;
-          for (int w = 0; w < TEAM; ++w) v += gram_col(gout + w * (STAGE + GOUT), lane);
-          A.partial[27 * c + lane] = v;
-        }
-        if (lane == 27) {
-          double su = 0.0;
-          for (int w = 0; w < TEAM; ++w) su += s_sup[warp + w];
-          A.wa[c] = A.arap_w * fmax(su, A.data_floor);
-        }
-      }
-      __syncthreads();
-    }
-    DSYNC(2);
-
-    // ---- P3: rigidity rows -> normal equations + first damped solve; rigidity cost ----
-    double* okn = A.oknorm + (size_t)parity * 2 * m;
-    for (int r = 0; r < team_rounds; ++r) {
-      const int c = r * GTEAM + gteam;
-      Gram G;
-      if (c < m) {
-        const int q0 = ldi(A.iptr + c), q1 = ldi(A.iptr + c + 1);
-        for (int base = q0 + 32 * tw; base < q1; base += 32 * TEAM) {
-          const int q = base + lane;
-          const bool live = q < q1;
-          int i0 = 0, i1 = 0, side = 0;
-          double sw = 0.0, swa = 0.0, swr = 0.0;
-          const double* er = A.erows;
-          if (live) {
-            const int e2 = ldi(A.ient + q);
-            const int e = e2 >> 1;
-            side = e2 & 1;
-            i0 = A.edges[2 * e];
-            i1 = A.edges[2 * e + 1];
-            const double base_w = A.ew[e] * 0.5 * (ld(A.wa + i0) + ld(A.wa + i1));
-            sw = sqrt(0.5 * base_w);
-            swa = sqrt(0.5 * base_w * A.angle_w);
-            swr = sqrt(0.5 * base_w * A.rot_w);
-            er = A.erows + (size_t)ER * e;
+        gram_store(G, gout);
+        TRACE(32);
+        __syncthreads();
+        if (tw == 0 && c < m) {
+          if (lane < 27) {
+            double v = 0.0;
+            for (int w = 0; w < TEAM; ++w) v += gram_col(gout + w * (STAGE + GOUT), lane);
+            v = ld(A.partial + 27 * c + lane) + v;
+            A.partial[27 * c + lane] = v;
+            s_col[team][lane] = v;
           }
-          double row[8];
-          // length row of this bin
-#pragma unroll
-          for (int i = 0; i < 6; ++i) row[i] = live ? sw * ld(er + 6 * side + i) : 0.0;
-          row[6] = live ? sw * ld(er + 12) : 0.0;
-          row[7] = 0.0;
-          gram_push(G, stage, row);
-          // angle 0->1: bin 0 is side a ([13,19)), bin 1 side b ([19,25))
-#pragma unroll
-          for (int i = 0; i < 6; ++i) row[i] = live ? swa * ld(er + 13 + 6 * side + i) : 0.0;
-          row[6] = live ? swa * ld(er + 25) : 0.0;
-          gram_push(G, stage, row);
-          // angle 1->0: bin 1 is side a ([26,32)), bin 0 side b ([32,38))
-#pragma unroll
-          for (int i = 0; i < 6; ++i) row[i] = live ? swa * ld(er + 32 - 6 * side + i) : 0.0;
-          row[6] = live ? swa * ld(er + 38) : 0.0;
-          gram_push(G, stage, row);
-#pragma unroll 1
-          for (int rr = 0; rr < 4; ++rr) {
-            if (live) {
-              rotation_row(s_w, i0, i1, side, swr, rr, row);
-            } else {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) row[i] = 0.0;
+          __syncwarp();
+          if (lane == 0) {
+            double d[6];
+            const bool good = solve6(s_col[team], ld(A.lam + c), d);
+            double nn = 0.0;
+            for (int i = 0; i < 6; ++i) {
+              A.delta[6 * c + i] = d[i];
+              nn += d[i] * d[i];
             }
-            gram_push(G, stage, row);
+            okn[2 * c] = good ? 1.0 : 0.0;
+            okn[2 * c + 1] = sqrt(nn);
           }
         }
+        __syncthreads();
+        TRACE(34);
       }
-      gram_store(G, gout);
-      TRACE(32);
-      __syncthreads();
-      if (tw == 0 && c < m) {
-        if (lane < 27) {
-          double v = 0.0;
-          for (int w = 0; w < TEAM; ++w) v += gram_col(gout + w * (STAGE + GOUT), lane);
-          v = ld(A.partial + 27 * c + lane) + v;
-          A.partial[27 * c + lane] = v;
-          s_col[team][lane] = v;
-        }
-        __syncwarp();
-        if (lane == 0) {
-          double d[6];
-          const bool good = solve6(s_col[team], ld(A.lam + c), d);
-          double nn = 0.0;
-          for (int i = 0; i < 6; ++i) {
-            A.delta[6 * c + i] = d[i];
-            nn += d[i] * d[i];
-          }
-          okn[2 * c] = good ? 1.0 : 0.0;
-          okn[2 * c + 1] = sqrt(nn);
-        }
+      for (int ch = gw_rev; ch < nch_e; ch += GW) {
+        double acc = 0.0;
+        const int e = ch * CHUNK + lane;
+        if (e < A.n_edges) acc = edge_cost_rows(A, s_w, A.wa, A.erows + (size_t)ER * e, e);
+        acc = warp_sum(acc);
+        if (lane == 0) cs_e0[ch] = acc;
       }
-      __syncthreads();
-      TRACE(34);
-    }
-    for (int ch = gw_rev; ch < nch_e; ch += GW) {
-      double acc = 0.0;
-      const int e = ch * CHUNK + lane;
-      if (e < A.n_edges) acc = edge_cost_rows(A, s_w, A.wa, A.erows + (size_t)ER * e, e);
-      acc = warp_sum(acc);
-      if (lane == 0) cs_e[ch] = acc;
+    } else {
+      // after a stall the iterate and its linearization are unchanged: re-solve the
+      // stored normal equations with the raised damping (solver.py:348-355)
+      for (int c = gt; c < m; c += GT) resolve_control(A, c, okn);
     }
     bool accepted = false;
     double cost_before = 0.0, cost_after = 0.0;
     for (int attempt = 0; attempt <= A.max_retries; ++attempt) {
       if (attempt > 0) {
         okn = A.oknorm + (size_t)parity * 2 * m;
-        for (int c = gt; c < m; c += GT) {
-          double part[27], d[6];
-          for (int i = 0; i < 27; ++i) part[i] = ld(A.partial + 27 * c + i);
-          const bool good = solve6(part, A.lam[c], d);
-          double nn = 0.0;
-          for (int i = 0; i < 6; ++i) {
-            A.delta[6 * c + i] = d[i];
-            nn += d[i] * d[i];
-          }
-          okn[2 * c] = good ? 1.0 : 0.0;
-          okn[2 * c + 1] = sqrt(nn);
-        }
+        for (int c = gt; c < m; c += GT) resolve_control(A, c, okn);
       }
       DSYNC(attempt == 0 ? 3 : 4);
       // prefetch this thread's step inputs (one control per thread when m <= 512)
@@ -337,9 +499,8 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         for (int i = 0; i < 6; ++i) pD[i] = ld(A.delta + 6 * pc + i);
       }
       if (attempt == 0) {
-        double t3[3];
-        block_totals(cs_p, nch_p, cs_m, nch_m, cs_e, nch_e, s_part, t3);
-        cost_before = t3[0] + t3[1] + t3[2];
+        if (need_lin) cb_arap = seg_total(cs_e0, nch_e, s_part);
+        cost_before = (cb_icp + cb_feat) + cb_arap;
       }
       TRACE(53);
       // all solves ok? largest step norm (identical in every CTA)
@@ -363,7 +524,6 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
           allok = fmin(allok, s_part[2 * w]);
           mx = fmax(mx, s_part[2 * w + 1]);
         }
-        __syncthreads();
         parity ^= 1;
         if (!(allok > 0.5)) {
           // raise the damping of the failed controls only, retry (solver.py:321-326)
@@ -394,38 +554,60 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         dq_to_transform(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
       for (int c = gt; c < m; c += GT)
         for (int i = 0; i < 8; ++i) tent[8 * c + i] = s_w[8 * c + i];
+      smem_is_cur = false;
       __syncthreads();
       TRACE(52);
-      // ---- P6: cost at the tentative warps, frozen weights and correspondences ----
-      for (int ch = gw; ch < nch_p + nch_m + nch_e; ch += GW) {
-        double acc = 0.0;
-        if (ch < nch_p) {
-          const int64_t p = (int64_t)ch * CHUNK + lane;
-          if (p < n) acc = point_value(A, s_w, p);
-          acc = warp_sum(acc);
-          if (lane == 0) cs_p[ch] = acc;
-        } else if (ch < nch_p + nch_m) {
-          const int64_t j = (int64_t)(ch - nch_p) * CHUNK + lane;
-          if (j < n_act) acc = match_eval(A, s_w, j, false, false);
-          acc = warp_sum(acc);
-          if (lane == 0) cs_m[ch - nch_p] = acc;
-        } else {
-          const int e = (ch - nch_p - nch_m) * CHUNK + lane;
-          if (e < A.n_edges) acc = edge_value(A, s_w, s_T, A.wa, e);
-          acc = warp_sum(acc);
-          if (lane == 0) cs_e[ch - nch_p - nch_m] = acc;
+      // ---- P6: cost at the tentative warps with frozen weights and correspondences
+      // (set 0) + speculative relinearization there (buffer 1 - pb, costs in set 1) ----
+      {
+        const PBuf ob = pbuf(A, pb);
+        const PBuf nb = pbuf(A, 1 - pb);
+        const MBuf nm = mbuf(A, 1 - pb);
+        for (int ch = gw; ch < nch_p + nch_m + nch_e; ch += GW) {
+          if (ch < nch_p) {
+            const int64_t p = (int64_t)ch * CHUNK + lane;
+            double co = 0.0, cn = 0.0;
+            int vd;
+            if (p < n) cn = point_step(A, s_w, p, &ob, nb, &co, &vd);
+            co = warp_sum(co);
+            cn = warp_sum(cn);
+            if (lane == 0) {
+              cs_p0[ch] = co;
+              cs_p1[ch] = cn;
+            }
+          } else if (ch < nch_p + nch_m) {
+            const int64_t j = (int64_t)(ch - nch_p) * CHUNK + lane;
+            double cf = 0.0;
+            if (j < n_act) cf = match_step(A, s_w, j, nm);
+            cf = warp_sum(cf);
+            if (lane == 0) {
+              cs_m0[ch - nch_p] = cf;
+              cs_m1[ch - nch_p] = cf;
+            }
+          } else {
+            const int e = (ch - nch_p - nch_m) * CHUNK + lane;
+            double acc = 0.0;
+            if (e < A.n_edges) acc = edge_value(A, s_w, s_T, A.wa, e);
+            acc = warp_sum(acc);
+            if (lane == 0) cs_e0[ch - nch_p - nch_m] = acc;
+          }
         }
       }
       DSYNC(6);
       {
-        double t3[3];
-        block_totals(cs_p, nch_p, cs_m, nch_m, cs_e, nch_e, s_part, t3);
-        cost_after = t3[0] + t3[1] + t3[2];
+        const double t_p = seg_total(cs_p0, nch_p, s_part);
+        const double t_m = seg_total(cs_m0, nch_m, s_part);
+        const double t_e = seg_total(cs_e0, nch_e, s_part);
+        cost_after = (t_p + t_m) + t_e;
       }
       if (cost_after < cost_before) {
         double* tmp = cur;
         cur = tent;
         tent = tmp;
+        pb = 1 - pb;
+        smem_is_cur = true;
+        cb_icp = seg_total(cs_p1, nch_p, s_part);
+        cb_feat = seg_total(cs_m1, nch_m, s_part);
         for (int c = gt; c < m; c += GT) A.lam[c] = fmax(A.lam[c] * A.lam_dec, A.lam_min);
         ++accepted_steps;
         if (rank == 0 && threadIdx.x == 0) {
@@ -458,69 +640,59 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     if (converged) break;
     if (!accepted) {
       stalled = true;
+      need_lin = false;
       if (rank == 0 && threadIdx.x == 0) A.stalled_hist[outer] = 1;
       continue;
     }
+    need_lin = true;
     if (cost_before - cost_after <= A.cost_tol * fmax(cost_before, 1e-30)) {
       converged = true;
       break;
     }
   }
 
-  // ---- final report: relink at the solution, recompute robust and rigidity weights
-  // (solver.py:360-376) ----
-  load_state(A, cur, s_w, s_T);
-  int my_valid = 0;
-  for (int ch = gw; ch < nch_p + nch_m; ch += GW) {
-    double acc = 0.0;
-    if (ch < nch_p) {
-      const int64_t p = (int64_t)ch * CHUNK + lane;
-      int v = 0;
-      if (p < n) acc = point_relink(A, s_w, p, false, &v);
-      my_valid += v;
-      acc = warp_sum(acc);
-      if (lane == 0) cs_p[ch] = acc;
-    } else {
-      const int64_t j = (int64_t)(ch - nch_p) * CHUNK + lane;
-      if (j < n_act) acc = match_eval(A, s_w, j, true, false);
-      acc = warp_sum(acc);
-      if (lane == 0) cs_m[ch - nch_p] = acc;
+  // ---- final report (solver.py:360-376). Record buffer pb is the relinearization at
+  // the solution (robust weights recomputed there), so only the support -> rigidity
+  // weights and the rigidity cost with them remain ----
+  if (!smem_is_cur) load_state(A, cur, s_w, s_T);
+  TRACE(72);
+  {
+    const PBuf cb = pbuf(A, pb);
+    int my_valid = 0;
+    for (int64_t p = gt; p < n; p += GT) my_valid += ldu8(cb.valid + p) ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) my_valid += __shfl_xor_sync(0xffffffffu, my_valid, o);
+    if (lane == 0) s_cnt[warp] = my_valid;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < NWARPS; ++w) t += s_cnt[w];
+      A.counts[rank] = t;
     }
-  }
-  for (int o = 16; o > 0; o >>= 1) my_valid += __shfl_xor_sync(0xffffffffu, my_valid, o);
-  if (lane == 0) s_cnt[warp] = my_valid;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < NWARPS; ++w) t += s_cnt[w];
-    A.counts[rank] = t;
-  }
-  for (int c = gt; c < m; c += GT)
-    for (int i = 0; i < 8; ++i) A.warps_out[8 * c + i] = s_w[8 * c + i];
-  DSYNC(7);
-  // support per control with the recomputed robust weights -> wa
-  for (int c = gw; c < m; c += GW) {
-    double sup = 0.0;
-    const int q0 = ldi(A.cptr + c), q1 = ldi(A.cptr + c + 1);
-    for (int q = q0 + lane; q < q1; q += 32) {
-      const int e = ldi(A.cent + q);
-      const int64_t p = e >> 3;
-      if (!ldu8(A.cvalid + p)) continue;
-      const double rs = ld(A.pr_rs + p);
-      sup += rs * rs * A.bw[p * A.k + (e & 7)];
-    }
-    if (n_act > 0) {
-      const int m0 = ldi(A.mptr + c), m1 = ldi(A.mptr + c + 1);
-      for (int q = m0 + lane; q < m1; q += 32) {
-        const int e = ldi(A.ment + q);
-        sup += A.fw * A.fwt[e / A.k] * A.fbw[e];
+    for (int c = gt; c < m; c += GT)
+      for (int i = 0; i < 8; ++i) A.warps_out[8 * c + i] = s_w[8 * c + i];
+    for (int c = gw; c < m; c += GW) {
+      double sup = 0.0;
+      const int q0 = ldi(A.cptr + c), q1 = ldi(A.cptr + c + 1);
+      for (int q = q0 + lane; q < q1; q += 32) {
+        const int e = ldi(A.cent + q);
+        const int64_t p = e >> 3;
+        if (!ldu8(cb.valid + p)) continue;
+        const double rs = ld(cb.rs + p);
+        sup += rs * rs * A.bw[p * A.k + (e & 7)];
       }
-    }
-    sup = warp_sum(sup);
-    if (lane == 0) {
-      const double w = A.arap_w * fmax(sup, A.data_floor);
-      A.wa[c] = w;
-      A.wa_out[c] = w;
+      if (n_act > 0) {
+        const int m0 = ldi(A.mptr + c), m1 = ldi(A.mptr + c + 1);
+        for (int q = m0 + lane; q < m1; q += 32) {
+          const int e = ldi(A.ment + q);
+          sup += A.fw * A.fwt[e / A.k] * A.fbw[e];
+        }
+      }
+      sup = warp_sum(sup);
+      if (lane == 0) {
+        const double w = A.arap_w * fmax(sup, A.data_floor);
+        A.wa[c] = w;
+        A.wa_out[c] = w;
+      }
     }
   }
   DSYNC(8);
@@ -529,17 +701,16 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     const int e = ch * CHUNK + lane;
     if (e < A.n_edges) acc = edge_value(A, s_w, s_T, A.wa, e);
     acc = warp_sum(acc);
-    if (lane == 0) cs_e[ch] = acc;
+    if (lane == 0) cs_e0[ch] = acc;
   }
   DSYNC(9);
-  double parts[3];
-  block_totals(cs_p, nch_p, cs_m, nch_m, cs_e, nch_e, s_part, parts);
+  const double t_arap = seg_total(cs_e0, nch_e, s_part);
   if (rank == 0 && threadIdx.x == 0) {
     dt_report* R = A.report;
-    R->icp_cost = parts[0];
-    R->feature_cost = parts[1];
-    R->arap_cost = parts[2];
-    R->total_cost = parts[0] + parts[1] + parts[2];
+    R->icp_cost = cb_icp;
+    R->feature_cost = cb_feat;
+    R->arap_cost = t_arap;
+    R->total_cost = (cb_icp + cb_feat) + t_arap;
     int nc = 0;
     for (int i = 0; i < C; ++i) nc += __ldcg(A.counts + i);
     R->n_correspondences = nc;

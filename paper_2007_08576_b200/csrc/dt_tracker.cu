@@ -384,14 +384,14 @@ int ensure_match_capacity(dt_tracker* t, int64_t cap) {
   DT_TRY(dalloc(t, &t->fbidx, k * cap));
   DT_TRY(dalloc(t, &t->fbw, k * cap));
   DT_TRY(dalloc(t, &t->ment, k * cap));
-  DT_TRY(dalloc(t, &t->fr_res, 3 * cap));
-  DT_TRY(dalloc(t, &t->fr_G, 24 * cap));
-  DT_TRY(dalloc(t, &t->fr_sgn, cap));
+  DT_TRY(dalloc(t, &t->fr_res, 2 * 3 * cap));
+  DT_TRY(dalloc(t, &t->fr_G, 2 * 24 * cap));
+  DT_TRY(dalloc(t, &t->fr_sgn, 2 * cap));
   t->match_cap = cap;
   {
     const int64_t nch = (t->n + CHUNK - 1) / CHUNK + (cap + CHUNK - 1) / CHUNK +
                         (t->ne + CHUNK - 1) / CHUNK;
-    DT_TRY(dalloc(t, &t->csum, nch));
+    DT_TRY(dalloc(t, &t->csum, 2 * nch));
   }
   t->args_dirty = true;
   return DT_OK;
@@ -440,6 +440,7 @@ void fill_args(dt_tracker* t) {
   a.cvalid = t->cvalid; a.cobs = t->cobs; a.cnrm = t->cnrm;
   a.pr_r = t->pr_r; a.pr_rs = t->pr_rs; a.pr_gn = t->pr_gn; a.pr_sgn = t->pr_sgn;
   a.fr_res = t->fr_res; a.fr_G = t->fr_G; a.fr_sgn = t->fr_sgn;
+  a.ma_cap = (int)t->match_cap;
   a.counts = t->counts;
   a.report = t->report;
   a.cost_hist = t->cost_hist;
@@ -809,13 +810,13 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_TRY(dalloc(t, &t->partial, 27 * m));
   DT_TRY(dalloc(t, &t->delta, 6 * m));
   DT_TRY(dalloc(t, &t->oknorm, 4 * m));
-  DT_TRY(dalloc(t, &t->cvalid, n));
-  DT_TRY(dalloc(t, &t->cobs, 3 * n));
-  DT_TRY(dalloc(t, &t->cnrm, 3 * n));
-  DT_TRY(dalloc(t, &t->pr_r, n));
-  DT_TRY(dalloc(t, &t->pr_rs, n));
-  DT_TRY(dalloc(t, &t->pr_gn, 8 * n));
-  DT_TRY(dalloc(t, &t->pr_sgn, n));
+  DT_TRY(dalloc(t, &t->cvalid, 2 * n));
+  DT_TRY(dalloc(t, &t->cobs, 2 * 3 * n));
+  DT_TRY(dalloc(t, &t->cnrm, 2 * 3 * n));
+  DT_TRY(dalloc(t, &t->pr_r, 2 * n));
+  DT_TRY(dalloc(t, &t->pr_rs, 2 * n));
+  DT_TRY(dalloc(t, &t->pr_gn, 2 * 8 * n));
+  DT_TRY(dalloc(t, &t->pr_sgn, 2 * n));
   DT_TRY(dalloc(t, &t->counts, 1024));
   DT_TRY(dalloc(t, &t->erows, 40 * (n_edges > 0 ? n_edges : 1)));
   DT_TRY(dalloc(t, &t->bad_flag, 1));

@@ -21,12 +21,12 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-NAMES = {0: "start", 1: "relink+linearize", 1.2: "  load warps+transforms",
+NAMES = {0: "start", 1: "relink+linearize",
          2: "data gather", 3: "rigidity: edge costs", 3.2: "  rigidity gather",
          3.4: "  team combine+solve", 5: "apply step", 5.2: "  transforms+tent store",
          5.3: "  cost_before totals", 5.4: "  ok/step-norm reduce", 5.5: "  apply_step x m",
          2.2: "  edge unit rows",
-         6: "value pass", 7: "final relink", 8: "final data", 9: "final rigidity", 99: "end"}
+         6: "value pass + spec relink", 7.2: "final load", 8: "final support", 1.2: "  load warps+transforms", 9: "final rigidity", 99: "end"}
 
 
 def main():
