@@ -285,6 +285,10 @@ int dt_tracker_get_phase_ms(dt_tracker* t, float* ms);
 /* With profiling on, the solver kernel stamps (phase code, globaltimer ns) pairs at every
  * cluster barrier of the last frame; returns the number of pairs copied into buf. */
 int dt_tracker_get_trace(dt_tracker* t, long long* buf, int cap);
+/* With profiling on, every CTA of the solver also stamps its ARRIVAL time at each barrier:
+ * buf[0] = CTAs, buf[1] = barriers stamped, buf[2 + cta * per_cta + b] = ns. Copies at
+ * most cap values; returns per_cta (the stride), 0 when profiling is off. */
+int dt_tracker_get_arrivals(dt_tracker* t, long long* buf, int cap);
 /* Per-outer-iteration histories of the last frame (host): cost_history
  * (max_outer_iters,2), lambda_history (max_outer_iters,2), stalled (max_outer_iters). */
 int dt_tracker_get_history(dt_tracker* t, double* cost_history, double* lambda_history,

@@ -124,6 +124,7 @@ _SIGNATURES: dict[str, list] = {
     "dt_tracker_set_profiling": [P, C.c_int],
     "dt_tracker_get_phase_ms": [P, P],
     "dt_tracker_get_trace": [P, P, C.c_int],
+    "dt_tracker_get_arrivals": [P, P, C.c_int],
 }
 
 N_PHASES = 6

@@ -268,6 +268,19 @@ class DeviceTracker:
             check(n, "dt_tracker_get_trace")
         return buf[:n].copy()
 
+    def arrivals(self) -> np.ndarray:
+        """(barriers, CTAs) globaltimer ns at which each CTA of the solver arrived at each
+        domain barrier (last frame, profiling on)."""
+        cap = 2 + 1024 * 256
+        buf = np.zeros(cap, dtype=np.int64)
+        stride = lib.dt_tracker_get_arrivals(self._h, _host_ptr(buf), cap)
+        if stride < 0:
+            check(stride, "dt_tracker_get_arrivals")
+        if stride == 0:
+            return np.zeros((0, 0), dtype=np.int64)
+        n_cta, n_bar = int(buf[0]), min(int(buf[1]), stride)
+        return buf[2:2 + n_cta * stride].reshape(n_cta, stride)[:, :n_bar].T.copy()
+
     def device_outputs(self):
         w, p, n = C.c_void_p(), C.c_void_p(), C.c_void_p()
         check(lib.dt_tracker_device_outputs(self._h, C.byref(w), C.byref(p), C.byref(n)),

@@ -226,6 +226,31 @@ __device__ __forceinline__ void dq_to_transform(const double* W, double R[9], do
   t[2] = 2.0 * (w * dz - dw * z - c2) / s2;
 }
 
+// dq_to_transform with one reciprocal instead of 12 divisions (ulp-level difference;
+// used inside the LM solver, whose parity is tolerance-based)
+__device__ __forceinline__ void dq_to_transform_fast(const double* W, double R[9], double t[3]) {
+  const double w = W[0], x = W[1], y = W[2], z = W[3];
+  const double dw = W[4], dx = W[5], dy = W[6], dz = W[7];
+  const double s2 = w * w + x * x + y * y + z * z;
+  const double is = 1.0 / s2;
+  R[0] = (w * w + x * x - y * y - z * z) * is;
+  R[1] = (2.0 * (x * y - w * z)) * is;
+  R[2] = (2.0 * (x * z + w * y)) * is;
+  R[3] = (2.0 * (x * y + w * z)) * is;
+  R[4] = (w * w - x * x + y * y - z * z) * is;
+  R[5] = (2.0 * (y * z - w * x)) * is;
+  R[6] = (2.0 * (x * z - w * y)) * is;
+  R[7] = (2.0 * (y * z + w * x)) * is;
+  R[8] = (w * w - x * x - y * y + z * z) * is;
+  // t = 2 (qw du - dw qu - du x qu) / s2 (cross3 order: geometry.py:51-63)
+  const double c0 = dy * z - dz * y;
+  const double c1 = dz * x - dx * z;
+  const double c2 = dx * y - dy * x;
+  t[0] = 2.0 * (w * dx - dw * x - c0) * is;
+  t[1] = 2.0 * (w * dy - dw * y - c1) * is;
+  t[2] = 2.0 * (w * dz - dw * z - c2) * is;
+}
+
 __device__ __forceinline__ void xform(const double R[9], const double t[3], double px, double py,
                                       double pz, double o[3]) {
   o[0] = R[0] * px + R[1] * py + R[2] * pz + t[0];
@@ -548,6 +573,46 @@ __device__ __forceinline__ void apply_step_one(const double* W, const double* de
   for (int i = 0; i < 4; ++i) {
     r[i] = real[i] / norm;
     d[i] = dual[i] / norm;
+  }
+  const double dot = r[0] * d[0] + r[1] * d[1] + r[2] * d[2] + r[3] * d[3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    out[i] = r[i];
+    out[4 + i] = d[i] - dot * r[i];
+  }
+}
+
+// apply_step_one with one sincos and one reciprocal (ulp-level; LM solver only)
+__device__ __forceinline__ void apply_step_one_fast(const double* W, const double* delta, double* out) {
+  const double o0 = delta[0], o1 = delta[1], o2 = delta[2];
+  const double angle = sqrt(o0 * o0 + o1 * o1 + o2 * o2);
+  // 0.5 * np.sinc(angle / (2 pi)); numpy 2.x: y = pi x, y := eps where y == 0, sin(y)/y
+  const double xs = angle / (2.0 * M_PI);
+  double y = M_PI * xs;
+  if (y == 0.0) y = 2.220446049250313e-16;
+  double sy, cy;
+  sincos(y, &sy, &cy);  // y = angle / 2 up to an ulp
+  const double half_sinc = 0.5 * (sy / y);
+  const double er[4] = {cy, o0 * half_sinc, o1 * half_sinc, o2 * half_sinc};
+  const double pv[4] = {0.0, delta[3], delta[4], delta[5]};
+  double ed[4];
+  quat_mul(pv, er, ed);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) ed[i] = 0.5 * ed[i];
+  double real[4], d1[4], d2[4];
+  quat_mul(er, W, real);
+  quat_mul(er, W + 4, d1);
+  quat_mul(ed, W, d2);
+  double dual[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) dual[i] = d1[i] + d2[i];
+  const double norm = sqrt(real[0] * real[0] + real[1] * real[1] + real[2] * real[2] + real[3] * real[3]);
+  const double inorm = 1.0 / norm;
+  double r[4], d[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    r[i] = real[i] * inorm;
+    d[i] = dual[i] * inorm;
   }
   const double dot = r[0] * d[0] + r[1] * d[1] + r[2] * d[2] + r[3] * d[3];
 #pragma unroll

@@ -45,7 +45,7 @@ constexpr int GOUT = 64;       // per-warp 8x8 Gram readout
 constexpr int M_MAX_SMEM = 1100;
 
 size_t solver_smem_bytes(int m) {
-  return sizeof(double) * ((size_t)20 * m + (size_t)NWARPS * (STAGE + GOUT));
+  return sizeof(double) * ((size_t)21 * m + (size_t)NWARPS * (STAGE + GOUT));
 }
 
 // 27 normal-equation columns from the 8x8 Gram of rows [J0..J5, wv, 0]:
@@ -148,7 +148,7 @@ __device__ __forceinline__ void load_state(const SolverArgs& A, const double* sr
   for (int i = threadIdx.x; i < n8; i += blockDim.x) s_w[i] = ld(src + i);
   __syncthreads();
   for (int c = threadIdx.x; c < A.m; c += blockDim.x)
-    dq_to_transform(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
+    dq_to_transform_fast(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
   __syncthreads();
 }
 
@@ -409,11 +409,14 @@ __device__ __forceinline__ bool solve6(const double* part, double lam, double de
       ++tn;                                                        \
     }                                                              \
   } while (0)
-#define DSYNC(phase)         \
-  do {                       \
-    TRACE(10 * (phase));     \
-    dom.sync();              \
-    TRACE(10 * (phase) + 1); \
+#define DSYNC(phase)                                                       \
+  do {                                                                     \
+    TRACE(10 * (phase));                                                   \
+    if (A.arrivals && threadIdx.x == 0 && nbar < A.arr_cap)                \
+      A.arrivals[2 + (size_t)rank * A.arr_cap + nbar] = gtimer();          \
+    ++nbar;                                                                \
+    dom.sync();                                                            \
+    TRACE(10 * (phase) + 1);                                               \
   } while (0)
 
 #include "dt_solver_kernel.cuh"

@@ -10,7 +10,10 @@
 
 namespace dt {
 
-constexpr int SOLVER_THREADS = 512;
+#ifndef DT_SOLVER_THREADS
+#define DT_SOLVER_THREADS 512
+#endif
+constexpr int SOLVER_THREADS = DT_SOLVER_THREADS;
 constexpr int CHUNK = 32;  // items per deterministic partial sum (one per lane)
 
 struct SolverArgs {
@@ -84,7 +87,18 @@ struct SolverArgs {
   // (code, globaltimer ns) pairs
   long long* trace;
   int trace_cap;
+  // optional per-CTA barrier arrival stamps: arrivals[0] = CTAs, [1] = count,
+  // arrivals[2 + rank * arr_cap + b]
+  long long* arrivals;
+  int arr_cap;
+  // last-arriver reduction slots (see red_commit): RED_SLOTS x (2 G + 2) doubles and
+  // RED_SLOTS x (G + 1) counters, G = red_g groups of 32 items
+  double* red;
+  unsigned* redc;
+  int red_g;
 };
+
+constexpr int RED_SLOTS = 5;
 
 size_t solver_smem_bytes(int m);
 // mode: 0 = one cluster of `cluster` CTAs per sequence; 1 = one cooperative grid over

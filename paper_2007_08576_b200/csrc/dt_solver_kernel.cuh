@@ -13,7 +13,10 @@
 // directly at P2; a stalled iteration keeps its linearization -- the reference recomputes
 // it at the same warps, bit for bit the same -- and only re-solves.
 
-constexpr int TEAM = 4;
+#ifndef DT_TEAM
+#define DT_TEAM 4
+#endif
+constexpr int TEAM = DT_TEAM;
 constexpr int TEAMS_PER_CTA = NWARPS / TEAM;
 
 // one of the two per-point record buffers (correspondence + linearization)
@@ -157,44 +160,116 @@ __device__ __forceinline__ double match_step(const SolverArgs& A, const double* 
   return cost;
 }
 
-// Fixed-order sum of one chunk-sum segment (4 loads in flight per thread, thread order,
-// warp xor tree, warps in order); identical in every CTA. Whole CTA; s_part >= NWARPS.
-__device__ __forceinline__ double seg_total(const double* a, int n, double* s_part) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bd = (int)blockDim.x;
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += 4 * bd) {
-    const double v0 = ld(a + i);
-    const double v1 = i + bd < n ? ld(a + i + bd) : 0.0;
-    const double v2 = i + 2 * bd < n ? ld(a + i + 2 * bd) : 0.0;
-    const double v3 = i + 3 * bd < n ? ld(a + i + 3 * bd) : 0.0;
-    acc += (v0 + v1) + (v2 + v3);
+// ---------------------------------------------------------------------------------
+// Last-arriver reductions. Every item (a chunk of 32 points / matches / edges, or one
+// control) commits its value(s); the last warp to commit an item of a 32-item group folds
+// the group in a fixed order, the last group folds the groups in a fixed order and
+// publishes the total. The folds never depend on which warp or CTA produced an item nor
+// on the arrival order, so totals are deterministic and independent of the launch shape,
+// and after the domain barrier every CTA reads one line instead of every item value
+// (all-CTA reads of the item arrays hot-spot L2: ~8 us per phase measured).
+// ---------------------------------------------------------------------------------
+
+struct RedSlot {
+  double* gsum;    // [2][G] group values
+  double* total;   // [2]
+  unsigned* gcnt;  // [G] per-group commit counters (reset by the group's last arriver)
+  unsigned* tcnt;  // group counter (reset by the last group)
+  int G;
+};
+
+// slots: 0 points (value-pass cost, relinearization cost), 1 matches, 2 rigidity cost of
+// the iterate (P3) and of the solution, 3 controls (all solves ok = min, max step norm),
+// 4 rigidity cost in the value pass
+__device__ __forceinline__ RedSlot red_slot(const SolverArgs& A, int s) {
+  const int G = A.red_g;
+  double* base = A.red + (size_t)s * (2 * G + 2);
+  unsigned* cb = A.redc + (size_t)s * (G + 1);
+  return {base, base + 2 * G, cb, cb + G, G};
+}
+
+// OP 0: sum; OP 1: (min, max)
+template <int OP>
+__device__ __forceinline__ double red_op(int k, double a, double b) {
+  if (OP == 0) return a + b;
+  return k == 0 ? fmin(a, b) : fmax(a, b);
+}
+
+template <int OP>
+__device__ __forceinline__ double red_id(int k) {
+  return OP == 0 ? 0.0 : (k == 0 ? INFINITY : -INFINITY);
+}
+
+template <int OP>
+__device__ __forceinline__ double warp_red(int k, double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = red_op<OP>(k, v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Commit item ch (of nch) with the warp-uniform values v[NV]. Whole warp.
+template <int NV, int OP>
+__device__ __forceinline__ void red_commit(const RedSlot& R, double* const (&vals)[NV], int ch,
+                                           int nch, const double (&v)[NV]) {
+  const int lane = threadIdx.x & 31;
+  const int g = ch >> 5;
+  unsigned old = 0;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) vals[k][ch] = v[k];
+    __threadfence();
+    old = atomicAdd(R.gcnt + g, 1u);
   }
-  acc = warp_sum(acc);
-  __syncthreads();
-  if (lane == 0) s_part[warp] = acc;
-  __syncthreads();
-  double t = 0.0;
-  for (int w = 0; w < NWARPS; ++w) t += s_part[w];
-  return t;
+  old = __shfl_sync(0xffffffffu, old, 0);
+  const int gs = min(32, nch - 32 * g);
+  if ((int)old != gs - 1) return;
+  __threadfence();
+  double x[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    x[k] = lane < gs ? ld(vals[k] + 32 * g + lane) : red_id<OP>(k);
+    x[k] = warp_red<OP>(k, x[k]);
+  }
+  unsigned old2 = 0;
+  if (lane == 0) {
+    R.gcnt[g] = 0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) R.gsum[k * R.G + g] = x[k];
+    __threadfence();
+    old2 = atomicAdd(R.tcnt, 1u);
+  }
+  old2 = __shfl_sync(0xffffffffu, old2, 0);
+  const int ng = (nch + 31) >> 5;
+  if ((int)old2 != ng - 1) return;
+  __threadfence();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double acc = red_id<OP>(k);
+    for (int q = lane; q < ng; q += 32) acc = red_op<OP>(k, acc, ld(R.gsum + k * R.G + q));
+    x[k] = warp_red<OP>(k, acc);
+  }
+  if (lane == 0) {
+    *R.tcnt = 0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) R.total[k] = x[k];
+  }
 }
 
-__device__ __forceinline__ unsigned long long dbits(double x) {
-  return (unsigned long long)__double_as_longlong(x);
-}
-
-// damped solve of control c from the stored normal equations -> delta, (ok, |delta|)
-__device__ __forceinline__ void resolve_control(const SolverArgs& A, int c, double* okn) {
+// damped solve of control c from the stored normal equations -> delta, ok / |delta|
+__device__ __forceinline__ void resolve_control(const SolverArgs& A, int c, double lam, double* ok,
+                                                double* nrm) {
   double part[27], d[6];
+#pragma unroll
   for (int i = 0; i < 27; ++i) part[i] = ld(A.partial + 27 * c + i);
-  const bool good = solve6(part, A.lam[c], d);
+  const bool good = solve6(part, lam, d);
   double nn = 0.0;
+#pragma unroll
   for (int i = 0; i < 6; ++i) {
     A.delta[6 * c + i] = d[i];
     nn += d[i] * d[i];
   }
-  okn[2 * c] = good ? 1.0 : 0.0;
-  okn[2 * c + 1] = sqrt(nn);
+  ok[c] = good ? 1.0 : 0.0;
+  nrm[c] = sqrt(nn);
 }
 
 template <bool GRID>
@@ -203,7 +278,8 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   const int C = dom.size();
   const int rank = dom.rank();
   __shared__ SolverArgs A;
-  __shared__ double s_part[3 * NWARPS];
+  __shared__ double s_part[8 * NWARPS];
+  __shared__ double s_tot[8];
   __shared__ double s_sup[NWARPS];
   __shared__ double s_col[TEAMS_PER_CTA][32];
   __shared__ int s_cnt[NWARPS];
@@ -216,13 +292,17 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   const int team = warp / TEAM, tw = warp % TEAM;
   double* s_w = smem;
   double* s_T = smem + 8 * m;
-  double* stage = smem + 20 * m + warp * (STAGE + GOUT);
+  double* s_lam = smem + 20 * m;  // per-control damping, replicated in every CTA
+  double* stage = smem + 21 * m + warp * (STAGE + GOUT);
   double* gout = stage + STAGE;
   // work items are dealt round-robin over the CTAs first (item i -> CTA i % C), so
   // every SM of the domain gets a share of each phase
   const int gw = warp * C + rank, GW = C * NWARPS;
   const int gw_rev = (NWARPS - 1 - warp) * C + rank;
   const int gt = rank * (int)blockDim.x + (int)threadIdx.x, GT = C * (int)blockDim.x;
+  // per-control work (re-solves, tentative store) is interleaved over the CTAs --
+  // control c belongs to CTA c % C -- so no CTA becomes the straggler
+  const int gc = (int)threadIdx.x * C + rank;
   const int gteam = team * C + rank, GTEAM = C * TEAMS_PER_CTA;
   const int team_rounds = (m + GTEAM - 1) / GTEAM;
   const int64_t n_act = A.n_active ? *A.n_active : 0;
@@ -236,17 +316,13 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   double* cs_m0 = cs_p0 + A.nch_p;
   double* cs_e0 = cs_m0 + A.nch_m;
   double* cs_p1 = A.csum + nch_tot;
-  double* cs_m1 = cs_p1 + A.nch_p;
-  unsigned long long* lam_hist = reinterpret_cast<unsigned long long*>(A.lam_hist);
+  const RedSlot RP = red_slot(A, 0), RM = red_slot(A, 1), RE = red_slot(A, 2),
+                RK = red_slot(A, 3), RV = red_slot(A, 4);
   long long* tr = A.trace;
-  int tn = 0;
+  int tn = 0, nbar = 0;
   TRACE(0);
 
-  for (int c = gt; c < m; c += GT) A.lam[c] = A.lam_init;
-  for (int i = gt; i < A.max_outer; i += GT) {
-    lam_hist[2 * i] = dbits(INFINITY);  // min over positive doubles = min of their bits
-    lam_hist[2 * i + 1] = 0ull;
-  }
+  for (int c = threadIdx.x; c < m; c += blockDim.x) s_lam[c] = A.lam_init;
 
   double* cur = A.warp_a;
   double* tent = A.warp_b;
@@ -272,22 +348,25 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         int vd;
         if (p < n) acc = point_step(A, s_w, p, nullptr, nb, nullptr, &vd);
         acc = warp_sum(acc);
-        if (lane == 0) cs_p1[ch] = acc;
+        red_commit<2, 0>(RP, {cs_p0, cs_p1}, ch, nch_p, {0.0, acc});
       } else {
         const int64_t j = (int64_t)(ch - nch_p) * CHUNK + lane;
         if (j < n_act) acc = match_step(A, s_w, j, nm);
         acc = warp_sum(acc);
-        if (lane == 0) cs_m1[ch - nch_p] = acc;
+        red_commit<1, 0>(RM, {cs_m0}, ch - nch_p, nch_m, {acc});
       }
     }
   }
   DSYNC(1);
-  cb_icp = seg_total(cs_p1, nch_p, s_part);
-  cb_feat = seg_total(cs_m1, nch_m, s_part);
+  if (threadIdx.x == 0) s_tot[0] = ld(RP.total + 1);
+  if (threadIdx.x == 1) s_tot[1] = nch_m > 0 ? ld(RM.total) : 0.0;
+  __syncthreads();
+  cb_icp = s_tot[0];
+  cb_feat = s_tot[1];
 
   for (int outer = 0; outer < A.max_outer; ++outer) {
     outer_done = outer + 1;
-    double* okn = A.oknorm + (size_t)parity * 2 * m;
+    double* okn = A.oknorm + (size_t)parity * 2 * m;  // [0, m) ok, [m, 2m) |delta|
     if (need_lin) {
       const PBuf cb = pbuf(A, pb);
       const MBuf cm = mbuf(A, pb);
@@ -367,6 +446,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             }
           }
         }
+        TRACE(23);
         gram_store(G, gout);
         sup = warp_sum(sup);
         if (lane == 0) s_sup[warp] = sup;
@@ -385,6 +465,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
           }
         }
         __syncthreads();
+        TRACE(24);
       }
       DSYNC(2);
 
@@ -442,6 +523,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             }
           }
         }
+        TRACE(33);
         gram_store(G, gout);
         TRACE(32);
         __syncthreads();
@@ -454,16 +536,21 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             s_col[team][lane] = v;
           }
           __syncwarp();
+          double okv = 0.0, nrm = 0.0;
           if (lane == 0) {
             double d[6];
-            const bool good = solve6(s_col[team], ld(A.lam + c), d);
+            const bool good = solve6(s_col[team], s_lam[c], d);
             double nn = 0.0;
             for (int i = 0; i < 6; ++i) {
               A.delta[6 * c + i] = d[i];
               nn += d[i] * d[i];
             }
-            okn[2 * c] = good ? 1.0 : 0.0;
-            okn[2 * c + 1] = sqrt(nn);
+            okv = good ? 1.0 : 0.0;
+            nrm = sqrt(nn);
+          }
+          if (lane == 0) {
+            okn[c] = okv;
+            okn[m + c] = nrm;
           }
         }
         __syncthreads();
@@ -479,14 +566,14 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     } else {
       // after a stall the iterate and its linearization are unchanged: re-solve the
       // stored normal equations with the raised damping (solver.py:348-355)
-      for (int c = gt; c < m; c += GT) resolve_control(A, c, okn);
+      for (int c = gc; c < m; c += GT) resolve_control(A, c, s_lam[c], okn, okn + m);
     }
     bool accepted = false;
     double cost_before = 0.0, cost_after = 0.0;
     for (int attempt = 0; attempt <= A.max_retries; ++attempt) {
       if (attempt > 0) {
         okn = A.oknorm + (size_t)parity * 2 * m;
-        for (int c = gt; c < m; c += GT) resolve_control(A, c, okn);
+        for (int c = gc; c < m; c += GT) resolve_control(A, c, s_lam[c], okn, okn + m);
       }
       DSYNC(attempt == 0 ? 3 : 4);
       // prefetch this thread's step inputs (one control per thread when m <= 512)
@@ -498,37 +585,47 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
 #pragma unroll
         for (int i = 0; i < 6; ++i) pD[i] = ld(A.delta + 6 * pc + i);
       }
-      if (attempt == 0) {
-        if (need_lin) cb_arap = seg_total(cs_e0, nch_e, s_part);
-        cost_before = (cb_icp + cb_feat) + cb_arap;
-      }
-      TRACE(53);
-      // all solves ok? largest step norm (identical in every CTA)
+      TRACE(57);
+      // all solves ok? largest step norm; after a fresh linearization also the rigidity
+      // cost of the iterate -- one batch of loads by every warp, one exchange (identical
+      // in every CTA; the P3 critical path stays free of commit atomics)
       {
-        double allok = 1.0, mx = 0.0;
+        const bool want_e = attempt == 0 && need_lin;
+        double allok = 1.0, mx = 0.0, es = 0.0;
         for (int i = threadIdx.x; i < m; i += blockDim.x) {
-          allok = fmin(allok, ld(okn + 2 * i));
-          mx = fmax(mx, ld(okn + 2 * i + 1));
+          allok = fmin(allok, ld(okn + i));
+          mx = fmax(mx, ld(okn + m + i));
         }
+        if (want_e)
+          for (int i = threadIdx.x; i < nch_e; i += blockDim.x) es += ld(cs_e0 + i);
         allok = warp_min(allok);
         mx = warp_max(mx);
+        es = warp_sum(es);
         __syncthreads();
         if (lane == 0) {
-          s_part[2 * warp] = allok;
-          s_part[2 * warp + 1] = mx;
+          s_part[3 * warp] = allok;
+          s_part[3 * warp + 1] = mx;
+          s_part[3 * warp + 2] = es;
         }
         __syncthreads();
         allok = 1.0;
         mx = 0.0;
+        es = 0.0;
         for (int w = 0; w < NWARPS; ++w) {
-          allok = fmin(allok, s_part[2 * w]);
-          mx = fmax(mx, s_part[2 * w + 1]);
+          allok = fmin(allok, s_part[3 * w]);
+          mx = fmax(mx, s_part[3 * w + 1]);
+          es += s_part[3 * w + 2];
         }
+        if (want_e) cb_arap = es;
+        if (attempt == 0) cost_before = (cb_icp + cb_feat) + cb_arap;
+        TRACE(53);
         parity ^= 1;
         if (!(allok > 0.5)) {
           // raise the damping of the failed controls only, retry (solver.py:321-326)
-          for (int c = gt; c < m; c += GT)
-            if (ld(okn + 2 * c) < 0.5) A.lam[c] = fmin(A.lam[c] * A.lam_inc, A.lam_max);
+          __syncthreads();
+          for (int c = threadIdx.x; c < m; c += blockDim.x)
+            if (ld(okn + c) < 0.5) s_lam[c] = fmin(s_lam[c] * A.lam_inc, A.lam_max);
+          __syncthreads();
           ++rejected_steps;
           continue;
         }
@@ -541,18 +638,18 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
       TRACE(54);
       // ---- tentative warps, applied redundantly by every CTA (no barrier) ----
       __syncthreads();
-      if (pc < m) apply_step_one(pW, pD, s_w + 8 * pc);
+      if (pc < m) apply_step_one_fast(pW, pD, s_w + 8 * pc);
       for (int c = threadIdx.x + blockDim.x; c < m; c += blockDim.x) {
         double W[8], d[6];
         for (int i = 0; i < 8; ++i) W[i] = ld(cur + 8 * c + i);
         for (int i = 0; i < 6; ++i) d[i] = ld(A.delta + 6 * c + i);
-        apply_step_one(W, d, s_w + 8 * c);
+        apply_step_one_fast(W, d, s_w + 8 * c);
       }
       __syncthreads();
       TRACE(55);
       for (int c = threadIdx.x; c < m; c += blockDim.x)
-        dq_to_transform(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
-      for (int c = gt; c < m; c += GT)
+        dq_to_transform_fast(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
+      for (int c = gc; c < m; c += GT)
         for (int i = 0; i < 8; ++i) tent[8 * c + i] = s_w[8 * c + i];
       smem_is_cur = false;
       __syncthreads();
@@ -571,44 +668,42 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             if (p < n) cn = point_step(A, s_w, p, &ob, nb, &co, &vd);
             co = warp_sum(co);
             cn = warp_sum(cn);
-            if (lane == 0) {
-              cs_p0[ch] = co;
-              cs_p1[ch] = cn;
-            }
+            red_commit<2, 0>(RP, {cs_p0, cs_p1}, ch, nch_p, {co, cn});
           } else if (ch < nch_p + nch_m) {
             const int64_t j = (int64_t)(ch - nch_p) * CHUNK + lane;
             double cf = 0.0;
             if (j < n_act) cf = match_step(A, s_w, j, nm);
             cf = warp_sum(cf);
-            if (lane == 0) {
-              cs_m0[ch - nch_p] = cf;
-              cs_m1[ch - nch_p] = cf;
-            }
+            red_commit<1, 0>(RM, {cs_m0}, ch - nch_p, nch_m, {cf});
           } else {
             const int e = (ch - nch_p - nch_m) * CHUNK + lane;
             double acc = 0.0;
             if (e < A.n_edges) acc = edge_value(A, s_w, s_T, A.wa, e);
             acc = warp_sum(acc);
-            if (lane == 0) cs_e0[ch - nch_p - nch_m] = acc;
+            red_commit<1, 0>(RV, {cs_e0}, ch - nch_p - nch_m, nch_e, {acc});
           }
         }
       }
       DSYNC(6);
-      {
-        const double t_p = seg_total(cs_p0, nch_p, s_part);
-        const double t_m = seg_total(cs_m0, nch_m, s_part);
-        const double t_e = seg_total(cs_e0, nch_e, s_part);
-        cost_after = (t_p + t_m) + t_e;
-      }
+      // value pass (points, matches, edges) + cost of the speculative relinearization
+      if (threadIdx.x == 0) s_tot[0] = ld(RP.total);
+      if (threadIdx.x == 1) s_tot[1] = ld(RP.total + 1);
+      if (threadIdx.x == 2) s_tot[2] = nch_m > 0 ? ld(RM.total) : 0.0;
+      if (threadIdx.x == 3) s_tot[3] = nch_e > 0 ? ld(RV.total) : 0.0;
+      __syncthreads();
+      cost_after = (s_tot[0] + s_tot[2]) + s_tot[3];
+      TRACE(63);
       if (cost_after < cost_before) {
         double* tmp = cur;
         cur = tent;
         tent = tmp;
         pb = 1 - pb;
         smem_is_cur = true;
-        cb_icp = seg_total(cs_p1, nch_p, s_part);
-        cb_feat = seg_total(cs_m1, nch_m, s_part);
-        for (int c = gt; c < m; c += GT) A.lam[c] = fmax(A.lam[c] * A.lam_dec, A.lam_min);
+        cb_icp = s_tot[1];
+        cb_feat = s_tot[2];
+        for (int c = threadIdx.x; c < m; c += blockDim.x)
+          s_lam[c] = fmax(s_lam[c] * A.lam_dec, A.lam_min);
+        TRACE(64);
         ++accepted_steps;
         if (rank == 0 && threadIdx.x == 0) {
           A.cost_hist[2 * n_hist] = cost_before;
@@ -618,25 +713,29 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         accepted = true;
         break;
       }
-      for (int c = gt; c < m; c += GT) A.lam[c] = fmin(A.lam[c] * A.lam_inc, A.lam_max);
+      for (int c = threadIdx.x; c < m; c += blockDim.x)
+        s_lam[c] = fmin(s_lam[c] * A.lam_inc, A.lam_max);
+      __syncthreads();
       ++rejected_steps;
     }
     // lambda_history (solver.py:345): min / max of the final per-control damping of this
-    // outer iteration, folded by the owners with order-independent integer atomics
-    for (int c0 = gt - lane; c0 < m; c0 += GT) {
-      const int c = c0 + lane;
-      unsigned long long lo = ~0ull, hi = 0ull;
-      if (c < m) lo = hi = dbits(A.lam[c]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    // outer iteration -- every CTA holds the same s_lam; one warp of CTA (outer % C)
+    // records it
+    __syncthreads();
+    if (rank == outer % C && warp == NWARPS - 1) {
+      double lo = INFINITY, hi = -INFINITY;
+      for (int c = lane; c < m; c += 32) {
+        lo = fmin(lo, s_lam[c]);
+        hi = fmax(hi, s_lam[c]);
       }
+      lo = warp_min(lo);
+      hi = warp_max(hi);
       if (lane == 0) {
-        atomicMin(lam_hist + 2 * outer, lo);
-        atomicMax(lam_hist + 2 * outer + 1, hi);
+        A.lam_hist[2 * outer] = lo;
+        A.lam_hist[2 * outer + 1] = hi;
       }
     }
+    TRACE(65);
     if (converged) break;
     if (!accepted) {
       stalled = true;
@@ -668,7 +767,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
       for (int w = 0; w < NWARPS; ++w) t += s_cnt[w];
       A.counts[rank] = t;
     }
-    for (int c = gt; c < m; c += GT)
+    for (int c = gc; c < m; c += GT)
       for (int i = 0; i < 8; ++i) A.warps_out[8 * c + i] = s_w[8 * c + i];
     for (int c = gw; c < m; c += GW) {
       double sup = 0.0;
@@ -701,10 +800,10 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     const int e = ch * CHUNK + lane;
     if (e < A.n_edges) acc = edge_value(A, s_w, s_T, A.wa, e);
     acc = warp_sum(acc);
-    if (lane == 0) cs_e0[ch] = acc;
+    red_commit<1, 0>(RE, {cs_e0}, ch, nch_e, {acc});
   }
   DSYNC(9);
-  const double t_arap = seg_total(cs_e0, nch_e, s_part);
+  const double t_arap = nch_e > 0 ? ld(RE.total) : 0.0;
   if (rank == 0 && threadIdx.x == 0) {
     dt_report* R = A.report;
     R->icp_cost = cb_icp;
@@ -724,4 +823,8 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   }
   TRACE(99);
   if (tr && rank == 0 && threadIdx.x == 0) tr[0] = tn;
+  if (A.arrivals && rank == 0 && threadIdx.x == 0) {
+    A.arrivals[0] = C;
+    A.arrivals[1] = nbar;
+  }
 }

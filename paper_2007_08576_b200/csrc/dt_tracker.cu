@@ -281,6 +281,11 @@ struct dt_tracker {
   bool profiling = false;
   long long* trace = nullptr;
   int trace_cap = 0;
+  double* red = nullptr;     // last-arriver reduction slots
+  unsigned* redc = nullptr;
+  int red_g = 0;
+  long long* arrivals = nullptr;  // 2 + 1024 * arr_cap per-CTA barrier arrival stamps
+  int arr_cap = 0;
   bool last_used = false;
   cudaEvent_t ev[DT_N_PHASES + 1] = {};
   std::vector<DevBuf> bufs;
@@ -392,6 +397,11 @@ int ensure_match_capacity(dt_tracker* t, int64_t cap) {
     const int64_t nch = (t->n + CHUNK - 1) / CHUNK + (cap + CHUNK - 1) / CHUNK +
                         (t->ne + CHUNK - 1) / CHUNK;
     DT_TRY(dalloc(t, &t->csum, 2 * nch));
+    int64_t items = std::max<int64_t>(std::max<int64_t>((t->n + CHUNK - 1) / CHUNK, (cap + CHUNK - 1) / CHUNK),
+                                      std::max<int64_t>((t->ne + CHUNK - 1) / CHUNK, t->m));
+    t->red_g = (int)((items + 31) / 32);
+    DT_TRY(dalloc(t, &t->red, (size_t)RED_SLOTS * (2 * t->red_g + 2)));
+    DT_TRY(dalloc(t, &t->redc, (size_t)RED_SLOTS * (t->red_g + 1)));
   }
   t->args_dirty = true;
   return DT_OK;
@@ -449,6 +459,11 @@ void fill_args(dt_tracker* t) {
   a.wa_out = t->wa_out;
   a.trace = t->profiling ? t->trace : nullptr;
   a.trace_cap = t->trace_cap;
+  a.arrivals = t->profiling ? t->arrivals : nullptr;
+  a.arr_cap = t->arr_cap;
+  a.red = t->red;
+  a.redc = t->redc;
+  a.red_g = t->red_g;
 }
 
 int push_args(dt_tracker* t) {
@@ -977,6 +992,20 @@ int dt_tracker_get_trace(dt_tracker* t, long long* buf, int cap) {
   return (int)cnt;
 }
 
+int dt_tracker_get_arrivals(dt_tracker* t, long long* buf, int cap) {
+  DT_REQUIRE(t != nullptr && buf != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!t->arrivals) return 0;
+  long long hdr[2] = {0, 0};
+  DT_CHECK_CUDA(cudaMemcpyAsync(hdr, t->arrivals, sizeof(hdr), cudaMemcpyDeviceToHost, t->stream));
+  DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
+  const long long want = std::min<long long>(cap, 2 + hdr[0] * (long long)t->arr_cap);
+  if (want > 0)
+    DT_CHECK_CUDA(cudaMemcpyAsync(buf, t->arrivals, sizeof(long long) * want, cudaMemcpyDeviceToHost,
+                                  t->stream));
+  DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
+  return t->arr_cap;
+}
+
 void* dt_tracker_stream(dt_tracker* t) { return t ? (void*)t->stream : nullptr; }
 
 int dt_tracker_set_profiling(dt_tracker* t, int on) {
@@ -986,6 +1015,8 @@ int dt_tracker_set_profiling(dt_tracker* t, int on) {
   if (on && !t->trace) {
     t->trace_cap = 4096;
     DT_TRY(dalloc(t, &t->trace, 1 + 2 * (size_t)t->trace_cap));
+    t->arr_cap = 256;
+    DT_TRY(dalloc(t, &t->arrivals, 2 + 1024 * (size_t)t->arr_cap));
   }
   t->profiling = on != 0;
   DT_TRY(push_args(t));

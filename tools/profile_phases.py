@@ -22,11 +22,11 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 NAMES = {0: "start", 1: "relink+linearize",
-         2: "data gather", 3: "rigidity: edge costs", 3.2: "  rigidity gather",
+         2: "data gather", 3: "rigidity: edge costs", 3.2: "  gram store",
          3.4: "  team combine+solve", 5: "apply step", 5.2: "  transforms+tent store",
          5.3: "  cost_before totals", 5.4: "  ok/step-norm reduce", 5.5: "  apply_step x m",
-         2.2: "  edge unit rows",
-         6: "value pass + spec relink", 7.2: "final load", 8: "final support", 1.2: "  load warps+transforms", 9: "final rigidity", 99: "end"}
+         2.2: "  accept + edge unit rows", 2.3: "  data rows -> Gram", 2.4: "  team combine", 3.3: "  rigidity rows -> Gram",
+         6: "value pass + spec relink", 6.3: "  value totals", 6.4: "  lambda update", 6.5: "  lambda history", 5.7: "  prefetch step inputs", 7.2: "final load", 8: "final support", 1.2: "  load warps+transforms", 9: "final rigidity", 99: "end"}
 
 
 def main():
@@ -56,6 +56,9 @@ def main():
     stages = []
     work = defaultdict(float)
     wait = defaultdict(float)
+    crit = defaultdict(float)   # last CTA arrival - previous release
+    blat = defaultdict(float)   # release - last CTA arrival
+    last_cta = defaultdict(list)
     for i, fr in enumerate(wl["frames"]):
         d = torch.from_numpy(fr.depth).to(dev)
         de = torch.from_numpy(fr.descriptors).to(dev)
@@ -66,8 +69,23 @@ def main():
         trk.enqueue(fi)
         stages.append(trk.phase_ms())
         tr = trk.trace()
+        arr = trk.arrivals()
         if i == 0:
             continue  # first frame: cold caches
+        # barrier k of the frame: CTA-0 stamps (10 ph) / (10 ph + 1), arrivals row k
+        rel_prev = tr[0, 1]
+        k = 0
+        codes = [int(c) for c in tr[:, 0]]
+        for idx in range(len(codes) - 1):
+            c0, c1 = codes[idx], codes[idx + 1]
+            if c0 % 10 == 0 and c0 != 0 and c1 == c0 + 1 and k < arr.shape[0]:
+                ph = c0 // 10
+                mx = int(arr[k].max())
+                crit[ph] += (mx - rel_prev) / 1e3
+                blat[ph] += (tr[idx + 1, 1] - mx) / 1e3
+                last_cta[ph].append(int(arr[k].argmax()))
+                rel_prev = tr[idx + 1, 1]
+                k += 1
         prev_t = tr[0, 1]
         for code, t in tr[1:]:
             ph, kind = divmod(int(code), 10)
@@ -91,6 +109,15 @@ def main():
         tot_b += b
         print(f"{NAMES.get(ph, ph):22s} {w:14.1f} {b:17.1f}")
     print(f"{'total':22s} {tot_w:14.1f} {tot_b:17.1f}")
+    print(f"{'barrier (phase)':22s} {'critical us/frame':>18s} {'sync us/frame':>14s} last CTAs")
+    tc = tb = 0.0
+    for ph in sorted(crit):
+        c, b = crit[ph] / nf, blat[ph] / nf
+        tc += c
+        tb += b
+        lc = np.bincount(last_cta[ph]).argsort()[::-1][:3].tolist()
+        print(f"{NAMES.get(ph, ph):22s} {c:18.1f} {b:14.1f} {lc}")
+    print(f"{'total':22s} {tc:18.1f} {tb:14.1f}")
     if args.json:
         Path(args.json).write_text(json.dumps({"stages_ms": st,
                                                "solver_work_us": {NAMES.get(k, k): v / nf for k, v in work.items()},
