@@ -47,7 +47,7 @@ UNIT = "frames/s"
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", type=int, default=2)
@@ -347,16 +347,18 @@ def run_b200(args, rank, world, local_rank):
     solver_ms = phase_avg["lm_solver"]
     achieved = solver_bytes / (solver_ms * 1e-3) / 1e9
     traffic = None
-    prof = ROOT / "profiles" / "solver_dram_bytes.json"
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-    roofline = {"kernel": "k_solve_frame (LM solver, one cluster launch per frame)",
+    # dram__bytes_read.sum + dram__bytes_write.sum of one `ncu --set full` capture of the
+    # same kernel on the same workload (committed under profiles/, newest round first)
+    for prof in sorted((ROOT / "profiles").glob("r*_solver_dram.json"), reverse=True):
+        traffic = json.loads(prof.read_text()).get("traffic_bytes_per_launch")
+        break
+    roofline = {"kernel": "k_solve_frame (LM solver, one persistent launch per frame)",
                 "bound": "hbm", "achieved": round(achieved, 3), "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": int(solver_bytes),
                 "launch_ms": solver_ms, "peak_source": peak_src,
                 "dominant_phase": dominant,
-                "note": "latency-bound: ~70 dependent phases/frame; see DESIGN.md §roofline"}
+                "note": "latency-bound: ~40 dependent phases/frame; see DESIGN.md §4"}
 
     value = world * K / (total_ms / 1e3)
     ms_per_step = total_ms / K
