@@ -111,6 +111,53 @@ __device__ __forceinline__ double gram_col(const double* out, int col) {
 }
 
 // ---------------------------------------------------------------------------------
+// Per-lane normal-equation accumulation (FP64 FMA) + warp reduce-scatter. Each lane
+// folds its rows [J0..J5, wv, sw] into 32 accumulators:
+//   [0, 21) triu(J^T J) in kernels.py:41-44 order, [21, 27) J^T wv,
+//   27: wv^2 (the rows' cost), 28: sw^2 (support), 29-31 unused;
+// the reduce-scatter (31 shuffles) leaves lane l with the warp's sum of accumulator l.
+// On B200 the FP64 tensor core (DMMA.8x8x4) runs at the DFMA rate (tools/fp64_probe.cu:
+// 36 vs 34 TFLOP/s), so the 29 useful products per row beat the 64 of an 8x8 Gram.
+// ---------------------------------------------------------------------------------
+
+__device__ __forceinline__ void acc_row(double (&a)[32], const double r[8]) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int j = i; j < 6; ++j) a[triu_col(i, j)] = fma(r[i], r[j], a[triu_col(i, j)]);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) a[21 + i] = fma(r[i], r[6], a[21 + i]);
+  a[27] = fma(r[6], r[6], a[27]);
+  a[28] = fma(r[7], r[7], a[28]);
+}
+
+// a rotation row: J3..J5 and sw are zero
+__device__ __forceinline__ void acc_rot(double (&a)[32], const double r[8]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) a[triu_col(i, j)] = fma(r[i], r[j], a[triu_col(i, j)]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) a[21 + i] = fma(r[i], r[6], a[21 + i]);
+  a[27] = fma(r[6], r[6], a[27]);
+}
+
+__device__ __forceinline__ double warp_reduce_scatter(double (&a)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double send = up ? a[i] : a[i + s];
+      const double keep = up ? a[i + s] : a[i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return a[0];
+}
+
+// ---------------------------------------------------------------------------------
 // sync domains
 // ---------------------------------------------------------------------------------
 
@@ -209,35 +256,33 @@ __device__ __forceinline__ void blend_gradient_fast(const double B[8], double px
   G[23] = 2.0 * qw * is;
 }
 
-// rigidity cost of one connection (both endpoint bins): 2 x (length + angle 0->1 +
-// angle 1->0 + rotation) with the transforms / quaternions in smem
-__device__ __forceinline__ double edge_value(const SolverArgs& A, const double* s_w,
-                                             const double* s_T, const double* wa, int e) {
-  const int i0 = A.edges[2 * e], i1 = A.edges[2 * e + 1];
-  double dummy[1] = {0.0};
-  double cost = 0.0;
-  arap_edge_bin(A.cpts + 3 * i0, A.cpts + 3 * i1, s_T + 12 * i0, s_T + 12 * i0 + 9, s_T + 12 * i1,
-                s_T + 12 * i1 + 9, s_w + 8 * i0, s_w + 8 * i1, A.ew[e], ld(wa + i0), ld(wa + i1),
-                A.angle_w, A.rot_w, 0, false, dummy, &cost);
-  return 2.0 * cost;
-}
-
 // ---------------------------------------------------------------------------------
 // rigidity rows, evaluated once per connection (kernels.py:341-467)
 // ---------------------------------------------------------------------------------
 // The rigidity weight of a connection only scales its rows (sqrt(0.5 base w_term)), so
 // the unit-weight rows of BOTH endpoint bins are evaluated once per edge in P2 -- in
-// parallel with the data gather, before the weights wa exist -- and P3 gathers them.
-// Layout per edge (ER doubles):
-//   [0,6) length J bin 0, [6,12) length J bin 1, [12] length value,
-//   [13,19) angle 0->1 J of bin 0 (side a), [19,25) of bin 1 (side b), [25] angle 0->1,
-//   [26,32) angle 1->0 J of bin 1 (side a), [32,38) of bin 0 (side b), [38] angle 1->0.
-// The rotation rows need only the two quaternions and are rebuilt from smem.
+// parallel with the data gather, before the weights wa exist -- and stored at the bins'
+// control-CSR positions (ipos), 3 rows x 8 per position:
+//   [length J of the bin, length value, 0]
+//   [angle 0->1 J of the bin, angle 0->1 value, 0]   (bin 0 = side a, bin 1 = side b)
+//   [angle 1->0 J of the bin, angle 1->0 value, 0]   (bin 1 = side a, bin 0 = side b)
+// so P3 streams each control's rows contiguously. The rotation rows need only the two
+// quaternions and are rebuilt from shared memory.
 
-constexpr int ER = 40;
+constexpr int EROW = 24;
 
+__device__ __forceinline__ void store_row8(double* dst, const double* J6, double v) {
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  d2[0] = make_double2(J6[0], J6[1]);
+  d2[1] = make_double2(J6[2], J6[3]);
+  d2[2] = make_double2(J6[4], J6[5]);
+  d2[3] = make_double2(v, 0.0);
+}
+
+// Writes the unit rows of edge e into `erow` (at the bins' CSR positions) and its three
+// values into `evals`; returns the values in v[3].
 __device__ __forceinline__ void edge_unit_rows(const SolverArgs& A, const double* s_T, int e,
-                                               double* out) {
+                                               double* erow, double* evals, double v[3]) {
   const int i0 = A.edges[2 * e], i1 = A.edges[2 * e + 1];
   const double* p0 = A.cpts + 3 * i0;
   const double* p1 = A.cpts + 3 * i1;
@@ -259,37 +304,33 @@ __device__ __forceinline__ void edge_unit_rows(const SolverArgs& A, const double
     bhy = by / ln;
     bhz = bz / ln;
   }
-  out[0] = p0t[1] * (-bhz) - p0t[2] * (-bhy);
-  out[1] = p0t[2] * (-bhx) - p0t[0] * (-bhz);
-  out[2] = p0t[0] * (-bhy) - p0t[1] * (-bhx);
-  out[3] = -bhx;
-  out[4] = -bhy;
-  out[5] = -bhz;
-  out[6] = p1t[1] * bhz - p1t[2] * bhy;
-  out[7] = p1t[2] * bhx - p1t[0] * bhz;
-  out[8] = p1t[0] * bhy - p1t[1] * bhx;
-  out[9] = bhx;
-  out[10] = bhy;
-  out[11] = bhz;
-  out[12] = ln - rest;
+  const double L0[6] = {p0t[1] * (-bhz) - p0t[2] * (-bhy), p0t[2] * (-bhx) - p0t[0] * (-bhz),
+                        p0t[0] * (-bhy) - p0t[1] * (-bhx), -bhx, -bhy, -bhz};
+  const double L1[6] = {p1t[1] * bhz - p1t[2] * bhy, p1t[2] * bhx - p1t[0] * bhz,
+                        p1t[0] * bhy - p1t[1] * bhx, bhx, bhy, bhz};
+  const double lv = ln - rest;
   // bending angle, both directions (kernels.py:400-417)
-  double Ja[6], Jb[6];
-  out[25] = angle_unit(c01[0] - p0t[0], c01[1] - p0t[1], c01[2] - p0t[2], p1t[0] - p0t[0],
-                       p1t[1] - p0t[1], p1t[2] - p0t[2], p0t[0], p0t[1], p0t[2], p1t[0], p1t[1],
-                       p1t[2], Ja, Jb);
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-    out[13 + i] = Ja[i];
-    out[19 + i] = Jb[i];
-  }
-  out[38] = angle_unit(c10[0] - p1t[0], c10[1] - p1t[1], c10[2] - p1t[2], p0t[0] - p1t[0],
-                       p0t[1] - p1t[1], p0t[2] - p1t[2], p1t[0], p1t[1], p1t[2], p0t[0], p0t[1],
-                       p0t[2], Ja, Jb);
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-    out[26 + i] = Ja[i];
-    out[32 + i] = Jb[i];
-  }
+  double A01a[6], A01b[6], A10a[6], A10b[6];
+  const double v01 = angle_unit(c01[0] - p0t[0], c01[1] - p0t[1], c01[2] - p0t[2],
+                                p1t[0] - p0t[0], p1t[1] - p0t[1], p1t[2] - p0t[2], p0t[0], p0t[1],
+                                p0t[2], p1t[0], p1t[1], p1t[2], A01a, A01b);
+  const double v10 = angle_unit(c10[0] - p1t[0], c10[1] - p1t[1], c10[2] - p1t[2],
+                                p0t[0] - p1t[0], p0t[1] - p1t[1], p0t[2] - p1t[2], p1t[0], p1t[1],
+                                p1t[2], p0t[0], p0t[1], p0t[2], A10a, A10b);
+  double* r0 = erow + (size_t)EROW * __ldg(A.ipos + 2 * e);
+  double* r1 = erow + (size_t)EROW * __ldg(A.ipos + 2 * e + 1);
+  store_row8(r0, L0, lv);
+  store_row8(r0 + 8, A01a, v01);
+  store_row8(r0 + 16, A10b, v10);
+  store_row8(r1, L1, lv);
+  store_row8(r1 + 8, A01b, v01);
+  store_row8(r1 + 16, A10a, v10);
+  evals[3 * e] = lv;
+  evals[3 * e + 1] = v01;
+  evals[3 * e + 2] = v10;
+  v[0] = lv;
+  v[1] = v01;
+  v[2] = v10;
 }
 
 // rotation row r (0..3) of the bin `side` of edge (i0, i1) with weight sw: the 0.5 left
@@ -319,18 +360,20 @@ __device__ __forceinline__ void rotation_row(const double* s_w, int i0, int i1, 
   row[7] = 0.0;
 }
 
-// rigidity cost of one connection at the iterate from its stored values: 2 x the bin
-// cost, accumulated in arap_edge_bin's order (length, angle 0->1, angle 1->0, rotation)
-__device__ __forceinline__ double edge_cost_rows(const SolverArgs& A, const double* s_w,
-                                                 const double* wa, const double* er, int e) {
+// rigidity cost of one connection from its three values (length, angle 0->1, angle
+// 1->0) and the rotation term from the quaternions in smem: 2 x the bin cost, in
+// arap_edge_bin's accumulation order (kernels.py:341-467)
+__device__ __forceinline__ double edge_cost_vals(const SolverArgs& A, const double* s_w,
+                                                 const double* wa, int e, double lv, double v01,
+                                                 double v10) {
   const int i0 = A.edges[2 * e], i1 = A.edges[2 * e + 1];
   const double base = A.ew[e] * 0.5 * (ld(wa + i0) + ld(wa + i1));
   const double sw = sqrt(0.5 * base);
   const double swa = sqrt(0.5 * base * A.angle_w);
   const double swr = sqrt(0.5 * base * A.rot_w);
-  const double wl = sw * ld(er + 12);
-  const double w01 = swa * ld(er + 25);
-  const double w10 = swa * ld(er + 38);
+  const double wl = sw * lv;
+  const double w01 = swa * v01;
+  const double w10 = swa * v10;
   const double* q0 = s_w + 8 * i0;
   const double* q1 = s_w + 8 * i1;
   const double dq = q0[0] * q1[0] + q0[1] * q1[1] + q0[2] * q1[2] + q0[3] * q1[3];

@@ -32,12 +32,16 @@ struct SolverArgs {
   const double* bw;
   const int* cptr;   // control -> template (point, slot) entries, encoded (p << 3) | slot
   const int* cent;
+  const int* cpos;   // (n*k) inverse: CSR position of (point, slot)
   // control graph (static)
   const double* cpts;
   const int32_t* edges;
   const double* ew;
   const int* iptr;   // control -> incident (edge << 1) | side
   const int* ient;
+  const int* ipos;   // (2E) inverse: CSR position of (edge, side)
+  const int* iinfo;  // (2E) per CSR position: (other endpoint << 1) | side
+  const double* iew; // (2E) per CSR position: edge weight
   // frame observation
   const double* depth;
   const uint8_t* dvalid;
@@ -51,6 +55,7 @@ struct SolverArgs {
   const double* fbw;
   const int* mptr;   // control -> (match * k + slot) entries
   const int* ment;
+  const int* mpos;   // (Ma*k) inverse: CSR position of (match, slot)
   // solver state / scratch
   double* warp_a;    // warm start in, scratch
   double* warp_b;    // scratch
@@ -59,23 +64,24 @@ struct SolverArgs {
   double* wa;
   double* partial;   // m x 27 normal-equation columns
   double* csum;      // 2 sets x (nch_p + nch_m + nch_e) deterministic chunk sums
-  double* erows;     // n_edges x 40 unit rigidity rows of both bins
+  double* erow;      // 2 x (2E) x 24: per CSR position the 3 unit rigidity rows of that
+                     // bin (length, angle 0->1, angle 1->0; [J0..J5, value, 0])
+  double* evals;     // 2 x (E) x 3: length / angle 0->1 / angle 1->0 values
   double* delta;     // m x 6
-  double* oknorm;    // 2 parities x m x 2 (ok, step norm)
-  // per-point / per-match linearization records, double-buffered (2 x n, 2 x Ma): the
-  // value pass at a tentative iterate relinearizes there speculatively into the other
-  // buffer, which becomes current when the step is accepted
-  uint8_t* cvalid;   // correspondence valid
-  double* cobs;      // x 3 observed point
-  double* cnrm;      // x 3 observed normal
-  double* pr_r;      // raw residual
-  double* pr_rs;     // robust sqrt weight (frozen for the tentative passes)
-  double* pr_gn;     // x 8 gradient of r w.r.t. the blend
-  uint8_t* pr_sgn;   // blend signs (bit per slot)
-  double* fr_res;    // x 3
-  double* fr_G;      // x 24
-  uint8_t* fr_sgn;
-  int ma_cap;        // match capacity (stride between the two match buffers)
+  double* oknorm;    // 2 parities x 3m: ok, step norm, rigidity cost of the control's bins
+  // linearization, double-buffered: the value pass at a tentative iterate relinearizes
+  // there speculatively into the other buffer, which becomes current when the step is
+  // accepted. Per point: the correspondence + robust weight (frozen for the tentative
+  // value passes); per (point, slot) and (match, slot, component): the normal-equation
+  // row [J0..J5, sqrt(w) r, sqrt(w)] of its control, stored at its control-CSR position
+  // so that every control's rows are contiguous
+  uint8_t* cvalid;   // 2 x n correspondence valid
+  double* cobs;      // 2 x n x 3 observed point
+  double* cnrm;      // 2 x n x 3 observed normal
+  double* pr_rs;     // 2 x n robust sqrt weight
+  double* prow;      // 2 x (n*k) x 8 point rows
+  double* mrow;      // 2 x (Ma*k*3) x 8 match rows
+  int ma_cap;        // match capacity Ma (stride between the two match row buffers)
   int* counts;       // per-CTA correspondence counts (<= 1024 CTAs)
   // outputs
   dt_report* report;

@@ -19,40 +19,58 @@
 constexpr int TEAM = DT_TEAM;
 constexpr int TEAMS_PER_CTA = NWARPS / TEAM;
 
-// one of the two per-point record buffers (correspondence + linearization)
+// one of the two linearization buffers
 struct PBuf {
-  uint8_t* valid;
-  double* obs;
-  double* nrm;
-  double* r;
-  double* rs;
-  double* gn;
-  uint8_t* sgn;
-};
-
-// one of the two per-match record buffers
-struct MBuf {
-  double* res;
-  double* G;
-  uint8_t* sgn;
+  uint8_t* valid;  // n
+  double* obs;     // n x 3
+  double* nrm;     // n x 3
+  double* rs;      // n
+  double* row;     // (n*k) x 8 rows at control-CSR positions
 };
 
 __device__ __forceinline__ PBuf pbuf(const SolverArgs& A, int b) {
   const int64_t n = A.n;
-  return {A.cvalid + b * n, A.cobs + 3 * b * n, A.cnrm + 3 * b * n, A.pr_r + b * n,
-          A.pr_rs + b * n,  A.pr_gn + 8 * b * n, A.pr_sgn + b * n};
+  return {A.cvalid + b * n, A.cobs + 3 * b * n, A.cnrm + 3 * b * n, A.pr_rs + b * n,
+          A.prow + (size_t)b * n * A.k * 8};
 }
 
-__device__ __forceinline__ MBuf mbuf(const SolverArgs& A, int b) {
-  const int64_t c = A.ma_cap;
-  return {A.fr_res + 3 * b * c, A.fr_G + 24 * b * c, A.fr_sgn + b * c};
+__device__ __forceinline__ double* mrows(const SolverArgs& A, int b) {
+  return A.mrow + (size_t)b * A.ma_cap * A.k * 3 * 8;
+}
+
+__device__ __forceinline__ double* erows_buf(const SolverArgs& A, int b) {
+  return A.erow + (size_t)b * 2 * A.n_edges * EROW;
+}
+
+__device__ __forceinline__ double* evals_buf(const SolverArgs& A, int b) {
+  return A.evals + (size_t)b * 3 * A.n_edges;
+}
+
+__device__ __forceinline__ void store_row(double* dst, const double r[8]) {
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  d2[0] = make_double2(r[0], r[1]);
+  d2[1] = make_double2(r[2], r[3]);
+  d2[2] = make_double2(r[4], r[5]);
+  d2[3] = make_double2(r[6], r[7]);
+}
+
+__device__ __forceinline__ void load_row(const double* src, double r[8]) {
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double2 v = __ldcg(s2 + i);
+    r[2 * i] = v.x;
+    r[2 * i + 1] = v.y;
+  }
 }
 
 // Relink point p at the warps in smem (kernels.py:483-569) and linearize it into `nb`
-// (kernels.py:173-197); returns the point's icp cost under the Tukey weight of the new
-// residual. With `ob`, *cost_old receives the point's cost at these warps under the
-// frozen correspondence and robust weight of record `ob` (the value pass,
-// solver.py:333-335).
+// (kernels.py:173-197): the correspondence + robust weight, and for every slot the
+// normal-equation row of its control [J0..J5, sqrt(w) r, sqrt(w)] (J = sw alpha sign
+// (gn . K_c), sw = rs sqrt(alpha)) at the slot's control-CSR position. Returns the
+// point's icp cost under the Tukey weight of the new residual. With `ob`, *cost_old
+// receives the point's cost at these warps under the frozen correspondence and robust
+// weight of record `ob` (the value pass, solver.py:333-335).
 __device__ __forceinline__ double point_step(const SolverArgs& A, const double* s_w, int64_t p,
                                              const PBuf* ob, const PBuf& nb, double* cost_old,
                                              int* valid_out) {
@@ -106,7 +124,13 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   }
   nb.valid[p] = ok ? 1 : 0;
   *valid_out = ok ? 1 : 0;
-  if (!ok) return 0.0;
+  if (!ok) {
+    const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s)
+      if (s < A.k) store_row(nb.row + 8 * (size_t)__ldg(A.cpos + p * A.k + s), z);
+    return 0.0;
+  }
   nb.obs[3 * p] = o0;
   nb.obs[3 * p + 1] = o1;
   nb.obs[3 * p + 2] = o2;
@@ -115,47 +139,71 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   nb.nrm[3 * p + 2] = g2;
   const double r = g0 * (x0 - o0) + g1 * (x1 - o1) + g2 * (x2 - o2);
   const double rs = tukey_sqrt(r, A.tukey);
-  nb.r[p] = r;
   nb.rs[p] = rs;
-  nb.sgn[p] = (uint8_t)sign_bits(sgn, A.k);
   double G[24];
   blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, G);
+  double gn[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) nb.gn[8 * p + e] = g0 * G[e] + g1 * G[8 + e] + g2 * G[16 + e];
+  for (int e = 0; e < 8; ++e) gn[e] = g0 * G[e] + g1 * G[8 + e] + g2 * G[16 + e];
   double cost = 0.0;
 #pragma unroll
   for (int s = 0; s < KMAX; ++s)
     if (s < A.k) {
-      const double wv = rs * sqrt(a[s]) * r;
+      const int c = A.bidx[p * A.k + s];
+      const double sw = rs * sqrt(a[s]);
+      const double wv = sw * r;
       cost += wv * wv;
+      const double coef = sw * a[s] * sgn[s];
+      Basis K;
+      make_basis(s_w + 8 * c, K);
+      double pr[6], row[8];
+      basis_project(gn, K.Kr, K.Kd, pr);
+#pragma unroll
+      for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
+      row[6] = wv;
+      row[7] = sw;
+      store_row(nb.row + 8 * (size_t)__ldg(A.cpos + p * A.k + s), row);
     }
   return cost;
 }
 
-// One active match at the warps in smem: residual + blend gradient into `nb`
-// (kernels.py:239-250); returns its feature cost (no robust weight, so the same value
-// serves the value pass and the relinearization).
+// One active match at the warps in smem (kernels.py:239-250): for every slot the three
+// rows [J0..J5, sqrt(w) res_c, (c == 0 ? sqrt(w) : 0)] at the slot's match-CSR position;
+// returns its feature cost (no robust weight, so the same value serves the value pass
+// and the relinearization).
 __device__ __forceinline__ double match_step(const SolverArgs& A, const double* s_w, int64_t j,
-                                             const MBuf& nb) {
+                                             double* rows) {
   double B[8], sgn[KMAX], a[KMAX];
   blend_rows(s_w, A.fbidx, A.fbw, j, A.k, B, sgn, a);
   const double px = A.fp[3 * j], py = A.fp[3 * j + 1], pz = A.fp[3 * j + 2];
   double x0, x1, x2, s2;
   apply_blend(B, px, py, pz, x0, x1, x2, s2);
-  const double e0 = x0 - A.fo[3 * j], e1 = x1 - A.fo[3 * j + 1], e2 = x2 - A.fo[3 * j + 2];
-  nb.res[3 * j] = e0;
-  nb.res[3 * j + 1] = e1;
-  nb.res[3 * j + 2] = e2;
-  nb.sgn[j] = (uint8_t)sign_bits(sgn, A.k);
-  blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, nb.G + 24 * j);
+  const double res[3] = {x0 - A.fo[3 * j], x1 - A.fo[3 * j + 1], x2 - A.fo[3 * j + 2]};
+  double G[24];
+  blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, G);
   const double w = A.fwt[j];
   double cost = 0.0;
 #pragma unroll
   for (int s = 0; s < KMAX; ++s)
     if (s < A.k) {
+      const int c = A.fbidx[j * A.k + s];
       const double sw = sqrt(A.fw * w * a[s]);
-      const double v0 = sw * e0, v1 = sw * e1, v2 = sw * e2;
+      const double v0 = sw * res[0], v1 = sw * res[1], v2 = sw * res[2];
       cost += v0 * v0 + v1 * v1 + v2 * v2;
+      const double coef = sw * a[s] * sgn[s];
+      Basis K;
+      make_basis(s_w + 8 * c, K);
+      double* dst = rows + 24 * (size_t)__ldg(A.mpos + j * A.k + s);
+#pragma unroll
+      for (int comp = 0; comp < 3; ++comp) {
+        double pr[6], row[8];
+        basis_project(G + 8 * comp, K.Kr, K.Kd, pr);
+#pragma unroll
+        for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
+        row[6] = sw * res[comp];
+        row[7] = comp == 0 ? sw : 0.0;
+        store_row(dst + 8 * comp, row);
+      }
     }
   return cost;
 }
@@ -335,13 +383,16 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   int parity = 0;
   double cb_icp = 0.0, cb_feat = 0.0, cb_arap = 0.0;
 
-  // ---- P1: relink + linearize at the warm start (record buffer 0) ----
+  // ---- P1: relink + linearize at the warm start (buffer 0): points, matches, unit
+  // rigidity rows of the connections ----
   load_state(A, cur, s_w, s_T);
   TRACE(12);
   {
     const PBuf nb = pbuf(A, 0);
-    const MBuf nm = mbuf(A, 0);
-    for (int ch = gw; ch < nch_p + nch_m; ch += GW) {
+    double* nm = mrows(A, 0);
+    double* ne = erows_buf(A, 0);
+    double* nv = evals_buf(A, 0);
+    for (int ch = gw; ch < nch_p + nch_m + nch_e; ch += GW) {
       double acc = 0.0;
       if (ch < nch_p) {
         const int64_t p = (int64_t)ch * CHUNK + lane;
@@ -349,11 +400,15 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         if (p < n) acc = point_step(A, s_w, p, nullptr, nb, nullptr, &vd);
         acc = warp_sum(acc);
         red_commit<2, 0>(RP, {cs_p0, cs_p1}, ch, nch_p, {0.0, acc});
-      } else {
+      } else if (ch < nch_p + nch_m) {
         const int64_t j = (int64_t)(ch - nch_p) * CHUNK + lane;
         if (j < n_act) acc = match_step(A, s_w, j, nm);
         acc = warp_sum(acc);
         red_commit<1, 0>(RM, {cs_m0}, ch - nch_p, nch_m, {acc});
+      } else {
+        const int e = (ch - nch_p - nch_m) * CHUNK + lane;
+        double v[3];
+        if (e < A.n_edges) edge_unit_rows(A, s_T, e, ne, nv, v);
       }
     }
   }
@@ -366,101 +421,55 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
 
   for (int outer = 0; outer < A.max_outer; ++outer) {
     outer_done = outer + 1;
-    double* okn = A.oknorm + (size_t)parity * 2 * m;  // [0, m) ok, [m, 2m) |delta|
+    // [0, m) ok, [m, 2m) |delta|, [2m, 3m) rigidity cost of the control's bins
+    double* okn = A.oknorm + (size_t)parity * 3 * m;
     if (need_lin) {
-      const PBuf cb = pbuf(A, pb);
-      const MBuf cm = mbuf(A, pb);
-      // ---- P2: unit rigidity rows of every connection (no wa needed) on the warps at
-      // the end of each CTA; data rows -> normal equations (FP64 tensor-core Gram) on
-      // the teams ----
-      for (int ch = gw_rev; ch < nch_e; ch += GW) {
-        const int e = ch * CHUNK + lane;
-        if (e < A.n_edges) edge_unit_rows(A, s_T, e, A.erows + (size_t)ER * e);
-      }
+      const double* prow = pbuf(A, pb).row;
+      const double* mrow = mrows(A, pb);
+      const double* erow = erows_buf(A, pb);
+      // ---- P2: each control's data rows (contiguous at its CSR positions) -> normal
+      // equations + support (per-lane FMA accumulation, warp reduce-scatter) ----
       TRACE(22);
       for (int r = 0; r < team_rounds; ++r) {
         const int c = r * GTEAM + gteam;
-        Gram G;
-        double sup = 0.0;
+        double acc[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = 0.0;
         if (c < m) {
-          Basis K;
-          make_basis(s_w + 8 * c, K);
-          const int q0 = ldi(A.cptr + c), q1 = ldi(A.cptr + c + 1);
-          for (int base = q0 + 32 * tw; base < q1; base += 32 * TEAM) {
-            const int q = base + lane;
-            double row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            if (q < q1) {
-              const int e = ldi(A.cent + q);
-              const int64_t p = e >> 3;
-              const int s = e & 7;
-              if (ldu8(cb.valid + p)) {
-                const double a = A.bw[p * A.k + s];
-                const double rs = ld(cb.rs + p);
-                sup += rs * rs * a;
-                const double sw = rs * sqrt(a);
-                const double sg = ((ldu8(cb.sgn + p) >> s) & 1u) ? -1.0 : 1.0;
-                const double coef = sw * a * sg;
-                double gn[8], pr[6];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) gn[i] = ld(cb.gn + 8 * p + i);
-                basis_project(gn, K.Kr, K.Kd, pr);
-#pragma unroll
-                for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
-                row[6] = sw * ld(cb.r + p);
-              }
-            }
-            gram_push(G, stage, row);
-          }
+          const int q0 = __ldg(A.cptr + c), q1 = __ldg(A.cptr + c + 1);
+          int m0 = 0, m1 = 0;
           if (n_act > 0) {
-            const int m0 = ldi(A.mptr + c), m1 = ldi(A.mptr + c + 1);
-            for (int base = m0 + 32 * tw; base < m1; base += 32 * TEAM) {
-              const int q = base + lane;
-              const bool live = q < m1;
-              int64_t j = 0;
-              double coef = 0.0, sw = 0.0;
-              if (live) {
-                const int e = ldi(A.ment + q);
-                j = e / A.k;
-                const int s = e - (int)j * A.k;
-                const double a = A.fbw[e];
-                const double w_pair = A.fw * A.fwt[j] * a;
-                sup += w_pair;
-                sw = sqrt(w_pair);
-                const double sg = ((ldu8(cm.sgn + j) >> s) & 1u) ? -1.0 : 1.0;
-                coef = sw * a * sg;
-              }
-#pragma unroll 1
-              for (int comp = 0; comp < 3; ++comp) {
-                double row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                if (live) {
-                  double g[8], pr[6];
-#pragma unroll
-                  for (int i = 0; i < 8; ++i) g[i] = ld(cm.G + 24 * j + 8 * comp + i);
-                  basis_project(g, K.Kr, K.Kd, pr);
-#pragma unroll
-                  for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
-                  row[6] = sw * ld(cm.res + 3 * j + comp);
-                }
-                gram_push(G, stage, row);
-              }
-            }
+            m0 = ldi(A.mptr + c);
+            m1 = ldi(A.mptr + c + 1);
+          }
+          const int np_rows = q1 - q0, total = np_rows + 3 * (m1 - m0);
+          const double* pbase = prow + 8 * (size_t)q0;
+          const double* mbase = mrow + 24 * (size_t)m0;
+          // two row blocks in flight per warp: blocks b and b + TEAM, pushed in order
+          for (int base = 32 * tw; base < total; base += 64 * TEAM) {
+            double ra[8] = {0, 0, 0, 0, 0, 0, 0, 0}, rb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const int ia = base + lane, ib = base + 32 * TEAM + lane;
+            if (ia < np_rows) load_row(pbase + 8 * (size_t)ia, ra);
+            else if (ia < total) load_row(mbase + 8 * (size_t)(ia - np_rows), ra);
+            if (ib < np_rows) load_row(pbase + 8 * (size_t)ib, rb);
+            else if (ib < total) load_row(mbase + 8 * (size_t)(ib - np_rows), rb);
+            acc_row(acc, ra);
+            if (base + 32 * TEAM < total) acc_row(acc, rb);
           }
         }
         TRACE(23);
-        gram_store(G, gout);
-        sup = warp_sum(sup);
-        if (lane == 0) s_sup[warp] = sup;
+        gout[lane] = warp_reduce_scatter(acc);
         __syncthreads();
         if (tw == 0 && c < m) {
-          // combine the team's Grams in warp order
+          // combine the team's warps in warp order; accumulator 28 = support
           if (lane < 27) {
             double v = 0.0;
-            for (int w = 0; w < TEAM; ++w) v += gram_col(gout + w * (STAGE + GOUT), lane);
+            for (int w = 0; w < TEAM; ++w) v += gout[w * (STAGE + GOUT) + lane];
             A.partial[27 * c + lane] = v;
           }
-          if (lane == 27) {
+          if (lane == 28) {
             double su = 0.0;
-            for (int w = 0; w < TEAM; ++w) su += s_sup[warp + w];
+            for (int w = 0; w < TEAM; ++w) su += gout[w * (STAGE + GOUT) + 28];
             A.wa[c] = A.arap_w * fmax(su, A.data_floor);
           }
         }
@@ -473,67 +482,74 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
       // of the iterate from the stored rows ----
       for (int r = 0; r < team_rounds; ++r) {
         const int c = r * GTEAM + gteam;
-        Gram G;
+        double acc[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = 0.0;
         if (c < m) {
-          const int q0 = ldi(A.iptr + c), q1 = ldi(A.iptr + c + 1);
+          const int q0 = __ldg(A.iptr + c), q1 = __ldg(A.iptr + c + 1);
+          const double wac = ld(A.wa + c);
           for (int base = q0 + 32 * tw; base < q1; base += 32 * TEAM) {
             const int q = base + lane;
             const bool live = q < q1;
-            int i0 = 0, i1 = 0, side = 0;
+            int i0 = c, i1 = c, side = 0;
             double sw = 0.0, swa = 0.0, swr = 0.0;
-            const double* er = A.erows;
+            double u0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, u1[8] = {0, 0, 0, 0, 0, 0, 0, 0},
+                   u2[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             if (live) {
-              const int e2 = ldi(A.ient + q);
-              const int e = e2 >> 1;
-              side = e2 & 1;
-              i0 = A.edges[2 * e];
-              i1 = A.edges[2 * e + 1];
-              const double base_w = A.ew[e] * 0.5 * (ld(A.wa + i0) + ld(A.wa + i1));
+              const int info = __ldg(A.iinfo + q);
+              const int o = info >> 1;
+              side = info & 1;
+              const double* er = erow + (size_t)EROW * q;
+              load_row(er, u0);
+              load_row(er + 8, u1);
+              load_row(er + 16, u2);
+              const double wao = ld(A.wa + o);
+              i0 = side == 0 ? c : o;
+              i1 = side == 0 ? o : c;
+              const double base_w =
+                  __ldg(A.iew + q) * 0.5 * (side == 0 ? wac + wao : wao + wac);
               sw = sqrt(0.5 * base_w);
               swa = sqrt(0.5 * base_w * A.angle_w);
               swr = sqrt(0.5 * base_w * A.rot_w);
-              er = A.erows + (size_t)ER * e;
             }
-            double row[8];
-            // length row of this bin
+            if (live) {
+              double row[8];
+              // length, angle 0->1, angle 1->0 rows of this bin (unit rows x weight)
 #pragma unroll
-            for (int i = 0; i < 6; ++i) row[i] = live ? sw * ld(er + 6 * side + i) : 0.0;
-            row[6] = live ? sw * ld(er + 12) : 0.0;
-            row[7] = 0.0;
-            gram_push(G, stage, row);
-            // angle 0->1: bin 0 is side a ([13,19)), bin 1 side b ([19,25))
+              for (int i = 0; i < 8; ++i) row[i] = sw * u0[i];
+              acc_row(acc, row);
 #pragma unroll
-            for (int i = 0; i < 6; ++i) row[i] = live ? swa * ld(er + 13 + 6 * side + i) : 0.0;
-            row[6] = live ? swa * ld(er + 25) : 0.0;
-            gram_push(G, stage, row);
-            // angle 1->0: bin 1 is side a ([26,32)), bin 0 side b ([32,38))
+              for (int i = 0; i < 8; ++i) row[i] = swa * u1[i];
+              acc_row(acc, row);
 #pragma unroll
-            for (int i = 0; i < 6; ++i) row[i] = live ? swa * ld(er + 32 - 6 * side + i) : 0.0;
-            row[6] = live ? swa * ld(er + 38) : 0.0;
-            gram_push(G, stage, row);
-#pragma unroll 1
-            for (int rr = 0; rr < 4; ++rr) {
-              if (live) {
+              for (int i = 0; i < 8; ++i) row[i] = swa * u2[i];
+              acc_row(acc, row);
+#pragma unroll
+              for (int rr = 0; rr < 4; ++rr) {
                 rotation_row(s_w, i0, i1, side, swr, rr, row);
-              } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) row[i] = 0.0;
+                acc_rot(acc, row);
               }
-              gram_push(G, stage, row);
             }
           }
         }
         TRACE(33);
-        gram_store(G, gout);
+        gout[lane] = warp_reduce_scatter(acc);
         TRACE(32);
         __syncthreads();
         if (tw == 0 && c < m) {
           if (lane < 27) {
             double v = 0.0;
-            for (int w = 0; w < TEAM; ++w) v += gram_col(gout + w * (STAGE + GOUT), lane);
+            for (int w = 0; w < TEAM; ++w) v += gout[w * (STAGE + GOUT) + lane];
             v = ld(A.partial + 27 * c + lane) + v;
             A.partial[27 * c + lane] = v;
             s_col[team][lane] = v;
+          }
+          if (lane == 27) {
+            // accumulator 27 of the rigidity rows = the rigidity cost of this control's
+            // bins (each connection's rows go to both bins: the bins sum to its cost)
+            double v = 0.0;
+            for (int w = 0; w < TEAM; ++w) v += gout[w * (STAGE + GOUT) + 27];
+            okn[2 * m + c] = v;
           }
           __syncwarp();
           double okv = 0.0, nrm = 0.0;
@@ -556,13 +572,6 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         __syncthreads();
         TRACE(34);
       }
-      for (int ch = gw_rev; ch < nch_e; ch += GW) {
-        double acc = 0.0;
-        const int e = ch * CHUNK + lane;
-        if (e < A.n_edges) acc = edge_cost_rows(A, s_w, A.wa, A.erows + (size_t)ER * e, e);
-        acc = warp_sum(acc);
-        if (lane == 0) cs_e0[ch] = acc;
-      }
     } else {
       // after a stall the iterate and its linearization are unchanged: re-solve the
       // stored normal equations with the raised damping (solver.py:348-355)
@@ -572,7 +581,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     double cost_before = 0.0, cost_after = 0.0;
     for (int attempt = 0; attempt <= A.max_retries; ++attempt) {
       if (attempt > 0) {
-        okn = A.oknorm + (size_t)parity * 2 * m;
+        okn = A.oknorm + (size_t)parity * 3 * m;
         for (int c = gc; c < m; c += GT) resolve_control(A, c, s_lam[c], okn, okn + m);
       }
       DSYNC(attempt == 0 ? 3 : 4);
@@ -597,7 +606,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
           mx = fmax(mx, ld(okn + m + i));
         }
         if (want_e)
-          for (int i = threadIdx.x; i < nch_e; i += blockDim.x) es += ld(cs_e0 + i);
+          for (int i = threadIdx.x; i < m; i += blockDim.x) es += ld(okn + 2 * m + i);
         allok = warp_min(allok);
         mx = warp_max(mx);
         es = warp_sum(es);
@@ -659,7 +668,9 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
       {
         const PBuf ob = pbuf(A, pb);
         const PBuf nb = pbuf(A, 1 - pb);
-        const MBuf nm = mbuf(A, 1 - pb);
+        double* nm = mrows(A, 1 - pb);
+        double* ne = erows_buf(A, 1 - pb);
+        double* nv = evals_buf(A, 1 - pb);
         for (int ch = gw; ch < nch_p + nch_m + nch_e; ch += GW) {
           if (ch < nch_p) {
             const int64_t p = (int64_t)ch * CHUNK + lane;
@@ -678,7 +689,11 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
           } else {
             const int e = (ch - nch_p - nch_m) * CHUNK + lane;
             double acc = 0.0;
-            if (e < A.n_edges) acc = edge_value(A, s_w, s_T, A.wa, e);
+            if (e < A.n_edges) {
+              double v[3];
+              edge_unit_rows(A, s_T, e, ne, nv, v);
+              acc = edge_cost_vals(A, s_w, A.wa, e, v[0], v[1], v[2]);
+            }
             acc = warp_sum(acc);
             red_commit<1, 0>(RV, {cs_e0}, ch - nch_p - nch_m, nch_e, {acc});
           }
@@ -769,21 +784,22 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     }
     for (int c = gc; c < m; c += GT)
       for (int i = 0; i < 8; ++i) A.warps_out[8 * c + i] = s_w[8 * c + i];
+    // support per control from its rows' last column: sum of sw^2 = rs^2 alpha (points)
+    // + w_pair (matches, component-0 rows)
+    const double* prow = cb.row;
+    const double* mrow = mrows(A, pb);
     for (int c = gw; c < m; c += GW) {
       double sup = 0.0;
-      const int q0 = ldi(A.cptr + c), q1 = ldi(A.cptr + c + 1);
+      const int q0 = __ldg(A.cptr + c), q1 = __ldg(A.cptr + c + 1);
       for (int q = q0 + lane; q < q1; q += 32) {
-        const int e = ldi(A.cent + q);
-        const int64_t p = e >> 3;
-        if (!ldu8(cb.valid + p)) continue;
-        const double rs = ld(cb.rs + p);
-        sup += rs * rs * A.bw[p * A.k + (e & 7)];
+        const double v = ld(prow + 8 * (size_t)q + 7);
+        sup += v * v;
       }
       if (n_act > 0) {
         const int m0 = ldi(A.mptr + c), m1 = ldi(A.mptr + c + 1);
         for (int q = m0 + lane; q < m1; q += 32) {
-          const int e = ldi(A.ment + q);
-          sup += A.fw * A.fwt[e / A.k] * A.fbw[e];
+          const double v = ld(mrow + 24 * (size_t)q + 7);
+          sup += v * v;
         }
       }
       sup = warp_sum(sup);
@@ -798,7 +814,10 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   for (int ch = gw; ch < nch_e; ch += GW) {
     double acc = 0.0;
     const int e = ch * CHUNK + lane;
-    if (e < A.n_edges) acc = edge_value(A, s_w, s_T, A.wa, e);
+    if (e < A.n_edges) {
+      const double* ev = evals_buf(A, pb) + 3 * e;
+      acc = edge_cost_vals(A, s_w, A.wa, e, ld(ev), ld(ev + 1), ld(ev + 2));
+    }
     acc = warp_sum(acc);
     red_commit<1, 0>(RE, {cs_e0}, ch, nch_e, {acc});
   }

@@ -212,7 +212,8 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const int* __restrict__ cn
 }
 
 __global__ void k_csr_fill_dev(const int32_t* __restrict__ keys, const int64_t* __restrict__ n_dev,
-                               int k, int m, const int* __restrict__ ptr, int* __restrict__ ent) {
+                               int k, int m, const int* __restrict__ ptr, int* __restrict__ ent,
+                               int* __restrict__ pos_of) {
   const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (warp >= m) return;
@@ -222,7 +223,11 @@ __global__ void k_csr_fill_dev(const int32_t* __restrict__ keys, const int64_t* 
     const int64_t e = base + lane;
     const bool hit = e < ne && keys[e] == warp;
     const unsigned bal = __ballot_sync(0xffffffffu, hit);
-    if (hit) ent[pos + __popc(bal & ((1u << lane) - 1u))] = (int)e;
+    if (hit) {
+      const int q = pos + __popc(bal & ((1u << lane) - 1u));
+      ent[q] = (int)e;
+      pos_of[e] = q;
+    }
     pos += __popc(bal);
   }
 }
@@ -320,13 +325,15 @@ struct dt_tracker {
   double* astats = nullptr;     // [0] weight sum [1] n flags
   double *fp = nullptr, *fo = nullptr, *fwt = nullptr, *fbw = nullptr;
   int32_t* fbidx = nullptr;
-  int *mptr = nullptr, *ment = nullptr, *mcnt = nullptr;
+  int *mptr = nullptr, *ment = nullptr, *mcnt = nullptr, *mpos = nullptr;
+  int *cpos = nullptr, *ipos = nullptr, *iinfo = nullptr;
+  double* iew = nullptr;
   // solver state
   double *warp_a = nullptr, *warp_b = nullptr, *warps_out = nullptr, *lam = nullptr, *wa = nullptr;
-  double *partial = nullptr, *csum = nullptr, *erows = nullptr, *delta = nullptr, *oknorm = nullptr;
-  uint8_t *cvalid = nullptr, *pr_sgn = nullptr, *fr_sgn = nullptr;
-  double *cobs = nullptr, *cnrm = nullptr, *pr_r = nullptr, *pr_rs = nullptr, *pr_gn = nullptr;
-  double *fr_res = nullptr, *fr_G = nullptr;
+  double *partial = nullptr, *csum = nullptr, *delta = nullptr, *oknorm = nullptr;
+  double *erow = nullptr, *evals = nullptr;
+  uint8_t* cvalid = nullptr;
+  double *cobs = nullptr, *cnrm = nullptr, *pr_rs = nullptr, *prow = nullptr, *mrow = nullptr;
   int* counts = nullptr;
   dt_report* report = nullptr;
   double *cost_hist = nullptr, *lam_hist = nullptr, *wa_out = nullptr;
@@ -389,9 +396,8 @@ int ensure_match_capacity(dt_tracker* t, int64_t cap) {
   DT_TRY(dalloc(t, &t->fbidx, k * cap));
   DT_TRY(dalloc(t, &t->fbw, k * cap));
   DT_TRY(dalloc(t, &t->ment, k * cap));
-  DT_TRY(dalloc(t, &t->fr_res, 2 * 3 * cap));
-  DT_TRY(dalloc(t, &t->fr_G, 2 * 24 * cap));
-  DT_TRY(dalloc(t, &t->fr_sgn, 2 * cap));
+  DT_TRY(dalloc(t, &t->mpos, k * cap));
+  DT_TRY(dalloc(t, &t->mrow, 2 * k * cap * 3 * 8));
   t->match_cap = cap;
   {
     const int64_t nch = (t->n + CHUNK - 1) / CHUNK + (cap + CHUNK - 1) / CHUNK +
@@ -435,21 +441,22 @@ void fill_args(dt_tracker* t) {
   a.step_tol = c.step_tol;
   a.cost_tol = c.cost_tol;
   a.tp = t->tp; a.tn = t->tn; a.bidx = t->bidx; a.bw = t->bw;
-  a.cptr = t->cptr; a.cent = t->cent;
+  a.cptr = t->cptr; a.cent = t->cent; a.cpos = t->cpos;
   a.cpts = t->cpts; a.edges = t->edges; a.ew = t->ew; a.iptr = t->iptr; a.ient = t->ient;
+  a.ipos = t->ipos; a.iinfo = t->iinfo; a.iew = t->iew;
   a.depth = t->depth; a.dvalid = t->dvalid; a.onrm = t->onrm;
   a.n_active = t->info + 3;
   a.fp = t->fp; a.fo = t->fo; a.fwt = t->fwt; a.fbidx = t->fbidx; a.fbw = t->fbw;
-  a.mptr = t->mptr; a.ment = t->ment;
+  a.mptr = t->mptr; a.ment = t->ment; a.mpos = t->mpos;
   a.warp_a = t->warp_a; a.warp_b = t->warp_b; a.warps_out = t->warps_out;
-  a.lam = t->lam; a.wa = t->wa; a.partial = t->partial; a.csum = t->csum; a.erows = t->erows;
+  a.lam = t->lam; a.wa = t->wa; a.partial = t->partial; a.csum = t->csum;
+  a.erow = t->erow; a.evals = t->evals;
   a.nch_p = (int)((t->n + CHUNK - 1) / CHUNK);
   a.nch_m = (int)((t->match_cap + CHUNK - 1) / CHUNK);
   a.nch_e = (int)((t->ne + CHUNK - 1) / CHUNK);
   a.delta = t->delta; a.oknorm = t->oknorm;
   a.cvalid = t->cvalid; a.cobs = t->cobs; a.cnrm = t->cnrm;
-  a.pr_r = t->pr_r; a.pr_rs = t->pr_rs; a.pr_gn = t->pr_gn; a.pr_sgn = t->pr_sgn;
-  a.fr_res = t->fr_res; a.fr_G = t->fr_G; a.fr_sgn = t->fr_sgn;
+  a.pr_rs = t->pr_rs; a.prow = t->prow; a.mrow = t->mrow;
   a.ma_cap = (int)t->match_cap;
   a.counts = t->counts;
   a.report = t->report;
@@ -656,7 +663,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   k_scan_counts<<<1, 1024, 0, s>>>(t->mcnt, (int)t->m, t->mptr);
   DT_CHECK_LAUNCH();
   k_csr_fill_dev<<<cblocks, cthreads, 0, s>>>(t->fbidx, t->info + 3, (int)t->k, (int)t->m, t->mptr,
-                                              t->ment);
+                                              t->ment, t->mpos);
   DT_CHECK_LAUNCH();
   t->launches += 4;
   mark(t, 4);
@@ -783,6 +790,17 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
       eents[2 * e + s] = (int)((e << 1) | s);
     }
   host_csr(ekeys, eents, (int)m, iptr, ient);
+  // inverse maps: the CSR position of every (point, slot) and (edge, side), and per edge
+  // position the other endpoint + side and the edge weight (static per sequence)
+  std::vector<int> cpos(n * k), ipos(2 * n_edges), iinfo(2 * n_edges);
+  std::vector<double> iew(2 * n_edges);
+  for (size_t q = 0; q < cent.size(); ++q) cpos[(cent[q] >> 3) * k + (cent[q] & 7)] = (int)q;
+  for (size_t q = 0; q < ient.size(); ++q) {
+    const int e = ient[q] >> 1, side = ient[q] & 1;
+    ipos[2 * e + side] = (int)q;
+    iinfo[q] = (edges32[2 * e + (1 - side)] << 1) | side;
+    iew[q] = edge_weights[e];
+  }
 
   DT_TRY(dalloc(t, &t->tp, 3 * n));
   DT_TRY(dalloc(t, &t->tn, 3 * n));
@@ -795,6 +813,10 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_TRY(dalloc(t, &t->ew, n_edges));
   DT_TRY(dalloc(t, &t->iptr, m + 1));
   DT_TRY(dalloc(t, &t->ient, 2 * n_edges));
+  DT_TRY(dalloc(t, &t->cpos, k * n));
+  DT_TRY(dalloc(t, &t->ipos, 2 * n_edges));
+  DT_TRY(dalloc(t, &t->iinfo, 2 * n_edges));
+  DT_TRY(dalloc(t, &t->iew, 2 * n_edges));
   DT_TRY(upload(t, t->tp, t_points, 3 * n));
   DT_TRY(upload(t, t->tn, t_normals, 3 * n));
   DT_TRY(upload(t, t->bidx, bidx32.data(), k * n));
@@ -806,6 +828,10 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_TRY(upload(t, t->ew, edge_weights, n_edges));
   DT_TRY(upload(t, t->iptr, iptr.data(), m + 1));
   DT_TRY(upload(t, t->ient, ient.data(), ient.size()));
+  DT_TRY(upload(t, t->cpos, cpos.data(), cpos.size()));
+  DT_TRY(upload(t, t->ipos, ipos.data(), ipos.size()));
+  DT_TRY(upload(t, t->iinfo, iinfo.data(), iinfo.size()));
+  DT_TRY(upload(t, t->iew, iew.data(), iew.size()));
   // frame buffers
   DT_TRY(dalloc(t, &t->depth, npix));
   DT_TRY(dalloc(t, &t->onrm, 3 * npix));
@@ -824,16 +850,15 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_TRY(dalloc(t, &t->wa, m));
   DT_TRY(dalloc(t, &t->partial, 27 * m));
   DT_TRY(dalloc(t, &t->delta, 6 * m));
-  DT_TRY(dalloc(t, &t->oknorm, 4 * m));
+  DT_TRY(dalloc(t, &t->oknorm, 6 * m));
   DT_TRY(dalloc(t, &t->cvalid, 2 * n));
   DT_TRY(dalloc(t, &t->cobs, 2 * 3 * n));
   DT_TRY(dalloc(t, &t->cnrm, 2 * 3 * n));
-  DT_TRY(dalloc(t, &t->pr_r, 2 * n));
   DT_TRY(dalloc(t, &t->pr_rs, 2 * n));
-  DT_TRY(dalloc(t, &t->pr_gn, 2 * 8 * n));
-  DT_TRY(dalloc(t, &t->pr_sgn, 2 * n));
+  DT_TRY(dalloc(t, &t->prow, 2 * k * n * 8));
   DT_TRY(dalloc(t, &t->counts, 1024));
-  DT_TRY(dalloc(t, &t->erows, 40 * (n_edges > 0 ? n_edges : 1)));
+  DT_TRY(dalloc(t, &t->erow, 2 * 2 * 24 * (n_edges > 0 ? n_edges : 1)));
+  DT_TRY(dalloc(t, &t->evals, 2 * 3 * (n_edges > 0 ? n_edges : 1)));
   DT_TRY(dalloc(t, &t->bad_flag, 1));
   DT_TRY(dalloc(t, &t->report, 1));
   DT_TRY(dalloc(t, &t->cost_hist, 2 * cfg->max_outer_iters));
