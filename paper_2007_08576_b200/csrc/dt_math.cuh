@@ -45,6 +45,28 @@ __device__ __forceinline__ void blend_at(const double* __restrict__ warps, const
   }
 }
 
+// blend_at with a compile-time slot bound KM (k <= KM)
+template <int KM, typename IndexT>
+__device__ __forceinline__ void blend_at_k(const double* __restrict__ warps, const IndexT* idx,
+                                         const double* w, int k, double B[8], double sgn[KM]) {
+  const double* r = warps + 8 * (int64_t)idx[0];
+  const double rw = r[0], rx = r[1], ry = r[2], rz = r[3];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) B[e] = 0.0;
+#pragma unroll
+  for (int s = 0; s < KM; ++s) {
+    if (s < k) {
+      const double* W = warps + 8 * (int64_t)idx[s];
+      const double dot = W[0] * rw + W[1] * rx + W[2] * ry + W[3] * rz;
+      const double sg = dot < 0.0 ? -1.0 : 1.0;
+      sgn[s] = sg;
+      const double coef = w[s] * sg;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) B[e] += coef * W[e];
+    }
+  }
+}
+
 // Normalized dual-quaternion action of an unnormalized sum B on point p
 // (kernels.py:81-101, geometry.dq_apply_batch geometry.py:215-235):
 // x = (q p q* + 2 vec(d q*)) / |q|^2.

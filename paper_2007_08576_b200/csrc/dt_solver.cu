@@ -199,26 +199,18 @@ __device__ __forceinline__ void load_state(const SolverArgs& A, const double* sr
   __syncthreads();
 }
 
-template <typename IdxT>
+template <int KM, typename IdxT>
 __device__ __forceinline__ void blend_rows(const double* s_w, const IdxT* bidx, const double* bw,
-                                           int64_t i, int k, double B[8], double sgn[KMAX],
-                                           double a[KMAX]) {
-  int idx[KMAX];
+                                           int64_t i, int k, double B[8], double sgn[KM],
+                                           double a[KM]) {
+  int idx[KM];
 #pragma unroll
-  for (int s = 0; s < KMAX; ++s)
+  for (int s = 0; s < KM; ++s)
     if (s < k) {
       idx[s] = bidx[i * k + s];
       a[s] = bw[i * k + s];
     }
-  blend_at(s_w, idx, a, k, B, sgn);
-}
-
-__device__ __forceinline__ unsigned sign_bits(const double sgn[KMAX], int k) {
-  unsigned bits = 0;
-#pragma unroll
-  for (int s = 0; s < KMAX; ++s)
-    if (s < k && sgn[s] < 0.0) bits |= 1u << s;
-  return bits;
+  blend_at_k<KM>(s_w, idx, a, k, B, sgn);
 }
 
 // d(action)/dB with one reciprocal of |q|^2 (the Jacobian does not need the
@@ -464,8 +456,17 @@ __device__ __forceinline__ bool solve6(const double* part, double lam, double de
 
 #include "dt_solver_kernel.cuh"
 
-template __global__ void k_solve_frame<false>(const SolverArgs* __restrict__);
-template __global__ void k_solve_frame<true>(const SolverArgs* __restrict__);
+// KM = 4: the reference's bind_k (SolverConfig / RunConfig default, warpfield.py:157);
+// KM = 8: any k <= 8 with runtime slot guards
+template __global__ void k_solve_frame<false, 4>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 4>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 8>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 8>(const SolverArgs* __restrict__);
+
+template <bool GRID>
+static void* solver_fn(int k) {
+  return k == 4 ? (void*)k_solve_frame<GRID, 4> : (void*)k_solve_frame<GRID, 8>;
+}
 
 static int g_max_cluster[16] = {0};
 
@@ -473,7 +474,7 @@ int solver_max_cluster(int device) {
   if (device < 0 || device >= 16) return 8;
   if (g_max_cluster[device] > 0) return g_max_cluster[device];
   int best = 1;
-  auto* fn = k_solve_frame<false>;
+  auto* fn = k_solve_frame<false, 8>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const size_t smem = solver_smem_bytes(1024);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -510,7 +511,7 @@ int solver_pick_cluster(int device, int requested, int m_max) {
 }
 
 int solver_grid_blocks(int device, int m_max) {
-  auto* fn = k_solve_frame<true>;
+  auto* fn = k_solve_frame<true, 8>;
   const size_t smem = solver_smem_bytes(m_max);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0, sms = 0;
@@ -520,14 +521,16 @@ int solver_grid_blocks(int device, int m_max) {
   return per_sm >= 1 ? sms : 0;  // one CTA per SM
 }
 
-int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, int grid_mode,
+int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, int k, int grid_mode,
                   cudaStream_t s) {
+  DT_REQUIRE(k >= 1 && k <= KMAX, DT_ERR_UNSUPPORTED, "bind_k=%d outside the device path (<= %d)", k,
+             KMAX);
   const size_t smem = solver_smem_bytes(m_max);
   DT_REQUIRE(m_max <= M_MAX_SMEM && smem <= 227 * 1024, DT_ERR_UNSUPPORTED,
              "control graph too large for the shared-memory warp table (m=%d)", m_max);
   if (grid_mode) {
     DT_REQUIRE(n_seq == 1, DT_ERR_UNSUPPORTED, "grid mode runs one sequence per launch");
-    auto* fn = k_solve_frame<true>;
+    void* fn = solver_fn<true>(k);
     DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0;
     DT_CHECK_CUDA(cudaGetDevice(&dev));
@@ -538,7 +541,7 @@ int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, i
                                               params, smem, s));
     return DT_OK;
   }
-  auto* fn = k_solve_frame<false>;
+  void* fn = solver_fn<false>(k);
   DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
@@ -553,7 +556,8 @@ int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, i
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  DT_CHECK_CUDA(cudaLaunchKernelEx(&cfg, fn, d_args));
+  void* params[] = {(void*)&d_args};
+  DT_CHECK_CUDA(cudaLaunchKernelExC(&cfg, fn, params));
   return DT_OK;
 }
 

@@ -109,7 +109,7 @@ constexpr int RED_SLOTS = 5;
 size_t solver_smem_bytes(int m);
 // mode: 0 = one cluster of `cluster` CTAs per sequence; 1 = one cooperative grid over
 // every SM for a single sequence
-int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, int grid_mode,
+int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, int k, int grid_mode,
                   cudaStream_t s);
 int solver_pick_cluster(int device, int requested, int m_max);
 int solver_grid_blocks(int device, int m_max);

@@ -71,11 +71,13 @@ __device__ __forceinline__ void load_row(const double* src, double r[8]) {
 // point's icp cost under the Tukey weight of the new residual. With `ob`, *cost_old
 // receives the point's cost at these warps under the frozen correspondence and robust
 // weight of record `ob` (the value pass, solver.py:333-335).
+template <int KM>
 __device__ __forceinline__ double point_step(const SolverArgs& A, const double* s_w, int64_t p,
                                              const PBuf* ob, const PBuf& nb, double* cost_old,
                                              int* valid_out) {
-  double B[8], sgn[KMAX], a[KMAX];
-  blend_rows(s_w, A.bidx, A.bw, p, A.k, B, sgn, a);
+  const int kk = KM == 4 ? 4 : A.k;
+  double B[8], sgn[KM], a[KM];
+  blend_rows<KM>(s_w, A.bidx, A.bw, p, kk, B, sgn, a);
   const double px = A.tp[3 * p], py = A.tp[3 * p + 1], pz = A.tp[3 * p + 2];
   double x0, x1, x2, s2;
   apply_blend(B, px, py, pz, x0, x1, x2, s2);
@@ -87,8 +89,8 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
                        ld(ob->nrm + 3 * p + 2) * (x2 - ld(ob->obs + 3 * p + 2));
       const double rs = ld(ob->rs + p);
 #pragma unroll
-      for (int s = 0; s < KMAX; ++s)
-        if (s < A.k) {
+      for (int s = 0; s < KM; ++s)
+        if (s < kk) {
           const double wv = rs * sqrt(a[s]) * r;
           co += wv * wv;
         }
@@ -127,8 +129,8 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   if (!ok) {
     const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int s = 0; s < KMAX; ++s)
-      if (s < A.k) store_row(nb.row + 8 * (size_t)__ldg(A.cpos + p * A.k + s), z);
+    for (int s = 0; s < KM; ++s)
+      if (s < kk) store_row(nb.row + 8 * (size_t)__ldg(A.cpos + p * kk + s), z);
     return 0.0;
   }
   nb.obs[3 * p] = o0;
@@ -147,9 +149,9 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   for (int e = 0; e < 8; ++e) gn[e] = g0 * G[e] + g1 * G[8 + e] + g2 * G[16 + e];
   double cost = 0.0;
 #pragma unroll
-  for (int s = 0; s < KMAX; ++s)
-    if (s < A.k) {
-      const int c = A.bidx[p * A.k + s];
+  for (int s = 0; s < KM; ++s)
+    if (s < kk) {
+      const int c = A.bidx[p * kk + s];
       const double sw = rs * sqrt(a[s]);
       const double wv = sw * r;
       cost += wv * wv;
@@ -162,7 +164,7 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
       for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
       row[6] = wv;
       row[7] = sw;
-      store_row(nb.row + 8 * (size_t)__ldg(A.cpos + p * A.k + s), row);
+      store_row(nb.row + 8 * (size_t)__ldg(A.cpos + p * kk + s), row);
     }
   return cost;
 }
@@ -171,10 +173,12 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
 // rows [J0..J5, sqrt(w) res_c, (c == 0 ? sqrt(w) : 0)] at the slot's match-CSR position;
 // returns its feature cost (no robust weight, so the same value serves the value pass
 // and the relinearization).
+template <int KM>
 __device__ __forceinline__ double match_step(const SolverArgs& A, const double* s_w, int64_t j,
                                              double* rows) {
-  double B[8], sgn[KMAX], a[KMAX];
-  blend_rows(s_w, A.fbidx, A.fbw, j, A.k, B, sgn, a);
+  const int kk = KM == 4 ? 4 : A.k;
+  double B[8], sgn[KM], a[KM];
+  blend_rows<KM>(s_w, A.fbidx, A.fbw, j, kk, B, sgn, a);
   const double px = A.fp[3 * j], py = A.fp[3 * j + 1], pz = A.fp[3 * j + 2];
   double x0, x1, x2, s2;
   apply_blend(B, px, py, pz, x0, x1, x2, s2);
@@ -184,16 +188,16 @@ __device__ __forceinline__ double match_step(const SolverArgs& A, const double* 
   const double w = A.fwt[j];
   double cost = 0.0;
 #pragma unroll
-  for (int s = 0; s < KMAX; ++s)
-    if (s < A.k) {
-      const int c = A.fbidx[j * A.k + s];
+  for (int s = 0; s < KM; ++s)
+    if (s < kk) {
+      const int c = A.fbidx[j * kk + s];
       const double sw = sqrt(A.fw * w * a[s]);
       const double v0 = sw * res[0], v1 = sw * res[1], v2 = sw * res[2];
       cost += v0 * v0 + v1 * v1 + v2 * v2;
       const double coef = sw * a[s] * sgn[s];
       Basis K;
       make_basis(s_w + 8 * c, K);
-      double* dst = rows + 24 * (size_t)__ldg(A.mpos + j * A.k + s);
+      double* dst = rows + 24 * (size_t)__ldg(A.mpos + j * kk + s);
 #pragma unroll
       for (int comp = 0; comp < 3; ++comp) {
         double pr[6], row[8];
@@ -255,10 +259,26 @@ __device__ __forceinline__ double warp_red(int k, double v) {
   return v;
 }
 
-// Commit item ch (of nch) with the warp-uniform values v[NV]. Whole warp.
+// item value arrays of a slot (chunk-sum scratch in A.csum): slot 0 points (2 arrays),
+// slot 1 matches, slots 2 / 4 edges
+__device__ __forceinline__ double* red_vals(const SolverArgs& A, int slot, int k) {
+  const int nch_tot = A.nch_p + A.nch_m + A.nch_e;
+  if (slot == 0) return A.csum + (k == 0 ? 0 : nch_tot);
+  if (slot == 1) return A.csum + A.nch_p;
+  return A.csum + A.nch_p + A.nch_m;
+}
+
+__device__ __forceinline__ const double* red_total(const SolverArgs& A, int slot) {
+  return A.red + (size_t)slot * (2 * A.red_g + 2) + 2 * A.red_g;
+}
+
+// Commit item ch (of nch) with the warp-uniform values v[NV]. Whole warp. The slot's
+// pointers are derived from A (shared memory) on use, not kept in registers.
 template <int NV, int OP>
-__device__ __forceinline__ void red_commit(const RedSlot& R, double* const (&vals)[NV], int ch,
-                                           int nch, const double (&v)[NV]) {
+__device__ __noinline__ void red_commit(const SolverArgs& A, int slot, int ch, int nch,
+                                        const double (&v)[NV]) {
+  const RedSlot R = red_slot(A, slot);
+  double* vals[2] = {red_vals(A, slot, 0), red_vals(A, slot, 1)};
   const int lane = threadIdx.x & 31;
   const int g = ch >> 5;
   unsigned old = 0;
@@ -320,7 +340,7 @@ __device__ __forceinline__ void resolve_control(const SolverArgs& A, int c, doub
   nrm[c] = sqrt(nn);
 }
 
-template <bool GRID>
+template <bool GRID, int KM>
 __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverArgs* __restrict__ all) {
   Dom<GRID> dom;
   const int C = dom.size();
@@ -360,12 +380,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   const int nch_tot = A.nch_p + A.nch_m + A.nch_e;
   // chunk-sum set 0: value pass (points, matches, edges) and the rigidity cost of the
   // iterate; set 1: icp / feature cost of each (speculative) relinearization
-  double* cs_p0 = A.csum;
-  double* cs_m0 = cs_p0 + A.nch_p;
-  double* cs_e0 = cs_m0 + A.nch_m;
-  double* cs_p1 = A.csum + nch_tot;
-  const RedSlot RP = red_slot(A, 0), RM = red_slot(A, 1), RE = red_slot(A, 2),
-                RK = red_slot(A, 3), RV = red_slot(A, 4);
+
   long long* tr = A.trace;
   int tn = 0, nbar = 0;
   TRACE(0);
@@ -397,14 +412,14 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
       if (ch < nch_p) {
         const int64_t p = (int64_t)ch * CHUNK + lane;
         int vd;
-        if (p < n) acc = point_step(A, s_w, p, nullptr, nb, nullptr, &vd);
+        if (p < n) acc = point_step<KM>(A, s_w, p, nullptr, nb, nullptr, &vd);
         acc = warp_sum(acc);
-        red_commit<2, 0>(RP, {cs_p0, cs_p1}, ch, nch_p, {0.0, acc});
+        red_commit<2, 0>(A, 0, ch, nch_p, {0.0, acc});
       } else if (ch < nch_p + nch_m) {
         const int64_t j = (int64_t)(ch - nch_p) * CHUNK + lane;
-        if (j < n_act) acc = match_step(A, s_w, j, nm);
+        if (j < n_act) acc = match_step<KM>(A, s_w, j, nm);
         acc = warp_sum(acc);
-        red_commit<1, 0>(RM, {cs_m0}, ch - nch_p, nch_m, {acc});
+        red_commit<1, 0>(A, 1, ch - nch_p, nch_m, {acc});
       } else {
         const int e = (ch - nch_p - nch_m) * CHUNK + lane;
         double v[3];
@@ -413,8 +428,8 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     }
   }
   DSYNC(1);
-  if (threadIdx.x == 0) s_tot[0] = ld(RP.total + 1);
-  if (threadIdx.x == 1) s_tot[1] = nch_m > 0 ? ld(RM.total) : 0.0;
+  if (threadIdx.x == 0) s_tot[0] = ld(red_total(A, 0) + 1);
+  if (threadIdx.x == 1) s_tot[1] = nch_m > 0 ? ld(red_total(A, 1)) : 0.0;
   __syncthreads();
   cb_icp = s_tot[0];
   cb_feat = s_tot[1];
@@ -585,37 +600,55 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         for (int c = gc; c < m; c += GT) resolve_control(A, c, s_lam[c], okn, okn + m);
       }
       DSYNC(attempt == 0 ? 3 : 4);
-      // prefetch this thread's step inputs (one control per thread when m <= 512)
-      double pW[8], pD[6];
+      // Issue this thread's loads first: step inputs (one control per thread when
+      // m <= 512) and the per-control solve results; then apply the tentative step
+      // speculatively into shared memory while those loads land, then decide (all
+      // solves ok? largest step norm; after a fresh linearization also the rigidity cost
+      // of the iterate) -- identical in every CTA.
+      const bool want_e = attempt == 0 && need_lin;
       const int pc = threadIdx.x;
+      double o_ok = 1.0, o_nm = 0.0, o_ar = 0.0;
       if (pc < m) {
+        o_ok = ld(okn + pc);
+        o_nm = ld(okn + m + pc);
+        if (want_e) o_ar = ld(okn + 2 * m + pc);
+      }
+      {
+        double pW[8], pD[6];
+        if (pc < m) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) pW[i] = ld(cur + 8 * pc + i);
+          for (int i = 0; i < 8; ++i) pW[i] = ld(cur + 8 * pc + i);
 #pragma unroll
-        for (int i = 0; i < 6; ++i) pD[i] = ld(A.delta + 6 * pc + i);
+          for (int i = 0; i < 6; ++i) pD[i] = ld(A.delta + 6 * pc + i);
+          apply_step_one_fast(pW, pD, s_w + 8 * pc);
+        }
+        for (int c = pc + blockDim.x; c < m; c += blockDim.x) {
+          double W[8], d[6];
+          for (int i = 0; i < 8; ++i) W[i] = ld(cur + 8 * c + i);
+          for (int i = 0; i < 6; ++i) d[i] = ld(A.delta + 6 * c + i);
+          apply_step_one_fast(W, d, s_w + 8 * c);
+        }
+        smem_is_cur = false;
       }
       TRACE(57);
-      // all solves ok? largest step norm; after a fresh linearization also the rigidity
-      // cost of the iterate -- one batch of loads by every warp, one exchange (identical
-      // in every CTA; the P3 critical path stays free of commit atomics)
       {
-        const bool want_e = attempt == 0 && need_lin;
-        double allok = 1.0, mx = 0.0, es = 0.0;
-        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        double allok = o_ok, mx = o_nm, es = o_ar;
+        for (int i = pc + blockDim.x; i < m; i += blockDim.x) {
           allok = fmin(allok, ld(okn + i));
           mx = fmax(mx, ld(okn + m + i));
+          if (want_e) es += ld(okn + 2 * m + i);
         }
-        if (want_e)
-          for (int i = threadIdx.x; i < m; i += blockDim.x) es += ld(okn + 2 * m + i);
         allok = warp_min(allok);
         mx = warp_max(mx);
         es = warp_sum(es);
-        __syncthreads();
+        __syncthreads();  // also: the tentative warps are complete in s_w
         if (lane == 0) {
           s_part[3 * warp] = allok;
           s_part[3 * warp + 1] = mx;
           s_part[3 * warp + 2] = es;
         }
+        for (int c = pc; c < m; c += blockDim.x)
+          dq_to_transform_fast(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
         __syncthreads();
         allok = 1.0;
         mx = 0.0;
@@ -631,7 +664,6 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         parity ^= 1;
         if (!(allok > 0.5)) {
           // raise the damping of the failed controls only, retry (solver.py:321-326)
-          __syncthreads();
           for (int c = threadIdx.x; c < m; c += blockDim.x)
             if (ld(okn + c) < 0.5) s_lam[c] = fmin(s_lam[c] * A.lam_inc, A.lam_max);
           __syncthreads();
@@ -645,23 +677,8 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         }
       }
       TRACE(54);
-      // ---- tentative warps, applied redundantly by every CTA (no barrier) ----
-      __syncthreads();
-      if (pc < m) apply_step_one_fast(pW, pD, s_w + 8 * pc);
-      for (int c = threadIdx.x + blockDim.x; c < m; c += blockDim.x) {
-        double W[8], d[6];
-        for (int i = 0; i < 8; ++i) W[i] = ld(cur + 8 * c + i);
-        for (int i = 0; i < 6; ++i) d[i] = ld(A.delta + 6 * c + i);
-        apply_step_one_fast(W, d, s_w + 8 * c);
-      }
-      __syncthreads();
-      TRACE(55);
-      for (int c = threadIdx.x; c < m; c += blockDim.x)
-        dq_to_transform_fast(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
       for (int c = gc; c < m; c += GT)
         for (int i = 0; i < 8; ++i) tent[8 * c + i] = s_w[8 * c + i];
-      smem_is_cur = false;
-      __syncthreads();
       TRACE(52);
       // ---- P6: cost at the tentative warps with frozen weights and correspondences
       // (set 0) + speculative relinearization there (buffer 1 - pb, costs in set 1) ----
@@ -676,16 +693,16 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             const int64_t p = (int64_t)ch * CHUNK + lane;
             double co = 0.0, cn = 0.0;
             int vd;
-            if (p < n) cn = point_step(A, s_w, p, &ob, nb, &co, &vd);
+            if (p < n) cn = point_step<KM>(A, s_w, p, &ob, nb, &co, &vd);
             co = warp_sum(co);
             cn = warp_sum(cn);
-            red_commit<2, 0>(RP, {cs_p0, cs_p1}, ch, nch_p, {co, cn});
+            red_commit<2, 0>(A, 0, ch, nch_p, {co, cn});
           } else if (ch < nch_p + nch_m) {
             const int64_t j = (int64_t)(ch - nch_p) * CHUNK + lane;
             double cf = 0.0;
-            if (j < n_act) cf = match_step(A, s_w, j, nm);
+            if (j < n_act) cf = match_step<KM>(A, s_w, j, nm);
             cf = warp_sum(cf);
-            red_commit<1, 0>(RM, {cs_m0}, ch - nch_p, nch_m, {cf});
+            red_commit<1, 0>(A, 1, ch - nch_p, nch_m, {cf});
           } else {
             const int e = (ch - nch_p - nch_m) * CHUNK + lane;
             double acc = 0.0;
@@ -695,16 +712,21 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
               acc = edge_cost_vals(A, s_w, A.wa, e, v[0], v[1], v[2]);
             }
             acc = warp_sum(acc);
-            red_commit<1, 0>(RV, {cs_e0}, ch - nch_p - nch_m, nch_e, {acc});
+            red_commit<1, 0>(A, 4, ch - nch_p - nch_m, nch_e, {acc});
           }
         }
       }
+#ifdef DT_WARP_TRACE
+      // debug: per-warp end of the value pass on every CTA, first attempt of outer 1
+      if (A.arrivals && outer == 1 && attempt == 0 && lane == 0)
+        A.arrivals[2 + (size_t)1024 * A.arr_cap + (size_t)rank * NWARPS + warp] = gtimer();
+#endif
       DSYNC(6);
       // value pass (points, matches, edges) + cost of the speculative relinearization
-      if (threadIdx.x == 0) s_tot[0] = ld(RP.total);
-      if (threadIdx.x == 1) s_tot[1] = ld(RP.total + 1);
-      if (threadIdx.x == 2) s_tot[2] = nch_m > 0 ? ld(RM.total) : 0.0;
-      if (threadIdx.x == 3) s_tot[3] = nch_e > 0 ? ld(RV.total) : 0.0;
+      if (threadIdx.x == 0) s_tot[0] = ld(red_total(A, 0));
+      if (threadIdx.x == 1) s_tot[1] = ld(red_total(A, 0) + 1);
+      if (threadIdx.x == 2) s_tot[2] = nch_m > 0 ? ld(red_total(A, 1)) : 0.0;
+      if (threadIdx.x == 3) s_tot[3] = nch_e > 0 ? ld(red_total(A, 4)) : 0.0;
       __syncthreads();
       cost_after = (s_tot[0] + s_tot[2]) + s_tot[3];
       TRACE(63);
@@ -819,10 +841,10 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
       acc = edge_cost_vals(A, s_w, A.wa, e, ld(ev), ld(ev + 1), ld(ev + 2));
     }
     acc = warp_sum(acc);
-    red_commit<1, 0>(RE, {cs_e0}, ch, nch_e, {acc});
+    red_commit<1, 0>(A, 2, ch, nch_e, {acc});
   }
   DSYNC(9);
-  const double t_arap = nch_e > 0 ? ld(RE.total) : 0.0;
+  const double t_arap = nch_e > 0 ? ld(red_total(A, 2)) : 0.0;
   if (rank == 0 && threadIdx.x == 0) {
     dt_report* R = A.report;
     R->icp_cost = cb_icp;

@@ -677,7 +677,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     t->args_dirty = false;
   }
   DT_CHECK_CUDA(cudaMemsetAsync(t->stalled_hist, 0, sizeof(int32_t) * c.max_outer_iters, s));
-  DT_TRY(solver_launch(t->dev_args, 1, t->cluster, (int)t->m, t->grid_mode, s));
+  DT_TRY(solver_launch(t->dev_args, 1, t->cluster, (int)t->m, (int)t->k, t->grid_mode, s));
   ++t->launches;
   mark(t, 5);
   // ---- output warp (tracking.py:87) ----
@@ -1023,7 +1023,11 @@ int dt_tracker_get_arrivals(dt_tracker* t, long long* buf, int cap) {
   long long hdr[2] = {0, 0};
   DT_CHECK_CUDA(cudaMemcpyAsync(hdr, t->arrivals, sizeof(hdr), cudaMemcpyDeviceToHost, t->stream));
   DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
-  const long long want = std::min<long long>(cap, 2 + hdr[0] * (long long)t->arr_cap);
+  // the header + every CTA's stamps (+ the debug per-warp area when cap reaches it)
+  const long long alloc = 2 + 1024LL * t->arr_cap + 1024LL * 32;
+  const long long want = std::min<long long>(cap, cap > 2 + 1024LL * t->arr_cap
+                                                      ? alloc
+                                                      : 2 + hdr[0] * (long long)t->arr_cap);
   if (want > 0)
     DT_CHECK_CUDA(cudaMemcpyAsync(buf, t->arrivals, sizeof(long long) * want, cudaMemcpyDeviceToHost,
                                   t->stream));
@@ -1041,7 +1045,7 @@ int dt_tracker_set_profiling(dt_tracker* t, int on) {
     t->trace_cap = 4096;
     DT_TRY(dalloc(t, &t->trace, 1 + 2 * (size_t)t->trace_cap));
     t->arr_cap = 256;
-    DT_TRY(dalloc(t, &t->arrivals, 2 + 1024 * (size_t)t->arr_cap));
+    DT_TRY(dalloc(t, &t->arrivals, 2 + 1024 * (size_t)t->arr_cap + 1024 * 32));
   }
   t->profiling = on != 0;
   DT_TRY(push_args(t));
