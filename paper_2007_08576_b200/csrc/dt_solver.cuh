@@ -68,6 +68,7 @@ struct SolverArgs {
                      // bin (length, angle 0->1, angle 1->0; [J0..J5, value, 0])
   double* evals;     // 2 x (E) x 3: length / angle 0->1 / angle 1->0 values
   double* delta;     // m x 6
+  double* tentT;     // m x 12 rigid transforms (R, t) of the tentative warps
   double* oknorm;    // 2 parities x 3m: ok, step norm, rigidity cost of the control's bins
   // linearization, double-buffered: the value pass at a tentative iterate relinearizes
   // there speculatively into the other buffer, which becomes current when the step is

@@ -76,29 +76,45 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
                                              const PBuf* ob, const PBuf& nb, double* cost_old,
                                              int* valid_out) {
   const int kk = KM == 4 ? 4 : A.k;
+  // every load that does not depend on this point's arithmetic is issued up front (one
+  // L2 round trip after the domain barrier instead of a chain of them)
+  int pos[KM];
+#pragma unroll
+  for (int s = 0; s < KM; ++s)
+    if (s < kk) pos[s] = __ldg(A.cpos + p * kk + s);
+  uint8_t ovalid = 0;
+  double oo0 = 0, oo1 = 0, oo2 = 0, on0 = 0, on1 = 0, on2 = 0, ors = 0;
+  if (ob) {
+    ovalid = ldu8(ob->valid + p);
+    oo0 = ld(ob->obs + 3 * p);
+    oo1 = ld(ob->obs + 3 * p + 1);
+    oo2 = ld(ob->obs + 3 * p + 2);
+    on0 = ld(ob->nrm + 3 * p);
+    on1 = ld(ob->nrm + 3 * p + 1);
+    on2 = ld(ob->nrm + 3 * p + 2);
+    ors = ld(ob->rs + p);
+  }
+  const double px = A.tp[3 * p], py = A.tp[3 * p + 1], pz = A.tp[3 * p + 2];
+  const double tn0 = A.tn[3 * p], tn1 = A.tn[3 * p + 1], tn2 = A.tn[3 * p + 2];
   double B[8], sgn[KM], a[KM];
   blend_rows<KM>(s_w, A.bidx, A.bw, p, kk, B, sgn, a);
-  const double px = A.tp[3 * p], py = A.tp[3 * p + 1], pz = A.tp[3 * p + 2];
   double x0, x1, x2, s2;
   apply_blend(B, px, py, pz, x0, x1, x2, s2);
   if (ob) {
     double co = 0.0;
-    if (ldu8(ob->valid + p)) {
-      const double r = ld(ob->nrm + 3 * p) * (x0 - ld(ob->obs + 3 * p)) +
-                       ld(ob->nrm + 3 * p + 1) * (x1 - ld(ob->obs + 3 * p + 1)) +
-                       ld(ob->nrm + 3 * p + 2) * (x2 - ld(ob->obs + 3 * p + 2));
-      const double rs = ld(ob->rs + p);
+    if (ovalid) {
+      const double r = on0 * (x0 - oo0) + on1 * (x1 - oo1) + on2 * (x2 - oo2);
 #pragma unroll
       for (int s = 0; s < KM; ++s)
         if (s < kk) {
-          const double wv = rs * sqrt(a[s]) * r;
+          const double wv = ors * sqrt(a[s]) * r;
           co += wv * wv;
         }
     }
     *cost_old = co;
   }
   double r0, r1, r2;
-  rotate_normal(B, A.tn[3 * p], A.tn[3 * p + 1], A.tn[3 * p + 2], r0, r1, r2);
+  rotate_normal(B, tn0, tn1, tn2, r0, r1, r2);
   bool ok = false;
   double o0 = 0, o1 = 0, o2 = 0, g0 = 0, g1 = 0, g2 = 0;
   // projection and gates, in the reference's IEEE order (kernels.py:537-568)
@@ -108,14 +124,17 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
     if (uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height) {
       const int ui = (int)uf, vi = (int)vf;
       const int64_t pix = (int64_t)vi * A.width + ui;
-      if (A.dvalid[pix]) {
-        const double d = A.depth[pix];
+      // the pixel's validity, depth and normal in one round trip
+      const uint8_t dv = A.dvalid[pix];
+      const double d = A.depth[pix];
+      const double h0 = A.onrm[3 * pix], h1 = A.onrm[3 * pix + 1], h2 = A.onrm[3 * pix + 2];
+      if (dv) {
         o0 = ((double)ui - A.cx) / A.fx * d;
         o1 = ((double)vi - A.cy) / A.fy * d;
         o2 = d;
-        g0 = A.onrm[3 * pix];
-        g1 = A.onrm[3 * pix + 1];
-        g2 = A.onrm[3 * pix + 2];
+        g0 = h0;
+        g1 = h1;
+        g2 = h2;
         if (g0 * g0 + g1 * g1 + g2 * g2 > 0.25) {
           const double dx = o0 - x0, dy = o1 - x1, dz = d - x2;
           ok = sqrt(dx * dx + dy * dy + dz * dz) < A.gate &&
@@ -130,7 +149,7 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
     const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int s = 0; s < KM; ++s)
-      if (s < kk) store_row(nb.row + 8 * (size_t)__ldg(A.cpos + p * kk + s), z);
+      if (s < kk) store_row(nb.row + 8 * (size_t)pos[s], z);
     return 0.0;
   }
   nb.obs[3 * p] = o0;
@@ -164,7 +183,7 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
       for (int d = 0; d < 6; ++d) row[d] = coef * pr[d];
       row[6] = wv;
       row[7] = sw;
-      store_row(nb.row + 8 * (size_t)__ldg(A.cpos + p * kk + s), row);
+      store_row(nb.row + 8 * (size_t)pos[s], row);
     }
   return cost;
 }
@@ -323,12 +342,30 @@ __device__ __noinline__ void red_commit(const SolverArgs& A, int slot, int ch, i
   }
 }
 
-// damped solve of control c from the stored normal equations -> delta, ok / |delta|
+// the tentative warp of control c, exp(delta) * W (solver.py:261-264), and its rigid
+// transform, published for every CTA's value pass
+__device__ __forceinline__ void publish_tentative(const SolverArgs& A, int c, const double W[8],
+                                                  const double d[6], double* tent) {
+  double tw[8], T[12];
+  apply_step_one_fast(W, d, tw);
+  dq_to_transform_fast(tw, T, T + 9);
+  double2* t2 = reinterpret_cast<double2*>(tent + 8 * c);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) t2[i] = make_double2(tw[2 * i], tw[2 * i + 1]);
+  double2* T2 = reinterpret_cast<double2*>(A.tentT + 12 * c);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) T2[i] = make_double2(T[2 * i], T[2 * i + 1]);
+}
+
+// damped solve of control c from the stored normal equations -> delta, ok / |delta|,
+// and the tentative warp from the current one
 __device__ __forceinline__ void resolve_control(const SolverArgs& A, int c, double lam, double* ok,
-                                                double* nrm) {
-  double part[27], d[6];
+                                                double* nrm, const double* cur, double* tent) {
+  double part[27], d[6], W[8];
 #pragma unroll
   for (int i = 0; i < 27; ++i) part[i] = ld(A.partial + 27 * c + i);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) W[i] = ld(cur + 8 * c + i);
   const bool good = solve6(part, lam, d);
   double nn = 0.0;
 #pragma unroll
@@ -338,6 +375,7 @@ __device__ __forceinline__ void resolve_control(const SolverArgs& A, int c, doub
   }
   ok[c] = good ? 1.0 : 0.0;
   nrm[c] = sqrt(nn);
+  publish_tentative(A, c, W, d, tent);
 }
 
 template <bool GRID, int KM>
@@ -578,6 +616,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             }
             okv = good ? 1.0 : 0.0;
             nrm = sqrt(nn);
+            publish_tentative(A, c, s_w + 8 * c, d, tent);
           }
           if (lane == 0) {
             okn[c] = okv;
@@ -590,21 +629,20 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     } else {
       // after a stall the iterate and its linearization are unchanged: re-solve the
       // stored normal equations with the raised damping (solver.py:348-355)
-      for (int c = gc; c < m; c += GT) resolve_control(A, c, s_lam[c], okn, okn + m);
+      for (int c = gc; c < m; c += GT) resolve_control(A, c, s_lam[c], okn, okn + m, cur, tent);
     }
     bool accepted = false;
     double cost_before = 0.0, cost_after = 0.0;
     for (int attempt = 0; attempt <= A.max_retries; ++attempt) {
       if (attempt > 0) {
         okn = A.oknorm + (size_t)parity * 3 * m;
-        for (int c = gc; c < m; c += GT) resolve_control(A, c, s_lam[c], okn, okn + m);
+        for (int c = gc; c < m; c += GT) resolve_control(A, c, s_lam[c], okn, okn + m, cur, tent);
       }
       DSYNC(attempt == 0 ? 3 : 4);
-      // Issue this thread's loads first: step inputs (one control per thread when
-      // m <= 512) and the per-control solve results; then apply the tentative step
-      // speculatively into shared memory while those loads land, then decide (all
-      // solves ok? largest step norm; after a fresh linearization also the rigidity cost
-      // of the iterate) -- identical in every CTA.
+      // The solvers published every control's tentative warp and transform; load them
+      // into shared memory together with the per-control solve results (one round
+      // trip), then decide (all solves ok? largest step norm; after a fresh
+      // linearization also the rigidity cost of the iterate) -- identical in every CTA.
       const bool want_e = attempt == 0 && need_lin;
       const int pc = threadIdx.x;
       double o_ok = 1.0, o_nm = 0.0, o_ar = 0.0;
@@ -613,23 +651,26 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         o_nm = ld(okn + m + pc);
         if (want_e) o_ar = ld(okn + 2 * m + pc);
       }
-      {
-        double pW[8], pD[6];
-        if (pc < m) {
+      for (int c = pc; c < m; c += blockDim.x) {
+        const double2* t2 = reinterpret_cast<const double2*>(tent + 8 * c);
+        const double2* T2 = reinterpret_cast<const double2*>(A.tentT + 12 * c);
+        double2 w[4], T[6];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) pW[i] = ld(cur + 8 * pc + i);
+        for (int i = 0; i < 4; ++i) w[i] = __ldcg(t2 + i);
 #pragma unroll
-          for (int i = 0; i < 6; ++i) pD[i] = ld(A.delta + 6 * pc + i);
-          apply_step_one_fast(pW, pD, s_w + 8 * pc);
+        for (int i = 0; i < 6; ++i) T[i] = __ldcg(T2 + i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          s_w[8 * c + 2 * i] = w[i].x;
+          s_w[8 * c + 2 * i + 1] = w[i].y;
         }
-        for (int c = pc + blockDim.x; c < m; c += blockDim.x) {
-          double W[8], d[6];
-          for (int i = 0; i < 8; ++i) W[i] = ld(cur + 8 * c + i);
-          for (int i = 0; i < 6; ++i) d[i] = ld(A.delta + 6 * c + i);
-          apply_step_one_fast(W, d, s_w + 8 * c);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          s_T[12 * c + 2 * i] = T[i].x;
+          s_T[12 * c + 2 * i + 1] = T[i].y;
         }
-        smem_is_cur = false;
       }
+      smem_is_cur = false;
       TRACE(57);
       {
         double allok = o_ok, mx = o_nm, es = o_ar;
@@ -641,15 +682,13 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         allok = warp_min(allok);
         mx = warp_max(mx);
         es = warp_sum(es);
-        __syncthreads();  // also: the tentative warps are complete in s_w
+        __syncthreads();
         if (lane == 0) {
           s_part[3 * warp] = allok;
           s_part[3 * warp + 1] = mx;
           s_part[3 * warp + 2] = es;
         }
-        for (int c = pc; c < m; c += blockDim.x)
-          dq_to_transform_fast(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
-        __syncthreads();
+        __syncthreads();  // also: the tentative warps / transforms are complete in smem
         allok = 1.0;
         mx = 0.0;
         es = 0.0;
@@ -677,8 +716,6 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         }
       }
       TRACE(54);
-      for (int c = gc; c < m; c += GT)
-        for (int i = 0; i < 8; ++i) tent[8 * c + i] = s_w[8 * c + i];
       TRACE(52);
       // ---- P6: cost at the tentative warps with frozen weights and correspondences
       // (set 0) + speculative relinearization there (buffer 1 - pb, costs in set 1) ----

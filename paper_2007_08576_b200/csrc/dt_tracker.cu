@@ -330,7 +330,7 @@ struct dt_tracker {
   double* iew = nullptr;
   // solver state
   double *warp_a = nullptr, *warp_b = nullptr, *warps_out = nullptr, *lam = nullptr, *wa = nullptr;
-  double *partial = nullptr, *csum = nullptr, *delta = nullptr, *oknorm = nullptr;
+  double *partial = nullptr, *csum = nullptr, *delta = nullptr, *oknorm = nullptr, *tentT = nullptr;
   double *erow = nullptr, *evals = nullptr;
   uint8_t* cvalid = nullptr;
   double *cobs = nullptr, *cnrm = nullptr, *pr_rs = nullptr, *prow = nullptr, *mrow = nullptr;
@@ -454,7 +454,7 @@ void fill_args(dt_tracker* t) {
   a.nch_p = (int)((t->n + CHUNK - 1) / CHUNK);
   a.nch_m = (int)((t->match_cap + CHUNK - 1) / CHUNK);
   a.nch_e = (int)((t->ne + CHUNK - 1) / CHUNK);
-  a.delta = t->delta; a.oknorm = t->oknorm;
+  a.delta = t->delta; a.oknorm = t->oknorm; a.tentT = t->tentT;
   a.cvalid = t->cvalid; a.cobs = t->cobs; a.cnrm = t->cnrm;
   a.pr_rs = t->pr_rs; a.prow = t->prow; a.mrow = t->mrow;
   a.ma_cap = (int)t->match_cap;
@@ -851,6 +851,7 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_TRY(dalloc(t, &t->partial, 27 * m));
   DT_TRY(dalloc(t, &t->delta, 6 * m));
   DT_TRY(dalloc(t, &t->oknorm, 6 * m));
+  DT_TRY(dalloc(t, &t->tentT, 12 * m));
   DT_TRY(dalloc(t, &t->cvalid, 2 * n));
   DT_TRY(dalloc(t, &t->cobs, 2 * 3 * n));
   DT_TRY(dalloc(t, &t->cnrm, 2 * 3 * n));
