@@ -383,6 +383,24 @@ __device__ __forceinline__ double edge_cost_vals(const SolverArgs& A, const doub
 // Cholesky of the damped 6x6 system on a packed lower triangle (solver.py:217-258):
 // M = A + lam diag(max(diag A, 1e-12)); forward / backward substitution in the
 // reference's order. false (delta = 0) on a non-positive pivot.
+template <int J>
+__device__ __forceinline__ void chol_col(double (&L)[21], double (&inv)[6], bool& ok) {
+  double s = L[J * (J + 1) / 2 + J];
+#pragma unroll
+  for (int q = 0; q < J; ++q) s -= L[J * (J + 1) / 2 + q] * L[J * (J + 1) / 2 + q];
+  ok = ok && (s > 0.0);
+  const double ljj = sqrt(s);
+  inv[J] = 1.0 / ljj;
+  L[J * (J + 1) / 2 + J] = ljj;
+#pragma unroll
+  for (int i = J + 1; i < 6; ++i) {
+    double v = L[i * (i + 1) / 2 + J];
+#pragma unroll
+    for (int q = 0; q < J; ++q) v -= L[i * (i + 1) / 2 + q] * L[J * (J + 1) / 2 + q];
+    L[i * (i + 1) / 2 + J] = v * inv[J];
+  }
+}
+
 __device__ __forceinline__ bool solve6(const double* part, double lam, double delta[6]) {
   double L[21];  // row-major packed lower triangle: L[i(i+1)/2 + j]
 #pragma unroll
@@ -396,23 +414,14 @@ __device__ __forceinline__ bool solve6(const double* part, double lam, double de
   }
   bool ok = true;
   double inv[6];  // one reciprocal per pivot instead of a division per entry
-#pragma unroll
-  for (int j = 0; j < 6; ++j) {
-    double s = L[j * (j + 1) / 2 + j];
-#pragma unroll
-    for (int q = 0; q < j; ++q) s -= L[j * (j + 1) / 2 + q] * L[j * (j + 1) / 2 + q];
-    ok = ok && (s > 0.0);
-    const double ljj = sqrt(s);
-    inv[j] = 1.0 / ljj;
-    L[j * (j + 1) / 2 + j] = ljj;
-#pragma unroll
-    for (int i = j + 1; i < 6; ++i) {
-      double v = L[i * (i + 1) / 2 + j];
-#pragma unroll
-      for (int q = 0; q < j; ++q) v -= L[i * (i + 1) / 2 + q] * L[j * (j + 1) / 2 + q];
-      L[i * (i + 1) / 2 + j] = v * inv[j];
-    }
-  }
+  // one column per instantiation: the sqrt slow-path call inside a loop would keep the
+  // compiler from unrolling it and push L[] to local memory
+  chol_col<0>(L, inv, ok);
+  chol_col<1>(L, inv, ok);
+  chol_col<2>(L, inv, ok);
+  chol_col<3>(L, inv, ok);
+  chol_col<4>(L, inv, ok);
+  chol_col<5>(L, inv, ok);
   if (!ok) {
 #pragma unroll
     for (int i = 0; i < 6; ++i) delta[i] = 0.0;

@@ -11,7 +11,7 @@
 namespace dt {
 
 #ifndef DT_SOLVER_THREADS
-#define DT_SOLVER_THREADS 512
+#define DT_SOLVER_THREADS 256
 #endif
 constexpr int SOLVER_THREADS = DT_SOLVER_THREADS;
 constexpr int CHUNK = 32;  // items per deterministic partial sum (one per lane)

@@ -14,7 +14,7 @@
 // it at the same warps, bit for bit the same -- and only re-solves.
 
 #ifndef DT_TEAM
-#define DT_TEAM 4
+#define DT_TEAM 2
 #endif
 constexpr int TEAM = DT_TEAM;
 constexpr int TEAMS_PER_CTA = NWARPS / TEAM;
