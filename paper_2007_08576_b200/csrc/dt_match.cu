@@ -13,6 +13,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -279,12 +280,21 @@ __device__ __forceinline__ double irls_weight(const double R[9], double a0, doub
   const double e1 = b1 - __fma_rn(a2, R[5], __fma_rn(a1, R[4], a0 * R[3]));
   const double e2 = b2 - __fma_rn(a2, R[8], __fma_rn(a1, R[7], a0 * R[6]));
   const double s = __fma_rn(e2, e2, __fma_rn(e1, e1, e0 * e0));
-  const double w = H * rsqrt(fmax(s, 1e-300));
-  return s > Hsq ? w : 1.0;
+  // 1/sqrt(s) for s > H^2: the MUFU double-precision estimate refined by two Newton
+  // steps (~1 ulp; the full-precision rsqrt(double) carries special-case branches, and
+  // the weight is only needed where s > H^2 > 0)
+  const double sc = fmax(s, Hsq);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(sc));
+  const double hs = 0.5 * sc;
+  y = y * __fma_rn(-hs, y * y, 1.5);
+  y = y * __fma_rn(-hs, y * y, 1.5);
+  return s > Hsq ? H * y : 1.0;
 }
 
-// Layout: a CTA of PS_SEGS x PS_REFS threads evaluates PS_REFS hypotheses; thread
-// (seg, r) owns hypothesis r and the matches k = seg (mod PS_SEGS). Each thread keeps its
+// Layout: a CTA of PS_SEGS x nref threads (nref <= PS_REFS, chosen per launch so that
+// every SM gets the same number of hypotheses to within one CTA) evaluates nref
+// hypotheses; thread (seg, r) owns hypothesis r and the matches k = seg (mod PS_SEGS). Each thread keeps its
 // hypothesis' rotation in registers and runs an independent, unrolled match loop; the
 // per-segment covariances are combined in a fixed order through shared memory and the
 // PS_REFS SVDs run at once on the lanes of warp 0.
@@ -297,17 +307,17 @@ k_preselect_refs(const double* __restrict__ src, const double* __restrict__ dst,
                  const int64_t* __restrict__ n_dev, int64_t n_fixed,
                  const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive, double H,
                  int iters, double min_support, double* __restrict__ ref_support,
-                 double* __restrict__ ref_rot, uint8_t* __restrict__ ref_valid) {
+                 double* __restrict__ ref_rot, uint8_t* __restrict__ ref_valid, int nref) {
   __shared__ double s_C[PS_SEGS][PS_REFS][9];
   __shared__ double s_R[PS_REFS][9];
   __shared__ int s_live[PS_REFS];
   const int tid = threadIdx.x;
-  const int r = tid & (PS_REFS - 1);
-  const int seg = tid / PS_REFS;
+  const int r = tid % nref;
+  const int seg = tid / nref;
   const int64_t n = n_dev ? *n_dev : n_fixed;
   const int64_t nr = exhaustive ? n : n_refs;
-  const int64_t w = (int64_t)blockIdx.x * PS_REFS + r;
-  if ((int64_t)blockIdx.x * PS_REFS >= nr) return;  // CTA-uniform
+  const int64_t w = (int64_t)blockIdx.x * nref + r;
+  if ((int64_t)blockIdx.x * nref >= nr) return;  // CTA-uniform
   int64_t ref = -1;
   if (w < nr) ref = exhaustive ? w : refs[w];
   bool live = n >= 3 && ref >= 0 && ref < n;
@@ -355,7 +365,7 @@ k_preselect_refs(const double* __restrict__ src, const double* __restrict__ dst,
       }
       double Rm[9];
       const bool ok = procrustes_lane(Cr, Vm, Rm);
-      if (tid < PS_REFS) {
+      if (tid < nref) {
 #pragma unroll
         for (int i = 0; i < 9; ++i) s_R[r][i] = Rm[i];
         s_live[r] = ok ? 1 : 0;
@@ -377,7 +387,7 @@ k_preselect_refs(const double* __restrict__ src, const double* __restrict__ dst,
                        __ldg(dst + 3 * k + 1) - rd1, __ldg(dst + 3 * k + 2) - rd2, H, Hsq);
   s_C[seg][r][0] = sup;
   __syncthreads();
-  if (tid < PS_REFS && w < nr) {
+  if (tid < nref && w < nr) {
     double s = 0.0;
     for (int g = 0; g < PS_SEGS; ++g) s += s_C[g][r][0];
     const bool ok = live && !(s < min_support * (double)n);
@@ -484,9 +494,20 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
                      double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s) {
   const int64_t nr = exhaustive ? n_max : n_refs;
   if (nr > 0) {
-    k_preselect_refs<<<(unsigned)((nr + PS_REFS - 1) / PS_REFS), PS_THREADS, 0, s>>>(
+    static int sms = 0;
+    if (sms == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+    }
+    // two co-resident CTAs per SM: nref hypotheses per CTA so that the grid covers the
+    // hypotheses in one wave with every SM holding the same count to within one CTA
+    const int64_t per = (nr + 2 * sms - 1) / (2 * sms);
+    const int nref = (int)std::max<int64_t>(1, std::min<int64_t>(PS_REFS, per));
+    k_preselect_refs<<<(unsigned)((nr + nref - 1) / nref), nref * PS_SEGS, 0, s>>>(
         src, dst, n_dev, n_max, refs, n_refs, exhaustive, H, iters, min_support, ref_support,
-        ref_rot, ref_valid);
+        ref_rot, ref_valid, nref);
     DT_CHECK_LAUNCH();
   }
   k_preselect_final<<<1, 512, 0, s>>>(src, dst, n_dev, n_max, refs, n_refs, exhaustive, H,
