@@ -169,6 +169,57 @@ k_active(const int64_t* __restrict__ n_dev, const double* __restrict__ weights,
   }
 }
 
+// ORB path: scatter the preselected pairs back to their template features (weight 0 for
+// every feature without an active match) and the report statistics n_preselected and
+// match_weight_sum (solver.py:368-370), summed in the same fixed order as k_active.
+__global__ void __launch_bounds__(1024)
+k_feature_weights(const int64_t* __restrict__ n_dev, int64_t n_feat, const double* __restrict__ weights,
+                  const uint8_t* __restrict__ flags, const double* __restrict__ dst,
+                  const int32_t* __restrict__ feat_id, double* __restrict__ ffo,
+                  double* __restrict__ ffw, int64_t* __restrict__ n_active, double* __restrict__ stats) {
+  __shared__ double s_sum[32];
+  __shared__ int s_cnt[32];
+  const int64_t n = *n_dev;
+  for (int64_t f = threadIdx.x; f < n_feat; f += blockDim.x) ffw[f] = 0.0;
+  __syncthreads();
+  double wsum = 0.0;
+  int64_t nflag = 0;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t j = base + threadIdx.x;
+    const bool in = j < n;
+    const double w = in ? weights[j] : 0.0;
+    if (in) {
+      const int f = feat_id[j];
+      ffw[f] = w;
+      ffo[3 * f] = dst[3 * j];
+      ffo[3 * f + 1] = dst[3 * j + 1];
+      ffo[3 * f + 2] = dst[3 * j + 2];
+    }
+    const double v = warp_sum(w);
+    int flg = (in && flags[j]) ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) flg += __shfl_xor_sync(0xffffffffu, flg, o);
+    if ((threadIdx.x & 31) == 0) {
+      s_sum[threadIdx.x >> 5] = v;
+      s_cnt[threadIdx.x >> 5] = flg;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double cs = 0.0;
+      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) {
+        cs += s_sum[w2];
+        nflag += s_cnt[w2];
+      }
+      wsum += cs;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *n_active = n_feat;
+    stats[0] = wsum;
+    stats[1] = (double)nflag;
+  }
+}
+
 // Control -> (match * k + slot) CSR over the active matches, count read on the device.
 __global__ void k_csr_count_dev(const int32_t* __restrict__ keys, const int64_t* __restrict__ n_dev,
                                 int k, int m, int* __restrict__ cnt) {
@@ -311,6 +362,12 @@ struct dt_tracker {
   int32_t* fkp = nullptr;
   int64_t fdesc_cap = 0;
   int32_t *ham_idx = nullptr, *ham_dist = nullptr;
+  // ORB path: the solver's match arrays are indexed by template feature -- points,
+  // binding and the control -> (feature, slot) CSR are static (set_features); per frame
+  // only the observed points and weights change (0 = not an active match)
+  int *fptr = nullptr, *fent = nullptr, *fpos = nullptr;
+  double *ffo = nullptr, *ffw = nullptr;
+  bool orb_static = false;
   // matches
   int64_t match_cap = 0;
   double *m_src = nullptr, *m_dst = nullptr, *m_w = nullptr, *m_res = nullptr, *m_bw = nullptr;
@@ -446,8 +503,13 @@ void fill_args(dt_tracker* t) {
   a.ipos = t->ipos; a.iinfo = t->iinfo; a.iew = t->iew;
   a.depth = t->depth; a.dvalid = t->dvalid; a.onrm = t->onrm;
   a.n_active = t->info + 3;
-  a.fp = t->fp; a.fo = t->fo; a.fwt = t->fwt; a.fbidx = t->fbidx; a.fbw = t->fbw;
-  a.mptr = t->mptr; a.ment = t->ment; a.mpos = t->mpos;
+  if (t->orb_static) {
+    a.fp = t->tfeat_pts; a.fo = t->ffo; a.fwt = t->ffw; a.fbidx = t->tfeat_bidx; a.fbw = t->tfeat_bw;
+    a.mptr = t->fptr; a.ment = t->fent; a.mpos = t->fpos;
+  } else {
+    a.fp = t->fp; a.fo = t->fo; a.fwt = t->fwt; a.fbidx = t->fbidx; a.fbw = t->fbw;
+    a.mptr = t->mptr; a.ment = t->ment; a.mpos = t->mpos;
+  }
   a.warp_a = t->warp_a; a.warp_b = t->warp_b; a.warps_out = t->warps_out;
   a.lam = t->lam; a.wa = t->wa; a.partial = t->partial; a.csum = t->csum;
   a.erow = t->erow; a.evals = t->evals;
@@ -652,20 +714,33 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     ++t->launches;
   }
   mark(t, 3);
-  k_active<<<1, 1024, 0, s>>>(t->info + 2, t->m_w, t->m_flags, t->m_src, t->m_dst, t->m_bidx,
-                              t->m_bw, (int)t->k, use ? 1 : 0, t->fp, t->fo, t->fwt, t->fbidx,
-                              t->fbw, t->info + 3, t->astats);
-  DT_CHECK_LAUNCH();
-  const int cthreads = 256;
-  const int cblocks = grid_for(t->m * 32, cthreads);
-  k_csr_count_dev<<<cblocks, cthreads, 0, s>>>(t->fbidx, t->info + 3, (int)t->k, (int)t->m, t->mcnt);
-  DT_CHECK_LAUNCH();
-  k_scan_counts<<<1, 1024, 0, s>>>(t->mcnt, (int)t->m, t->mptr);
-  DT_CHECK_LAUNCH();
-  k_csr_fill_dev<<<cblocks, cthreads, 0, s>>>(t->fbidx, t->info + 3, (int)t->k, (int)t->m, t->mptr,
-                                              t->ment, t->mpos);
-  DT_CHECK_LAUNCH();
-  t->launches += 4;
+  const bool orb_static = use && in->frame_desc != nullptr;
+  if (orb_static != t->orb_static) {
+    t->orb_static = orb_static;
+    t->args_dirty = true;
+  }
+  if (orb_static) {
+    // matches indexed by template feature: static points / binding / CSR
+    k_feature_weights<<<1, 1024, 0, s>>>(t->info + 2, t->n_feat, t->m_w, t->m_flags, t->m_dst,
+                                         t->m_feat, t->ffo, t->ffw, t->info + 3, t->astats);
+    DT_CHECK_LAUNCH();
+    t->launches += 1;
+  } else {
+    k_active<<<1, 1024, 0, s>>>(t->info + 2, t->m_w, t->m_flags, t->m_src, t->m_dst, t->m_bidx,
+                                t->m_bw, (int)t->k, use ? 1 : 0, t->fp, t->fo, t->fwt, t->fbidx,
+                                t->fbw, t->info + 3, t->astats);
+    DT_CHECK_LAUNCH();
+    const int cthreads = 256;
+    const int cblocks = grid_for(t->m * 32, cthreads);
+    k_csr_count_dev<<<cblocks, cthreads, 0, s>>>(t->fbidx, t->info + 3, (int)t->k, (int)t->m, t->mcnt);
+    DT_CHECK_LAUNCH();
+    k_scan_counts<<<1, 1024, 0, s>>>(t->mcnt, (int)t->m, t->mptr);
+    DT_CHECK_LAUNCH();
+    k_csr_fill_dev<<<cblocks, cthreads, 0, s>>>(t->fbidx, t->info + 3, (int)t->k, (int)t->m, t->mptr,
+                                                t->ment, t->mpos);
+    DT_CHECK_LAUNCH();
+    t->launches += 4;
+  }
   mark(t, 4);
 
   // ---- solve ----
@@ -915,6 +990,32 @@ int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* po
   } else {
     DT_TRY(launch_bind_points_i32(t->tfeat_pts, n_features, t->cpts, (int)t->m, (int)t->k,
                                   t->cfg.sampling_radius, t->tfeat_bidx, t->tfeat_bw, t->stream));
+  }
+  // static control -> (feature, slot) CSR of the ORB path, built on the host once
+  {
+    const int64_t k = t->k;
+    std::vector<int32_t> fb(n_features * k);
+    if (n_features > 0) {
+      DT_CHECK_CUDA(cudaMemcpyAsync(fb.data(), t->tfeat_bidx, sizeof(int32_t) * fb.size(),
+                                    cudaMemcpyDeviceToHost, t->stream));
+      DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
+    }
+    std::vector<int> keys(fb.begin(), fb.end()), ents(n_features * k), fptr, fent;
+    for (int64_t i = 0; i < n_features * k; ++i) ents[i] = (int)i;
+    host_csr(keys, ents, (int)t->m, fptr, fent);
+    std::vector<int> fpos(n_features * k);
+    for (size_t q = 0; q < fent.size(); ++q) fpos[fent[q]] = (int)q;
+    DT_TRY(dalloc(t, &t->fptr, t->m + 1));
+    DT_TRY(dalloc(t, &t->fent, std::max<int64_t>(1, n_features * k)));
+    DT_TRY(dalloc(t, &t->fpos, std::max<int64_t>(1, n_features * k)));
+    DT_TRY(dalloc(t, &t->ffo, 3 * std::max<int64_t>(1, n_features)));
+    DT_TRY(dalloc(t, &t->ffw, std::max<int64_t>(1, n_features)));
+    DT_TRY(upload(t, t->fptr, fptr.data(), fptr.size()));
+    if (!fent.empty()) {
+      DT_TRY(upload(t, t->fent, fent.data(), fent.size()));
+      DT_TRY(upload(t, t->fpos, fpos.data(), fpos.size()));
+    }
+    DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
   }
   DT_TRY(push_args(t));
   return DT_OK;
