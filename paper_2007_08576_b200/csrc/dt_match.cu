@@ -27,7 +27,7 @@ namespace dt {
 // ---------------------------------------------------------------------------------
 
 constexpr int HAM_TPW = 2;                 // template descriptors per warp
-constexpr int HAM_WARPS = 8;               // warps per CTA
+constexpr int HAM_WARPS = 4;               // warps per CTA (2000 templates -> 250 CTAs)
 constexpr int HAM_TILE = 512;              // frame descriptors per smem tile (16 KB)
 
 __global__ void __launch_bounds__(HAM_WARPS * 32)

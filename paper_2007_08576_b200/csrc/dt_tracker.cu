@@ -63,48 +63,90 @@ __device__ __forceinline__ int block_scan_flag(bool flag, int* s_warp, int* tota
   return off;
 }
 
+// Block-wide exclusive scan of per-thread counts (1024-thread CTA, warp shuffles + one
+// pass over the warp totals). Returns this thread's offset; *total = the block's sum.
+__device__ __forceinline__ int block_scan_count(int cnt, int* s_warp, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      const int v = s_warp[w];
+      s_warp[w] = run;
+      run += v;
+    }
+    s_warp[32] = run;
+  }
+  __syncthreads();
+  const int off = s_warp[warp] + inc - cnt;
+  *total = s_warp[32];
+  __syncthreads();
+  return off;
+}
+
 // ORB path: keep, in template-feature order, every feature whose best frame match passes
 // the Hamming gate and lands on a valid depth pixel; the observed point is the keypoint
 // back-projected through the frame's depth (geometry.back_project, geometry.py:387-396).
+// Each thread owns BM_PER consecutive features per round, so every load of a round is in
+// flight before the single block scan.
+constexpr int BM_PER = 4;
+
 __global__ void __launch_bounds__(1024)
 k_build_matches(int64_t nt, const int32_t* __restrict__ best_idx, const int32_t* __restrict__ best_dist,
                 int max_ham, const int32_t* __restrict__ kp, int64_t nf,
                 const double* __restrict__ depth, const uint8_t* __restrict__ dvalid, int width,
                 int height, double fx, double fy, double cx, double cy,
-                const double* __restrict__ tpts, const int32_t* __restrict__ tbidx,
-                const double* __restrict__ tbw, int k, double* __restrict__ src,
-                double* __restrict__ dst, int32_t* __restrict__ bidx, double* __restrict__ bw,
-                int32_t* __restrict__ feat_id, int64_t* __restrict__ n_out) {
+                const double* __restrict__ tpts, double* __restrict__ src,
+                double* __restrict__ dst, int32_t* __restrict__ feat_id, int64_t* __restrict__ n_out) {
   __shared__ int s_warp[33];
   int64_t base_out = 0;
-  for (int64_t base = 0; base < nt; base += blockDim.x) {
-    const int64_t t = base + threadIdx.x;
-    bool ok = false;
-    int u = 0, v = 0;
-    if (t < nt) {
-      const int f = best_idx[t];
-      if (f >= 0 && f < nf && best_dist[t] <= max_ham) {
-        u = kp[2 * f];
-        v = kp[2 * f + 1];
-        ok = u >= 0 && u < width && v >= 0 && v < height && dvalid[(int64_t)v * width + u];
+  for (int64_t base = 0; base < nt; base += (int64_t)blockDim.x * BM_PER) {
+    const int64_t t0 = base + (int64_t)threadIdx.x * BM_PER;
+    int fi[BM_PER], u[BM_PER], v[BM_PER];
+    bool ok[BM_PER];
+#pragma unroll
+    for (int e = 0; e < BM_PER; ++e) {
+      const int64_t t = t0 + e;
+      fi[e] = -1;
+      if (t < nt && best_dist[t] <= max_ham) fi[e] = best_idx[t];
+    }
+#pragma unroll
+    for (int e = 0; e < BM_PER; ++e) {
+      u[e] = v[e] = -1;
+      if (fi[e] >= 0 && fi[e] < nf) {
+        u[e] = kp[2 * fi[e]];
+        v[e] = kp[2 * fi[e] + 1];
       }
     }
+    int cnt = 0;
+#pragma unroll
+    for (int e = 0; e < BM_PER; ++e) {
+      ok[e] = u[e] >= 0 && u[e] < width && v[e] >= 0 && v[e] < height &&
+              dvalid[(int64_t)v[e] * width + u[e]];
+      cnt += ok[e] ? 1 : 0;
+    }
     int total;
-    const int off = block_scan_flag(ok, s_warp, &total);
-    if (ok) {
-      const int64_t o = base_out + off;
-      const double d = depth[(int64_t)v * width + u];
+    int64_t o = base_out + block_scan_count(cnt, s_warp, &total);
+#pragma unroll
+    for (int e = 0; e < BM_PER; ++e) {
+      if (!ok[e]) continue;
+      const int64_t t = t0 + e;
+      const double d = depth[(int64_t)v[e] * width + u[e]];
       src[3 * o] = tpts[3 * t];
       src[3 * o + 1] = tpts[3 * t + 1];
       src[3 * o + 2] = tpts[3 * t + 2];
-      dst[3 * o] = ((double)u - cx) / fx * d;
-      dst[3 * o + 1] = ((double)v - cy) / fy * d;
+      dst[3 * o] = ((double)u[e] - cx) / fx * d;
+      dst[3 * o + 1] = ((double)v[e] - cy) / fy * d;
       dst[3 * o + 2] = d;
-      for (int s = 0; s < k; ++s) {
-        bidx[o * k + s] = tbidx[t * k + s];
-        bw[o * k + s] = tbw[t * k + s];
-      }
       feat_id[o] = (int32_t)t;
+      ++o;
     }
     base_out += total;
   }
@@ -653,8 +695,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     DT_TRY(launch_hamming(t->tdesc, t->n_feat, t->fdesc, in->n_frame, t->ham_idx, t->ham_dist, s));
     k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_idx, t->ham_dist, c.max_hamming, t->fkp,
                                        in->n_frame, t->depth, t->dvalid, c.width, c.height, c.fx,
-                                       c.fy, c.cx, c.cy, t->tfeat_pts, t->tfeat_bidx, t->tfeat_bw,
-                                       (int)t->k, t->m_src, t->m_dst, t->m_bidx, t->m_bw, t->m_feat,
+                                       c.fy, c.cx, c.cy, t->tfeat_pts, t->m_src, t->m_dst, t->m_feat,
                                        t->info + 2);
     DT_CHECK_LAUNCH();
     t->launches += 2;
