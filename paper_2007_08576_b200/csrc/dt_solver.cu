@@ -360,22 +360,19 @@ __device__ __forceinline__ double edge_cost_vals(const SolverArgs& A, const doub
                                                  double v10) {
   const int i0 = A.edges[2 * e], i1 = A.edges[2 * e + 1];
   const double base = A.ew[e] * 0.5 * (ld(wa + i0) + ld(wa + i1));
-  const double sw = sqrt(0.5 * base);
-  const double swa = sqrt(0.5 * base * A.angle_w);
-  const double swr = sqrt(0.5 * base * A.rot_w);
-  const double wl = sw * lv;
-  const double w01 = swa * v01;
-  const double w10 = swa * v10;
+  // (sqrt(0.5 base w) v)^2 without the square roots: the same value to an ulp
+  const double hb = 0.5 * base;
+  const double hba = hb * A.angle_w;
   const double* q0 = s_w + 8 * i0;
   const double* q1 = s_w + 8 * i1;
   const double dq = q0[0] * q1[0] + q0[1] * q1[1] + q0[2] * q1[2] + q0[3] * q1[3];
   const double sg = dq < 0.0 ? -1.0 : 1.0;
   const double d0 = q0[0] - sg * q1[0], d1 = q0[1] - sg * q1[1], d2 = q0[2] - sg * q1[2],
                d3 = q0[3] - sg * q1[3];
-  double c = wl * wl;
-  c += w01 * w01;
-  c += w10 * w10;
-  c += swr * swr * (d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3);
+  double c = hb * (lv * lv);
+  c += hba * (v01 * v01);
+  c += hba * (v10 * v10);
+  c += hb * A.rot_w * (d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3);
   return 2.0 * c;
 }
 

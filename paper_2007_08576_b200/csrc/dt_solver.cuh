@@ -23,6 +23,7 @@ struct SolverArgs {
   // camera, gates and energy weights
   double fx, fy, cx, cy, gate, cos_gate;
   double tukey, fw, arap_w, angle_w, rot_w, data_floor;
+  double sq_angle_w, sq_rot_w;  // sqrt(angle_w), sqrt(rot_w)
   // damping schedule and tolerances (SolverConfig, solver.py:43-71)
   double lam_init, lam_dec, lam_inc, lam_min, lam_max, step_tol, cost_tol;
   // bound template (static per sequence)
@@ -30,6 +31,7 @@ struct SolverArgs {
   const double* tn;
   const int32_t* bidx;
   const double* bw;
+  const double* bws;  // (n*k) sqrt of the binding weights (correctly rounded, = the reference's sqrt(alpha))
   const int* cptr;   // control -> template (point, slot) entries, encoded (p << 3) | slot
   const int* cent;
   const int* cpos;   // (n*k) inverse: CSR position of (point, slot)

@@ -79,9 +79,13 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   // every load that does not depend on this point's arithmetic is issued up front (one
   // L2 round trip after the domain barrier instead of a chain of them)
   int pos[KM];
+  double sqa[KM];  // sqrt(alpha), precomputed (correctly rounded: the reference's value)
 #pragma unroll
   for (int s = 0; s < KM; ++s)
-    if (s < kk) pos[s] = __ldg(A.cpos + p * kk + s);
+    if (s < kk) {
+      pos[s] = __ldg(A.cpos + p * kk + s);
+      sqa[s] = __ldg(A.bws + p * kk + s);
+    }
   uint8_t ovalid = 0;
   double oo0 = 0, oo1 = 0, oo2 = 0, on0 = 0, on1 = 0, on2 = 0, ors = 0;
   if (ob) {
@@ -107,7 +111,7 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
 #pragma unroll
       for (int s = 0; s < KM; ++s)
         if (s < kk) {
-          const double wv = ors * sqrt(a[s]) * r;
+          const double wv = ors * sqa[s] * r;
           co += wv * wv;
         }
     }
@@ -171,7 +175,7 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   for (int s = 0; s < KM; ++s)
     if (s < kk) {
       const int c = A.bidx[p * kk + s];
-      const double sw = rs * sqrt(a[s]);
+      const double sw = rs * sqa[s];
       const double wv = sw * r;
       cost += wv * wv;
       const double coef = sw * a[s] * sgn[s];
@@ -562,8 +566,8 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
               const double base_w =
                   __ldg(A.iew + q) * 0.5 * (side == 0 ? wac + wao : wao + wac);
               sw = sqrt(0.5 * base_w);
-              swa = sqrt(0.5 * base_w * A.angle_w);
-              swr = sqrt(0.5 * base_w * A.rot_w);
+              swa = sw * A.sq_angle_w;  // = sqrt(0.5 base angle_w) to an ulp
+              swr = sw * A.sq_rot_w;
             }
             if (live) {
               double row[8];

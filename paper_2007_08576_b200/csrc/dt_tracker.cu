@@ -388,7 +388,7 @@ struct dt_tracker {
   cudaEvent_t ev[DT_N_PHASES + 1] = {};
   std::vector<DevBuf> bufs;
   // template / graph
-  double *tp = nullptr, *tn = nullptr, *bw = nullptr, *cpts = nullptr, *ew = nullptr;
+  double *tp = nullptr, *tn = nullptr, *bw = nullptr, *bws = nullptr, *cpts = nullptr, *ew = nullptr;
   int32_t *bidx = nullptr, *edges = nullptr;
   int *cptr = nullptr, *cent = nullptr, *iptr = nullptr, *ient = nullptr;
   // frame
@@ -531,6 +531,8 @@ void fill_args(dt_tracker* t) {
   a.arap_w = c.arap_weight;
   a.angle_w = c.angle_weight;
   a.rot_w = c.rotation_weight;
+  a.sq_angle_w = std::sqrt(c.angle_weight);
+  a.sq_rot_w = std::sqrt(c.rotation_weight);
   a.data_floor = c.data_floor;
   a.lam_init = c.lambda_init;
   a.lam_dec = c.lambda_decrease;
@@ -539,7 +541,7 @@ void fill_args(dt_tracker* t) {
   a.lam_max = c.lambda_max;
   a.step_tol = c.step_tol;
   a.cost_tol = c.cost_tol;
-  a.tp = t->tp; a.tn = t->tn; a.bidx = t->bidx; a.bw = t->bw;
+  a.tp = t->tp; a.tn = t->tn; a.bidx = t->bidx; a.bw = t->bw; a.bws = t->bws;
   a.cptr = t->cptr; a.cent = t->cent; a.cpos = t->cpos;
   a.cpts = t->cpts; a.edges = t->edges; a.ew = t->ew; a.iptr = t->iptr; a.ient = t->ient;
   a.ipos = t->ipos; a.iinfo = t->iinfo; a.iew = t->iew;
@@ -922,6 +924,7 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_TRY(dalloc(t, &t->tn, 3 * n));
   DT_TRY(dalloc(t, &t->bidx, k * n));
   DT_TRY(dalloc(t, &t->bw, k * n));
+  DT_TRY(dalloc(t, &t->bws, k * n));
   DT_TRY(dalloc(t, &t->cptr, m + 1));
   DT_TRY(dalloc(t, &t->cent, k * n));
   DT_TRY(dalloc(t, &t->cpts, 3 * m));
@@ -937,6 +940,12 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   DT_TRY(upload(t, t->tn, t_normals, 3 * n));
   DT_TRY(upload(t, t->bidx, bidx32.data(), k * n));
   DT_TRY(upload(t, t->bw, bind_w, k * n));
+  {
+    std::vector<double> bws(k * n);
+    for (int64_t i = 0; i < k * n; ++i) bws[i] = std::sqrt(bind_w[i]);
+    DT_TRY(upload(t, t->bws, bws.data(), bws.size()));
+    DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));  // bws is stack-owned
+  }
   DT_TRY(upload(t, t->cptr, cptr.data(), m + 1));
   DT_TRY(upload(t, t->cent, cent.data(), cent.size()));
   DT_TRY(upload(t, t->cpts, ctrl_points, 3 * m));

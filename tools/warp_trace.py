@@ -39,7 +39,8 @@ def main():
     buf = np.zeros(cap, dtype=np.int64)
     lib.dt_tracker_get_arrivals(trk._h, _host_ptr(buf), cap)
     n_cta = int(buf[0])
-    warps = buf[2 + 1024 * 256: 2 + 1024 * 256 + n_cta * 16].reshape(n_cta, 16)
+    nw = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+    warps = buf[2 + 1024 * 256: 2 + 1024 * 256 + n_cta * nw].reshape(n_cta, nw)
     # release of the barrier before the value pass of outer 1 (codes 31 / 41 in order)
     rel = [t for c, t in tr if c == 31]
     t0 = rel[1] if len(rel) > 1 else rel[0]
