@@ -113,6 +113,9 @@ def workload_config(wl, n_gpus, rank_frames_desc):
 
 
 class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms DURING the timed region
+    (one streaming `nvidia-smi -lms` child, stopped by its own PID)."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -120,29 +123,37 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
-        self._stop = threading.Event()
+        self._p = None
         self._t = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _read(self):
+        for line in self._p.stdout:
+            parts = [x.strip() for x in line.strip().split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.15)  # first sample lands before the timed region starts
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is not None:
+            time.sleep(0.1)
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except Exception:
+                self._p.kill()
+            self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
@@ -155,6 +166,23 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.samples)}
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    """Max of a per-rank time over all ranks (all_reduce MAX; identity at world 1)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_throughput(frames_per_rank: int, world: int, max_ms: float) -> float:
+    """Whole-job frames/s of `world` independent replicas timed to the slowest rank."""
+    return world * frames_per_rank / (max_ms / 1e3)
 
 
 # ---------------------------------------------------------------------------------
@@ -262,11 +290,7 @@ def run_b200(args, rank, world, local_rank):
         stream.synchronize()
     torch.cuda.synchronize()
     per_frame_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = float(sum(per_frame_ms))
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(float(sum(per_frame_ms)), world, dev)
 
     # report of the last timed frame (outputs resident on the device)
     rep = Report()
@@ -326,14 +350,10 @@ def run_b200(args, rank, world, local_rank):
             t0 = time.perf_counter()
             trk.track_raw(fi, fo)
             wall += time.perf_counter() - t0
-        wall_ms = wall * 1e3
-        if world > 1:
-            t = torch.tensor([wall_ms], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            wall_ms = float(t.item())
+        wall_ms = max_over_ranks(wall * 1e3, world, dev)
         h2d = frames[0].depth.nbytes + frames[0].descriptors.nbytes + frames[0].keypoints.nbytes
         d2h = out_w.numel() * 8 + out_p.numel() * 8 + out_n.numel() * 8 + C.sizeof(Report)
-        e2e = {"value": world * K / (wall_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": replica_throughput(K, world, wall_ms), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": wall_ms / K,
                "api": "dt_track_frame (C-ABI) via paper_2007_08576_b200._session.DeviceTracker.track_raw"}
 
@@ -360,7 +380,7 @@ def run_b200(args, rank, world, local_rank):
                 "dominant_phase": dominant,
                 "note": "latency-bound: ~40 dependent phases/frame; see DESIGN.md §4"}
 
-    value = world * K / (total_ms / 1e3)
+    value = replica_throughput(K, world, total_ms)
     ms_per_step = total_ms / K
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
@@ -431,28 +451,39 @@ def cpu_baseline(wl, n_frames):
             "ms_per_frame": dt * 1e3 / n_frames}
 
 
+# The reference arm runs the whole frame on the host cores (~1.5 s per config-2 frame on
+# 16 cores), so the run is bounded: at most REF_MAX_FRAMES timed frames and
+# REF_MAX_WARMUP warm-up frames whatever --steps / --warmup ask for (each step is one
+# full frame; the sample is stated in the JSON line).
+REF_MAX_FRAMES = 40
+REF_MAX_WARMUP = 1
+
+
 def run_reference(args, rank, world):
     if rank != 0:
-        return None
+        return None  # replicas are independent: rank 0 alone times the host reference
     wl = make_workload(args.config, args.frames, seed=0)
     step, OK = oracle_frame_runner(wl)
     cores = os.cpu_count() or 1
     OK.set_threads(cores)
     frames = wl["frames"]
-    for w in range(args.warmup):
+    warm = min(args.warmup, REF_MAX_WARMUP)
+    steps = max(1, min(args.steps, REF_MAX_FRAMES))
+    for w in range(warm):
         step(frames[w % len(frames)])
     t0 = time.perf_counter()
-    for i in range(args.steps):
-        step(frames[(args.warmup + i) % len(frames)])
+    for i in range(steps):
+        step(frames[(warm + i) % len(frames)])
     dt = time.perf_counter() - t0
-    value = args.steps / dt
-    sample = (f"{args.steps} consecutive config-2 frames, one full frame per step (normals, "
-              f"Hamming, exhaustive preselection, 10 LM iterations, warp), oracle port of the "
-              f"reference on {cores} host threads")
+    value = steps / dt
+    sample = (f"{steps} consecutive config-2 frames after {warm} warm-up (of --steps "
+              f"{args.steps} / --warmup {args.warmup}; bounded to {REF_MAX_FRAMES}), one full "
+              f"frame per step (normals, Hamming, exhaustive preselection, 10 LM iterations, "
+              f"warp), oracle port of the reference on {cores} host threads")
     return {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-        "ms_per_gn_iteration": dt * 1e3 / args.steps / wl["iters"], "higher_is_better": True,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": warm, "ms_per_step": dt * 1e3 / steps,
+        "ms_per_gn_iteration": dt * 1e3 / steps / wl["iters"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(wl, 1, f"{len(frames)} distinct frames cycled"),
         "impl": "reference",
