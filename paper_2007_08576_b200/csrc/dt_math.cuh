@@ -215,6 +215,12 @@ __device__ __forceinline__ void fold_row(double* acc, const double J[6], double 
 }
 
 // Tukey square-root weight |1 - u^2| inside |u| < 1 (kernels.py:184-192).
+// tukey_sqrt with a precomputed 1/scale and sqrt(w^2) = w (ulp-level; solver-internal)
+__device__ __forceinline__ double tukey_fast(double r, double inv_scale) {
+  const double u = r * inv_scale;
+  return fabs(u) < 1.0 ? 1.0 - u * u : 0.0;
+}
+
 __device__ __forceinline__ double tukey_sqrt(double r, double scale) {
   const double u = r / scale;
   if (fabs(u) < 1.0) {
@@ -338,17 +344,30 @@ __device__ __forceinline__ double angle_row(double ax, double ay, double az, dou
 // Unit-weight bending-angle row of one direction with BOTH bins' Jacobians
 // (kernels.py:287-338 with sw = 1): Ja for the rotating side a, Jb for side b; returns
 // the angle value. angle_row(...) with weight sw equals sw * (these rows, this value).
+// 1/sqrt(x) for normal positive x: MUFU estimate + two Newton steps (~1 ulp), without the
+// special-case branches of the full-precision rsqrt (solver-internal rows only)
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx, y * y, 1.5);
+  y = y * fma(-hx, y * y, 1.5);
+  return y;
+}
+
 __device__ __forceinline__ double angle_unit(double ax, double ay, double az, double bx, double by,
                                              double bz, double patx, double paty, double patz,
                                              double pbtx, double pbty, double pbtz, double Ja[6],
                                              double Jb[6]) {
-  const double na = sqrt(ax * ax + ay * ay + az * az);
-  const double nb = sqrt(bx * bx + by * by + bz * bz);
-  const bool ok = na > ANGLE_MIN_NORM && nb > ANGLE_MIN_NORM;
-  const double na_s = ok ? na : 1.0;
-  const double nb_s = ok ? nb : 1.0;
-  const double ahx = ax / na_s, ahy = ay / na_s, ahz = az / na_s;
-  const double bhx = bx / nb_s, bhy = by / nb_s, bhz = bz / nb_s;
+  // reciprocal norms instead of 12 divisions (ulp-level; the LM solver's parity is
+  // tolerance-based; the operator-level arap_reduce keeps the reference's divisions)
+  const double sa = ax * ax + ay * ay + az * az;
+  const double sb = bx * bx + by * by + bz * bz;
+  const bool ok = sa > ANGLE_MIN_NORM * ANGLE_MIN_NORM && sb > ANGLE_MIN_NORM * ANGLE_MIN_NORM;
+  const double ia = ok ? rsqrt_nr(sa) : 1.0;
+  const double ib = ok ? rsqrt_nr(sb) : 1.0;
+  const double ahx = ax * ia, ahy = ay * ia, ahz = az * ia;
+  const double bhx = bx * ib, bhy = by * ib, bhz = bz * ib;
   double cth = ahx * bhx + ahy * bhy + ahz * bhz;
   if (cth > 1.0) cth = 1.0;
   else if (cth < -1.0) cth = -1.0;
@@ -356,13 +375,14 @@ __device__ __forceinline__ double angle_unit(double ax, double ay, double az, do
   const bool near_pi = (1.0 + cth) < ANGLE_COLLINEAR_EPS;
   const double val = (ok && !near_zero) ? acos(cth) : 0.0;
   const bool grad_ok = ok && !near_zero && !near_pi;
-  const double inv_sin = grad_ok ? -1.0 / sqrt(fmax(1.0 - cth * cth, 1e-300)) : 0.0;
-  const double gax = inv_sin * (bhx - cth * ahx) / na_s;
-  const double gay = inv_sin * (bhy - cth * ahy) / na_s;
-  const double gaz = inv_sin * (bhz - cth * ahz) / na_s;
-  const double gbx = inv_sin * (ahx - cth * bhx) / nb_s;
-  const double gby = inv_sin * (ahy - cth * bhy) / nb_s;
-  const double gbz = inv_sin * (ahz - cth * bhz) / nb_s;
+  const double inv_sin = grad_ok ? -rsqrt_nr(fmax(1.0 - cth * cth, 1e-300)) : 0.0;
+  const double fa = inv_sin * ia, fb = inv_sin * ib;
+  const double gax = fa * (bhx - cth * ahx);
+  const double gay = fa * (bhy - cth * ahy);
+  const double gaz = fa * (bhz - cth * ahz);
+  const double gbx = fb * (ahx - cth * bhx);
+  const double gby = fb * (ahy - cth * bhy);
+  const double gbz = fb * (ahz - cth * bhz);
   Ja[0] = (ay * gaz - az * gay) - (paty * gbz - patz * gby);
   Ja[1] = (az * gax - ax * gaz) - (patz * gbx - patx * gbz);
   Ja[2] = (ax * gay - ay * gax) - (patx * gby - paty * gbx);
@@ -628,8 +648,8 @@ __device__ __forceinline__ void apply_step_one_fast(const double* W, const doubl
   double dual[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) dual[i] = d1[i] + d2[i];
-  const double norm = sqrt(real[0] * real[0] + real[1] * real[1] + real[2] * real[2] + real[3] * real[3]);
-  const double inorm = 1.0 / norm;
+  const double inorm =
+      rsqrt_nr(real[0] * real[0] + real[1] * real[1] + real[2] * real[2] + real[3] * real[3]);
   double r[4], d[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {

@@ -289,12 +289,14 @@ __device__ __forceinline__ void edge_unit_rows(const SolverArgs& A, const double
   const double rx = p1[0] - p0[0], ry = p1[1] - p0[1], rz = p1[2] - p0[2];
   const double rest = sqrt(rx * rx + ry * ry + rz * rz);
   const double bx = p1t[0] - p0t[0], by = p1t[1] - p0t[1], bz = p1t[2] - p0t[2];
-  const double ln = sqrt(bx * bx + by * by + bz * bz);
+  const double ln2 = bx * bx + by * by + bz * bz;
+  const double iln = rsqrt_nr(fmax(ln2, 1e-300));
+  const double ln = ln2 * iln;  // |b| to an ulp
   double bhx = 0.0, bhy = 0.0, bhz = 0.0;
   if (ln > 1e-9) {
-    bhx = bx / ln;
-    bhy = by / ln;
-    bhz = bz / ln;
+    bhx = bx * iln;
+    bhy = by * iln;
+    bhz = bz * iln;
   }
   const double L0[6] = {p0t[1] * (-bhz) - p0t[2] * (-bhy), p0t[2] * (-bhx) - p0t[0] * (-bhz),
                         p0t[0] * (-bhy) - p0t[1] * (-bhx), -bhx, -bhy, -bhz};
@@ -386,9 +388,11 @@ __device__ __forceinline__ void chol_col(double (&L)[21], double (&inv)[6], bool
 #pragma unroll
   for (int q = 0; q < J; ++q) s -= L[J * (J + 1) / 2 + q] * L[J * (J + 1) / 2 + q];
   ok = ok && (s > 0.0);
-  const double ljj = sqrt(s);
-  inv[J] = 1.0 / ljj;
-  L[J * (J + 1) / 2 + J] = ljj;
+  // 1/l_jj = rsqrt(s) in one MUFU + Newton chain, l_jj = s / sqrt(s) (ulp-level vs
+  // sqrt + division; the pivot test s > 0 is the reference's)
+  const double il = rsqrt_nr(fmax(s, 1e-300));
+  inv[J] = il;
+  L[J * (J + 1) / 2 + J] = s * il;
 #pragma unroll
   for (int i = J + 1; i < 6; ++i) {
     double v = L[i * (i + 1) / 2 + J];

@@ -24,6 +24,7 @@ struct SolverArgs {
   double fx, fy, cx, cy, gate, cos_gate;
   double tukey, fw, arap_w, angle_w, rot_w, data_floor;
   double sq_angle_w, sq_rot_w;  // sqrt(angle_w), sqrt(rot_w)
+  double inv_tukey;             // 1 / tukey scale
   // damping schedule and tolerances (SolverConfig, solver.py:43-71)
   double lam_init, lam_dec, lam_inc, lam_min, lam_max, step_tol, cost_tol;
   // bound template (static per sequence)

@@ -163,7 +163,7 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   nb.nrm[3 * p + 1] = g1;
   nb.nrm[3 * p + 2] = g2;
   const double r = g0 * (x0 - o0) + g1 * (x1 - o1) + g2 * (x2 - o2);
-  const double rs = tukey_sqrt(r, A.tukey);
+  const double rs = tukey_fast(r, A.inv_tukey);
   nb.rs[p] = rs;
   double G[24];
   blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, G);

@@ -533,6 +533,7 @@ void fill_args(dt_tracker* t) {
   a.rot_w = c.rotation_weight;
   a.sq_angle_w = std::sqrt(c.angle_weight);
   a.sq_rot_w = std::sqrt(c.rotation_weight);
+  a.inv_tukey = 1.0 / c.tukey_scale;
   a.data_floor = c.data_floor;
   a.lam_init = c.lambda_init;
   a.lam_dec = c.lambda_decrease;
