@@ -274,6 +274,16 @@ int dt_track_frame(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out
  * dt_tracker_collect copies them out later. */
 int dt_track_frame_async(dt_tracker* t, const dt_frame_input* in);
 int dt_tracker_collect(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out);
+/* Pipelined streaming (host inputs): dt_track_frame_submit stages the frame's depth and
+ * ORB features (HOST pointers) into one of two device slots on a copy stream while the
+ * previous frame computes, runs the frame, and copies warps / points / normals /
+ * control_data_weights back into `out` (pinned host memory recommended) while the next
+ * frame computes. At most two frames are in flight (submit waits for the oldest when
+ * needed); `out` must stay valid until dt_tracker_wait returns for that frame.
+ * dt_tracker_wait waits for the oldest frame in flight and fills its out->report.
+ * Frames are still solved strictly in order (each warm-starts from the previous). */
+int dt_track_frame_submit(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out);
+int dt_tracker_wait(dt_tracker* t);
 /* The tracker's CUDA stream (cudaStream_t). */
 void* dt_tracker_stream(dt_tracker* t);
 /* Per-phase device timing of each frame (CUDA events between the pipeline stages):

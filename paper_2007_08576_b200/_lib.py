@@ -121,6 +121,8 @@ _SIGNATURES: dict[str, list] = {
                                 I32, P],
     "dt_track_frame_async": [P, C.POINTER(FrameInput)],
     "dt_tracker_collect": [P, C.POINTER(FrameInput), C.POINTER(FrameOutput)],
+    "dt_track_frame_submit": [P, C.POINTER(FrameInput), C.POINTER(FrameOutput)],
+    "dt_tracker_wait": [P],
     "dt_tracker_set_profiling": [P, C.c_int],
     "dt_tracker_get_phase_ms": [P, P],
     "dt_tracker_get_trace": [P, P, C.c_int],

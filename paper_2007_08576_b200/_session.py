@@ -238,6 +238,19 @@ class DeviceTracker:
         """Lowest-overhead entry: caller-built dt_frame_input / dt_frame_output."""
         check(lib.dt_track_frame(self._h, C.byref(fi), C.byref(fo)), "dt_track_frame")
 
+    def submit(self, fi: FrameInput, fo: FrameOutput) -> None:
+        """Pipelined streaming: stage host inputs on the copy stream, run the frame, copy
+        the outputs back into `fo` (filled once `wait` returns for this frame)."""
+        check(lib.dt_track_frame_submit(self._h, C.byref(fi), C.byref(fo)), "dt_track_frame_submit")
+
+    def sync(self) -> None:
+        """Drain the pipeline and the tracker stream."""
+        check(lib.dt_tracker_sync(self._h), "dt_tracker_sync")
+
+    def wait(self) -> None:
+        """Wait for the oldest frame in flight (fills its report)."""
+        check(lib.dt_tracker_wait(self._h), "dt_tracker_wait")
+
     def enqueue(self, fi: FrameInput) -> None:
         """Enqueue one frame on the tracker stream; no host outputs, no synchronization."""
         check(lib.dt_track_frame_async(self._h, C.byref(fi)), "dt_track_frame_async")

@@ -410,6 +410,26 @@ struct dt_tracker {
   int *fptr = nullptr, *fent = nullptr, *fpos = nullptr;
   double *ffo = nullptr, *ffw = nullptr;
   bool orb_static = false;
+  // pipelined submission (dt_track_frame_submit / dt_tracker_wait): host inputs are staged
+  // into one of two device slots on a copy stream while the previous frame computes;
+  // outputs are copied back on the copy stream while the next frame computes
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_in_ready[2] = {nullptr, nullptr}, ev_in_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_out_copied[2] = {nullptr, nullptr};
+  cudaEvent_t pre_solver_wait = nullptr;  // compute stream waits on it before the solver
+  double* in_depth[2] = {nullptr, nullptr};
+  uint8_t* in_desc[2] = {nullptr, nullptr};
+  int32_t* in_kp[2] = {nullptr, nullptr};
+  int64_t in_desc_cap = 0;
+  int64_t* stage_info[2] = {nullptr, nullptr};   // device snapshot: info[4], stats[3], report
+  int64_t* h_stage[2] = {nullptr, nullptr};      // pinned host copy of the snapshot
+  struct Pending {
+    bool active = false, used = false;
+    int32_t frame_id = 0;
+    dt_frame_output out;
+  } pend[2];
+  int64_t pipe_next = 0;   // frames submitted
+  int64_t pipe_waited = 0; // frames waited for
   // matches
   int64_t match_cap = 0;
   double *m_src = nullptr, *m_dst = nullptr, *m_w = nullptr, *m_res = nullptr, *m_bw = nullptr;
@@ -796,6 +816,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     t->args_dirty = false;
   }
   DT_CHECK_CUDA(cudaMemsetAsync(t->stalled_hist, 0, sizeof(int32_t) * c.max_outer_iters, s));
+  if (t->pre_solver_wait) DT_CHECK_CUDA(cudaStreamWaitEvent(s, t->pre_solver_wait, 0));
   DT_TRY(solver_launch(t->dev_args, 1, t->cluster, (int)t->m, (int)t->k, t->grid_mode, s));
   ++t->launches;
   mark(t, 5);
@@ -1010,6 +1031,15 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
 int dt_tracker_destroy(dt_tracker* t) {
   if (!t) return DT_OK;
   cudaStreamSynchronize(t->stream);
+  if (t->copy_stream) {
+    cudaStreamSynchronize(t->copy_stream);
+    cudaStreamDestroy(t->copy_stream);
+  }
+  for (int i = 0; i < 2; ++i) {
+    for (cudaEvent_t e : {t->ev_in_ready[i], t->ev_in_free[i], t->ev_done[i], t->ev_out_copied[i]})
+      if (e) cudaEventDestroy(e);
+    if (t->h_stage[i]) cudaFreeHost(t->h_stage[i]);
+  }
   for (auto& e : t->ev)
     if (e) cudaEventDestroy(e);
   for (auto& b : t->bufs) cudaFree(b.p);
@@ -1105,8 +1135,11 @@ int dt_tracker_set_config(dt_tracker* t, const dt_config* cfg) {
   return DT_OK;
 }
 
+int dt_tracker_wait(dt_tracker* t);
+
 int dt_tracker_sync(dt_tracker* t) {
   DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
+  while (t->pipe_waited < t->pipe_next) DT_TRY(dt_tracker_wait(t));  // drain the pipeline
   DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
   return DT_OK;
 }
@@ -1117,6 +1150,153 @@ int dt_track_frame(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out
   DT_TRY(enqueue_frame(t, in, &used));
   t->last_used = used;
   return collect_outputs(t, in, out, used);
+}
+
+int dt_tracker_get_history(dt_tracker* t, double* cost_history, double* lambda_history,
+                           int32_t* stalled);
+}  // extern "C"
+
+namespace {
+
+constexpr int STAGE_WORDS = 4 + 3 + (int)((sizeof(dt_report) + 7) / 8);
+
+__global__ void k_stage_outputs(const int64_t* __restrict__ info, const double* __restrict__ astats,
+                                const double* __restrict__ pstats, const dt_report* __restrict__ rep,
+                                int64_t* __restrict__ stage) {
+  const int i = threadIdx.x;
+  if (i < 4) stage[i] = info[i];
+  if (i < 2) reinterpret_cast<double*>(stage + 4)[i] = astats[i];
+  if (i == 0) reinterpret_cast<double*>(stage + 4)[2] = pstats[0];
+  const int nw = (int)((sizeof(dt_report) + 7) / 8);
+  if (i < nw) stage[7 + i] = reinterpret_cast<const int64_t*>(rep)[i];
+}
+
+int ensure_pipeline(dt_tracker* t, int64_t n_desc) {
+  if (!t->copy_stream) {
+    DT_CHECK_CUDA(cudaStreamCreateWithFlags(&t->copy_stream, cudaStreamNonBlocking));
+    const int64_t npix = (int64_t)t->cfg.width * t->cfg.height;
+    for (int i = 0; i < 2; ++i) {
+      DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_in_ready[i], cudaEventDisableTiming));
+      DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_in_free[i], cudaEventDisableTiming));
+      DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_done[i], cudaEventDisableTiming));
+      DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_out_copied[i], cudaEventDisableTiming));
+      DT_TRY(dalloc(t, &t->in_depth[i], npix));
+      DT_TRY(dalloc(t, &t->stage_info[i], STAGE_WORDS));
+      DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_stage[i], sizeof(int64_t) * STAGE_WORDS));
+    }
+  }
+  if (n_desc > t->in_desc_cap) {
+    const int64_t cap = std::max<int64_t>(n_desc, 256);
+    for (int i = 0; i < 2; ++i) {
+      DT_TRY(dalloc(t, &t->in_desc[i], 32 * cap));
+      DT_TRY(dalloc(t, &t->in_kp[i], 2 * cap));
+    }
+    t->in_desc_cap = cap;
+  }
+  return DT_OK;
+}
+
+// host side of a finished pipelined frame: the report from the staged snapshot
+void finish_pending(dt_tracker* t, int slot) {
+  dt_tracker::Pending& pd = t->pend[slot];
+  const int64_t* st = t->h_stage[slot];
+  const double* stats = reinterpret_cast<const double*>(st + 4);
+  dt_report R;
+  std::memcpy(&R, st + 7, sizeof(dt_report));
+  R.frame_id = pd.frame_id;
+  if (pd.used) {
+    R.n_matches = (int32_t)st[2];
+    R.n_preselected = (int32_t)stats[1];
+    R.match_weight_sum = stats[0];
+    R.preselect_status = (int32_t)st[0];
+    R.preselect_reference = (int32_t)st[1];
+    R.preselect_support = stats[2];
+  } else {
+    R.n_matches = R.n_preselected = 0;
+    R.match_weight_sum = R.preselect_support = 0.0;
+    R.preselect_status = DT_OK;
+    R.preselect_reference = -1;
+  }
+  if (pd.out.report) *pd.out.report = R;
+  pd.active = false;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dt_tracker_wait(dt_tracker* t) {
+  DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
+  if (t->pipe_waited >= t->pipe_next) return DT_OK;  // nothing in flight
+  const int slot = (int)(t->pipe_waited % 2);
+  DT_CHECK_CUDA(cudaEventSynchronize(t->ev_out_copied[slot]));
+  finish_pending(t, slot);
+  ++t->pipe_waited;
+  return DT_OK;
+}
+
+int dt_track_frame_submit(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out) {
+  DT_REQUIRE(t != nullptr && in != nullptr && out != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  DT_REQUIRE(!in->on_device, DT_ERR_INVALID_ARGUMENT, "dt_track_frame_submit takes host inputs");
+  DT_REQUIRE(in->depth != nullptr, DT_ERR_INVALID_ARGUMENT, "depth is required");
+  DT_REQUIRE(in->normals == nullptr && (in->frame_desc != nullptr || !in->use_matches),
+             DT_ERR_UNSUPPORTED, "the pipelined path takes depth + ORB features");
+  // at most two frames in flight
+  if (t->pipe_next - t->pipe_waited >= 2) DT_TRY(dt_tracker_wait(t));
+  const int64_t nd = in->frame_desc ? in->n_frame : 0;
+  DT_TRY(ensure_pipeline(t, nd));
+  const int slot = (int)(t->pipe_next % 2);
+  const int64_t npix = (int64_t)t->cfg.width * t->cfg.height;
+  cudaStream_t cs = t->copy_stream, s = t->stream;
+  // stage the inputs once the frame that used this slot has consumed them
+  DT_CHECK_CUDA(cudaStreamWaitEvent(cs, t->ev_in_free[slot], 0));
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->in_depth[slot], in->depth, sizeof(double) * npix,
+                                cudaMemcpyHostToDevice, cs));
+  if (nd > 0) {
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->in_desc[slot], in->frame_desc, 32 * nd, cudaMemcpyHostToDevice, cs));
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->in_kp[slot], in->frame_kp, sizeof(int32_t) * 2 * nd,
+                                  cudaMemcpyHostToDevice, cs));
+  }
+  DT_CHECK_CUDA(cudaEventRecord(t->ev_in_ready[slot], cs));
+  // compute: wait for the inputs; the solver (which rewrites warps / report / weights)
+  // waits until the previous frame's outputs are copied out
+  DT_CHECK_CUDA(cudaStreamWaitEvent(s, t->ev_in_ready[slot], 0));
+  dt_frame_input din = *in;
+  din.on_device = 1;
+  din.depth = t->in_depth[slot];
+  din.frame_desc = nd > 0 ? t->in_desc[slot] : nullptr;
+  din.frame_kp = nd > 0 ? t->in_kp[slot] : nullptr;
+  t->pre_solver_wait = t->pipe_next > 0 ? t->ev_out_copied[1 - slot] : nullptr;
+  bool used = false;
+  const int st = enqueue_frame(t, &din, &used);
+  t->pre_solver_wait = nullptr;
+  DT_TRY(st);
+  t->last_used = used;
+  DT_CHECK_CUDA(cudaEventRecord(t->ev_in_free[slot], s));
+  k_stage_outputs<<<1, 64, 0, s>>>(t->info, t->astats, t->pstats, t->report, t->stage_info[slot]);
+  DT_CHECK_LAUNCH();
+  DT_CHECK_CUDA(cudaEventRecord(t->ev_done[slot], s));
+  // outputs back on the copy stream while the next frame computes
+  DT_CHECK_CUDA(cudaStreamWaitEvent(cs, t->ev_done[slot], 0));
+  if (out->warps)
+    DT_CHECK_CUDA(cudaMemcpyAsync(out->warps, t->warps_out, sizeof(double) * 8 * t->m, cudaMemcpyDeviceToHost, cs));
+  if (out->points)
+    DT_CHECK_CUDA(cudaMemcpyAsync(out->points, t->out_p, sizeof(double) * 3 * t->n, cudaMemcpyDeviceToHost, cs));
+  if (out->normals)
+    DT_CHECK_CUDA(cudaMemcpyAsync(out->normals, t->out_n, sizeof(double) * 3 * t->n, cudaMemcpyDeviceToHost, cs));
+  if (out->control_data_weights)
+    DT_CHECK_CUDA(cudaMemcpyAsync(out->control_data_weights, t->wa_out, sizeof(double) * t->m,
+                                  cudaMemcpyDeviceToHost, cs));
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->h_stage[slot], t->stage_info[slot], sizeof(int64_t) * STAGE_WORDS,
+                                cudaMemcpyDeviceToHost, cs));
+  DT_CHECK_CUDA(cudaEventRecord(t->ev_out_copied[slot], cs));
+  dt_tracker::Pending& pd = t->pend[slot];
+  pd.active = true;
+  pd.used = used;
+  pd.frame_id = in->frame_id;
+  pd.out = *out;
+  ++t->pipe_next;
+  return DT_OK;
 }
 
 int dt_tracker_get_history(dt_tracker* t, double* cost_history, double* lambda_history,

@@ -1,0 +1,88 @@
+"""The pipelined streaming API (dt_track_frame_submit / dt_tracker_wait) solves the same
+frames in the same order as the synchronous dt_track_frame: identical warps, points and
+reports, bit for bit, with host inputs staged on the copy stream."""
+
+import ctypes as C
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+pytestmark = pytest.mark.gpu
+
+
+def _tracker(wl):
+    from paper_2007_08576_b200._session import DeviceTracker, make_config
+    from paper_2007_08576_b200.warpfield import bind_points
+
+    cfg = wl["cfg"]
+    dcfg = make_config(wl["cam"], cfg.energy, cfg.make_solver_config(), cfg.make_preselect_config(),
+                       sampling_radius=wl["graph"].sampling_radius)
+    trk = DeviceTracker(wl["tpl"], wl["graph"], dcfg)
+    f = wl["feats"]
+    trk.set_features(f.descriptors, f.points,
+                     bind_points(f.points, wl["graph"].points, 4, wl["graph"].sampling_radius))
+    return trk
+
+
+def _inputs(fr, fid):
+    from paper_2007_08576_b200._lib import FrameInput
+
+    d = np.ascontiguousarray(fr.depth)
+    de = np.ascontiguousarray(fr.descriptors)
+    kp = np.ascontiguousarray(fr.keypoints)
+    fi = FrameInput()
+    fi.depth, fi.frame_desc, fi.frame_kp = d.ctypes.data, de.ctypes.data, kp.ctypes.data
+    fi.n_frame, fi.use_matches, fi.on_device, fi.frame_id = de.shape[0], 1, 0, fid
+    return fi, (d, de, kp)
+
+
+def _outputs(m, n):
+    from paper_2007_08576_b200._lib import FrameOutput, Report
+
+    w = np.zeros((m, 8))
+    p = np.zeros((n, 3))
+    rep = Report()
+    fo = FrameOutput()
+    fo.warps, fo.points = w.ctypes.data, p.ctypes.data
+    fo.report = C.cast(C.pointer(rep), C.c_void_p).value
+    return fo, (w, p, rep)
+
+
+def test_pipelined_frames_match_synchronous_frames():
+    import bench
+
+    wl = bench.make_workload(1, 5, seed=3)
+    m, n = len(wl["graph"]), len(wl["tpl"])
+    frames = wl["frames"]
+
+    trk = _tracker(wl)
+    sync = []
+    for i, fr in enumerate(frames):
+        fi, keep = _inputs(fr, i)
+        fo, (w, p, rep) = _outputs(m, n)
+        trk.track_raw(fi, fo)
+        sync.append((w.copy(), p.copy(), rep.total_cost, rep.n_correspondences, rep.n_preselected))
+    trk.close()
+
+    trk = _tracker(wl)
+    keep_alive, outs = [], []
+    for i, fr in enumerate(frames):
+        fi, keep = _inputs(fr, i)
+        fo, bufs = _outputs(m, n)
+        keep_alive.append((keep, fo, bufs))
+        trk.submit(fi, fo)
+        outs.append(bufs)
+    trk.sync()
+    for i, (w, p, rep) in enumerate(outs):
+        sw, sp, cost, ncorr, npre = sync[i]
+        np.testing.assert_array_equal(w, sw)
+        np.testing.assert_array_equal(p, sp)
+        assert rep.total_cost == cost
+        assert rep.n_correspondences == ncorr and rep.n_preselected == npre
+        assert rep.frame_id == i
+    trk.close()
