@@ -55,12 +55,17 @@ __constant__ unsigned char kColRow[27] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2,
 __constant__ unsigned char kColCol[27] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5,
                                           4, 5, 5, 6, 6, 6, 6, 6, 6};
 
-// L2-coherent loads for data produced by other CTAs.
-__device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
+// Loads of data produced by other CTAs in an earlier phase: L1-cacheable (every domain
+// barrier has acquire semantics and invalidates L1 -- measured, tools/l1_probe.cu), so
+// the several loads of one line within a phase (e.g. the four 16-byte pieces of a
+// normal-equation row) are served by one L2 fill instead of one L2 trip each.
+__device__ __forceinline__ double ld(const double* p) { return __ldca(p); }
 __device__ __forceinline__ uint8_t ldu8(const uint8_t* p) {
-  return (uint8_t)__ldcg(reinterpret_cast<const unsigned char*>(p));
+  return (uint8_t)__ldca(reinterpret_cast<const unsigned char*>(p));
 }
-__device__ __forceinline__ int ldi(const int* p) { return __ldcg(p); }
+__device__ __forceinline__ int ldi(const int* p) { return __ldca(p); }
+// data published by other CTAs WITHIN the phase (last-arriver reductions): L2 only
+__device__ __forceinline__ double ldl2(const double* p) { return __ldcg(p); }
 
 __device__ __forceinline__ long long gtimer() {
   long long t;

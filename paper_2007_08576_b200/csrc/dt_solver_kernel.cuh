@@ -58,7 +58,7 @@ __device__ __forceinline__ void load_row(const double* src, double r[8]) {
   const double2* s2 = reinterpret_cast<const double2*>(src);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const double2 v = __ldcg(s2 + i);
+    const double2 v = __ldca(s2 + i);
     r[2 * i] = v.x;
     r[2 * i + 1] = v.y;
   }
@@ -74,7 +74,18 @@ __device__ __forceinline__ void load_row(const double* src, double r[8]) {
 template <int KM>
 __device__ __forceinline__ double point_step(const SolverArgs& A, const double* s_w, int64_t p,
                                              const PBuf* ob, const PBuf& nb, double* cost_old,
-                                             int* valid_out) {
+                                             int* valid_out, long long* dbg = nullptr) {
+#ifdef DT_WARP_TRACE
+#define PSTAMP(i)                        \
+  do {                                   \
+    if (dbg) dbg[i] = clock64();         \
+  } while (0)
+#else
+#define PSTAMP(i) \
+  do {            \
+  } while (0)
+#endif
+  PSTAMP(0);
   const int kk = KM == 4 ? 4 : A.k;
   // every load that does not depend on this point's arithmetic is issued up front (one
   // L2 round trip after the domain barrier instead of a chain of them)
@@ -102,8 +113,10 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   const double tn0 = A.tn[3 * p], tn1 = A.tn[3 * p + 1], tn2 = A.tn[3 * p + 2];
   double B[8], sgn[KM], a[KM];
   blend_rows<KM>(s_w, A.bidx, A.bw, p, kk, B, sgn, a);
+  PSTAMP(1);
   double x0, x1, x2, s2;
   apply_blend(B, px, py, pz, x0, x1, x2, s2);
+  PSTAMP(2);
   if (ob) {
     double co = 0.0;
     if (ovalid) {
@@ -132,6 +145,7 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
       const uint8_t dv = A.dvalid[pix];
       const double d = A.depth[pix];
       const double h0 = A.onrm[3 * pix], h1 = A.onrm[3 * pix + 1], h2 = A.onrm[3 * pix + 2];
+      PSTAMP(3);
       if (dv) {
         o0 = ((double)ui - A.cx) / A.fx * d;
         o1 = ((double)vi - A.cy) / A.fy * d;
@@ -164,12 +178,14 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   nb.nrm[3 * p + 2] = g2;
   const double r = g0 * (x0 - o0) + g1 * (x1 - o1) + g2 * (x2 - o2);
   const double rs = tukey_fast(r, A.inv_tukey);
+  PSTAMP(4);
   nb.rs[p] = rs;
   double G[24];
   blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, G);
   double gn[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) gn[e] = g0 * G[e] + g1 * G[8 + e] + g2 * G[16 + e];
+  PSTAMP(5);
   double cost = 0.0;
 #pragma unroll
   for (int s = 0; s < KM; ++s)
@@ -189,6 +205,7 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
       row[7] = sw;
       store_row(nb.row + 8 * (size_t)pos[s], row);
     }
+  PSTAMP(6);
   return cost;
 }
 
@@ -318,7 +335,7 @@ __device__ __noinline__ void red_commit(const SolverArgs& A, int slot, int ch, i
   double x[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    x[k] = lane < gs ? ld(vals[k] + 32 * g + lane) : red_id<OP>(k);
+    x[k] = lane < gs ? ldl2(vals[k] + 32 * g + lane) : red_id<OP>(k);
     x[k] = warp_red<OP>(k, x[k]);
   }
   unsigned old2 = 0;
@@ -336,7 +353,7 @@ __device__ __noinline__ void red_commit(const SolverArgs& A, int slot, int ch, i
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     double acc = red_id<OP>(k);
-    for (int q = lane; q < ng; q += 32) acc = red_op<OP>(k, acc, ld(R.gsum + k * R.G + q));
+    for (int q = lane; q < ng; q += 32) acc = red_op<OP>(k, acc, ldl2(R.gsum + k * R.G + q));
     x[k] = warp_red<OP>(k, acc);
   }
   if (lane == 0) {
@@ -660,9 +677,9 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         const double2* T2 = reinterpret_cast<const double2*>(A.tentT + 12 * c);
         double2 w[4], T[6];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) w[i] = __ldcg(t2 + i);
+        for (int i = 0; i < 4; ++i) w[i] = __ldca(t2 + i);
 #pragma unroll
-        for (int i = 0; i < 6; ++i) T[i] = __ldcg(T2 + i);
+        for (int i = 0; i < 6; ++i) T[i] = __ldca(T2 + i);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           s_w[8 * c + 2 * i] = w[i].x;
@@ -734,7 +751,12 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             const int64_t p = (int64_t)ch * CHUNK + lane;
             double co = 0.0, cn = 0.0;
             int vd;
-            if (p < n) cn = point_step<KM>(A, s_w, p, &ob, nb, &co, &vd);
+            long long* dbg = nullptr;
+#ifdef DT_WARP_TRACE
+            if (A.arrivals && outer == 1 && attempt == 0 && lane == 0 && rank < 8)
+              dbg = A.arrivals + 2 + (size_t)1024 * A.arr_cap + 20000 + (rank * NWARPS + warp) * 8;
+#endif
+            if (p < n) cn = point_step<KM>(A, s_w, p, &ob, nb, &co, &vd, dbg);
             co = warp_sum(co);
             cn = warp_sum(cn);
             red_commit<2, 0>(A, 0, ch, nch_p, {co, cn});

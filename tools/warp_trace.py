@@ -9,6 +9,13 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 
+def point_stamps(buf, n_cta=8, nw=8):
+    """clock64 stamps inside point_step (debug build) for lane 0 of each warp of CTAs 0..7."""
+    base = 2 + 1024 * 256 + 20000
+    out = buf[base: base + n_cta * nw * 8].reshape(n_cta, nw, 8)
+    return out
+
+
 def main():
     import bench
     from paper_2007_08576_b200._lib import FrameInput, lib
@@ -50,6 +57,15 @@ def main():
         print(r, np.round(rel_w[r], 2).tolist())
     print("max over CTAs per warp:", np.round(rel_w.max(axis=0), 2).tolist())
     print("mean over CTAs per warp:", np.round(rel_w.mean(axis=0), 2).tolist())
+    st = point_stamps(buf, 8, nw)
+    names = ["loads+blend", "apply", "project+pixel", "gates+tukey", "gradient", "rows"]
+    for r in range(3):
+        for w in range(nw):
+            s0 = st[r, w]
+            if s0[0] == 0 or s0[6] == 0:
+                continue
+            d = np.diff(s0[:7])
+            print(f"cta {r} warp {w}: total {s0[6]-s0[0]} cyc  " + "  ".join(f"{nm} {int(v)}" for nm, v in zip(names, d)))
     trk.close()
 
 
