@@ -18,6 +18,7 @@
 #include <cstdint>
 
 #include "dt_common.cuh"
+#include "dt_math.cuh"
 #include "dt_ops.cuh"
 
 namespace dt {
@@ -218,9 +219,13 @@ __device__ __forceinline__ bool procrustes_lane(const double C[9], double V[9], 
         rotated = true;
         const double zeta = (beta - alpha) / (2.0 * gamma);
         double t;
-        if (fabs(zeta) > 1e150) t = 0.5 / zeta;
-        else t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = rsqrt(1.0 + t * t);
+        if (fabs(zeta) > 1e150) {
+          t = 0.5 / zeta;
+        } else {
+          const double q = 1.0 + zeta * zeta;
+          t = copysign(1.0, zeta) / (fabs(zeta) + q * rsqrt_nr(q));
+        }
+        const double c = rsqrt_nr(1.0 + t * t);
         const double sn = c * t;
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
@@ -235,9 +240,14 @@ __device__ __forceinline__ bool procrustes_lane(const double C[9], double V[9], 
     }
     if (!__any_sync(0xffffffffu, rotated)) break;
   }
-  double s0 = sqrt(A[0] * A[0] + A[3] * A[3] + A[6] * A[6]);
-  double s1 = sqrt(A[1] * A[1] + A[4] * A[4] + A[7] * A[7]);
-  double s2 = sqrt(A[2] * A[2] + A[5] * A[5] + A[8] * A[8]);
+  // column norms as x * rsqrt(x) (within an ulp of sqrt; the reference's degeneracy test
+  // S1 <= 1e-9 S0 is far from that resolution)
+  const double q0 = A[0] * A[0] + A[3] * A[3] + A[6] * A[6];
+  const double q1 = A[1] * A[1] + A[4] * A[4] + A[7] * A[7];
+  const double q2 = A[2] * A[2] + A[5] * A[5] + A[8] * A[8];
+  double s0 = q0 > 0.0 ? q0 * rsqrt_nr(q0) : 0.0;
+  double s1 = q1 > 0.0 ? q1 * rsqrt_nr(q1) : 0.0;
+  double s2 = q2 > 0.0 ? q2 * rsqrt_nr(q2) : 0.0;
   // order the columns by singular value (descending, stable)
   int o0 = 0, o1 = 1;
   double S0 = s0, S1 = s1;
@@ -247,13 +257,14 @@ __device__ __forceinline__ bool procrustes_lane(const double C[9], double V[9], 
     else { o1 = 2; S1 = s2; }
   }
   if (!(S0 > 0.0) || S1 <= 1e-9 * S0) return false;
+  const double iS0 = 1.0 / S0, iS1 = 1.0 / S1;
   double u1[3], u2[3], v1[3], v2[3];
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     const double a0 = o0 == 0 ? A[r * 3] : (o0 == 1 ? A[r * 3 + 1] : A[r * 3 + 2]);
     const double a1 = o1 == 0 ? A[r * 3] : (o1 == 1 ? A[r * 3 + 1] : A[r * 3 + 2]);
-    u1[r] = a0 / S0;
-    u2[r] = a1 / S1;
+    u1[r] = a0 * iS0;
+    u2[r] = a1 * iS1;
     v1[r] = o0 == 0 ? V[r * 3] : (o0 == 1 ? V[r * 3 + 1] : V[r * 3 + 2]);
     v2[r] = o1 == 0 ? V[r * 3] : (o1 == 1 ? V[r * 3 + 1] : V[r * 3 + 2]);
   }
