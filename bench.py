@@ -65,7 +65,24 @@ def parse_args():
 # ---------------------------------------------------------------------------------
 
 
-def make_workload(config_id: int, n_frames: int, seed: int):
+def host_prepare_template(tpl0, cfg):
+    """The reference's template build on the host (oracle restatement of the greedy
+    thinning + dense connections, kd-tree binding): the host-reference arm touches none of
+    the device code, not even at setup."""
+    from oracle import pipeline as OP
+    from paper_2007_08576_b200.warpfield import ControlGraph, bind_template
+
+    r = cfg.sampling.radius
+    ctrl = OP.sample_controls(tpl0.points, r)
+    edges, ew = OP.connections(ctrl, cfg.sampling.effective_connection_sigma)
+    warps = np.zeros((len(ctrl), 8))
+    warps[:, 0] = 1.0
+    graph = ControlGraph(ctrl, warps, edges, ew, sampling_radius=r)
+    return bind_template(tpl0, graph, k=cfg.sampling.bind_k,
+                         sigma=cfg.sampling.effective_bind_sigma), graph
+
+
+def make_workload(config_id: int, n_frames: int, seed: int, host_template: bool = False):
     from dataclasses import replace
 
     from paper_2007_08576_b200 import synth
@@ -82,7 +99,7 @@ def make_workload(config_id: int, n_frames: int, seed: int):
     tpl0 = synth.make_template(scene)
     feats = synth.make_features(scene, tpl0)
     frames = [synth.make_frame(scene, cam, tpl0, feats, f) for f in range(1, n_frames + 1)]
-    tpl, graph = prepare_template(tpl0, cfg)
+    tpl, graph = host_prepare_template(tpl0, cfg) if host_template else prepare_template(tpl0, cfg)
     return dict(scene=scene, cfg=cfg, cam=cam, tpl=tpl, graph=graph, feats=feats, frames=frames,
                 iters=spec["iters"], radius=spec["radius"])
 
@@ -474,7 +491,7 @@ REF_MAX_WARMUP = 1
 def run_reference(args, rank, world):
     if rank != 0:
         return None  # replicas are independent: rank 0 alone times the host reference
-    wl = make_workload(args.config, args.frames, seed=0)
+    wl = make_workload(args.config, args.frames, seed=0, host_template=True)
     step, OK = oracle_frame_runner(wl)
     cores = os.cpu_count() or 1
     OK.set_threads(cores)

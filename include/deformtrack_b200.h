@@ -149,6 +149,24 @@ int dt_preselect(const double* src, const double* dst, int64_t n,
                  int64_t* info, double* support, void* stream);
 
 /* ------------------------------------------------------------------------------
+ * Template time: graph construction on the device. HOST arrays in
+ * and out (once per sequence); bit-identical to the reference.
+ * ---------------------------------------------------------------------------- */
+
+/* warpfield.sample_control_points' greedy radius thinning (warpfield.py:77-109): the
+ * storage-order indices of the accepted control points (capacity n) and their count. */
+int dt_sample_control_points(const double* points, int64_t n, double radius,
+                             int64_t* control_index, int64_t* m_out, int device);
+
+/* Candidate connections of warpfield.build_connections (warpfield.py:112-137): every pair
+ * i < j with squared distance <= d2_max (the reference's order of evaluation), in
+ * lexicographic order, with that squared distance. edges (capacity x 2) int64, d2
+ * (capacity) f64; *e_out = the candidate count (pass edges = NULL to query it). The
+ * caller applies the reference's weight expression and prune. */
+int dt_connection_candidates(const double* ctrl, int64_t m, double d2_max, int64_t* edges,
+                             double* d2, int64_t capacity, int64_t* e_out, int device);
+
+/* ------------------------------------------------------------------------------
  * Frame level: a device-resident tracker (one per sequence / stream).
  * Replaces solver.solve_frame (solver.py:267-378) and tracking.track_frame
  * (tracking.py:67-95): preselect -> bind matches -> LM loop -> warp_all, with the

@@ -106,23 +106,6 @@ def test_estimator_params():
         MatchInlierSelector._check_pairs(np.zeros((4, 5)))
 
 
-def test_template_graph_build_matches_oracle():
-    from paper_2007_08576_b200 import synth
-    from paper_2007_08576_b200.warpfield import build_connections, sample_control_points
-
-    from oracle import pipeline as OP
-
-    scene = synth.Scene(surface="height-field", resolution=30, n_features=10)
-    tpl = synth.make_template(scene)
-    g = sample_control_points(tpl, 8.0)
-    np.testing.assert_array_equal(g.points, OP.sample_controls(tpl.points, 8.0))
-    e, w = build_connections(g.points, 16.0)
-    e2, w2 = OP.connections(g.points, 16.0)
-    np.testing.assert_array_equal(e, e2)
-    np.testing.assert_array_equal(w, w2)
-    assert np.all(e[:, 0] < e[:, 1]) and np.all(w >= 0.01)
-
-
 def test_synth_scene_shapes_and_outliers():
     from paper_2007_08576_b200 import synth
 
