@@ -30,10 +30,16 @@ namespace dt {
 constexpr int HAM_TPW = 2;                 // template descriptors per warp
 constexpr int HAM_WARPS = 4;               // warps per CTA (2000 templates -> 250 CTAs)
 constexpr int HAM_TILE = 512;              // frame descriptors per smem tile (16 KB)
+constexpr int HAM_SPLITS = 4;              // frame-descriptor ranges (grid rows) per template
 
+// blockIdx.y selects a contiguous range of frame descriptors; with `packed` the per-range
+// winners are folded by a 64-bit atomicMin of (distance << 32 | index) -- the
+// lexicographic (distance, index) minimum whatever the order of the ranges, i.e. ties
+// still resolve to the lowest frame index.
 __global__ void __launch_bounds__(HAM_WARPS * 32)
 k_hamming(const uint4* __restrict__ tdesc, int64_t nt, const uint4* __restrict__ fdesc, int64_t nf,
-          int32_t* __restrict__ best_idx, int32_t* __restrict__ best_dist) {
+          int64_t per_split, int32_t* __restrict__ best_idx, int32_t* __restrict__ best_dist,
+          unsigned long long* __restrict__ packed) {
   __shared__ uint4 s_tile[HAM_TILE * 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t0 = ((int64_t)blockIdx.x * HAM_WARPS + warp) * HAM_TPW;
@@ -55,8 +61,10 @@ k_hamming(const uint4* __restrict__ tdesc, int64_t nt, const uint4* __restrict__
     bd[j] = 0x7fffffff;
     bi[j] = 0x7fffffff;
   }
-  for (int64_t base = 0; base < nf; base += HAM_TILE) {
-    const int cnt = (int)((nf - base) < HAM_TILE ? (nf - base) : HAM_TILE);
+  const int64_t f_begin = (int64_t)blockIdx.y * per_split;
+  const int64_t f_end = f_begin + per_split < nf ? f_begin + per_split : nf;
+  for (int64_t base = f_begin; base < f_end; base += HAM_TILE) {
+    const int cnt = (int)((f_end - base) < HAM_TILE ? (f_end - base) : HAM_TILE);
     __syncthreads();
     for (int i = threadIdx.x; i < 2 * cnt; i += blockDim.x) s_tile[i] = fdesc[2 * base + i];
     __syncthreads();
@@ -88,19 +96,47 @@ k_hamming(const uint4* __restrict__ tdesc, int64_t nt, const uint4* __restrict__
     }
     const int64_t t = t0 + j;
     if (lane == 0 && t < nt) {
-      best_idx[t] = nf > 0 ? i : -1;
-      best_dist[t] = nf > 0 ? d : 257;
+      if (packed) {
+        if (f_begin < f_end)
+          atomicMin(packed + t, ((unsigned long long)(unsigned)d << 32) | (unsigned)i);
+      } else {
+        best_idx[t] = nf > 0 ? i : -1;
+        best_dist[t] = nf > 0 ? d : 257;
+      }
     }
   }
 }
 
+__global__ void k_unpack_hamming(const unsigned long long* __restrict__ packed, int64_t nt, int64_t nf,
+                                 int32_t* __restrict__ best_idx, int32_t* __restrict__ best_dist) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const unsigned long long v = packed[t];
+  best_idx[t] = nf > 0 ? (int32_t)(v & 0xffffffffull) : -1;
+  best_dist[t] = nf > 0 ? (int32_t)(v >> 32) : 257;
+}
+
+// With `packed` (nt uint64 scratch) the frame descriptors are split over HAM_SPLITS grid
+// rows and the results stay packed (dist << 32 | idx; the ORB match build reads them);
+// otherwise one pass writes best_idx / best_dist.
 int launch_hamming(const uint8_t* tdesc, int64_t nt, const uint8_t* fdesc, int64_t nf,
-                   int32_t* best_idx, int32_t* best_dist, cudaStream_t s) {
+                   int32_t* best_idx, int32_t* best_dist, cudaStream_t s,
+                   unsigned long long* packed) {
   if (nt == 0) return DT_OK;
   const int per_cta = HAM_WARPS * HAM_TPW;
-  k_hamming<<<grid_for(nt, per_cta), HAM_WARPS * 32, 0, s>>>(
-      reinterpret_cast<const uint4*>(tdesc), nt, reinterpret_cast<const uint4*>(fdesc), nf,
-      best_idx, best_dist);
+  int splits = 1;
+  int64_t per = nf;
+  if (packed) {
+    DT_CHECK_CUDA(cudaMemsetAsync(packed, 0xff, sizeof(unsigned long long) * nt, s));
+    splits = HAM_SPLITS;
+    per = ((nf + splits - 1) / splits + 31) / 32 * 32;
+    if (per <= 0) per = 32;
+    splits = (int)std::max<int64_t>(1, (nf + per - 1) / per);
+  }
+  const dim3 grid((unsigned)grid_for(nt, per_cta), (unsigned)splits);
+  k_hamming<<<grid, HAM_WARPS * 32, 0, s>>>(reinterpret_cast<const uint4*>(tdesc), nt,
+                                            reinterpret_cast<const uint4*>(fdesc), nf, per,
+                                            best_idx, best_dist, packed);
   DT_CHECK_LAUNCH();
   return DT_OK;
 }
@@ -537,8 +573,19 @@ extern "C" {
 int dt_hamming_match(const uint8_t* template_desc, int64_t n_template, const uint8_t* frame_desc,
                      int64_t n_frame, int32_t* best_idx, int32_t* best_dist, void* stream) {
   DT_REQUIRE(n_template >= 0 && n_frame >= 0, DT_ERR_INVALID_ARGUMENT, "negative descriptor count");
-  return launch_hamming(template_desc, n_template, frame_desc, n_frame, best_idx, best_dist,
-                        as_stream(stream));
+  cudaStream_t s = as_stream(stream);
+  if (n_template == 0) return DT_OK;
+  unsigned long long* packed = nullptr;
+  DT_CHECK_CUDA(cudaMallocAsync((void**)&packed, sizeof(unsigned long long) * n_template, s));
+  const int st = launch_hamming(template_desc, n_template, frame_desc, n_frame, nullptr, nullptr, s,
+                                packed);
+  if (st == DT_OK) {
+    k_unpack_hamming<<<grid_for(n_template, 256), 256, 0, s>>>(packed, n_template, n_frame,
+                                                              best_idx, best_dist);
+  }
+  cudaFreeAsync(packed, s);
+  DT_CHECK_LAUNCH();
+  return st;
 }
 
 int dt_preselect(const double* src, const double* dst, int64_t n, const int64_t* refs,

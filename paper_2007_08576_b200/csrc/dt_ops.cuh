@@ -39,7 +39,8 @@ int launch_warp_all_i32(const double* pts, const double* nrm, const int32_t* bid
 
 // dt_match.cu
 int launch_hamming(const uint8_t* tdesc, int64_t nt, const uint8_t* fdesc, int64_t nf,
-                   int32_t* best_idx, int32_t* best_dist, cudaStream_t s);
+                   int32_t* best_idx, int32_t* best_dist, cudaStream_t s,
+                   unsigned long long* packed = nullptr);
 struct PreselectWork;
 int launch_preselect(const double* src, const double* dst, const int64_t* n_dev, int64_t n_max,
                      const int64_t* refs, int64_t n_refs, int exhaustive, double H, int iters,

@@ -99,7 +99,7 @@ __device__ __forceinline__ int block_scan_count(int cnt, int* s_warp, int* total
 constexpr int BM_PER = 4;
 
 __global__ void __launch_bounds__(1024)
-k_build_matches(int64_t nt, const int32_t* __restrict__ best_idx, const int32_t* __restrict__ best_dist,
+k_build_matches(int64_t nt, const unsigned long long* __restrict__ packed,
                 int max_ham, const int32_t* __restrict__ kp, int64_t nf,
                 const double* __restrict__ depth, const uint8_t* __restrict__ dvalid, int width,
                 int height, double fx, double fy, double cx, double cy,
@@ -115,7 +115,10 @@ k_build_matches(int64_t nt, const int32_t* __restrict__ best_idx, const int32_t*
     for (int e = 0; e < BM_PER; ++e) {
       const int64_t t = t0 + e;
       fi[e] = -1;
-      if (t < nt && best_dist[t] <= max_ham) fi[e] = best_idx[t];
+      if (t < nt && nf > 0) {
+        const unsigned long long v = packed[t];  // (distance << 32) | frame index
+        if ((long long)(v >> 32) <= (long long)max_ham) fi[e] = (int)(v & 0xffffffffull);
+      }
     }
 #pragma unroll
     for (int e = 0; e < BM_PER; ++e) {
@@ -404,6 +407,7 @@ struct dt_tracker {
   int32_t* fkp = nullptr;
   int64_t fdesc_cap = 0;
   int32_t *ham_idx = nullptr, *ham_dist = nullptr;
+  unsigned long long* ham_packed = nullptr;  // (distance << 32) | index per template feature
   // ORB path: the solver's match arrays are indexed by template feature -- points,
   // binding and the control -> (feature, slot) CSR are static (set_features); per frame
   // only the observed points and weights change (0 = not an active match)
@@ -715,8 +719,9 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     }
     DT_CHECK_CUDA(cudaMemcpyAsync(t->fdesc, in->frame_desc, 32 * in->n_frame, kind, s));
     DT_CHECK_CUDA(cudaMemcpyAsync(t->fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
-    DT_TRY(launch_hamming(t->tdesc, t->n_feat, t->fdesc, in->n_frame, t->ham_idx, t->ham_dist, s));
-    k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_idx, t->ham_dist, c.max_hamming, t->fkp,
+    DT_TRY(launch_hamming(t->tdesc, t->n_feat, t->fdesc, in->n_frame, nullptr, nullptr, s,
+                          t->ham_packed));
+    k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_packed, c.max_hamming, t->fkp,
                                        in->n_frame, t->depth, t->dvalid, c.width, c.height, c.fx,
                                        c.fy, c.cx, c.cy, t->tfeat_pts, t->m_src, t->m_dst, t->m_feat,
                                        t->info + 2);
@@ -1062,6 +1067,7 @@ int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* po
   DT_TRY(dalloc(t, &t->tfeat_bw, t->k * n_features));
   DT_TRY(dalloc(t, &t->ham_idx, n_features));
   DT_TRY(dalloc(t, &t->ham_dist, n_features));
+  DT_TRY(dalloc(t, &t->ham_packed, n_features));
   DT_TRY(upload(t, t->tdesc, desc, 32 * n_features));
   DT_TRY(upload(t, t->tfeat_pts, points, 3 * n_features));
   // the match binding depends only on the template-side point (SURVEY §8a invariant):
