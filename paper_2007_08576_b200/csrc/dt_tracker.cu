@@ -414,6 +414,13 @@ struct dt_tracker {
   int *fptr = nullptr, *fent = nullptr, *fpos = nullptr;
   double *ffo = nullptr, *ffw = nullptr;
   bool orb_static = false;
+  // CUDA graph of the ORB frame body (everything after the input staging), captured once
+  // per input signature and replayed: one launch instead of ~14 stream operations
+  cudaGraphExec_t gexec = nullptr;
+  int64_t g_nframe = -1;
+  int g_launches = 0;
+  bool g_used = false;
+  bool graphs_off = false;
   // pipelined submission (dt_track_frame_submit / dt_tracker_wait): host inputs are staged
   // into one of two device slots on a copy stream while the previous frame computes;
   // outputs are copied back on the copy stream while the next frame computes
@@ -694,7 +701,8 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   // warm start: the previous solution (or set_warps) is in warps_out
   DT_CHECK_CUDA(cudaMemcpyAsync(t->warp_a, t->warps_out, sizeof(double) * 8 * t->m,
                                 cudaMemcpyDeviceToDevice, s));
-  DT_CHECK_CUDA(cudaMemcpyAsync(t->depth, in->depth, sizeof(double) * npix, kind, s));
+  if (in->depth != t->depth)
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->depth, in->depth, sizeof(double) * npix, kind, s));
   if (in->normals) {
     DT_CHECK_CUDA(cudaMemcpyAsync(t->onrm, in->normals, sizeof(double) * 3 * npix, kind, s));
     k_valid_mask<<<grid_for(npix, 256), 256, 0, s>>>(t->depth, npix, c.z_min, c.z_max, t->dvalid);
@@ -717,8 +725,10 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
       DT_TRY(dalloc(t, &t->fkp, 2 * cap));
       t->fdesc_cap = cap;
     }
-    DT_CHECK_CUDA(cudaMemcpyAsync(t->fdesc, in->frame_desc, 32 * in->n_frame, kind, s));
-    DT_CHECK_CUDA(cudaMemcpyAsync(t->fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
+    if (in->frame_desc != t->fdesc)
+      DT_CHECK_CUDA(cudaMemcpyAsync(t->fdesc, in->frame_desc, 32 * in->n_frame, kind, s));
+    if (in->frame_kp != t->fkp)
+      DT_CHECK_CUDA(cudaMemcpyAsync(t->fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
     DT_TRY(launch_hamming(t->tdesc, t->n_feat, t->fdesc, in->n_frame, nullptr, nullptr, s,
                           t->ham_packed));
     k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_packed, c.max_hamming, t->fkp,
@@ -882,6 +892,66 @@ int collect_outputs(dt_tracker* t, const dt_frame_input* in, dt_frame_output* ou
   return DT_OK;
 }
 
+void drop_graph(dt_tracker* t) {
+  if (t->gexec) cudaGraphExecDestroy(t->gexec);
+  t->gexec = nullptr;
+  t->g_nframe = -1;
+}
+
+// A frame through the CUDA graph when it is the steady-state ORB case (depth + frame
+// descriptors, no precomputed normals, profiling off, solver arguments already on the
+// device): stage the inputs into the tracker's own buffers, then replay the captured
+// body. Anything else -- or a failed capture -- runs the stream-ordered path.
+int run_frame(dt_tracker* t, const dt_frame_input* in, bool* used) {
+  const bool eligible = !t->graphs_off && !t->profiling && !t->args_dirty &&
+                        t->pre_solver_wait == nullptr && in->depth != nullptr &&
+                        in->normals == nullptr && in->use_matches && in->frame_desc != nullptr &&
+                        in->frame_kp != nullptr && in->n_frame > 0 && in->n_frame <= t->fdesc_cap &&
+                        t->orb_static;
+  if (!eligible) return enqueue_frame(t, in, used);
+  cudaStream_t s = t->stream;
+  const cudaMemcpyKind kind = in->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const int64_t npix = (int64_t)t->cfg.width * t->cfg.height;
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->depth, in->depth, sizeof(double) * npix, kind, s));
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->fdesc, in->frame_desc, 32 * in->n_frame, kind, s));
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
+  dt_frame_input gin = *in;
+  gin.on_device = 1;
+  gin.depth = t->depth;
+  gin.frame_desc = t->fdesc;
+  gin.frame_kp = t->fkp;
+  if (t->gexec == nullptr || t->g_nframe != in->n_frame) {
+    drop_graph(t);
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      t->graphs_off = true;
+      return enqueue_frame(t, &gin, used);
+    }
+    bool u = false;
+    const int st = enqueue_frame(t, &gin, &u);
+    const cudaError_t ce = cudaStreamEndCapture(s, &g);
+    cudaGraphExec_t ge = nullptr;
+    if (st != DT_OK || ce != cudaSuccess || g == nullptr ||
+        cudaGraphInstantiate(&ge, g, 0) != cudaSuccess || t->args_dirty) {
+      cudaGetLastError();
+      if (g) cudaGraphDestroy(g);
+      if (ge) cudaGraphExecDestroy(ge);
+      t->graphs_off = true;  // capture unsupported here: stream-ordered from now on
+      return enqueue_frame(t, &gin, used);
+    }
+    cudaGraphDestroy(g);
+    t->gexec = ge;
+    t->g_nframe = in->n_frame;
+    t->g_launches = t->launches;
+    t->g_used = u;
+  }
+  DT_CHECK_CUDA(cudaGraphLaunch(t->gexec, s));
+  t->launches = t->g_launches;
+  *used = t->g_used;
+  return DT_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1036,6 +1106,7 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
 int dt_tracker_destroy(dt_tracker* t) {
   if (!t) return DT_OK;
   cudaStreamSynchronize(t->stream);
+  drop_graph(t);
   if (t->copy_stream) {
     cudaStreamSynchronize(t->copy_stream);
     cudaStreamDestroy(t->copy_stream);
@@ -1059,6 +1130,7 @@ int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* po
                             const int64_t* bind_idx, const double* bind_w) {
   DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
   DT_REQUIRE(n_features >= 0, DT_ERR_INVALID_ARGUMENT, "negative feature count");
+  drop_graph(t);
   t->n_feat = n_features;
   DT_TRY(ensure_match_capacity(t, n_features));
   DT_TRY(dalloc(t, &t->tdesc, 32 * n_features));
@@ -1127,6 +1199,7 @@ int dt_tracker_get_warps(dt_tracker* t, double* warps_host) {
 
 int dt_tracker_set_config(dt_tracker* t, const dt_config* cfg) {
   DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
+  drop_graph(t);
   DT_TRY(validate_config(cfg));
   DT_REQUIRE(cfg->width == t->cfg.width && cfg->height == t->cfg.height, DT_ERR_INVALID_ARGUMENT,
              "camera size cannot change on a live tracker");
@@ -1153,7 +1226,7 @@ int dt_tracker_sync(dt_tracker* t) {
 int dt_track_frame(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out) {
   DT_REQUIRE(t != nullptr && in != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
   bool used = false;
-  DT_TRY(enqueue_frame(t, in, &used));
+  DT_TRY(run_frame(t, in, &used));
   t->last_used = used;
   return collect_outputs(t, in, out, used);
 }
@@ -1332,7 +1405,7 @@ int dt_tracker_last_launches(dt_tracker* t) { return t ? t->launches : 0; }
 int dt_track_frame_async(dt_tracker* t, const dt_frame_input* in) {
   DT_REQUIRE(t != nullptr && in != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
   bool used = false;
-  DT_TRY(enqueue_frame(t, in, &used));
+  DT_TRY(run_frame(t, in, &used));
   t->last_used = used;
   return DT_OK;
 }
@@ -1378,6 +1451,7 @@ void* dt_tracker_stream(dt_tracker* t) { return t ? (void*)t->stream : nullptr; 
 
 int dt_tracker_set_profiling(dt_tracker* t, int on) {
   DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
+  drop_graph(t);
   if (on && !t->ev[0])
     for (auto& e : t->ev) DT_CHECK_CUDA(cudaEventCreate(&e));
   if (on && !t->trace) {
