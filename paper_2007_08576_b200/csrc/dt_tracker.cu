@@ -416,10 +416,11 @@ struct dt_tracker {
   bool orb_static = false;
   // CUDA graph of the ORB frame body (everything after the input staging), captured once
   // per input signature and replayed: one launch instead of ~14 stream operations
-  cudaGraphExec_t gexec = nullptr;
-  int64_t g_nframe = -1;
-  int g_launches = 0;
-  bool g_used = false;
+  // [0] no pre-solver wait, [1] / [2] the pipelined path waiting on ev_out_copied[0 / 1]
+  cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};
+  int64_t g_nframe[3] = {-1, -1, -1};
+  int g_launches[3] = {0, 0, 0};
+  bool g_used[3] = {false, false, false};
   bool graphs_off = false;
   // pipelined submission (dt_track_frame_submit / dt_tracker_wait): host inputs are staged
   // into one of two device slots on a copy stream while the previous frame computes;
@@ -893,9 +894,11 @@ int collect_outputs(dt_tracker* t, const dt_frame_input* in, dt_frame_output* ou
 }
 
 void drop_graph(dt_tracker* t) {
-  if (t->gexec) cudaGraphExecDestroy(t->gexec);
-  t->gexec = nullptr;
-  t->g_nframe = -1;
+  for (int i = 0; i < 3; ++i) {
+    if (t->gexec[i]) cudaGraphExecDestroy(t->gexec[i]);
+    t->gexec[i] = nullptr;
+    t->g_nframe[i] = -1;
+  }
 }
 
 // A frame through the CUDA graph when it is the steady-state ORB case (depth + frame
@@ -903,8 +906,7 @@ void drop_graph(dt_tracker* t) {
 // device): stage the inputs into the tracker's own buffers, then replay the captured
 // body. Anything else -- or a failed capture -- runs the stream-ordered path.
 int run_frame(dt_tracker* t, const dt_frame_input* in, bool* used) {
-  const bool eligible = !t->graphs_off && !t->profiling && !t->args_dirty &&
-                        t->pre_solver_wait == nullptr && in->depth != nullptr &&
+  const bool eligible = !t->graphs_off && !t->profiling && !t->args_dirty && in->depth != nullptr &&
                         in->normals == nullptr && in->use_matches && in->frame_desc != nullptr &&
                         in->frame_kp != nullptr && in->n_frame > 0 && in->n_frame <= t->fdesc_cap &&
                         t->orb_static;
@@ -920,8 +922,11 @@ int run_frame(dt_tracker* t, const dt_frame_input* in, bool* used) {
   gin.depth = t->depth;
   gin.frame_desc = t->fdesc;
   gin.frame_kp = t->fkp;
-  if (t->gexec == nullptr || t->g_nframe != in->n_frame) {
-    drop_graph(t);
+  const int gi = t->pre_solver_wait == nullptr ? 0
+                 : (t->copy_stream && t->pre_solver_wait == t->ev_out_copied[0] ? 1 : 2);
+  if (t->gexec[gi] == nullptr || t->g_nframe[gi] != in->n_frame) {
+    if (t->gexec[gi]) cudaGraphExecDestroy(t->gexec[gi]);
+    t->gexec[gi] = nullptr;
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       cudaGetLastError();
@@ -941,14 +946,14 @@ int run_frame(dt_tracker* t, const dt_frame_input* in, bool* used) {
       return enqueue_frame(t, &gin, used);
     }
     cudaGraphDestroy(g);
-    t->gexec = ge;
-    t->g_nframe = in->n_frame;
-    t->g_launches = t->launches;
-    t->g_used = u;
+    t->gexec[gi] = ge;
+    t->g_nframe[gi] = in->n_frame;
+    t->g_launches[gi] = t->launches;
+    t->g_used[gi] = u;
   }
-  DT_CHECK_CUDA(cudaGraphLaunch(t->gexec, s));
-  t->launches = t->g_launches;
-  *used = t->g_used;
+  DT_CHECK_CUDA(cudaGraphLaunch(t->gexec[gi], s));
+  t->launches = t->g_launches[gi];
+  *used = t->g_used[gi];
   return DT_OK;
 }
 
@@ -1347,7 +1352,7 @@ int dt_track_frame_submit(dt_tracker* t, const dt_frame_input* in, dt_frame_outp
   din.frame_kp = nd > 0 ? t->in_kp[slot] : nullptr;
   t->pre_solver_wait = t->pipe_next > 0 ? t->ev_out_copied[1 - slot] : nullptr;
   bool used = false;
-  const int st = enqueue_frame(t, &din, &used);
+  const int st = run_frame(t, &din, &used);
   t->pre_solver_wait = nullptr;
   DT_TRY(st);
   t->last_used = used;
