@@ -40,20 +40,12 @@ namespace cg = cooperative_groups;
 namespace dt {
 
 constexpr int NWARPS = SOLVER_THREADS / 32;
-constexpr int STAGE = 32 * 9;  // per-warp row staging (32 rows x 8 cols, padded to 9)
-constexpr int GOUT = 64;       // per-warp 8x8 Gram readout
-constexpr int M_MAX_SMEM = 1100;
+constexpr int GOUT = 32;  // per-warp reduce-scatter readout (one accumulator per lane)
+constexpr int M_MAX_SMEM = 1300;
 
 size_t solver_smem_bytes(int m) {
-  return sizeof(double) * ((size_t)21 * m + (size_t)NWARPS * (STAGE + GOUT));
+  return sizeof(double) * ((size_t)21 * m + (size_t)NWARPS * GOUT);
 }
-
-// 27 normal-equation columns from the 8x8 Gram of rows [J0..J5, wv, 0]:
-// triu(J^T J) in kernels.py:41-44 order, then J^T wv.
-__constant__ unsigned char kColRow[27] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3,
-                                          4, 4, 5, 0, 1, 2, 3, 4, 5};
-__constant__ unsigned char kColCol[27] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5,
-                                          4, 5, 5, 6, 6, 6, 6, 6, 6};
 
 // Loads of data produced by other CTAs in an earlier phase: L1-cacheable (every domain
 // barrier has acquire semantics and invalidates L1 -- measured, tools/l1_probe.cu), so
@@ -74,55 +66,14 @@ __device__ __forceinline__ long long gtimer() {
 }
 
 // ---------------------------------------------------------------------------------
-// FP64 tensor-core Gram accumulation: every lane contributes one 8-column row per push;
-// C += R^T R over the 32 rows as 8 DMMA.8x8x4 steps (fragment: lane = 4 g + t holds
-// R[4q + t][g] as both the A and the B element; C[g][2t..2t+1] per lane).
-// ---------------------------------------------------------------------------------
-
-struct Gram {
-  double c0 = 0.0, c1 = 0.0;
-};
-
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ void gram_push(Gram& G, double* stage, const double row[8]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) stage[lane * 9 + c] = row[c];
-  __syncwarp();
-  const int t = lane & 3, g = lane >> 2;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const double v = stage[(4 * q + t) * 9 + g];
-    dmma884(G.c0, G.c1, v, v);
-  }
-  __syncwarp();
-}
-
-__device__ __forceinline__ void gram_store(const Gram& G, double* out) {
-  const int lane = threadIdx.x & 31;
-  const int t = lane & 3, g = lane >> 2;
-  out[g * 8 + 2 * t] = G.c0;
-  out[g * 8 + 2 * t + 1] = G.c1;
-  __syncwarp();
-}
-
-__device__ __forceinline__ double gram_col(const double* out, int col) {
-  return out[kColRow[col] * 8 + kColCol[col]];
-}
-
-// ---------------------------------------------------------------------------------
 // Per-lane normal-equation accumulation (FP64 FMA) + warp reduce-scatter. Each lane
 // folds its rows [J0..J5, wv, sw] into 32 accumulators:
 //   [0, 21) triu(J^T J) in kernels.py:41-44 order, [21, 27) J^T wv,
 //   27: wv^2 (the rows' cost), 28: sw^2 (support), 29-31 unused;
 // the reduce-scatter (31 shuffles) leaves lane l with the warp's sum of accumulator l.
-// On B200 the FP64 tensor core (DMMA.8x8x4) runs at the DFMA rate (tools/fp64_probe.cu:
-// 36 vs 34 TFLOP/s), so the 29 useful products per row beat the 64 of an 8x8 Gram.
+// On B200 the FP64 tensor core (DMMA.8x8x4, mma.sync.m8n8k4.f64) runs at the DFMA rate
+// (tools/fp64_probe.cu: 36 vs 34 TFLOP/s), so the 29 useful products per row beat the 64
+// of an 8x8 Gram (the first version of these folds; ~3x slower end to end).
 // ---------------------------------------------------------------------------------
 
 __device__ __forceinline__ void acc_row(double (&a)[32], const double r[8]) {

@@ -420,8 +420,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   double* s_w = smem;
   double* s_T = smem + 8 * m;
   double* s_lam = smem + 20 * m;  // per-control damping, replicated in every CTA
-  double* stage = smem + 21 * m + warp * (STAGE + GOUT);
-  double* gout = stage + STAGE;
+  double* gout = smem + 21 * m + warp * GOUT;
   // work items are dealt round-robin over the CTAs first (item i -> CTA i % C), so
   // every SM of the domain gets a share of each phase
   const int gw = warp * C + rank, GW = C * NWARPS;
@@ -538,12 +537,12 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
           // combine the team's warps in warp order; accumulator 28 = support
           if (lane < 27) {
             double v = 0.0;
-            for (int w = 0; w < TEAM; ++w) v += gout[w * (STAGE + GOUT) + lane];
+            for (int w = 0; w < TEAM; ++w) v += gout[w * GOUT + lane];
             A.partial[27 * c + lane] = v;
           }
           if (lane == 28) {
             double su = 0.0;
-            for (int w = 0; w < TEAM; ++w) su += gout[w * (STAGE + GOUT) + 28];
+            for (int w = 0; w < TEAM; ++w) su += gout[w * GOUT + 28];
             A.wa[c] = A.arap_w * fmax(su, A.data_floor);
           }
         }
@@ -613,7 +612,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         if (tw == 0 && c < m) {
           if (lane < 27) {
             double v = 0.0;
-            for (int w = 0; w < TEAM; ++w) v += gout[w * (STAGE + GOUT) + lane];
+            for (int w = 0; w < TEAM; ++w) v += gout[w * GOUT + lane];
             v = ld(A.partial + 27 * c + lane) + v;
             A.partial[27 * c + lane] = v;
             s_col[team][lane] = v;
@@ -622,7 +621,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             // accumulator 27 of the rigidity rows = the rigidity cost of this control's
             // bins (each connection's rows go to both bins: the bins sum to its cost)
             double v = 0.0;
-            for (int w = 0; w < TEAM; ++w) v += gout[w * (STAGE + GOUT) + 27];
+            for (int w = 0; w < TEAM; ++w) v += gout[w * GOUT + 27];
             okn[2 * m + c] = v;
           }
           __syncwarp();
