@@ -21,12 +21,13 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-NAMES = {0: "start", 1: "relink+linearize",
-         2: "data gather", 3: "rigidity: edge costs", 3.2: "  gram store",
-         3.4: "  team combine+solve", 5: "apply step", 5.2: "  transforms+tent store",
-         5.3: "  cost_before totals", 5.4: "  ok/step-norm reduce", 5.5: "  apply_step x m",
-         2.2: "  accept + edge unit rows", 2.3: "  data rows -> Gram", 2.4: "  team combine", 3.3: "  rigidity rows -> Gram",
-         6: "value pass + spec relink", 6.3: "  value totals", 6.4: "  lambda update", 6.5: "  lambda history", 5.7: "  prefetch step inputs", 7.2: "final load", 8: "final support", 1.2: "  load warps+transforms", 9: "final rigidity", 99: "end"}
+NAMES = {0: "start", 1: "P1 warm-start relinearization", 1.2: "  load warps + transforms",
+         2: "P2 data folds", 2.2: "  accept decision", 2.3: "  data rows fold", 2.4: "  team combine",
+         3: "P3 rigidity folds + solve", 3.3: "  rigidity rows fold", 3.2: "  reduce-scatter",
+         3.4: "  combine + Cholesky + publish", 5.7: "  load tentative state", 5.3: "  decide reductions",
+         5.4: "  step-norm / ok", 5.2: "  (unused)", 5.5: "  (unused)",
+         6: "P6 value pass + speculative relinearization", 6.3: "  value totals", 6.4: "  damping update",
+         6.5: "  damping history", 7.2: "final load", 8: "final support", 9: "final rigidity", 99: "end"}
 
 
 def main():
