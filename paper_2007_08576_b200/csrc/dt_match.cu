@@ -323,9 +323,10 @@ __device__ __forceinline__ bool procrustes_lane(const double C[9], double V[9], 
 __device__ __forceinline__ double irls_weight(const double R[9], double a0, double a1, double a2,
                                               double b0, double b1, double b2, double H,
                                               double Hsq) {
-  const double e0 = b0 - __fma_rn(a2, R[2], __fma_rn(a1, R[1], a0 * R[0]));
-  const double e1 = b1 - __fma_rn(a2, R[5], __fma_rn(a1, R[4], a0 * R[3]));
-  const double e2 = b2 - __fma_rn(a2, R[8], __fma_rn(a1, R[7], a0 * R[6]));
+  // e = b - R a as one fused chain per component (3 FMA, no separate multiply / subtract)
+  const double e0 = __fma_rn(-R[0], a0, __fma_rn(-R[1], a1, __fma_rn(-R[2], a2, b0)));
+  const double e1 = __fma_rn(-R[3], a0, __fma_rn(-R[4], a1, __fma_rn(-R[5], a2, b1)));
+  const double e2 = __fma_rn(-R[6], a0, __fma_rn(-R[7], a1, __fma_rn(-R[8], a2, b2)));
   const double s = __fma_rn(e2, e2, __fma_rn(e1, e1, e0 * e0));
   // 1/sqrt(s) for s > H^2: the MUFU double-precision estimate refined by two Newton
   // steps (~1 ulp; the full-precision rsqrt(double) carries special-case branches, and
@@ -334,8 +335,9 @@ __device__ __forceinline__ double irls_weight(const double R[9], double a0, doub
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(sc));
   const double hs = 0.5 * sc;
-  y = y * __fma_rn(-hs, y * y, 1.5);
-  y = y * __fma_rn(-hs, y * y, 1.5);
+  // y <- y + y (0.5 - hs y^2), fused
+  y = __fma_rn(y, __fma_rn(-hs * y, y, 0.5), y);
+  y = __fma_rn(y, __fma_rn(-hs * y, y, 0.5), y);
   return s > Hsq ? H * y : 1.0;
 }
 
