@@ -425,7 +425,8 @@ struct dt_tracker {
   // pipelined submission (dt_track_frame_submit / dt_tracker_wait): host inputs are staged
   // into one of two device slots on a copy stream while the previous frame computes;
   // outputs are copied back on the copy stream while the next frame computes
-  cudaStream_t copy_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host -> device staging
+  cudaStream_t out_stream = nullptr;   // device -> host outputs (not queued behind staging)
   cudaEvent_t ev_in_ready[2] = {nullptr, nullptr}, ev_in_free[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_out_copied[2] = {nullptr, nullptr};
   cudaEvent_t pre_solver_wait = nullptr;  // compute stream waits on it before the solver
@@ -1116,6 +1117,10 @@ int dt_tracker_destroy(dt_tracker* t) {
     cudaStreamSynchronize(t->copy_stream);
     cudaStreamDestroy(t->copy_stream);
   }
+  if (t->out_stream) {
+    cudaStreamSynchronize(t->out_stream);
+    cudaStreamDestroy(t->out_stream);
+  }
   for (int i = 0; i < 2; ++i) {
     for (cudaEvent_t e : {t->ev_in_ready[i], t->ev_in_free[i], t->ev_done[i], t->ev_out_copied[i]})
       if (e) cudaEventDestroy(e);
@@ -1258,6 +1263,7 @@ __global__ void k_stage_outputs(const int64_t* __restrict__ info, const double* 
 int ensure_pipeline(dt_tracker* t, int64_t n_desc) {
   if (!t->copy_stream) {
     DT_CHECK_CUDA(cudaStreamCreateWithFlags(&t->copy_stream, cudaStreamNonBlocking));
+    DT_CHECK_CUDA(cudaStreamCreateWithFlags(&t->out_stream, cudaStreamNonBlocking));
     const int64_t npix = (int64_t)t->cfg.width * t->cfg.height;
     for (int i = 0; i < 2; ++i) {
       DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_in_ready[i], cudaEventDisableTiming));
@@ -1360,20 +1366,22 @@ int dt_track_frame_submit(dt_tracker* t, const dt_frame_input* in, dt_frame_outp
   k_stage_outputs<<<1, 64, 0, s>>>(t->info, t->astats, t->pstats, t->report, t->stage_info[slot]);
   DT_CHECK_LAUNCH();
   DT_CHECK_CUDA(cudaEventRecord(t->ev_done[slot], s));
-  // outputs back on the copy stream while the next frame computes
-  DT_CHECK_CUDA(cudaStreamWaitEvent(cs, t->ev_done[slot], 0));
+  // outputs back on their own stream while the next frame computes (a single copy stream
+  // would queue the next frame's input staging behind this frame's output copies)
+  cudaStream_t os = t->out_stream;
+  DT_CHECK_CUDA(cudaStreamWaitEvent(os, t->ev_done[slot], 0));
   if (out->warps)
-    DT_CHECK_CUDA(cudaMemcpyAsync(out->warps, t->warps_out, sizeof(double) * 8 * t->m, cudaMemcpyDeviceToHost, cs));
+    DT_CHECK_CUDA(cudaMemcpyAsync(out->warps, t->warps_out, sizeof(double) * 8 * t->m, cudaMemcpyDeviceToHost, os));
   if (out->points)
-    DT_CHECK_CUDA(cudaMemcpyAsync(out->points, t->out_p, sizeof(double) * 3 * t->n, cudaMemcpyDeviceToHost, cs));
+    DT_CHECK_CUDA(cudaMemcpyAsync(out->points, t->out_p, sizeof(double) * 3 * t->n, cudaMemcpyDeviceToHost, os));
   if (out->normals)
-    DT_CHECK_CUDA(cudaMemcpyAsync(out->normals, t->out_n, sizeof(double) * 3 * t->n, cudaMemcpyDeviceToHost, cs));
+    DT_CHECK_CUDA(cudaMemcpyAsync(out->normals, t->out_n, sizeof(double) * 3 * t->n, cudaMemcpyDeviceToHost, os));
   if (out->control_data_weights)
     DT_CHECK_CUDA(cudaMemcpyAsync(out->control_data_weights, t->wa_out, sizeof(double) * t->m,
-                                  cudaMemcpyDeviceToHost, cs));
+                                  cudaMemcpyDeviceToHost, os));
   DT_CHECK_CUDA(cudaMemcpyAsync(t->h_stage[slot], t->stage_info[slot], sizeof(int64_t) * STAGE_WORDS,
-                                cudaMemcpyDeviceToHost, cs));
-  DT_CHECK_CUDA(cudaEventRecord(t->ev_out_copied[slot], cs));
+                                cudaMemcpyDeviceToHost, os));
+  DT_CHECK_CUDA(cudaEventRecord(t->ev_out_copied[slot], os));
   dt_tracker::Pending& pd = t->pend[slot];
   pd.active = true;
   pd.used = used;
