@@ -6,21 +6,24 @@
 //
 // Two sync domains from one kernel body:
 //   * cluster mode: a thread-block cluster (<= 16 CTAs, barrier.cluster) owns one
-//     sequence; many sequences run as many clusters of one launch (BASELINE config 5);
-//   * grid mode: a cooperative grid over every SM owns one sequence (lowest latency).
+//     sequence; many sequences run concurrently on their own streams (BASELINE config 5);
+//   * grid mode: a cooperative grid of one 256-thread CTA per SM owns one sequence
+//     (lowest latency, the default for a single sequence).
 //
-// Phases of one outer iteration (each ends at a domain barrier):
-//   P1  points & matches: warp + project + gate + residual + Tukey + blend gradient
-//       (kernels.py:483-569, 173-197, 239-250); icp / feature cost of the iterate
-//   P2  controls: data rows -> normal equations (FP64 tensor-core Gram products,
-//       mma.sync m8n8k4 f64), support -> rigidity weight wa (energy.py:394-402)
-//   P3  controls: rigidity rows (kernels.py:341-467) -> normal equations, first damped
-//       6x6 Cholesky (solver.py:217-258); edges: rigidity cost of the iterate
-//   P5  controls: exp(delta) * W, renormalize (solver.py:261-264)
-//   P6  points / matches / edges: cost at the tentative warps with frozen robust and
-//       rigidity weights (solver.py:333-335); accept iff strictly lower (solver.py:336)
+// Phases (each ends at a domain barrier; details in dt_solver_kernel.cuh):
+//   P1  (once) points & matches at the warm start: warp + project + gate + residual +
+//       Tukey + blend gradient (kernels.py:483-569, 173-197, 239-250), normal-equation
+//       rows at control-CSR positions; unit rigidity rows of every connection
+//   P2  controls: fold the data rows -> 27 normal-equation columns + support -> rigidity
+//       weight wa (energy.py:394-402)
+//   P3  controls: fold the rigidity rows (kernels.py:341-467) with the fresh wa, damped
+//       6x6 Cholesky (solver.py:217-258), publish delta + the tentative warp
+//       exp(delta) * W (solver.py:261-264) and its rigid transform
+//   P6  decide (solver.py:321-331), then points / matches / edges: cost at the tentative
+//       warps with frozen robust and rigidity weights (solver.py:333-335) + speculative
+//       relinearization there; accept iff strictly lower (solver.py:336)
 // Every reduction is deterministic and independent of the launch shape: normal equations
-// are per control in CSR order, costs are per fixed 32-item chunk then summed in chunk
+// are folded per control in CSR order, costs per fixed 32-item chunk then folded in chunk
 // order, and every CTA evaluates the totals identically, so all CTAs take the same
 // control-flow decisions.
 

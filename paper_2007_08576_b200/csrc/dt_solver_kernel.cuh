@@ -1,17 +1,18 @@
 // dt_solver_kernel.cuh -- body of the persistent LM kernel (included by dt_solver.cu).
 //
-// Work units inside the sync domain (C CTAs x 16 warps), dealt round-robin over the CTAs:
+// Work units inside the sync domain (C CTAs x 8 warps), dealt round-robin over the CTAs:
 //   * points / matches / edges: one item per lane, fixed 32-item chunks whose partial
-//     sums land in csum (deterministic, independent of C);
-//   * controls: a team of TEAM warps of one CTA per control; each warp folds every
-//     TEAM-th block of 32 rows into its own FP64 tensor-core Gram, the team combines the
-//     Grams in warp order (deterministic, independent of C).
-// Barriers per accepted outer iteration: P2 | P3 (+ first solve) | value pass. The
-// tentative step is applied redundantly by every CTA into its own shared memory (no
-// barrier), and the value pass also relinearizes at the tentative warps into the second
-// record buffer ("speculative relink"), so an accepted step starts the next iteration
-// directly at P2; a stalled iteration keeps its linearization -- the reference recomputes
-// it at the same warps, bit for bit the same -- and only re-solves.
+//     sums are folded by the last-arriving warp (red_commit; deterministic, independent
+//     of C);
+//   * controls: a team of TEAM warps of one CTA per control; each lane folds its rows
+//     into 32 FP64 accumulators, a warp reduce-scatter leaves lane l with accumulator l,
+//     the team combines its warps in warp order (deterministic, independent of C).
+// Barriers per accepted outer iteration: P2 | P3 | value pass. The solvers publish the
+// tentative warps, every CTA loads them into its own shared memory, and the value pass
+// also relinearizes at the tentative warps into the second buffer ("speculative
+// relinearization"), so an accepted step starts the next iteration directly at P2; a
+// stalled iteration keeps its linearization -- the reference recomputes it at the same
+// warps, bit for bit the same -- and only re-solves.
 
 #ifndef DT_TEAM
 #define DT_TEAM 2
