@@ -72,10 +72,56 @@ __device__ __forceinline__ void load_row(const double* src, double r[8]) {
 // point's icp cost under the Tukey weight of the new residual. With `ob`, *cost_old
 // receives the point's cost at these warps under the frozen correspondence and robust
 // weight of record `ob` (the value pass, solver.py:333-335).
+// Everything point p's step reads that does not depend on the warps: the template point
+// and normal, its binding (+ sqrt alpha, CSR positions) and -- for the value pass -- the
+// frozen correspondence of record `ob`. Issued before the value pass's decide prologue so
+// this L2 round trip overlaps it.
+template <int KM>
+struct PointIn {
+  int idx[KM], pos[KM];
+  double a[KM], sqa[KM];
+  double px, py, pz, tn0, tn1, tn2;
+  double oo0, oo1, oo2, on0, on1, on2, ors;
+  uint8_t ovalid;
+};
+
+template <int KM>
+__device__ __forceinline__ void point_load(const SolverArgs& A, int64_t p, const PBuf* ob,
+                                           PointIn<KM>& in) {
+  const int kk = KM == 4 ? 4 : A.k;
+#pragma unroll
+  for (int s = 0; s < KM; ++s)
+    if (s < kk) {
+      in.idx[s] = A.bidx[p * kk + s];
+      in.a[s] = A.bw[p * kk + s];
+      in.pos[s] = __ldg(A.cpos + p * kk + s);
+      in.sqa[s] = __ldg(A.bws + p * kk + s);  // sqrt(alpha), correctly rounded: the reference's
+    }
+  in.ovalid = 0;
+  in.oo0 = in.oo1 = in.oo2 = in.on0 = in.on1 = in.on2 = in.ors = 0.0;
+  if (ob) {
+    in.ovalid = ldu8(ob->valid + p);
+    in.oo0 = ld(ob->obs + 3 * p);
+    in.oo1 = ld(ob->obs + 3 * p + 1);
+    in.oo2 = ld(ob->obs + 3 * p + 2);
+    in.on0 = ld(ob->nrm + 3 * p);
+    in.on1 = ld(ob->nrm + 3 * p + 1);
+    in.on2 = ld(ob->nrm + 3 * p + 2);
+    in.ors = ld(ob->rs + p);
+  }
+  in.px = A.tp[3 * p];
+  in.py = A.tp[3 * p + 1];
+  in.pz = A.tp[3 * p + 2];
+  in.tn0 = A.tn[3 * p];
+  in.tn1 = A.tn[3 * p + 1];
+  in.tn2 = A.tn[3 * p + 2];
+}
+
 template <int KM>
 __device__ __forceinline__ double point_step(const SolverArgs& A, const double* s_w, int64_t p,
-                                             const PBuf* ob, const PBuf& nb, double* cost_old,
-                                             int* valid_out, long long* dbg = nullptr) {
+                                             const PointIn<KM>& in, bool value_pass,
+                                             const PBuf& nb, double* cost_old, int* valid_out,
+                                             long long* dbg = nullptr) {
 #ifdef DT_WARP_TRACE
 #define PSTAMP(i)                        \
   do {                                   \
@@ -88,51 +134,31 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
 #endif
   PSTAMP(0);
   const int kk = KM == 4 ? 4 : A.k;
-  // every load that does not depend on this point's arithmetic is issued up front (one
-  // L2 round trip after the domain barrier instead of a chain of them)
-  int pos[KM];
-  double sqa[KM];  // sqrt(alpha), precomputed (correctly rounded: the reference's value)
-#pragma unroll
-  for (int s = 0; s < KM; ++s)
-    if (s < kk) {
-      pos[s] = __ldg(A.cpos + p * kk + s);
-      sqa[s] = __ldg(A.bws + p * kk + s);
-    }
-  uint8_t ovalid = 0;
-  double oo0 = 0, oo1 = 0, oo2 = 0, on0 = 0, on1 = 0, on2 = 0, ors = 0;
-  if (ob) {
-    ovalid = ldu8(ob->valid + p);
-    oo0 = ld(ob->obs + 3 * p);
-    oo1 = ld(ob->obs + 3 * p + 1);
-    oo2 = ld(ob->obs + 3 * p + 2);
-    on0 = ld(ob->nrm + 3 * p);
-    on1 = ld(ob->nrm + 3 * p + 1);
-    on2 = ld(ob->nrm + 3 * p + 2);
-    ors = ld(ob->rs + p);
-  }
-  const double px = A.tp[3 * p], py = A.tp[3 * p + 1], pz = A.tp[3 * p + 2];
-  const double tn0 = A.tn[3 * p], tn1 = A.tn[3 * p + 1], tn2 = A.tn[3 * p + 2];
-  double B[8], sgn[KM], a[KM];
-  blend_rows<KM>(s_w, A.bidx, A.bw, p, kk, B, sgn, a);
+  const int* pos = in.pos;
+  const double* sqa = in.sqa;
+  const double* a = in.a;
+  const double px = in.px, py = in.py, pz = in.pz;
+  double B[8], sgn[KM];
+  blend_at_k<KM>(s_w, in.idx, in.a, kk, B, sgn);
   PSTAMP(1);
   double x0, x1, x2, s2;
   apply_blend(B, px, py, pz, x0, x1, x2, s2);
   PSTAMP(2);
-  if (ob) {
+  if (value_pass) {
     double co = 0.0;
-    if (ovalid) {
-      const double r = on0 * (x0 - oo0) + on1 * (x1 - oo1) + on2 * (x2 - oo2);
+    if (in.ovalid) {
+      const double r = in.on0 * (x0 - in.oo0) + in.on1 * (x1 - in.oo1) + in.on2 * (x2 - in.oo2);
 #pragma unroll
       for (int s = 0; s < KM; ++s)
         if (s < kk) {
-          const double wv = ors * sqa[s] * r;
+          const double wv = in.ors * sqa[s] * r;
           co += wv * wv;
         }
     }
     *cost_old = co;
   }
   double r0, r1, r2;
-  rotate_normal(B, tn0, tn1, tn2, r0, r1, r2);
+  rotate_normal(B, in.tn0, in.tn1, in.tn2, r0, r1, r2);
   bool ok = false;
   double o0 = 0, o1 = 0, o2 = 0, g0 = 0, g1 = 0, g2 = 0;
   // projection and gates, in the reference's IEEE order (kernels.py:537-568)
@@ -191,7 +217,7 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
 #pragma unroll
   for (int s = 0; s < KM; ++s)
     if (s < kk) {
-      const int c = A.bidx[p * kk + s];
+      const int c = in.idx[s];
       const double sw = rs * sqa[s];
       const double wv = sw * r;
       cost += wv * wv;
@@ -471,7 +497,11 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
       if (ch < nch_p) {
         const int64_t p = (int64_t)ch * CHUNK + lane;
         int vd;
-        if (p < n) acc = point_step<KM>(A, s_w, p, nullptr, nb, nullptr, &vd);
+        if (p < n) {
+          PointIn<KM> pin;
+          point_load<KM>(A, p, nullptr, pin);
+          acc = point_step<KM>(A, s_w, p, pin, false, nb, nullptr, &vd);
+        }
         acc = warp_sum(acc);
         red_commit<2, 0>(A, 0, ch, nch_p, {0.0, acc});
       } else if (ch < nch_p + nch_m) {
@@ -660,6 +690,15 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         for (int c = gc; c < m; c += GT) resolve_control(A, c, s_lam[c], okn, okn + m, cur, tent);
       }
       DSYNC(attempt == 0 ? 3 : 4);
+      // this warp's first value-pass point: its warp-independent inputs are loaded now,
+      // overlapping the decide prologue's round trip
+      PointIn<KM> pin0;
+      const int64_t p0 = (int64_t)gw * CHUNK + lane;
+      const bool pre = gw < nch_p && p0 < n;
+      if (pre) {
+        const PBuf ob0 = pbuf(A, pb);
+        point_load<KM>(A, p0, &ob0, pin0);
+      }
       // The solvers published every control's tentative warp and transform; load them
       // into shared memory together with the per-control solve results (one round
       // trip), then decide (all solves ok? largest step norm; after a fresh
@@ -756,7 +795,15 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             if (A.arrivals && outer == 1 && attempt == 0 && lane == 0 && rank < 8)
               dbg = A.arrivals + 2 + (size_t)1024 * A.arr_cap + 20000 + (rank * NWARPS + warp) * 8;
 #endif
-            if (p < n) cn = point_step<KM>(A, s_w, p, &ob, nb, &co, &vd, dbg);
+            if (p < n) {
+              if (ch == gw && pre) {
+                cn = point_step<KM>(A, s_w, p, pin0, true, nb, &co, &vd, dbg);
+              } else {
+                PointIn<KM> pin;
+                point_load<KM>(A, p, &ob, pin);
+                cn = point_step<KM>(A, s_w, p, pin, true, nb, &co, &vd, dbg);
+              }
+            }
             co = warp_sum(co);
             cn = warp_sum(cn);
             red_commit<2, 0>(A, 0, ch, nch_p, {co, cn});
