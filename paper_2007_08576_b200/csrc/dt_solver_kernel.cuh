@@ -482,6 +482,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   double final_step_norm = 0.0;
   int parity = 0;
   double cb_icp = 0.0, cb_feat = 0.0, cb_arap = 0.0;
+  double pd0 = 0.0, pd1 = 0.0;  // P2 -> P3: this team-lane's data column, team rounds 0 / 1
 
   // ---- P1: relink + linearize at the warm start (buffer 0): points, matches, unit
   // rigidity rows of the connections ----
@@ -565,11 +566,15 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         gout[lane] = warp_reduce_scatter(acc);
         __syncthreads();
         if (tw == 0 && c < m) {
-          // combine the team's warps in warp order; accumulator 28 = support
+          // combine the team's warps in warp order; accumulator 28 = support. The same
+          // team folds this control's rigidity rows in P3, so the data columns stay in a
+          // register (P3 publishes data + rigidity for the re-solves)
           if (lane < 27) {
             double v = 0.0;
             for (int w = 0; w < TEAM; ++w) v += gout[w * GOUT + lane];
-            A.partial[27 * c + lane] = v;
+            if (r == 0) pd0 = v;
+            else if (r == 1) pd1 = v;
+            else A.partial[27 * c + lane] = v;
           }
           if (lane == 28) {
             double su = 0.0;
@@ -644,7 +649,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
           if (lane < 27) {
             double v = 0.0;
             for (int w = 0; w < TEAM; ++w) v += gout[w * GOUT + lane];
-            v = ld(A.partial + 27 * c + lane) + v;
+            v = (r == 0 ? pd0 : (r == 1 ? pd1 : ld(A.partial + 27 * c + lane))) + v;
             A.partial[27 * c + lane] = v;
             s_col[team][lane] = v;
           }
