@@ -4,7 +4,7 @@
 //    reference has no implementation). popc(a ^ b) over 8 x 32-bit words,
 //    frame descriptors staged through shared memory, per-lane running argmin and a
 //    warp-shuffle (dist, index) argmin; ties resolve to the lowest frame index.
-//  * k_preselect_refs / k_preselect_final: matching.preselect_inliers
+//  * k_preselect_warp / k_preselect_final: matching.preselect_inliers
 //    (matching.py:174-226). One warp per reference hypothesis runs the whole
 //    rectify -> (weighted Procrustes -> residuals -> reweight) x iters alternation
 //    (matching.py:145-171); the 3x3 Procrustes uses a one-sided Jacobi SVD whose singular
@@ -142,79 +142,9 @@ int launch_hamming(const uint8_t* tdesc, int64_t nt, const uint8_t* fdesc, int64
 }
 
 // ---------------------------------------------------------------------------------
-// Weighted Procrustes rotation (matching.weighted_rotation, matching.py:108-125).
-// C is the 3x3 weighted cross-covariance sum_k w_k s2_k s1_k^T, row-major. Returns false
-// when the weighted vectors span fewer than two dimensions.
+// Weighted Procrustes rotation (matching.weighted_rotation, matching.py:108-125): see
+// procrustes_lane below (C = the 3x3 weighted cross-covariance sum_k w_k s2_k s1_k^T).
 // ---------------------------------------------------------------------------------
-
-__device__ __forceinline__ bool procrustes(const double C[9], double R[9]) {
-  double A[9], V[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-#pragma unroll
-  for (int i = 0; i < 9; ++i) A[i] = C[i];
-  const int P[3] = {0, 0, 1}, Q[3] = {1, 2, 2};
-  for (int sweep = 0; sweep < 16; ++sweep) {
-    bool rotated = false;
-#pragma unroll
-    for (int pq = 0; pq < 3; ++pq) {
-      const int p = P[pq], q = Q[pq];
-      double alpha = 0.0, beta = 0.0, gamma = 0.0;
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        alpha += A[r * 3 + p] * A[r * 3 + p];
-        beta += A[r * 3 + q] * A[r * 3 + q];
-        gamma += A[r * 3 + p] * A[r * 3 + q];
-      }
-      if (gamma != 0.0 && fabs(gamma) > 1e-16 * sqrt(alpha * beta)) {
-        rotated = true;
-        const double zeta = (beta - alpha) / (2.0 * gamma);
-        double t;
-        if (fabs(zeta) > 1e150) t = 0.5 / zeta;
-        else t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t);
-        const double sn = c * t;
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          const double ap = A[r * 3 + p], aq = A[r * 3 + q];
-          A[r * 3 + p] = c * ap - sn * aq;
-          A[r * 3 + q] = sn * ap + c * aq;
-          const double vp = V[r * 3 + p], vq = V[r * 3 + q];
-          V[r * 3 + p] = c * vp - sn * vq;
-          V[r * 3 + q] = sn * vp + c * vq;
-        }
-      }
-    }
-    if (!rotated) break;
-  }
-  double sig[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-    sig[i] = sqrt(A[0 * 3 + i] * A[0 * 3 + i] + A[1 * 3 + i] * A[1 * 3 + i] + A[2 * 3 + i] * A[2 * 3 + i]);
-  // order the singular values descending (stable)
-  int o0 = 0, o1 = 1, o2 = 2;
-  if (sig[o1] > sig[o0]) { int x = o0; o0 = o1; o1 = x; }
-  if (sig[o2] > sig[o1]) { int x = o1; o1 = o2; o2 = x; }
-  if (sig[o1] > sig[o0]) { int x = o0; o0 = o1; o1 = x; }
-  const double S0 = sig[o0], S1 = sig[o1];
-  if (!(S0 > 0.0) || S1 <= 1e-9 * S0) return false;
-  double u1[3], u2[3], v1[3], v2[3];
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    u1[r] = A[r * 3 + o0] / S0;
-    u2[r] = A[r * 3 + o1] / S1;
-    v1[r] = V[r * 3 + o0];
-    v2[r] = V[r * 3 + o1];
-  }
-  // R = U diag(1,1,sign det(U V^T)) V^T = u1 v1^T + u2 v2^T + (u1 x u2)(v1 x v2)^T
-  const double u3[3] = {u1[1] * u2[2] - u1[2] * u2[1], u1[2] * u2[0] - u1[0] * u2[2],
-                        u1[0] * u2[1] - u1[1] * u2[0]};
-  const double v3[3] = {v1[1] * v2[2] - v1[2] * v2[1], v1[2] * v2[0] - v1[0] * v2[2],
-                        v1[0] * v2[1] - v1[1] * v2[0]};
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b) R[a * 3 + b] = u1[a] * v1[b] + u2[a] * v2[b] + u3[a] * v3[b];
-  return true;
-}
 
 // residual |s2 - R s1| (matching.rotation_residuals, matching.py:128-130)
 __device__ __forceinline__ double rot_residual(const double R[9], const double s1[3], const double s2[3]) {
@@ -341,48 +271,34 @@ __device__ __forceinline__ double irls_weight(const double R[9], double a0, doub
   return s > Hsq ? H * y : 1.0;
 }
 
-// Layout: a CTA of PS_SEGS x nref threads (nref <= PS_REFS, chosen per launch so that
-// every SM gets the same number of hypotheses to within one CTA) evaluates nref
-// hypotheses; thread (seg, r) owns hypothesis r and the matches k = seg (mod PS_SEGS). Each thread keeps its
-// hypothesis' rotation in registers and runs an independent, unrolled match loop; the
-// per-segment covariances are combined in a fixed order through shared memory and the
-// PS_REFS SVDs run at once on the lanes of warp 0.
-constexpr int PS_REFS = 8;
-constexpr int PS_SEGS = 32;
-constexpr int PS_THREADS = PS_REFS * PS_SEGS;
-
-__global__ void __launch_bounds__(PS_THREADS, 2)
-k_preselect_refs(const double* __restrict__ src, const double* __restrict__ dst,
+// One warp per reference hypothesis: lane l owns
+// the matches k = l (mod 32); the per-lane covariances are combined by a 5-level xor
+// butterfly (bitwise-identical on every lane) and all 32 lanes run the 3x3 SVD
+// redundantly -- no shared memory and no CTA barrier, so warps drift apart and one
+// warp's SVD overlaps the other warps' match loops.
+__global__ void __launch_bounds__(256, 2)
+k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
                  const int64_t* __restrict__ n_dev, int64_t n_fixed,
                  const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive, double H,
                  int iters, double min_support, double* __restrict__ ref_support,
-                 double* __restrict__ ref_rot, uint8_t* __restrict__ ref_valid, int nref) {
-  __shared__ double s_C[PS_SEGS][PS_REFS][9];
-  __shared__ double s_R[PS_REFS][9];
-  __shared__ int s_live[PS_REFS];
-  const int tid = threadIdx.x;
-  const int r = tid % nref;
-  const int seg = tid / nref;
+                 double* __restrict__ ref_rot, uint8_t* __restrict__ ref_valid) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t n = n_dev ? *n_dev : n_fixed;
   const int64_t nr = exhaustive ? n : n_refs;
-  const int64_t w = (int64_t)blockIdx.x * nref + r;
-  if ((int64_t)blockIdx.x * nref >= nr) return;  // CTA-uniform
-  int64_t ref = -1;
-  if (w < nr) ref = exhaustive ? w : refs[w];
+  if (w >= nr) return;  // warp-uniform
+  const int64_t ref = exhaustive ? w : refs[w];
   bool live = n >= 3 && ref >= 0 && ref < n;
   const int64_t rr = live ? ref : 0;
-  double rs0 = 0, rs1 = 0, rs2 = 0, rd0 = 0, rd1 = 0, rd2 = 0;
-  if (n > 0) {
-    rs0 = __ldg(src + 3 * rr); rs1 = __ldg(src + 3 * rr + 1); rs2 = __ldg(src + 3 * rr + 2);
-    rd0 = __ldg(dst + 3 * rr); rd1 = __ldg(dst + 3 * rr + 1); rd2 = __ldg(dst + 3 * rr + 2);
-  }
+  const double rs0 = __ldg(src + 3 * rr), rs1 = __ldg(src + 3 * rr + 1), rs2 = __ldg(src + 3 * rr + 2);
+  const double rd0 = __ldg(dst + 3 * rr), rd1 = __ldg(dst + 3 * rr + 1), rd2 = __ldg(dst + 3 * rr + 2);
   const double Hsq = H * H;
   double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-  double Vm[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};  // used by warp 0 only
+  double V[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
   for (int it = 0; it < iters; ++it) {
     double C[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll 4
-    for (int64_t k = seg; k < n; k += PS_SEGS) {
+    for (int64_t k = lane; k < n; k += 32) {
       const double a0 = __ldg(src + 3 * k) - rs0, a1 = __ldg(src + 3 * k + 1) - rs1,
                    a2 = __ldg(src + 3 * k + 2) - rs2;
       const double b0 = __ldg(dst + 3 * k) - rd0, b1 = __ldg(dst + 3 * k + 1) - rd1,
@@ -400,48 +316,29 @@ k_preselect_refs(const double* __restrict__ src, const double* __restrict__ dst,
       C[8] = __fma_rn(c2, a2, C[8]);
     }
 #pragma unroll
-    for (int i = 0; i < 9; ++i) s_C[seg][r][i] = C[i];
-    __syncthreads();
-    if (tid < 32) {
-      // lane r (and its duplicates r + 8, r + 16, r + 24) combines hypothesis r in
-      // segment order
-      double Cr[9];
+    for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
-      for (int i = 0; i < 9; ++i) {
-        double acc = 0.0;
-        for (int g = 0; g < PS_SEGS; ++g) acc += s_C[g][r][i];
-        Cr[i] = acc;
-      }
-      double Rm[9];
-      const bool ok = procrustes_lane(Cr, Vm, Rm);
-      if (tid < nref) {
-#pragma unroll
-        for (int i = 0; i < 9; ++i) s_R[r][i] = Rm[i];
-        s_live[r] = ok ? 1 : 0;
-      }
-    }
-    __syncthreads();
-    if (!s_live[r]) live = false;
+      for (int i = 0; i < 9; ++i) C[i] += __shfl_xor_sync(0xffffffffu, C[i], o);
+    double Rm[9];
+    const bool ok = procrustes_lane(C, V, Rm);
+    if (!ok) live = false;
     if (live) {
 #pragma unroll
-      for (int i = 0; i < 9; ++i) R[i] = s_R[r][i];
+      for (int i = 0; i < 9; ++i) R[i] = Rm[i];
     }
-    __syncthreads();
   }
   double sup = 0.0;
 #pragma unroll 4
-  for (int64_t k = seg; k < n; k += PS_SEGS)
+  for (int64_t k = lane; k < n; k += 32)
     sup += irls_weight(R, __ldg(src + 3 * k) - rs0, __ldg(src + 3 * k + 1) - rs1,
                        __ldg(src + 3 * k + 2) - rs2, __ldg(dst + 3 * k) - rd0,
                        __ldg(dst + 3 * k + 1) - rd1, __ldg(dst + 3 * k + 2) - rd2, H, Hsq);
-  s_C[seg][r][0] = sup;
-  __syncthreads();
-  if (tid < nref && w < nr) {
-    double s = 0.0;
-    for (int g = 0; g < PS_SEGS; ++g) s += s_C[g][r][0];
-    const bool ok = live && !(s < min_support * (double)n);
-    ref_valid[w] = ok ? 1 : 0;
-    ref_support[w] = ok ? s : 0.0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) sup += __shfl_xor_sync(0xffffffffu, sup, o);
+  if (lane == 0) {
+    const bool good = live && !(sup < min_support * (double)n);
+    ref_valid[w] = good ? 1 : 0;
+    ref_support[w] = good ? sup : 0.0;
 #pragma unroll
     for (int i = 0; i < 9; ++i) ref_rot[9 * w + i] = R[i];
   }
@@ -543,20 +440,10 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
                      double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s) {
   const int64_t nr = exhaustive ? n_max : n_refs;
   if (nr > 0) {
-    static int sms = 0;
-    if (sms == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (sms <= 0) sms = 148;
-    }
-    // two co-resident CTAs per SM: nref hypotheses per CTA so that the grid covers the
-    // hypotheses in one wave with every SM holding the same count to within one CTA
-    const int64_t per = (nr + 2 * sms - 1) / (2 * sms);
-    const int nref = (int)std::max<int64_t>(1, std::min<int64_t>(PS_REFS, per));
-    k_preselect_refs<<<(unsigned)((nr + nref - 1) / nref), nref * PS_SEGS, 0, s>>>(
+    // one warp per hypothesis, 8 per CTA: one wave on 148 SMs x 2 CTAs for n <= 2,368
+    k_preselect_warp<<<(unsigned)((nr + 7) / 8), 256, 0, s>>>(
         src, dst, n_dev, n_max, refs, n_refs, exhaustive, H, iters, min_support, ref_support,
-        ref_rot, ref_valid, nref);
+        ref_rot, ref_valid);
     DT_CHECK_LAUNCH();
   }
   k_preselect_final<<<1, 512, 0, s>>>(src, dst, n_dev, n_max, refs, n_refs, exhaustive, H,

@@ -3,7 +3,7 @@
 // Per frame (tracking.track_frame, tracking.py:67-95):
 //   depth -> normals + validity            k_observation_normals   (correspond.py:36-73)
 //   [ORB] Hamming match + back-projection  k_hamming, k_build_matches (north-star 3a)
-//   preselection                           k_preselect_refs/final  (matching.py:174-226)
+//   preselection                           k_preselect_warp/final  (matching.py:174-226)
 //   active matches, binding, control CSR   k_active, k_csr_*_dev   (solver.py:113-119, 292-296)
 //   LM solve                               k_solve_frame (cluster) (solver.py:267-378)
 //   output warp                            k_warp_all              (warpfield.py:236-250)
