@@ -487,7 +487,7 @@ def cpu_baseline(wl, n_frames):
 # REF_MAX_WARMUP warm-up frames whatever --steps / --warmup ask for (each step is one
 # full frame; the sample is stated in the JSON line).
 REF_MAX_FRAMES = 40
-REF_MAX_WARMUP = 1
+REF_MAX_WARMUP = 3
 
 
 def run_reference(args, rank, world):

@@ -101,7 +101,7 @@ constexpr int BM_PER = 4;
 __global__ void __launch_bounds__(1024)
 k_build_matches(int64_t nt, const unsigned long long* __restrict__ packed,
                 int max_ham, const int32_t* __restrict__ kp, int64_t nf,
-                const double* __restrict__ depth, const uint8_t* __restrict__ dvalid, int width,
+                const double* __restrict__ depth, double zmin, double zmax, int width,
                 int height, double fx, double fy, double cx, double cy,
                 const double* __restrict__ tpts, double* __restrict__ src,
                 double* __restrict__ dst, int32_t* __restrict__ feat_id, int64_t* __restrict__ n_out) {
@@ -128,11 +128,19 @@ k_build_matches(int64_t nt, const unsigned long long* __restrict__ packed,
         v[e] = kp[2 * fi[e] + 1];
       }
     }
+    // the depth-validity test of the observation (correspond.valid_depth_mask,
+    // correspond.py:23-26) evaluated here from the depth itself: the matching chain has
+    // no dependency on the observation-normals kernel
+    double z[BM_PER];
+#pragma unroll
+    for (int e = 0; e < BM_PER; ++e) {
+      ok[e] = u[e] >= 0 && u[e] < width && v[e] >= 0 && v[e] < height;
+      z[e] = ok[e] ? depth[(int64_t)v[e] * width + u[e]] : 0.0;
+    }
     int cnt = 0;
 #pragma unroll
     for (int e = 0; e < BM_PER; ++e) {
-      ok[e] = u[e] >= 0 && u[e] < width && v[e] >= 0 && v[e] < height &&
-              dvalid[(int64_t)v[e] * width + u[e]];
+      ok[e] = ok[e] && isfinite(z[e]) && z[e] > zmin && z[e] < zmax;
       cnt += ok[e] ? 1 : 0;
     }
     int total;
@@ -141,7 +149,7 @@ k_build_matches(int64_t nt, const unsigned long long* __restrict__ packed,
     for (int e = 0; e < BM_PER; ++e) {
       if (!ok[e]) continue;
       const int64_t t = t0 + e;
-      const double d = depth[(int64_t)v[e] * width + u[e]];
+      const double d = z[e];
       src[3 * o] = tpts[3 * t];
       src[3 * o + 1] = tpts[3 * t + 1];
       src[3 * o + 2] = tpts[3 * t + 2];
@@ -430,6 +438,7 @@ struct dt_tracker {
   cudaEvent_t ev_in_ready[2] = {nullptr, nullptr}, ev_in_free[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_out_copied[2] = {nullptr, nullptr};
   cudaEvent_t pre_solver_wait = nullptr;  // compute stream waits on it before the solver
+  bool own_stream = false;  // created by dt_tracker_create (destroyed with the tracker)
   double* in_depth[2] = {nullptr, nullptr};
   uint8_t* in_desc[2] = {nullptr, nullptr};
   int32_t* in_kp[2] = {nullptr, nullptr};
@@ -705,7 +714,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
                                 cudaMemcpyDeviceToDevice, s));
   if (in->depth != t->depth)
     DT_CHECK_CUDA(cudaMemcpyAsync(t->depth, in->depth, sizeof(double) * npix, kind, s));
-  if (in->normals) {
+    if (in->normals) {
     DT_CHECK_CUDA(cudaMemcpyAsync(t->onrm, in->normals, sizeof(double) * 3 * npix, kind, s));
     k_valid_mask<<<grid_for(npix, 256), 256, 0, s>>>(t->depth, npix, c.z_min, c.z_max, t->dvalid);
     DT_CHECK_LAUNCH();
@@ -734,7 +743,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     DT_TRY(launch_hamming(t->tdesc, t->n_feat, t->fdesc, in->n_frame, nullptr, nullptr, s,
                           t->ham_packed));
     k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_packed, c.max_hamming, t->fkp,
-                                       in->n_frame, t->depth, t->dvalid, c.width, c.height, c.fx,
+                                       in->n_frame, t->depth, c.z_min, c.z_max, c.width, c.height, c.fx,
                                        c.fy, c.cx, c.cy, t->tfeat_pts, t->m_src, t->m_dst, t->m_feat,
                                        t->info + 2);
     DT_CHECK_LAUNCH();
@@ -983,8 +992,12 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
   t->k = k;
   t->m = m;
   t->ne = n_edges;
-  if (stream) t->stream = as_stream(stream);
-  else DT_CHECK_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+  if (stream) {
+    t->stream = as_stream(stream);
+  } else {
+    DT_CHECK_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+    t->own_stream = true;
+  }
   const int64_t npix = (int64_t)cfg->width * cfg->height;
   // static data
   std::vector<int32_t> bidx32(n * k), edges32(2 * n_edges);
@@ -1128,6 +1141,7 @@ int dt_tracker_destroy(dt_tracker* t) {
   }
   for (auto& e : t->ev)
     if (e) cudaEventDestroy(e);
+  if (t->own_stream) cudaStreamDestroy(t->stream);
   for (auto& b : t->bufs) cudaFree(b.p);
   if (t->h_report) cudaFreeHost(t->h_report);
   if (t->h_info) cudaFreeHost(t->h_info);
