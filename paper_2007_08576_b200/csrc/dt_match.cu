@@ -259,16 +259,108 @@ __device__ __forceinline__ double irls_weight(const double R[9], double a0, doub
   const double e2 = __fma_rn(-R[6], a0, __fma_rn(-R[7], a1, __fma_rn(-R[8], a2, b2)));
   const double s = __fma_rn(e2, e2, __fma_rn(e1, e1, e0 * e0));
   // 1/sqrt(s) for s > H^2: the MUFU double-precision estimate refined by two Newton
-  // steps (~1 ulp; the full-precision rsqrt(double) carries special-case branches, and
-  // the weight is only needed where s > H^2 > 0)
-  const double sc = fmax(s, Hsq);
+  // steps (~1 ulp; the full-precision rsqrt(double) carries special-case branches). For
+  // s <= H^2 the value is discarded (s = 0 gives NaN there, never selected).
   double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(sc));
-  const double hs = 0.5 * sc;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+  const double hs = 0.5 * s;
   // y <- y + y (0.5 - hs y^2), fused
   y = __fma_rn(y, __fma_rn(-hs * y, y, 0.5), y);
   y = __fma_rn(y, __fma_rn(-hs * y, y, 0.5), y);
-  return s > Hsq ? H * y : 1.0;
+  // s > H^2 on the bit patterns (both >= +0, so the integer order is the IEEE order) on
+  // the integer pipe instead of the FP64 one; a NaN residual keeps weight 1 like the
+  // reference's `d > threshold` test
+  const long long sb = __double_as_longlong(s);
+  const bool far = sb > __double_as_longlong(Hsq) && sb <= 0x7ff0000000000000ll;
+  return far ? H * y : 1.0;
+}
+
+// One lane's share of a covariance pass: C += sum_k w_k b_k a_k^T over k = lane (mod 32)
+// in increasing k (w = 1 in the first IRLS step). Four matches per trip are loaded and
+// weighted as independent chains before being folded into C in order, so the result is
+// the same as the one-match-at-a-time loop while the chains overlap.
+template <bool WEIGHTED>
+__device__ __forceinline__ void cov_pass(const double* __restrict__ src,
+                                         const double* __restrict__ dst, int64_t n, int lane,
+                                         double rs0, double rs1, double rs2, double rd0,
+                                         double rd1, double rd2, const double R[9], double H,
+                                         double Hsq, double C[9]) {
+  int64_t k = lane;
+  for (; k + 96 < n; k += 128) {
+    double a[4][3], b[4][3], w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double* ps = src + 3 * (k + 32 * u);
+      const double* pd = dst + 3 * (k + 32 * u);
+      a[u][0] = __ldg(ps) - rs0;
+      a[u][1] = __ldg(ps + 1) - rs1;
+      a[u][2] = __ldg(ps + 2) - rs2;
+      b[u][0] = __ldg(pd) - rd0;
+      b[u][1] = __ldg(pd + 1) - rd1;
+      b[u][2] = __ldg(pd + 2) - rd2;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      w[u] = WEIGHTED ? irls_weight(R, a[u][0], a[u][1], a[u][2], b[u][0], b[u][1], b[u][2], H, Hsq)
+                      : 1.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double c0 = b[u][0] * w[u], c1 = b[u][1] * w[u], c2 = b[u][2] * w[u];
+      C[0] = __fma_rn(c0, a[u][0], C[0]);
+      C[1] = __fma_rn(c0, a[u][1], C[1]);
+      C[2] = __fma_rn(c0, a[u][2], C[2]);
+      C[3] = __fma_rn(c1, a[u][0], C[3]);
+      C[4] = __fma_rn(c1, a[u][1], C[4]);
+      C[5] = __fma_rn(c1, a[u][2], C[5]);
+      C[6] = __fma_rn(c2, a[u][0], C[6]);
+      C[7] = __fma_rn(c2, a[u][1], C[7]);
+      C[8] = __fma_rn(c2, a[u][2], C[8]);
+    }
+  }
+  for (; k < n; k += 32) {
+    const double a0 = __ldg(src + 3 * k) - rs0, a1 = __ldg(src + 3 * k + 1) - rs1,
+                 a2 = __ldg(src + 3 * k + 2) - rs2;
+    const double b0 = __ldg(dst + 3 * k) - rd0, b1 = __ldg(dst + 3 * k + 1) - rd1,
+                 b2 = __ldg(dst + 3 * k + 2) - rd2;
+    const double wk = WEIGHTED ? irls_weight(R, a0, a1, a2, b0, b1, b2, H, Hsq) : 1.0;
+    const double c0 = b0 * wk, c1 = b1 * wk, c2 = b2 * wk;
+    C[0] = __fma_rn(c0, a0, C[0]);
+    C[1] = __fma_rn(c0, a1, C[1]);
+    C[2] = __fma_rn(c0, a2, C[2]);
+    C[3] = __fma_rn(c1, a0, C[3]);
+    C[4] = __fma_rn(c1, a1, C[4]);
+    C[5] = __fma_rn(c1, a2, C[5]);
+    C[6] = __fma_rn(c2, a0, C[6]);
+    C[7] = __fma_rn(c2, a1, C[7]);
+    C[8] = __fma_rn(c2, a2, C[8]);
+  }
+}
+
+// Support of one lane's matches (sum of IRLS weights in increasing k), same trip shape.
+__device__ __forceinline__ double support_pass(const double* __restrict__ src,
+                                               const double* __restrict__ dst, int64_t n,
+                                               int lane, double rs0, double rs1, double rs2,
+                                               double rd0, double rd1, double rd2,
+                                               const double R[9], double H, double Hsq) {
+  double sup = 0.0;
+  int64_t k = lane;
+  for (; k + 96 < n; k += 128) {
+    double w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double* ps = src + 3 * (k + 32 * u);
+      const double* pd = dst + 3 * (k + 32 * u);
+      w[u] = irls_weight(R, __ldg(ps) - rs0, __ldg(ps + 1) - rs1, __ldg(ps + 2) - rs2,
+                         __ldg(pd) - rd0, __ldg(pd + 1) - rd1, __ldg(pd + 2) - rd2, H, Hsq);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sup += w[u];
+  }
+  for (; k < n; k += 32)
+    sup += irls_weight(R, __ldg(src + 3 * k) - rs0, __ldg(src + 3 * k + 1) - rs1,
+                       __ldg(src + 3 * k + 2) - rs2, __ldg(dst + 3 * k) - rd0,
+                       __ldg(dst + 3 * k + 1) - rd1, __ldg(dst + 3 * k + 2) - rd2, H, Hsq);
+  return sup;
 }
 
 // One warp per reference hypothesis: lane l owns
@@ -276,7 +368,7 @@ __device__ __forceinline__ double irls_weight(const double R[9], double a0, doub
 // butterfly (bitwise-identical on every lane) and all 32 lanes run the 3x3 SVD
 // redundantly -- no shared memory and no CTA barrier, so warps drift apart and one
 // warp's SVD overlaps the other warps' match loops.
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(512, 1)
 k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
                  const int64_t* __restrict__ n_dev, int64_t n_fixed,
                  const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive, double H,
@@ -297,24 +389,10 @@ k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
   double V[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
   for (int it = 0; it < iters; ++it) {
     double C[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 4
-    for (int64_t k = lane; k < n; k += 32) {
-      const double a0 = __ldg(src + 3 * k) - rs0, a1 = __ldg(src + 3 * k + 1) - rs1,
-                   a2 = __ldg(src + 3 * k + 2) - rs2;
-      const double b0 = __ldg(dst + 3 * k) - rd0, b1 = __ldg(dst + 3 * k + 1) - rd1,
-                   b2 = __ldg(dst + 3 * k + 2) - rd2;
-      const double wk = it == 0 ? 1.0 : irls_weight(R, a0, a1, a2, b0, b1, b2, H, Hsq);
-      const double c0 = b0 * wk, c1 = b1 * wk, c2 = b2 * wk;
-      C[0] = __fma_rn(c0, a0, C[0]);
-      C[1] = __fma_rn(c0, a1, C[1]);
-      C[2] = __fma_rn(c0, a2, C[2]);
-      C[3] = __fma_rn(c1, a0, C[3]);
-      C[4] = __fma_rn(c1, a1, C[4]);
-      C[5] = __fma_rn(c1, a2, C[5]);
-      C[6] = __fma_rn(c2, a0, C[6]);
-      C[7] = __fma_rn(c2, a1, C[7]);
-      C[8] = __fma_rn(c2, a2, C[8]);
-    }
+    if (it == 0)
+      cov_pass<false>(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq, C);
+    else
+      cov_pass<true>(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq, C);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
@@ -327,12 +405,7 @@ k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
       for (int i = 0; i < 9; ++i) R[i] = Rm[i];
     }
   }
-  double sup = 0.0;
-#pragma unroll 4
-  for (int64_t k = lane; k < n; k += 32)
-    sup += irls_weight(R, __ldg(src + 3 * k) - rs0, __ldg(src + 3 * k + 1) - rs1,
-                       __ldg(src + 3 * k + 2) - rs2, __ldg(dst + 3 * k) - rd0,
-                       __ldg(dst + 3 * k + 1) - rd1, __ldg(dst + 3 * k + 2) - rd2, H, Hsq);
+  double sup = support_pass(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq);
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) sup += __shfl_xor_sync(0xffffffffu, sup, o);
   if (lane == 0) {
@@ -440,10 +513,20 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
                      double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s) {
   const int64_t nr = exhaustive ? n_max : n_refs;
   if (nr > 0) {
-    // one warp per hypothesis, 8 per CTA: one wave on 148 SMs x 2 CTAs for n <= 2,368
-    // (1-, 2- and 4-warp CTAs measured no faster: the kernel is bound by each warp's own
-    // dependent chain, not by the per-SM balance of a 250-CTA grid)
-    k_preselect_warp<<<(unsigned)((nr + 7) / 8), 256, 0, s>>>(
+    // One warp per hypothesis. The busiest SM sets the time (FP64 pipe ~76 % busy there),
+    // so the warps are spread evenly: one CTA of ceil(nr / SMs) warps per SM (<= 16, the
+    // register limit), e.g. 2,000 hypotheses -> 143 CTAs x 14 warps instead of 8-warp CTAs
+    // that leave 102 SMs with 16 warps and 46 with 8. The block scheduler's greedy fill
+    // defeats smaller CTAs.
+    static int sms = 0;
+    if (sms == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+    }
+    const int64_t wpc = std::min<int64_t>(16, std::max<int64_t>(1, (nr + sms - 1) / sms));
+    k_preselect_warp<<<(unsigned)((nr + wpc - 1) / wpc), (unsigned)(32 * wpc), 0, s>>>(
         src, dst, n_dev, n_max, refs, n_refs, exhaustive, H, iters, min_support, ref_support,
         ref_rot, ref_valid);
     DT_CHECK_LAUNCH();
