@@ -250,7 +250,10 @@ __device__ __forceinline__ void edge_unit_rows(const SolverArgs& A, const double
   const double bx = p1t[0] - p0t[0], by = p1t[1] - p0t[1], bz = p1t[2] - p0t[2];
   const double ln2 = bx * bx + by * by + bz * bz;
   const double iln = rsqrt_nr(fmax(ln2, 1e-300));
-  const double ln = ln2 * iln;  // |b| to an ulp
+  // |b| correctly rounded like `rest`, so an undeformed connection has a length residual
+  // of exactly 0 as in the reference (an ulp-level |b| would leave ~1e-26 of rigidity
+  // cost at rest and let the LM accept noise steps where the reference stalls)
+  const double ln = sqrt(ln2);
   double bhx = 0.0, bhy = 0.0, bhz = 0.0;
   if (ln > 1e-9) {
     bhx = bx * iln;

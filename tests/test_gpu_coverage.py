@@ -179,3 +179,61 @@ def test_hard_regimes_match_oracle(cid, over):
     assert float(np.abs(res.points - opts).max()) < VERTEX_TOL_MM
     assert res.report.n_correspondences == ores.n_correspondences
     assert res.report.accepted_steps == ores.accepted_steps
+
+
+def test_frame_without_valid_depth_matches_oracle():
+    """A frame whose depth is entirely invalid (0 < z_min): no ICP correspondences and no
+    ORB match lands on valid depth, so the solve is rigidity-only (reference: empty
+    CorrespondenceSet, solver.py:113-119) -- counts and vertices as the oracle's."""
+    from paper_2007_08576_b200 import synth
+
+    scene, spec = _scene(1)
+    dt, cfg, cam, tpl0, feats, tpl, graph = _setup(scene, spec["radius"], spec["iters"])
+    fr = synth.make_frame(scene, cam, tpl0, feats, 2)
+    fr = replace(fr, depth=np.zeros_like(fr.depth))
+    trk = dt.Tracker(tpl, graph, cam, cfg)
+    trk.set_features(feats.descriptors, feats.points)
+    trk.set_exhaustive(True)
+    res = trk.track(fr.depth, descriptors=fr.descriptors, keypoints=fr.keypoints)
+    trk.close()
+    ores, osel, opts, _ = _oracle_frame(tpl, graph, graph.warps, fr, feats, cam, spec["iters"])
+    assert res.report.n_correspondences == ores.n_correspondences == 0
+    assert res.report.n_matches == 0
+    # zero energy at rest: every step is rejected and every iteration stalls, as in the
+    # reference (an ulp of residual noise here would turn into accepted noise steps)
+    assert res.report.accepted_steps == ores.accepted_steps
+    assert res.report.rejected_steps == ores.rejected_steps
+    assert bool(res.report.stalled) == bool(ores.stalled)
+    assert float(np.abs(res.points - opts).max()) < VERTEX_TOL_MM
+
+
+def test_too_few_matches_is_no_valid_hypothesis():
+    """Two template features -> at most two matches: preselection reports
+    NoValidHypothesis (matching.py:181-182), the frame is tracked on depth alone."""
+    from paper_2007_08576_b200 import synth
+
+    scene, spec = _scene(1)
+    dt, cfg, cam, tpl0, feats, tpl, graph = _setup(scene, spec["radius"], spec["iters"])
+    fr = synth.make_frame(scene, cam, tpl0, feats, 2)
+    trk = dt.Tracker(tpl, graph, cam, cfg)
+    trk.set_features(feats.descriptors[:2], feats.points[:2])
+    trk.set_exhaustive(True)
+    res = trk.track(fr.depth, descriptors=fr.descriptors, keypoints=fr.keypoints)
+    trk.close()
+    assert res.report.n_matches <= 2
+    assert res.report.n_preselected == 0
+    assert not np.any(res.matches.preselected)
+    if res.report.n_matches:
+        assert any("preselection failed" in w for w in res.report.warnings)
+    # the oracle's depth-only solve from the same warm start
+    from oracle import pipeline as OP
+
+    camt = (cam.fx, cam.fy, cam.cx, cam.cy)
+    tplt = (tpl.points, tpl.normals, tpl.bind_indices, tpl.bind_weights)
+    grt = (graph.points, graph.edges, graph.edge_weights)
+    s = OP.Schedule(max_outer_iters=spec["iters"], step_tol=0.0, cost_tol=0.0)
+    ores, _, opts, _ = OP.track(tplt, grt, graph.warps, fr.depth,
+                                OP.observation_normals(fr.depth, *camt), camt, None,
+                                OP.Weights(), s, graph.sampling_radius)
+    assert res.report.n_correspondences == ores.n_correspondences
+    assert float(np.abs(res.points - opts).max()) < VERTEX_TOL_MM
