@@ -38,7 +38,7 @@ def solver_case(name: str):
 
 
 SOLVER_CASES = ["solver_fixed_point", "solver_translation", "solver_rigid_matches",
-                "solver_occluded"]
+                "solver_occluded", "solver_no_data", "solver_no_data_stall"]
 
 
 def hamming_kat_descriptors(seed: int = 0, nt: int = 40, nf: int = 70):

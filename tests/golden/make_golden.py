@@ -222,6 +222,22 @@ def make_solver_cases():
     cfg = SolverConfig()
     out, rep = solve_frame(tpl, graph, Observation.from_depth(depth, cam), None, w, cfg)
     pack_case("solver_occluded", cam, tpl, graph, depth, None, w, cfg, out.warps, rep)
+    make_no_data_cases()
+
+
+def make_no_data_cases():
+    """No valid depth from the rest pose (test_solver.py:209-218): zero energy, so with the
+    default tolerances the solve converges at once, and with tolerances 0 every step is
+    rejected and every iteration stalls."""
+    w = EnergyWeights()
+    cam, tpl, graph, _, _ = plane_scene()
+    depth = np.zeros((cam.height, cam.width))
+    cfg = SolverConfig()
+    out, rep = solve_frame(tpl, graph, Observation.from_depth(depth, cam), None, w, cfg)
+    pack_case("solver_no_data", cam, tpl, graph, depth, None, w, cfg, out.warps, rep)
+    cfg = SolverConfig(max_outer_iters=5, step_tol=0.0, cost_tol=0.0)
+    out, rep = solve_frame(tpl, graph, Observation.from_depth(depth, cam), None, w, cfg)
+    pack_case("solver_no_data_stall", cam, tpl, graph, depth, None, w, cfg, out.warps, rep)
 
 
 def rigid_matches(n, outlier_fraction, seed, angle_deg=15.0, translation=10.0, box=100.0):
