@@ -196,6 +196,73 @@ def test_preselect_matches_reference():
         assert abs(res.support - float(z[f"c{i}_support"])) <= 1e-9 * len(z[f"c{i}_src"])
 
 
+def _rigid_matches(n, outlier_fraction, seed, grid=None, angle_deg=15.0, translation=10.0,
+                   box=100.0):
+    """The reference's matching fixture shape (test_matching.py:17-47): a rigid motion of
+    uniform points plus uniform outliers, optionally snapped to a dyadic grid."""
+    rng = np.random.default_rng(seed)
+    axis = rng.normal(size=3)
+    axis /= np.linalg.norm(axis)
+    th = np.deg2rad(angle_deg)
+    K = np.array([[0, -axis[2], axis[1]], [axis[2], 0, -axis[0]], [-axis[1], axis[0], 0]])
+    R = np.eye(3) + np.sin(th) * K + (1 - np.cos(th)) * K @ K
+    t = rng.normal(size=3)
+    t *= translation / np.linalg.norm(t)
+    src = rng.uniform(-box / 2.0, box / 2.0, (n, 3))
+    dst = src @ R.T + t
+    n_out = round(n * outlier_fraction)
+    out_idx = rng.choice(n, size=n_out, replace=False)
+    dst[out_idx] = rng.uniform(-box / 2.0, box / 2.0, (n_out, 3))
+    if grid is not None:
+        src = np.round(src / grid) * grid
+        dst = np.round(dst / grid) * grid
+    inlier = np.ones(n, dtype=bool)
+    inlier[out_idx] = False
+    return src, dst, inlier
+
+
+def test_preselect_all_outliers_raises():
+    """Pure noise: every hypothesis falls below the support floor (test_matching.py:246-254)."""
+    from paper_2007_08576_b200.exceptions import NoValidHypothesis
+    from paper_2007_08576_b200.matching import MatchSet, PreselectConfig, preselect_inliers
+
+    rng = np.random.default_rng(14)
+    src = rng.uniform(-500.0, 500.0, (50, 3))
+    dst = rng.uniform(-500.0, 500.0, (50, 3))
+    with pytest.raises(NoValidHypothesis):
+        preselect_inliers(MatchSet.from_pairs(src, dst), PreselectConfig(seed=0))
+
+
+def test_preselect_translation_invariance_bitwise_on_grid():
+    """Shifting the observed points by a grid-exact vector changes no bit of the result
+    (test_matching.py:209-223): rectification cancels the shift exactly."""
+    from paper_2007_08576_b200.matching import MatchSet, PreselectConfig, preselect_inliers
+
+    grid = 1.0 / 1024.0
+    src, dst, _ = _rigid_matches(64, 0.3, seed=11, grid=grid)
+    shift = np.array([32.0 + 5.0 * grid, -640.0 * grid, 12.25])
+    cfg = PreselectConfig(seed=3)
+    a = preselect_inliers(MatchSet.from_pairs(src, dst), cfg)
+    b = preselect_inliers(MatchSet.from_pairs(src, dst + shift), cfg)
+    assert a.reference_index == b.reference_index
+    np.testing.assert_array_equal(a.matches.weights, b.matches.weights)
+    np.testing.assert_array_equal(a.matches.preselected, b.matches.preselected)
+    np.testing.assert_array_equal(a.rotation, b.rotation)
+    np.testing.assert_array_equal(a.residuals, b.residuals)
+
+
+def test_preselect_small_sets_use_every_reference():
+    """Below n_references the search is exhaustive, so the seed is irrelevant
+    (test_matching.py:200-206); every true inlier is flagged."""
+    from paper_2007_08576_b200.matching import MatchSet, PreselectConfig, preselect_inliers
+
+    src, dst, inlier = _rigid_matches(12, 0.25, seed=10)
+    a = preselect_inliers(MatchSet.from_pairs(src, dst), PreselectConfig(seed=0))
+    b = preselect_inliers(MatchSet.from_pairs(src, dst), PreselectConfig(seed=999))
+    np.testing.assert_array_equal(a.matches.weights, b.matches.weights)
+    assert a.matches.preselected[inlier].all()
+
+
 def test_preselect_degenerate_and_too_few():
     from paper_2007_08576_b200.exceptions import NoValidHypothesis
     from paper_2007_08576_b200.matching import MatchSet, PreselectConfig, preselect_inliers
