@@ -62,6 +62,34 @@ __device__ __forceinline__ int ldi(const int* p) { return __ldca(p); }
 // data published by other CTAs WITHIN the phase (last-arriver reductions): L2 only
 __device__ __forceinline__ double ldl2(const double* p) { return __ldcg(p); }
 
+// Bulk (non-tensor TMA) global -> shared copies completing on an mbarrier: one thread
+// streams a whole per-control table into shared memory while the others go on.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -148,11 +176,15 @@ struct Dom<true> {
 // ---------------------------------------------------------------------------------
 
 __device__ __forceinline__ void load_state(const SolverArgs& A, const double* src, double* s_w,
-                                           double* s_T) {
-  const int n8 = 8 * A.m;
+                                           double* s_T, uint64_t* bar, uint32_t& phase) {
   __syncthreads();
-  for (int i = threadIdx.x; i < n8; i += blockDim.x) s_w[i] = ld(src + i);
-  __syncthreads();
+  if (threadIdx.x == 0) {  // the warps (8m doubles) by one bulk copy
+    asm volatile("fence.proxy.async;" ::: "memory");
+    mbar_expect_tx(bar, (uint32_t)(64 * A.m));
+    bulk_g2s(s_w, src, (uint32_t)(64 * A.m), bar);
+  }
+  mbar_wait(bar, phase);
+  phase ^= 1;
   for (int c = threadIdx.x; c < A.m; c += blockDim.x)
     dq_to_transform_fast(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
   __syncthreads();

@@ -437,9 +437,15 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   __shared__ double s_sup[NWARPS];
   __shared__ double s_col[TEAMS_PER_CTA][32];
   __shared__ int s_cnt[NWARPS];
-  extern __shared__ double smem[];
-  if (threadIdx.x == 0) A = all[dom.seq()];
+  extern __shared__ __align__(128) double smem[];
+  __shared__ uint64_t s_bar;  // completion of the bulk tentative-state loads
+  if (threadIdx.x == 0) {
+    A = all[dom.seq()];
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
+  uint32_t bar_phase = 0;
   const int m = A.m;
   const int64_t n = A.n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -486,7 +492,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
 
   // ---- P1: relink + linearize at the warm start (buffer 0): points, matches, unit
   // rigidity rows of the connections ----
-  load_state(A, cur, s_w, s_T);
+  load_state(A, cur, s_w, s_T, &s_bar, bar_phase);
   TRACE(12);
   {
     const PBuf nb = pbuf(A, 0);
@@ -710,30 +716,20 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
       // linearization also the rigidity cost of the iterate) -- identical in every CTA.
       const bool want_e = attempt == 0 && need_lin;
       const int pc = threadIdx.x;
+      if (threadIdx.x == 0) {
+        // tentative warps (8m) and transforms (12m) -> s_w / s_T by two bulk copies; the
+        // proxy fence orders this CTA's earlier generic shared-memory accesses (and the
+        // barrier-acquired global writes) before the async-proxy copies
+        asm volatile("fence.proxy.async;" ::: "memory");
+        mbar_expect_tx(&s_bar, (uint32_t)(160 * m));
+        bulk_g2s(s_w, tent, (uint32_t)(64 * m), &s_bar);
+        bulk_g2s(s_T, A.tentT, (uint32_t)(96 * m), &s_bar);
+      }
       double o_ok = 1.0, o_nm = 0.0, o_ar = 0.0;
       if (pc < m) {
         o_ok = ld(okn + pc);
         o_nm = ld(okn + m + pc);
         if (want_e) o_ar = ld(okn + 2 * m + pc);
-      }
-      for (int c = pc; c < m; c += blockDim.x) {
-        const double2* t2 = reinterpret_cast<const double2*>(tent + 8 * c);
-        const double2* T2 = reinterpret_cast<const double2*>(A.tentT + 12 * c);
-        double2 w[4], T[6];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) w[i] = __ldca(t2 + i);
-#pragma unroll
-        for (int i = 0; i < 6; ++i) T[i] = __ldca(T2 + i);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          s_w[8 * c + 2 * i] = w[i].x;
-          s_w[8 * c + 2 * i + 1] = w[i].y;
-        }
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-          s_T[12 * c + 2 * i] = T[i].x;
-          s_T[12 * c + 2 * i + 1] = T[i].y;
-        }
       }
       smem_is_cur = false;
       TRACE(57);
@@ -753,7 +749,9 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
           s_part[3 * warp + 1] = mx;
           s_part[3 * warp + 2] = es;
         }
-        __syncthreads();  // also: the tentative warps / transforms are complete in smem
+        mbar_wait(&s_bar, bar_phase);  // the tentative warps / transforms are in smem
+        bar_phase ^= 1;
+        __syncthreads();
         allok = 1.0;
         mx = 0.0;
         es = 0.0;
@@ -905,7 +903,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   // ---- final report (solver.py:360-376). Record buffer pb is the relinearization at
   // the solution (robust weights recomputed there), so only the support -> rigidity
   // weights and the rigidity cost with them remain ----
-  if (!smem_is_cur) load_state(A, cur, s_w, s_T);
+  if (!smem_is_cur) load_state(A, cur, s_w, s_T, &s_bar, bar_phase);
   TRACE(72);
   {
     const PBuf cb = pbuf(A, pb);
