@@ -166,6 +166,14 @@ int dt_sample_control_points(const double* points, int64_t n, double radius,
 int dt_connection_candidates(const double* ctrl, int64_t m, double d2_max, int64_t* edges,
                              double* d2, int64_t capacity, int64_t* e_out, int device);
 
+/* Local-PCA normals of an unordered cloud (correspond.estimate_point_normals,
+ * correspond.py:198-220): the k nearest points (itself included; exact, ties at the
+ * k-th neighbour -> lower index), smallest-eigenvalue eigenvector of their scatter,
+ * oriented toward the camera (n . p < 0), unit length. points / normals are host
+ * (n x 3) f64; k <= 16; n < 3 or k < 3 gives (0, 0, -1) everywhere. */
+int dt_estimate_point_normals(const double* points, int64_t n, int64_t k, double* normals,
+                              int device);
+
 /* ------------------------------------------------------------------------------
  * Frame level: a device-resident tracker (one per sequence / stream).
  * Replaces solver.solve_frame (solver.py:267-378) and tracking.track_frame

@@ -138,26 +138,23 @@ def occlusion_mask(observation: Observation, region: tuple[int, int, int, int]) 
 def estimate_point_normals(points, k: int = 12) -> np.ndarray:
     """Local-PCA normals oriented toward the camera at the origin (correspond.py:198-220).
 
-    Template-time setup (fit() without normals): host scipy/numpy.
-    """
-    from scipy.spatial import cKDTree
+    Template-time setup (``fit()`` without normals), on the device
+    (``dt_estimate_point_normals``): exact k nearest neighbours by brute force (ties at
+    the k-th neighbour to the lower index; the reference's kd-tree leaves that order
+    unspecified), scatter in nearest-first order, Jacobi eigenvector of the smallest
+    eigenvalue."""
+    import ctypes as C
 
-    pts = np.asarray(points, dtype=np.float64)
-    n = pts.shape[0]
-    k = min(k, n)
-    out = np.tile([0.0, 0.0, -1.0], (n, 1))
-    if n < 3 or k < 3:
+    from .warpfield import _device_index
+
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    out = np.empty_like(pts)
+    if pts.shape[0] == 0:
         return out
-    _, nn = cKDTree(pts).query(pts, k=k)
-    nb = pts[nn]
-    centered = nb - nb.mean(axis=1, keepdims=True)
-    cov = np.einsum("nki,nkj->nij", centered, centered)
-    _, vecs = np.linalg.eigh(cov)
-    cand = vecs[:, :, 0]
-    flip = np.sum(cand * pts, axis=1) > 0.0
-    cand[flip] *= -1.0
-    norms = np.linalg.norm(cand, axis=1, keepdims=True)
-    return cand / np.where(norms > 0.0, norms, 1.0)
+    check(lib.dt_estimate_point_normals(pts.ctypes.data, pts.shape[0], int(k),
+                                        out.ctypes.data, _device_index()),
+          "dt_estimate_point_normals")
+    return out
 
 
 __all__ = [

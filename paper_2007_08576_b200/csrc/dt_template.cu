@@ -176,6 +176,163 @@ int dmalloc(T** p, size_t count) {
   return DT_OK;
 }
 
+// ---------------------------------------------------------------------------------
+// correspond.estimate_point_normals (correspond.py:198-220): the k nearest points of
+// every point (itself included; exact brute force with the key (squared distance,
+// index), i.e. ties at the k-th neighbour go to the lower index), their mean and 3x3
+// scatter in nearest-first order, the eigenvector of the smallest eigenvalue (cyclic
+// Jacobi), oriented toward the camera at the origin (n . p < 0) and normalized.
+// One thread per point; candidates stream through shared memory in tiles.
+// ---------------------------------------------------------------------------------
+constexpr int NRM_KMAX = 16;
+constexpr int NRM_TILE = 256;
+
+__device__ __forceinline__ bool key_less(double d, int j, double e, int i) {
+  return d < e || (d == e && j < i);
+}
+
+__device__ void sym3_min_eigvec(double a00, double a01, double a02, double a11, double a12,
+                                double a22, double v[3]) {
+  double a[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
+  double V[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  for (int sweep = 0; sweep < 32; ++sweep) {
+    const double off = a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2];
+    const double dia = a[0][0] * a[0][0] + a[1][1] * a[1][1] + a[2][2] * a[2][2];
+    if (off == 0.0 || off <= 1e-36 * dia) break;
+#pragma unroll
+    for (int pq = 0; pq < 3; ++pq) {
+      const int p = pq == 2 ? 1 : 0, q = pq == 0 ? 1 : 2;
+      if (a[p][q] == 0.0) continue;
+      const double th = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+      const double t = th == 0.0 ? 1.0 : copysign(1.0, th) / (fabs(th) + sqrt(th * th + 1.0));
+      const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const double ap = a[r][p], aq = a[r][q];
+        a[r][p] = c * ap - sn * aq;
+        a[r][q] = sn * ap + c * aq;
+      }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const double ap = a[p][r], aq = a[q][r];
+        a[p][r] = c * ap - sn * aq;
+        a[q][r] = sn * ap + c * aq;
+      }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const double vp = V[r][p], vq = V[r][q];
+        V[r][p] = c * vp - sn * vq;
+        V[r][q] = sn * vp + c * vq;
+      }
+    }
+  }
+  int im = 0;
+  if (a[1][1] < a[im][im]) im = 1;
+  if (a[2][2] < a[im][im]) im = 2;
+  v[0] = V[0][im];
+  v[1] = V[1][im];
+  v[2] = V[2][im];
+}
+
+__global__ void __launch_bounds__(NRM_TILE)
+k_point_normals(const double* __restrict__ pts, int64_t n, int k, double* __restrict__ out) {
+  __shared__ double sx[NRM_TILE], sy[NRM_TILE], sz[NRM_TILE];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < n;
+  double px = 0.0, py = 0.0, pz = 0.0;
+  if (live) {
+    px = pts[3 * i];
+    py = pts[3 * i + 1];
+    pz = pts[3 * i + 2];
+  }
+  double bd[NRM_KMAX];
+  int bi[NRM_KMAX];
+#pragma unroll
+  for (int s = 0; s < NRM_KMAX; ++s) {
+    bd[s] = INFINITY;
+    bi[s] = 0x7fffffff;
+  }
+  double thr = INFINITY;  // key of the current k-th neighbour
+  int thi = 0x7fffffff;
+  for (int64_t base = 0; base < n; base += NRM_TILE) {
+    const int64_t j = base + threadIdx.x;
+    __syncthreads();
+    if (j < n) {
+      sx[threadIdx.x] = pts[3 * j];
+      sy[threadIdx.x] = pts[3 * j + 1];
+      sz[threadIdx.x] = pts[3 * j + 2];
+    }
+    __syncthreads();
+    const int cnt = (int)(n - base < NRM_TILE ? n - base : NRM_TILE);
+    if (!live) continue;
+    for (int u = 0; u < cnt; ++u) {
+      const double dx = sx[u] - px, dy = sy[u] - py, dz = sz[u] - pz;
+      const double d = dx * dx + dy * dy + dz * dz;
+      const int jj = (int)(base + u);
+      if (!key_less(d, jj, thr, thi)) continue;
+      // sorted insertion of (d, jj)
+#pragma unroll
+      for (int s = NRM_KMAX - 1; s > 0; --s) {
+        if (key_less(d, jj, bd[s - 1], bi[s - 1])) {
+          bd[s] = bd[s - 1];
+          bi[s] = bi[s - 1];
+        } else if (key_less(d, jj, bd[s], bi[s])) {
+          bd[s] = d;
+          bi[s] = jj;
+        }
+      }
+      if (key_less(d, jj, bd[0], bi[0])) {
+        bd[0] = d;
+        bi[0] = jj;
+      }
+#pragma unroll
+      for (int s = 0; s < NRM_KMAX; ++s)
+        if (s == k - 1) {
+          thr = bd[s];
+          thi = bi[s];
+        }
+    }
+  }
+  if (!live) return;
+  // neighbourhood mean and scatter in nearest-first order
+  double mx = 0.0, my = 0.0, mz = 0.0;
+#pragma unroll
+  for (int s = 0; s < NRM_KMAX; ++s)
+    if (s < k) {
+      mx += pts[3 * (int64_t)bi[s]];
+      my += pts[3 * (int64_t)bi[s] + 1];
+      mz += pts[3 * (int64_t)bi[s] + 2];
+    }
+  mx /= (double)k;
+  my /= (double)k;
+  mz /= (double)k;
+  double c00 = 0, c01 = 0, c02 = 0, c11 = 0, c12 = 0, c22 = 0;
+#pragma unroll
+  for (int s = 0; s < NRM_KMAX; ++s)
+    if (s < k) {
+      const double x = pts[3 * (int64_t)bi[s]] - mx, y = pts[3 * (int64_t)bi[s] + 1] - my,
+                   z = pts[3 * (int64_t)bi[s] + 2] - mz;
+      c00 += x * x;
+      c01 += x * y;
+      c02 += x * z;
+      c11 += y * y;
+      c12 += y * z;
+      c22 += z * z;
+    }
+  double v[3];
+  sym3_min_eigvec(c00, c01, c02, c11, c12, c22, v);
+  if (v[0] * px + v[1] * py + v[2] * pz > 0.0) {
+    v[0] = -v[0];
+    v[1] = -v[1];
+    v[2] = -v[2];
+  }
+  const double nn = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  const double den = nn > 0.0 ? nn : 1.0;
+  out[3 * i] = v[0] / den;
+  out[3 * i + 1] = v[1] / den;
+  out[3 * i + 2] = v[2] / den;
+}
+
 struct Freer {
   std::vector<void*> ptrs;
   ~Freer() {
@@ -326,6 +483,36 @@ int dt_connection_candidates(const double* ctrl, int64_t m, double d2_max, int64
   DT_CHECK_LAUNCH();
   DT_CHECK_CUDA(cudaMemcpy(edges, d_e, sizeof(int64_t) * 2 * e, cudaMemcpyDeviceToHost));
   DT_CHECK_CUDA(cudaMemcpy(d2, d_d2, sizeof(double) * e, cudaMemcpyDeviceToHost));
+  return DT_OK;
+}
+
+int dt_estimate_point_normals(const double* points, int64_t n, int64_t k, double* normals,
+                              int device) {
+  DT_REQUIRE(points != nullptr && normals != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  DT_REQUIRE(n >= 0 && n < (1ll << 31), DT_ERR_UNSUPPORTED, "point count out of range");
+  DT_REQUIRE(k >= 1, DT_ERR_INVALID_ARGUMENT, "k must be positive");
+  const int64_t ke = std::min<int64_t>(k, n);
+  if (n < 3 || ke < 3) {  // too few points: the camera-facing default (correspond.py:205-207)
+    for (int64_t i = 0; i < n; ++i) {
+      normals[3 * i] = 0.0;
+      normals[3 * i + 1] = 0.0;
+      normals[3 * i + 2] = -1.0;
+    }
+    return DT_OK;
+  }
+  DT_REQUIRE(ke <= NRM_KMAX, DT_ERR_UNSUPPORTED, "k=%lld above the device limit %d", (long long)ke,
+             NRM_KMAX);
+  DT_CHECK_CUDA(cudaSetDevice(device));
+  Freer fr;
+  double *d_p, *d_n;
+  DT_TRY(dmalloc(&d_p, 3 * n));
+  fr.ptrs.push_back(d_p);
+  DT_TRY(dmalloc(&d_n, 3 * n));
+  fr.ptrs.push_back(d_n);
+  DT_CHECK_CUDA(cudaMemcpy(d_p, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+  k_point_normals<<<(unsigned)((n + NRM_TILE - 1) / NRM_TILE), NRM_TILE>>>(d_p, n, (int)ke, d_n);
+  DT_CHECK_LAUNCH();
+  DT_CHECK_CUDA(cudaMemcpy(normals, d_n, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
   return DT_OK;
 }
 

@@ -345,11 +345,38 @@ def make_tracking_cfg1():
     np.savez_compressed(OUT / "tracking_cfg1.npz", **d)
 
 
+def point_normal_clouds():
+    """Clouds for correspond.estimate_point_normals: a curved grid patch (spacing 1,
+    relief), an unstructured cloud, and the small-n cases (k clipped to n; n < 3)."""
+    rng = np.random.default_rng(21)
+    u, v = np.meshgrid(np.arange(-20.0, 21.0), np.arange(-20.0, 21.0), indexing="ij")
+    patch = np.stack([u.ravel(), v.ravel(),
+                      300.0 + 0.02 * (u.ravel() ** 2) - 0.015 * (v.ravel() ** 2)
+                      + 0.3 * np.sin(u.ravel() / 3.0)], axis=1)
+    cloud = rng.normal(size=(1500, 3)) * np.array([40.0, 30.0, 2.0]) + np.array([0, 0, 250.0])
+    small = rng.normal(size=(5, 3)) + np.array([0, 0, 100.0])
+    tiny = rng.normal(size=(2, 3)) + np.array([0, 0, 100.0])
+    return {"patch": (patch, 12), "cloud": (cloud, 12), "cloud_k6": (cloud, 6),
+            "small": (small, 12), "tiny": (tiny, 12)}
+
+
+def make_point_normals():
+    from deformtrack.correspond import estimate_point_normals
+
+    out = {}
+    for name, (pts, k) in point_normal_clouds().items():
+        out[f"{name}_pts"] = pts
+        out[f"{name}_k"] = np.array(k)
+        out[f"{name}_nrm"] = estimate_point_normals(pts, k=k)
+    np.savez_compressed(OUT / "point_normals.npz", **out)
+
+
 if __name__ == "__main__":
     make_kernels()
     make_solver_cases()
     make_matching()
     make_tracking()
     make_tracking_cfg1()
+    make_point_normals()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)

@@ -237,3 +237,24 @@ def test_too_few_matches_is_no_valid_hypothesis():
                                 OP.Weights(), s, graph.sampling_radius)
     assert res.report.n_correspondences == ores.n_correspondences
     assert float(np.abs(res.points - opts).max()) < VERTEX_TOL_MM
+
+
+def test_estimator_estimates_missing_normals():
+    """fit() without normals estimates them on the device (test_estimators.py:92-98):
+    camera-facing, close to the analytic surface normals, and equal to the reference
+    algorithm (oracle) wherever the neighbour set is unique."""
+    from oracle import pipeline as OP
+    from paper_2007_08576_b200 import synth
+
+    scene, spec = _scene(1)
+    tpl0 = synth.make_template(scene)
+    import paper_2007_08576_b200 as dt
+
+    est = dt.SurfaceDeformationTracker(sampling_radius=spec["radius"], max_outer_iters=2,
+                                       camera=synth.camera_for(scene))
+    est.fit(tpl0.points)
+    nrm = est.template_.normals
+    assert np.all(nrm[:, 2] < 0.0)
+    assert float(np.mean(np.sum(nrm * tpl0.normals, axis=1))) > 0.95
+    ref, tie = OP.point_normals(tpl0.points)
+    np.testing.assert_allclose(nrm[~tie], ref[~tie], rtol=0, atol=1e-9)

@@ -162,3 +162,12 @@ def test_track_frame_reproduces_reference(fixture):
         assert res.n_correspondences == rep["counts"]["correspondences"]
         # warp_all uses einsum blending in the reference; allow its last-ulp rounding
         np.testing.assert_allclose(pts, z[f"f{f}_points"], rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["patch", "cloud", "cloud_k6", "small", "tiny"])
+def test_point_normals_reproduce_reference(name):
+    """The oracle's estimate_point_normals restatement against the reference's own
+    output (correspond.py:198-220)."""
+    z = load("point_normals")
+    nrm, _ = OP.point_normals(z[f"{name}_pts"], int(z[f"{name}_k"]))
+    np.testing.assert_array_equal(nrm, z[f"{name}_nrm"])
