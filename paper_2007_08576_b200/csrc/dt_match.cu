@@ -518,13 +518,10 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
     // register limit), e.g. 2,000 hypotheses -> 143 CTAs x 14 warps instead of 8-warp CTAs
     // that leave 102 SMs with 16 warps and 46 with 8. The block scheduler's greedy fill
     // defeats smaller CTAs.
-    static int sms = 0;
-    if (sms == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (sms <= 0) sms = 148;
-    }
+    int dev = 0, sms = 0;  // a cheap attribute query; no process-global cache
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
     const int64_t wpc = std::min<int64_t>(16, std::max<int64_t>(1, (nr + sms - 1) / sms));
     k_preselect_warp<<<(unsigned)((nr + wpc - 1) / wpc), (unsigned)(32 * wpc), 0, s>>>(
         src, dst, n_dev, n_max, refs, n_refs, exhaustive, H, iters, min_support, ref_support,

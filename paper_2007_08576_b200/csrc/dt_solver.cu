@@ -30,6 +30,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <cmath>
 #include <cstdint>
 
@@ -472,11 +474,14 @@ static void* solver_fn(int k) {
   return k == 4 ? (void*)k_solve_frame<GRID, 4> : (void*)k_solve_frame<GRID, 8>;
 }
 
-static int g_max_cluster[16] = {0};
+// per-device cache of the occupancy probe (a hardware property; atomic so concurrent
+// tracker creation on several host threads is race-free)
+static std::atomic<int> g_max_cluster[16];
 
 int solver_max_cluster(int device) {
   if (device < 0 || device >= 16) return 8;
-  if (g_max_cluster[device] > 0) return g_max_cluster[device];
+  const int cached = g_max_cluster[device].load(std::memory_order_relaxed);
+  if (cached > 0) return cached;
   int best = 1;
   auto* fn = k_solve_frame<false, 8>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -501,7 +506,7 @@ int solver_max_cluster(int device) {
     }
     cudaGetLastError();
   }
-  g_max_cluster[device] = best;
+  g_max_cluster[device].store(best, std::memory_order_relaxed);
   return best;
 }
 

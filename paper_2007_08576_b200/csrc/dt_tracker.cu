@@ -971,21 +971,13 @@ int run_frame(dt_tracker* t, const dt_frame_input* in, bool* used) {
 
 extern "C" {
 
-int dt_tracker_create(const dt_config* cfg, const double* t_points, const double* t_normals,
-                      const int64_t* bind_idx, const double* bind_w, int64_t n, int64_t k,
-                      const double* ctrl_points, const double* warps, int64_t m,
-                      const int64_t* edges, const double* edge_weights, int64_t n_edges,
-                      int device, void* stream, dt_tracker** out) {
-  DT_TRY(validate_config(cfg));
-  DT_REQUIRE(out != nullptr, DT_ERR_INVALID_ARGUMENT, "out is NULL");
-  DT_REQUIRE(m >= 1, DT_ERR_EMPTY_TEMPLATE, "control graph is empty");
-  DT_REQUIRE(k >= 1 && k <= KMAX, DT_ERR_UNSUPPORTED, "bind_k outside [1, %d]", KMAX);
-  DT_REQUIRE(bind_idx != nullptr && bind_w != nullptr, DT_ERR_NOT_BOUND,
-             "template must be bound to the control graph first");
-  DT_REQUIRE(n < (1ll << 28), DT_ERR_UNSUPPORTED, "template too large");
-  DT_CHECK_CUDA(cudaSetDevice(device));
-  dt_tracker* t = new (std::nothrow) dt_tracker();
-  DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "out of host memory");
+// Everything after the allocation of the handle; on failure dt_tracker_create destroys
+// the partly built tracker (buffers, streams, events) instead of leaking it.
+static int tracker_init(dt_tracker* t, const dt_config* cfg, const double* t_points, const double* t_normals,
+                const int64_t* bind_idx, const double* bind_w, int64_t n, int64_t k,
+                const double* ctrl_points, const double* warps, int64_t m,
+                const int64_t* edges, const double* edge_weights, int64_t n_edges,
+                int device, void* stream) {
   t->cfg = *cfg;
   t->device = device;
   t->n = n;
@@ -1118,6 +1110,30 @@ int dt_tracker_create(const dt_config* cfg, const double* t_points, const double
              (long long)m);
   pick_mode(t);
   DT_TRY(push_args(t));
+  return DT_OK;
+}
+
+int dt_tracker_create(const dt_config* cfg, const double* t_points, const double* t_normals,
+                      const int64_t* bind_idx, const double* bind_w, int64_t n, int64_t k,
+                      const double* ctrl_points, const double* warps, int64_t m,
+                      const int64_t* edges, const double* edge_weights, int64_t n_edges,
+                      int device, void* stream, dt_tracker** out) {
+  DT_TRY(validate_config(cfg));
+  DT_REQUIRE(out != nullptr, DT_ERR_INVALID_ARGUMENT, "out is NULL");
+  DT_REQUIRE(m >= 1, DT_ERR_EMPTY_TEMPLATE, "control graph is empty");
+  DT_REQUIRE(k >= 1 && k <= KMAX, DT_ERR_UNSUPPORTED, "bind_k outside [1, %d]", KMAX);
+  DT_REQUIRE(bind_idx != nullptr && bind_w != nullptr, DT_ERR_NOT_BOUND,
+             "template must be bound to the control graph first");
+  DT_REQUIRE(n < (1ll << 28), DT_ERR_UNSUPPORTED, "template too large");
+  DT_CHECK_CUDA(cudaSetDevice(device));
+  dt_tracker* t = new (std::nothrow) dt_tracker();
+  DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "out of host memory");
+  const int st = tracker_init(t, cfg, t_points, t_normals, bind_idx, bind_w, n, k, ctrl_points,
+                              warps, m, edges, edge_weights, n_edges, device, stream);
+  if (st != DT_OK) {
+    dt_tracker_destroy(t);
+    return st;
+  }
   *out = t;
   return DT_OK;
 }

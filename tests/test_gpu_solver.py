@@ -179,3 +179,25 @@ def test_device_binding_on_grid_ties_within_north_star_bar():
     dev = float(np.abs(res.points - z["f1_points"]).max())
     assert dev < VERTEX_TOL_MM, dev
     np.testing.assert_array_equal(res.matches.preselected, z["f1_m_flags"])
+
+
+def test_tracker_create_rejects_bad_binding_and_recovers():
+    """A bind index outside the control graph fails tracker creation with ValueError
+    (the partly built handle is released), and a valid tracker works afterwards."""
+    dt = _api()
+    from dataclasses import replace
+
+    c = solver_case("solver_fixed_point")
+    fx, fy, cx, cy = c["cam"]
+    cam = dt.PinholeCamera(fx, fy, cx, cy, *c["dims"])
+    tpl, graph = _template_graph(dt, c["tpl"], c["graph"], c["warps_in"], c["radius"])
+    bad = tpl.bind_indices.copy()
+    bad[0, 0] = len(graph) + 5
+    cfg = dt.load_config({})
+    for _ in range(3):
+        with pytest.raises(ValueError):
+            dt.Tracker(replace(tpl, bind_indices=bad), graph, cam, cfg)
+    trk = dt.Tracker(tpl, graph, cam, cfg)
+    res = trk.track(c["depth"])
+    trk.close()
+    assert res.report.n_correspondences > 0
