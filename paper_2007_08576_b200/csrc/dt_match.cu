@@ -397,15 +397,29 @@ k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
     for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
       for (int i = 0; i < 9; ++i) C[i] += __shfl_xor_sync(0xffffffffu, C[i], o);
-    double Rm[9];
-    const bool ok = procrustes_lane(C, V, Rm);
-    if (!ok) live = false;
-    if (live) {
+    double Rm[9], V0[9];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) R[i] = Rm[i];
+    for (int i = 0; i < 9; ++i) V0[i] = V[i];
+    const bool ok = procrustes_lane(C, V, Rm);
+    if (!ok) {
+      live = false;  // degenerate: the hypothesis is discarded whatever follows
+      break;
     }
+    // Exact early exit: after a weighted step, if (R, V) came back bit for bit unchanged,
+    // every later step recomputes the same weights, covariance and warm-started SVD, so
+    // the remaining iterations cannot change a bit (all lanes hold identical values, so
+    // the test is warp-uniform).
+    bool same = it > 0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+      same = same && __double_as_longlong(Rm[i]) == __double_as_longlong(R[i]) &&
+             __double_as_longlong(V[i]) == __double_as_longlong(V0[i]);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = Rm[i];
+    if (same) break;
   }
-  double sup = support_pass(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq);
+  double sup = 0.0;
+  if (live) sup = support_pass(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq);
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) sup += __shfl_xor_sync(0xffffffffu, sup, o);
   if (lane == 0) {
