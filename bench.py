@@ -204,6 +204,8 @@ def replica_throughput(frames_per_rank: int, world: int, max_ms: float) -> float
 
 
 # ---------------------------------------------------------------------------------
+FP64_PEAK_TFLOPS = 34.0  # DFMA, measured on this pool's B200 with tools/fp64_probe.cu
+
 # algorithmic bytes for the roofline of the LM solver kernel
 # ---------------------------------------------------------------------------------
 
@@ -411,6 +413,21 @@ def run_b200(args, rank, world, local_rank):
                 "dominant_phase": dominant,
                 "note": "latency-bound: ~40 dependent phases/frame; see DESIGN.md §4"}
 
+    # the FP64-bound stage beside it: exhaustive preselection, SURVEY.md §8(d)'s
+    # 40 flop x hypotheses x (IRLS iterations + support pass) x matches, against the
+    # measured DFMA throughput (tools/fp64_probe.cu)
+    n_match = int(getattr(rep, "n_matches", 0) or 0)
+    pre_ms = phase_avg.get("preselect", 0.0)
+    pre_flop = 40.0 * n_match * (wl["cfg"].preselect.n_reweight_iters + 1) * n_match
+    roofline_pre = None
+    if pre_ms > 0 and n_match > 0:
+        ach = pre_flop / (pre_ms * 1e-3) / 1e12
+        roofline_pre = {"kernel": "k_preselect_warp + k_preselect_final", "bound": "fp64",
+                        "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                        "frac": ach / FP64_PEAK_TFLOPS, "algorithmic_flop": pre_flop,
+                        "launch_ms": pre_ms,
+                        "peak_source": "measured DFMA throughput on B200 (tools/fp64_probe.cu)"}
+
     value = replica_throughput(K, world, total_ms)
     ms_per_step = total_ms / K
     result = {
@@ -420,7 +437,8 @@ def run_b200(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (builder sphere-patch generator, seeded; random 256-bit descriptors)",
         "config": workload_config(wl, world, f"{F} distinct frames cycled (period 20)"),
-        "e2e": e2e, "roofline": roofline, "gpu_launches": launches,
+        "e2e": e2e, "roofline": roofline, "roofline_preselect": roofline_pre,
+        "gpu_launches": launches,
         "phase_ms": phase_avg, "clocks": clocks.summary(),
         "frame_report": {"n_correspondences": int(rep.n_correspondences),
                          "n_matches": int(rep.n_matches), "n_preselected": int(rep.n_preselected),
