@@ -86,3 +86,38 @@ def test_pipelined_frames_match_synchronous_frames():
         assert rep.n_correspondences == ncorr and rep.n_preselected == npre
         assert rep.frame_id == i
     trk.close()
+
+
+def test_changing_feature_counts_recapture_the_frame_graph():
+    """Frames with different numbers of ORB features (the frame body is a CUDA graph keyed
+    by the feature count) give exactly what a fresh tracker gives for each frame from the
+    same warm start, in both the synchronous and the pipelined paths."""
+    from dataclasses import replace
+
+    import bench
+
+    wl = bench.make_workload(1, 4, seed=5)
+    m, n = len(wl["graph"]), len(wl["tpl"])
+    frames = list(wl["frames"])
+    for i, keep in ((1, 300), (3, 411)):  # fewer frame features on frames 1 and 3
+        fr = frames[i]
+        frames[i] = replace(fr, descriptors=fr.descriptors[:keep], keypoints=fr.keypoints[:keep])
+
+    def run(trk, fr, fid, warps):
+        trk.set_warps(warps)
+        fi, keep = _inputs(fr, fid)
+        fo, (w, p, rep) = _outputs(m, n)
+        trk.track_raw(fi, fo)
+        return w.copy(), p.copy(), rep.total_cost, rep.n_matches
+
+    warm = wl["graph"].warps
+    shared = _tracker(wl)
+    for i, fr in enumerate(frames * 2):  # twice round: graphs get reused and re-captured
+        a = run(shared, fr, i, warm)
+        fresh = _tracker(wl)
+        b = run(fresh, fr, i, warm)
+        fresh.close()
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])
+        assert a[2] == b[2] and a[3] == b[3]
+    shared.close()
