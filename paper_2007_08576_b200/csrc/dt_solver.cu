@@ -46,9 +46,9 @@ namespace dt {
 
 constexpr int NWARPS = SOLVER_THREADS / 32;
 constexpr int GOUT = 32;  // per-warp reduce-scatter readout (one accumulator per lane)
-constexpr int M_MAX_SMEM = 1300;
 
 size_t solver_smem_bytes(int m) {
+  if (m > M_MAX_SMEM) return sizeof(double) * (size_t)NWARPS * GOUT;  // global-state variant
   return sizeof(double) * ((size_t)21 * m + (size_t)NWARPS * GOUT);
 }
 
@@ -189,6 +189,14 @@ __device__ __forceinline__ void load_state(const SolverArgs& A, const double* sr
   phase ^= 1;
   for (int c = threadIdx.x; c < A.m; c += blockDim.x)
     dq_to_transform_fast(s_w + 8 * c, s_T + 12 * c, s_T + 12 * c + 9);
+  __syncthreads();
+}
+
+// global-state variant: the warps stay where they are; this CTA's transforms of them
+__device__ __forceinline__ void load_transforms(const SolverArgs& A, const double* w, double* T) {
+  __syncthreads();
+  for (int c = threadIdx.x; c < A.m; c += blockDim.x)
+    dq_to_transform_fast(w + 8 * c, T + 12 * c, T + 12 * c + 9);
   __syncthreads();
 }
 
@@ -464,14 +472,19 @@ __device__ __forceinline__ bool solve6(const double* part, double lam, double de
 
 // KM = 4: the reference's bind_k (SolverConfig / RunConfig default, warpfield.py:157);
 // KM = 8: any k <= 8 with runtime slot guards
-template __global__ void k_solve_frame<false, 4>(const SolverArgs* __restrict__);
-template __global__ void k_solve_frame<true, 4>(const SolverArgs* __restrict__);
-template __global__ void k_solve_frame<false, 8>(const SolverArgs* __restrict__);
-template __global__ void k_solve_frame<true, 8>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 4, false>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 4, false>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 8, false>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 8, false>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 4, true>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 4, true>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 8, true>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 8, true>(const SolverArgs* __restrict__);
 
 template <bool GRID>
-static void* solver_fn(int k) {
-  return k == 4 ? (void*)k_solve_frame<GRID, 4> : (void*)k_solve_frame<GRID, 8>;
+static void* solver_fn(int k, bool big) {
+  if (big) return k == 4 ? (void*)k_solve_frame<GRID, 4, true> : (void*)k_solve_frame<GRID, 8, true>;
+  return k == 4 ? (void*)k_solve_frame<GRID, 4, false> : (void*)k_solve_frame<GRID, 8, false>;
 }
 
 // per-device cache of the occupancy probe (a hardware property; atomic so concurrent
@@ -483,7 +496,7 @@ int solver_max_cluster(int device) {
   const int cached = g_max_cluster[device].load(std::memory_order_relaxed);
   if (cached > 0) return cached;
   int best = 1;
-  auto* fn = k_solve_frame<false, 8>;
+  auto* fn = k_solve_frame<false, 8, false>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const size_t smem = solver_smem_bytes(1024);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -520,7 +533,7 @@ int solver_pick_cluster(int device, int requested, int m_max) {
 }
 
 int solver_grid_blocks(int device, int m_max) {
-  auto* fn = k_solve_frame<true, 8>;
+  auto* fn = m_max > M_MAX_SMEM ? k_solve_frame<true, 8, true> : k_solve_frame<true, 8, false>;
   const size_t smem = solver_smem_bytes(m_max);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0, sms = 0;
@@ -535,11 +548,10 @@ int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, i
   DT_REQUIRE(k >= 1 && k <= KMAX, DT_ERR_UNSUPPORTED, "bind_k=%d outside the device path (<= %d)", k,
              KMAX);
   const size_t smem = solver_smem_bytes(m_max);
-  DT_REQUIRE(m_max <= M_MAX_SMEM && smem <= 227 * 1024, DT_ERR_UNSUPPORTED,
-             "control graph too large for the shared-memory warp table (m=%d)", m_max);
+  const bool big = m_max > M_MAX_SMEM;
   if (grid_mode) {
     DT_REQUIRE(n_seq == 1, DT_ERR_UNSUPPORTED, "grid mode runs one sequence per launch");
-    void* fn = solver_fn<true>(k);
+    void* fn = solver_fn<true>(k, big);
     DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0;
     DT_CHECK_CUDA(cudaGetDevice(&dev));
@@ -550,7 +562,7 @@ int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, i
                                               params, smem, s));
     return DT_OK;
   }
-  void* fn = solver_fn<false>(k);
+  void* fn = solver_fn<false>(k, big);
   DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};

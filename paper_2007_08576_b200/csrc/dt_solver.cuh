@@ -65,6 +65,7 @@ struct SolverArgs {
   double* warps_out; // solution
   double* lam;
   double* wa;
+  double* gstate;    // m > M_MAX_SMEM only: per CTA 12m transforms + m damping
   double* partial;   // m x 27 normal-equation columns
   double* csum;      // 2 sets x (nch_p + nch_m + nch_e) deterministic chunk sums
   double* erow;      // 2 x (2E) x 24: per CSR position the 3 unit rigidity rows of that
@@ -110,6 +111,9 @@ struct SolverArgs {
 
 constexpr int RED_SLOTS = 5;
 
+// control graphs up to this size keep their state in shared memory; larger ones run the
+// global-state kernel variant (needs SolverArgs::gstate)
+constexpr int M_MAX_SMEM = 1300;
 size_t solver_smem_bytes(int m);
 // mode: 0 = one cluster of `cluster` CTAs per sequence; 1 = one cooperative grid over
 // every SM for a single sequence

@@ -426,7 +426,11 @@ __device__ __forceinline__ void resolve_control(const SolverArgs& A, int c, doub
   publish_tentative(A, c, W, d, tent);
 }
 
-template <bool GRID, int KM>
+// BIG: control graphs whose state does not fit in shared memory (m > M_MAX_SMEM): the
+// warps and tentative transforms are read in place from global memory (L1-cached after
+// each barrier), the current transforms and the damping live in this CTA's slice of
+// A.gstate; everything else is the same kernel.
+template <bool GRID, int KM, bool BIG>
 __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverArgs* __restrict__ all) {
   Dom<GRID> dom;
   const int C = dom.size();
@@ -450,10 +454,11 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   const int64_t n = A.n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int team = warp / TEAM, tw = warp % TEAM;
-  double* s_w = smem;
-  double* s_T = smem + 8 * m;
-  double* s_lam = smem + 20 * m;  // per-control damping, replicated in every CTA
-  double* gout = smem + 21 * m + warp * GOUT;
+  double* s_w = BIG ? A.warp_a : smem;
+  double* const s_Tcur = BIG ? A.gstate + (size_t)rank * 13 * m : smem + 8 * m;
+  double* s_T = s_Tcur;
+  double* s_lam = BIG ? s_Tcur + 12 * m : smem + 20 * m;  // per-control damping, per CTA
+  double* gout = (BIG ? smem : smem + 21 * m) + warp * GOUT;
   // work items are dealt round-robin over the CTAs first (item i -> CTA i % C), so
   // every SM of the domain gets a share of each phase
   const int gw = warp * C + rank, GW = C * NWARPS;
@@ -492,7 +497,13 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
 
   // ---- P1: relink + linearize at the warm start (buffer 0): points, matches, unit
   // rigidity rows of the connections ----
-  load_state(A, cur, s_w, s_T, &s_bar, bar_phase);
+  if (BIG) {
+    s_w = cur;
+    s_T = s_Tcur;
+    load_transforms(A, s_w, s_T);
+  } else {
+    load_state(A, cur, s_w, s_T, &s_bar, bar_phase);
+  }
   TRACE(12);
   {
     const PBuf nb = pbuf(A, 0);
@@ -716,7 +727,10 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
       // linearization also the rigidity cost of the iterate) -- identical in every CTA.
       const bool want_e = attempt == 0 && need_lin;
       const int pc = threadIdx.x;
-      if (threadIdx.x == 0) {
+      if (BIG) {
+        s_w = tent;  // read in place
+        s_T = A.tentT;
+      } else if (threadIdx.x == 0) {
         // tentative warps (8m) and transforms (12m) -> s_w / s_T by two bulk copies; the
         // proxy fence orders this CTA's earlier generic shared-memory accesses (and the
         // barrier-acquired global writes) before the async-proxy copies
@@ -749,8 +763,10 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
           s_part[3 * warp + 1] = mx;
           s_part[3 * warp + 2] = es;
         }
-        mbar_wait(&s_bar, bar_phase);  // the tentative warps / transforms are in smem
-        bar_phase ^= 1;
+        if (!BIG) {
+          mbar_wait(&s_bar, bar_phase);  // the tentative warps / transforms are in smem
+          bar_phase ^= 1;
+        }
         __syncthreads();
         allok = 1.0;
         mx = 0.0;
@@ -903,7 +919,15 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   // ---- final report (solver.py:360-376). Record buffer pb is the relinearization at
   // the solution (robust weights recomputed there), so only the support -> rigidity
   // weights and the rigidity cost with them remain ----
-  if (!smem_is_cur) load_state(A, cur, s_w, s_T, &s_bar, bar_phase);
+  if (BIG) {
+    if (!smem_is_cur) {
+      s_w = cur;
+      s_T = s_Tcur;
+      load_transforms(A, s_w, s_T);
+    }
+  } else if (!smem_is_cur) {
+    load_state(A, cur, s_w, s_T, &s_bar, bar_phase);
+  }
   TRACE(72);
   {
     const PBuf cb = pbuf(A, pb);

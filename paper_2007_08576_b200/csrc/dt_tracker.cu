@@ -478,6 +478,7 @@ struct dt_tracker {
   int* counts = nullptr;
   dt_report* report = nullptr;
   double *cost_hist = nullptr, *lam_hist = nullptr, *wa_out = nullptr;
+  double* gstate = nullptr;  // m > M_MAX_SMEM: per-CTA solver state
   int32_t* stalled_hist = nullptr;
   int* bad_flag = nullptr;
   // outputs
@@ -599,6 +600,7 @@ void fill_args(dt_tracker* t) {
   }
   a.warp_a = t->warp_a; a.warp_b = t->warp_b; a.warps_out = t->warps_out;
   a.lam = t->lam; a.wa = t->wa; a.partial = t->partial; a.csum = t->csum;
+  a.gstate = t->gstate;
   a.erow = t->erow; a.evals = t->evals;
   a.nch_p = (int)((t->n + CHUNK - 1) / CHUNK);
   a.nch_m = (int)((t->match_cap + CHUNK - 1) / CHUNK);
@@ -1106,8 +1108,13 @@ static int tracker_init(dt_tracker* t, const dt_config* cfg, const double* t_poi
   DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_info, sizeof(int64_t) * 4));
   DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_stats, sizeof(double) * 4));
   DT_CHECK_CUDA(cudaMemcpyAsync(t->warps_out, warps, sizeof(double) * 8 * m, cudaMemcpyHostToDevice, t->stream));
-  DT_REQUIRE(solver_smem_bytes((int)m) <= 227 * 1024, DT_ERR_UNSUPPORTED, "too many control points (%lld)",
-             (long long)m);
+  if (m > M_MAX_SMEM) {
+    // large control graph: the global-state solver variant keeps per-CTA transforms and
+    // damping here (one slice per CTA of the largest domain: the grid or a cluster)
+    int sms = 0;
+    DT_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    DT_TRY(dalloc(t, &t->gstate, (size_t)std::max(sms, 16) * 13 * m));
+  }
   pick_mode(t);
   DT_TRY(push_args(t));
   return DT_OK;

@@ -258,3 +258,25 @@ def test_estimator_estimates_missing_normals():
     assert float(np.mean(np.sum(nrm * tpl0.normals, axis=1))) > 0.95
     ref, tie = OP.point_normals(tpl0.points)
     np.testing.assert_allclose(nrm[~tie], ref[~tie], rtol=0, atol=1e-9)
+
+
+def test_large_control_graph_uses_global_state_solver():
+    """A control graph beyond the shared-memory state table (m > 1300: config 2's patch at
+    radius 2.3, ~2,000 controls) runs the global-state solver variant; one frame against
+    the oracle to the same bars as the benchmark configs."""
+    from paper_2007_08576_b200 import synth
+
+    scene, spec = _scene(2, n_features=800)
+    dt, cfg, cam, tpl0, feats, tpl, graph = _setup(scene, 2.3, 5)
+    assert len(graph) > 1300
+    fr = synth.make_frame(scene, cam, tpl0, feats, 1)
+    trk = dt.Tracker(tpl, graph, cam, cfg)
+    trk.set_features(feats.descriptors, feats.points)
+    trk.set_exhaustive(True)
+    res = trk.track(fr.depth, descriptors=fr.descriptors, keypoints=fr.keypoints)
+    trk.close()
+    ores, osel, opts, _ = _oracle_frame(tpl, graph, graph.warps, fr, feats, cam, 5)
+    np.testing.assert_array_equal(res.matches.preselected, osel.flags)
+    assert res.report.n_correspondences == ores.n_correspondences
+    assert res.report.accepted_steps == ores.accepted_steps
+    assert float(np.abs(res.points - opts).max()) < VERTEX_TOL_MM
