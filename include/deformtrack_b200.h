@@ -174,6 +174,23 @@ int dt_connection_candidates(const double* ctrl, int64_t m, double d2_max, int64
 int dt_estimate_point_normals(const double* points, int64_t n, int64_t k, double* normals,
                               int device);
 
+/* ORB front end (not in the reference): FAST-9 corners,
+ * 3x3 non-maximum suppression, uniform suppression (best per_cell per cell of `cell`
+ * px, then the best n_max), intensity-centroid orientation in 30 sectors and 256-bit
+ * rotated BRIEF on 5x5 box sums. pattern_rot (30 x 256 x 4 int8: the test offsets
+ * (ax, ay, bx, by) rotated to each sector) and boundaries (31 x 2 f64 sector-boundary
+ * unit vectors) are built by the caller (paper_2007_08576_b200.orb). One context per
+ * image size; outputs in order of score (descending), ties by pixel index. */
+typedef struct dt_orb dt_orb;
+int dt_orb_create(int height, int width, int threshold, int cell, int per_cell, int n_max,
+                  const int8_t* pattern_rot, const double* boundaries, int device, dt_orb** out);
+int dt_orb_destroy(dt_orb* orb);
+/* image: h x w uint8 (host, or device with on_device); outputs host arrays with room for
+ * n_max: keypoints (n, 2) int32 (u, v), descriptors (n, 32) uint8, scores and sectors
+ * int32 (each may be NULL); *n_out = n. */
+int dt_orb_detect(dt_orb* orb, const uint8_t* image, int on_device, int32_t* keypoints,
+                  uint8_t* descriptors, int32_t* scores, int32_t* sectors, int64_t* n_out);
+
 /* ------------------------------------------------------------------------------
  * Frame level: a device-resident tracker (one per sequence / stream).
  * Replaces solver.solve_frame (solver.py:267-378) and tracking.track_frame

@@ -108,6 +108,10 @@ _SIGNATURES: dict[str, list] = {
     "dt_sample_control_points": [P, I64, F64, P, P, C.c_int],
     "dt_connection_candidates": [P, I64, F64, P, P, I64, P, C.c_int],
     "dt_estimate_point_normals": [P, I64, I64, P, C.c_int],
+    "dt_orb_create": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P, C.c_int,
+                      C.POINTER(P)],
+    "dt_orb_destroy": [P],
+    "dt_orb_detect": [P, P, C.c_int, P, P, P, P, P],
     "dt_tracker_create": [C.POINTER(Config), P, P, P, P, I64, I64, P, P, I64, P, P, I64, C.c_int,
                           P, C.POINTER(P)],
     "dt_tracker_destroy": [P],
