@@ -619,9 +619,6 @@ int launch_bind_points_i32(const double* pts, int64_t n, const double* ctrl, int
   return DT_OK;
 }
 
-int launch_warp_all_i32(const double* pts, const double* nrm, const int32_t* bidx,
-                        const double* alpha, int64_t n, int k, const double* warps, double* out_p,
-                        double* out_n, cudaStream_t s);
 
 }  // namespace dt
 

@@ -33,9 +33,6 @@ int launch_observation_normals(const double* depth, int64_t h, int64_t w, double
                                uint8_t* valid, cudaStream_t s);
 int launch_bind_points_i32(const double* pts, int64_t n, const double* ctrl, int m, int k,
                            double sigma, int32_t* idx, double* w, cudaStream_t s);
-int launch_warp_all_i32(const double* pts, const double* nrm, const int32_t* bidx,
-                        const double* alpha, int64_t n, int k, const double* warps, double* out_p,
-                        double* out_n, cudaStream_t s);
 
 // dt_match.cu
 int launch_hamming(const uint8_t* tdesc, int64_t nt, const uint8_t* fdesc, int64_t nf,

@@ -94,6 +94,8 @@ struct SolverArgs {
   double* lam_hist;   // max_outer x 2
   int32_t* stalled_hist;
   double* wa_out;     // m control_data_weights
+  double* out_p;      // optional (n x 3): the template warped by the solution (tracking.py:87)
+  double* out_n;      // optional (n x 3): its rotated normals
   // optional in-kernel phase trace (CTA 0, thread 0): trace[0] = count, then
   // (code, globaltimer ns) pairs
   long long* trace;

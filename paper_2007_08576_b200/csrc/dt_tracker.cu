@@ -336,35 +336,6 @@ __global__ void k_csr_fill_dev(const int32_t* __restrict__ keys, const int64_t* 
   }
 }
 
-__global__ void k_warp_all_i32(const double* __restrict__ pts, const double* __restrict__ nrm,
-                               const int32_t* __restrict__ bidx, const double* __restrict__ alpha,
-                               int64_t n, int k, const double* __restrict__ warps, double* out_p,
-                               double* out_n) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  double B[8], sgn[KMAX];
-  blend_at(warps, bidx + c * k, alpha + c * k, k, B, sgn);
-  double x0, x1, x2, s2;
-  apply_blend(B, pts[3 * c], pts[3 * c + 1], pts[3 * c + 2], x0, x1, x2, s2);
-  double r0, r1, r2;
-  rotate_normal(B, nrm[3 * c], nrm[3 * c + 1], nrm[3 * c + 2], r0, r1, r2);
-  out_p[3 * c] = x0;
-  out_p[3 * c + 1] = x1;
-  out_p[3 * c + 2] = x2;
-  out_n[3 * c] = r0;
-  out_n[3 * c + 1] = r1;
-  out_n[3 * c + 2] = r2;
-}
-
-int launch_warp_all_i32(const double* pts, const double* nrm, const int32_t* bidx,
-                        const double* alpha, int64_t n, int k, const double* warps, double* out_p,
-                        double* out_n, cudaStream_t s) {
-  if (n == 0) return DT_OK;
-  k_warp_all_i32<<<grid_for(n, 128), 128, 0, s>>>(pts, nrm, bidx, alpha, n, k, warps, out_p, out_n);
-  DT_CHECK_LAUNCH();
-  return DT_OK;
-}
-
 }  // namespace dt
 
 using namespace dt;
@@ -615,6 +586,8 @@ void fill_args(dt_tracker* t) {
   a.lam_hist = t->lam_hist;
   a.stalled_hist = t->stalled_hist;
   a.wa_out = t->wa_out;
+  a.out_p = t->out_p;
+  a.out_n = t->out_n;
   a.trace = t->profiling ? t->trace : nullptr;
   a.trace_cap = t->trace_cap;
   a.arrivals = t->profiling ? t->arrivals : nullptr;
@@ -848,10 +821,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   DT_TRY(solver_launch(t->dev_args, 1, t->cluster, (int)t->m, (int)t->k, t->grid_mode, s));
   ++t->launches;
   mark(t, 5);
-  // ---- output warp (tracking.py:87) ----
-  DT_TRY(launch_warp_all_i32(t->tp, t->tn, t->bidx, t->bw, t->n, (int)t->k, t->warps_out, t->out_p,
-                             t->out_n, s));
-  ++t->launches;
+  // ---- output warp (tracking.py:87): done by the solver's final phase ----
   mark(t, 6);
   return DT_OK;
 }
