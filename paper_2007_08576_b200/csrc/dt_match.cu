@@ -433,18 +433,22 @@ k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
 
 // Winner = max support, ties -> lower reference index (matching.py:198-206); then the
 // flags and weights of every match (matching.py:210-213).
-__global__ void k_preselect_final(const double* __restrict__ src, const double* __restrict__ dst,
-                                  const int64_t* __restrict__ n_dev, int64_t n_fixed,
-                                  const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive,
-                                  double H, double inlier_min,
-                                  const double* __restrict__ ref_support,
-                                  const double* __restrict__ ref_rot,
-                                  const uint8_t* __restrict__ ref_valid, double* weights,
-                                  uint8_t* flags, double* residuals, double* rotation,
-                                  int64_t* info, double* support_out) {
-  __shared__ double s_sup[512];
-  __shared__ int64_t s_ref[512];
-  __shared__ int64_t s_pos[512];
+// (support, reference) of b beats a: larger support, ties -> lower reference index
+__device__ __forceinline__ bool ref_better(double bs, int64_t br, double as, int64_t ar) {
+  return br >= 0 && (ar < 0 || bs > as || (bs == as && br < ar));
+}
+
+__global__ void __launch_bounds__(1024)
+k_preselect_final(const double* __restrict__ src, const double* __restrict__ dst,
+                  const int64_t* __restrict__ n_dev, int64_t n_fixed,
+                  const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive, double H,
+                  double inlier_min, const double* __restrict__ ref_support,
+                  const double* __restrict__ ref_rot, const uint8_t* __restrict__ ref_valid,
+                  double* weights, uint8_t* flags, double* residuals, double* rotation,
+                  int64_t* info, double* support_out, FeatureScatter scatter, int do_scatter) {
+  __shared__ double s_sup[32];
+  __shared__ int64_t s_ref[32], s_pos[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = n_dev ? *n_dev : n_fixed;
   const int64_t nr = exhaustive ? n : n_refs;
   double best = -1.0;
@@ -453,32 +457,41 @@ __global__ void k_preselect_final(const double* __restrict__ src, const double* 
     if (!ref_valid[w]) continue;
     const int64_t ref = exhaustive ? w : refs[w];
     const double sp = ref_support[w];
-    if (best_ref < 0 || sp > best || (sp == best && ref < best_ref)) {
+    if (ref_better(sp, ref, best, best_ref)) {
       best = sp;
       best_ref = ref;
       best_pos = w;
     }
   }
-  s_sup[threadIdx.x] = best;
-  s_ref[threadIdx.x] = best_ref;
-  s_pos[threadIdx.x] = best_pos;
-  __syncthreads();
-  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
-    if ((int)threadIdx.x < off) {
-      const double os = s_sup[threadIdx.x + off];
-      const int64_t orf = s_ref[threadIdx.x + off];
-      const int64_t op = s_pos[threadIdx.x + off];
-      const int64_t me = s_ref[threadIdx.x];
-      if (orf >= 0 && (me < 0 || os > s_sup[threadIdx.x] || (os == s_sup[threadIdx.x] && orf < me))) {
-        s_sup[threadIdx.x] = os;
-        s_ref[threadIdx.x] = orf;
-        s_pos[threadIdx.x] = op;
-      }
+  // argmax in a total order: warp shuffles, then the warps' winners
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double os = __shfl_xor_sync(0xffffffffu, best, o);
+    const int64_t orf = __shfl_xor_sync(0xffffffffu, best_ref, o);
+    const int64_t op = __shfl_xor_sync(0xffffffffu, best_pos, o);
+    if (ref_better(os, orf, best, best_ref)) {
+      best = os;
+      best_ref = orf;
+      best_pos = op;
     }
-    __syncthreads();
   }
-  const int64_t ref = s_ref[0];
-  const int64_t pos = s_pos[0];
+  if (lane == 0) {
+    s_sup[warp] = best;
+    s_ref[warp] = best_ref;
+    s_pos[warp] = best_pos;
+  }
+  __syncthreads();
+  const int nw = (int)(blockDim.x >> 5);
+  best = -1.0;
+  best_ref = -1;
+  best_pos = -1;
+  for (int w2 = 0; w2 < nw; ++w2)
+    if (ref_better(s_sup[w2], s_ref[w2], best, best_ref)) {
+      best = s_sup[w2];
+      best_ref = s_ref[w2];
+      best_pos = s_pos[w2];
+    }
+  const int64_t ref = best_ref, pos = best_pos;
   if (ref < 0) {
     for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
       weights[k] = 0.0;
@@ -492,31 +505,37 @@ __global__ void k_preselect_final(const double* __restrict__ src, const double* 
       if (rotation)
         for (int i = 0; i < 9; ++i) rotation[i] = (i % 4 == 0) ? 1.0 : 0.0;
     }
-    return;
-  }
-  double R[9];
+  } else {
+    double R[9];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) R[i] = ref_rot[9 * pos + i];
-  const double rs0 = src[3 * ref], rs1 = src[3 * ref + 1], rs2 = src[3 * ref + 2];
-  const double rd0 = dst[3 * ref], rd1 = dst[3 * ref + 1], rd2 = dst[3 * ref + 2];
-  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
-    const double s1[3] = {src[3 * k] - rs0, src[3 * k + 1] - rs1, src[3 * k + 2] - rs2};
-    const double s2[3] = {dst[3 * k] - rd0, dst[3 * k + 1] - rd1, dst[3 * k + 2] - rd2};
-    const double d = rot_residual(R, s1, s2);
-    const double fw = reweight(d, H);
-    const bool flag = fw >= inlier_min;
-    double soft = 1.0 - d / (5.0 * H);
-    soft = soft < 0.0 ? 0.0 : (soft > 1.0 ? 1.0 : soft);
-    weights[k] = flag ? fw : soft;
-    flags[k] = flag ? 1 : 0;
-    if (residuals) residuals[k] = d;
+    for (int i = 0; i < 9; ++i) R[i] = ref_rot[9 * pos + i];
+    const double rs0 = src[3 * ref], rs1 = src[3 * ref + 1], rs2 = src[3 * ref + 2];
+    const double rd0 = dst[3 * ref], rd1 = dst[3 * ref + 1], rd2 = dst[3 * ref + 2];
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+      const double s1[3] = {src[3 * k] - rs0, src[3 * k + 1] - rs1, src[3 * k + 2] - rs2};
+      const double s2[3] = {dst[3 * k] - rd0, dst[3 * k + 1] - rd1, dst[3 * k + 2] - rd2};
+      const double d = rot_residual(R, s1, s2);
+      const double fw = reweight(d, H);
+      const bool flag = fw >= inlier_min;
+      double soft = 1.0 - d / (5.0 * H);
+      soft = soft < 0.0 ? 0.0 : (soft > 1.0 ? 1.0 : soft);
+      weights[k] = flag ? fw : soft;
+      flags[k] = flag ? 1 : 0;
+      if (residuals) residuals[k] = d;
+    }
+    if (threadIdx.x == 0) {
+      info[0] = DT_OK;
+      info[1] = ref;
+      if (support_out) support_out[0] = best;
+      if (rotation)
+        for (int i = 0; i < 9; ++i) rotation[i] = R[i];
+    }
   }
-  if (threadIdx.x == 0) {
-    info[0] = DT_OK;
-    info[1] = ref;
-    if (support_out) support_out[0] = s_sup[0];
-    if (rotation)
-      for (int i = 0; i < 9; ++i) rotation[i] = R[i];
+  // ORB path: the weights to their template features + the report statistics, in the
+  // same CTA (this CTA's global writes above are visible after the barrier)
+  if (do_scatter) {
+    __syncthreads();
+    feature_scatter_block(scatter, n, weights, flags);
   }
 }
 
@@ -524,7 +543,8 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
                      const int64_t* refs, int64_t n_refs, int exhaustive, double H, int iters,
                      double inlier_min, double min_support, double* weights, uint8_t* flags,
                      double* residuals, double* rotation, int64_t* info, double* support,
-                     double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s) {
+                     double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s,
+                     const FeatureScatter* scatter) {
   const int64_t nr = exhaustive ? n_max : n_refs;
   if (nr > 0) {
     // One warp per hypothesis. The busiest SM sets the time (FP64 pipe ~76 % busy there),
@@ -542,9 +562,11 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
         ref_rot, ref_valid);
     DT_CHECK_LAUNCH();
   }
-  k_preselect_final<<<1, 512, 0, s>>>(src, dst, n_dev, n_max, refs, n_refs, exhaustive, H,
-                                       inlier_min, ref_support, ref_rot, ref_valid, weights, flags,
-                                       residuals, rotation, info, support);
+  const FeatureScatter fs = scatter ? *scatter : FeatureScatter{};
+  k_preselect_final<<<1, 1024, 0, s>>>(src, dst, n_dev, n_max, refs, n_refs, exhaustive, H,
+                                        inlier_min, ref_support, ref_rot, ref_valid, weights, flags,
+                                        residuals, rotation, info, support, fs,
+                                        scatter ? 1 : 0);
   DT_CHECK_LAUNCH();
   return DT_OK;
 }

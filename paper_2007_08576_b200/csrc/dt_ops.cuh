@@ -5,6 +5,8 @@
 
 #include <cstdint>
 
+#include "dt_common.cuh"
+
 namespace dt {
 
 // Per-correspondence ICP record (stage 1 of kernels.icp_reduce): raw residual, robust
@@ -34,6 +36,65 @@ int launch_observation_normals(const double* depth, int64_t h, int64_t w, double
 int launch_bind_points_i32(const double* pts, int64_t n, const double* ctrl, int m, int k,
                            double sigma, int32_t* idx, double* w, cudaStream_t s);
 
+// ORB path: scatter the preselected pairs back to their template features (weight 0 for
+// every feature without an active match) and the report statistics n_preselected and
+// match_weight_sum (solver.py:368-370), summed in a fixed order (warp sums of each
+// 1024-thread round, warps in order). Whole CTA of 1024 threads.
+struct FeatureScatter {
+  int64_t n_feat;
+  const double* dst;       // (n, 3) observed points of the compacted matches
+  const int32_t* feat_id;  // (n,) template feature of each match
+  double* ffo;             // (n_feat, 3) observed point per feature
+  double* ffw;             // (n_feat,) weight per feature
+  int64_t* n_active;
+  double* stats;           // [match_weight_sum, n_preselected]
+};
+
+__device__ __forceinline__ void feature_scatter_block(const FeatureScatter& F, int64_t n,
+                                                      const double* weights,
+                                                      const uint8_t* flags) {
+  __shared__ double s_fsum[32];
+  __shared__ int s_fcnt[32];
+  for (int64_t f = threadIdx.x; f < F.n_feat; f += blockDim.x) F.ffw[f] = 0.0;
+  __syncthreads();
+  double wsum = 0.0;
+  int64_t nflag = 0;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t j = base + threadIdx.x;
+    const bool in = j < n;
+    const double w = in ? weights[j] : 0.0;
+    if (in) {
+      const int f = F.feat_id[j];
+      F.ffw[f] = w;
+      F.ffo[3 * f] = F.dst[3 * j];
+      F.ffo[3 * f + 1] = F.dst[3 * j + 1];
+      F.ffo[3 * f + 2] = F.dst[3 * j + 2];
+    }
+    const double v = warp_sum(w);
+    int flg = (in && flags[j]) ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) flg += __shfl_xor_sync(0xffffffffu, flg, o);
+    if ((threadIdx.x & 31) == 0) {
+      s_fsum[threadIdx.x >> 5] = v;
+      s_fcnt[threadIdx.x >> 5] = flg;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double cs = 0.0;
+      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) {
+        cs += s_fsum[w2];
+        nflag += s_fcnt[w2];
+      }
+      wsum += cs;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *F.n_active = F.n_feat;
+    F.stats[0] = wsum;
+    F.stats[1] = (double)nflag;
+  }
+}
+
 // dt_match.cu
 int launch_hamming(const uint8_t* tdesc, int64_t nt, const uint8_t* fdesc, int64_t nf,
                    int32_t* best_idx, int32_t* best_dist, cudaStream_t s,
@@ -43,7 +104,8 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
                      const int64_t* refs, int64_t n_refs, int exhaustive, double H, int iters,
                      double inlier_min, double min_support, double* weights, uint8_t* flags,
                      double* residuals, double* rotation, int64_t* info, double* support,
-                     double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s);
+                     double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s,
+                     const FeatureScatter* scatter = nullptr);
 
 // dt_solver.cu
 int solver_max_cluster(int device);

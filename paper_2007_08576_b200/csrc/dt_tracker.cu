@@ -222,57 +222,6 @@ k_active(const int64_t* __restrict__ n_dev, const double* __restrict__ weights,
   }
 }
 
-// ORB path: scatter the preselected pairs back to their template features (weight 0 for
-// every feature without an active match) and the report statistics n_preselected and
-// match_weight_sum (solver.py:368-370), summed in the same fixed order as k_active.
-__global__ void __launch_bounds__(1024)
-k_feature_weights(const int64_t* __restrict__ n_dev, int64_t n_feat, const double* __restrict__ weights,
-                  const uint8_t* __restrict__ flags, const double* __restrict__ dst,
-                  const int32_t* __restrict__ feat_id, double* __restrict__ ffo,
-                  double* __restrict__ ffw, int64_t* __restrict__ n_active, double* __restrict__ stats) {
-  __shared__ double s_sum[32];
-  __shared__ int s_cnt[32];
-  const int64_t n = *n_dev;
-  for (int64_t f = threadIdx.x; f < n_feat; f += blockDim.x) ffw[f] = 0.0;
-  __syncthreads();
-  double wsum = 0.0;
-  int64_t nflag = 0;
-  for (int64_t base = 0; base < n; base += blockDim.x) {
-    const int64_t j = base + threadIdx.x;
-    const bool in = j < n;
-    const double w = in ? weights[j] : 0.0;
-    if (in) {
-      const int f = feat_id[j];
-      ffw[f] = w;
-      ffo[3 * f] = dst[3 * j];
-      ffo[3 * f + 1] = dst[3 * j + 1];
-      ffo[3 * f + 2] = dst[3 * j + 2];
-    }
-    const double v = warp_sum(w);
-    int flg = (in && flags[j]) ? 1 : 0;
-    for (int o = 16; o > 0; o >>= 1) flg += __shfl_xor_sync(0xffffffffu, flg, o);
-    if ((threadIdx.x & 31) == 0) {
-      s_sum[threadIdx.x >> 5] = v;
-      s_cnt[threadIdx.x >> 5] = flg;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double cs = 0.0;
-      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) {
-        cs += s_sum[w2];
-        nflag += s_cnt[w2];
-      }
-      wsum += cs;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    *n_active = n_feat;
-    stats[0] = wsum;
-    stats[1] = (double)nflag;
-  }
-}
-
 // Control -> (match * k + slot) CSR over the active matches, count read on the device.
 __global__ void k_csr_count_dev(const int32_t* __restrict__ keys, const int64_t* __restrict__ n_dev,
                                 int k, int m, int* __restrict__ cnt) {
@@ -767,11 +716,15 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
       n_refs = in->n_refs;
     }
     if (!exhaustive && n_refs > t->match_cap) DT_TRY(ensure_match_capacity(t, n_refs));
+    // ORB path: the final preselection kernel also scatters the weights to the template
+    // features (matches indexed by feature: static points / binding / CSR)
+    FeatureScatter fs{t->n_feat, t->m_dst, t->m_feat, t->ffo, t->ffw, t->info + 3, t->astats};
     DT_TRY(launch_preselect(t->m_src, t->m_dst, t->info + 2, n_max, t->refs, n_refs, exhaustive,
                             c.preselect.distance_threshold, c.preselect.n_reweight_iters,
                             c.preselect.inlier_weight_min, c.preselect.min_support, t->m_w,
                             t->m_flags, t->m_res, nullptr, t->info, t->pstats, t->ref_support,
-                            t->ref_rot, t->ref_valid, s));
+                            t->ref_rot, t->ref_valid, s,
+                            in->frame_desc != nullptr ? &fs : nullptr));
     t->launches += 2;
   } else {
     k_set_i64<<<1, 1, 0, s>>>(t->info + 2, 0);
@@ -784,13 +737,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     t->orb_static = orb_static;
     t->args_dirty = true;
   }
-  if (orb_static) {
-    // matches indexed by template feature: static points / binding / CSR
-    k_feature_weights<<<1, 1024, 0, s>>>(t->info + 2, t->n_feat, t->m_w, t->m_flags, t->m_dst,
-                                         t->m_feat, t->ffo, t->ffw, t->info + 3, t->astats);
-    DT_CHECK_LAUNCH();
-    t->launches += 1;
-  } else {
+  if (!orb_static) {
     k_active<<<1, 1024, 0, s>>>(t->info + 2, t->m_w, t->m_flags, t->m_src, t->m_dst, t->m_bidx,
                                 t->m_bw, (int)t->k, use ? 1 : 0, t->fp, t->fo, t->fwt, t->fbidx,
                                 t->fbw, t->info + 3, t->astats);
