@@ -215,7 +215,8 @@ def solver_algorithmic_bytes(n, m, e, k, n_valid, n_active, report):
     relink 100 B/point (p, n, binding, depth + obs-normal gather, writes); linearization
     68 B/valid correspondence + 60 B/match + 232 B/control; rigidity pass 16 B/edge +
     312 B/control; damped solve 328 B/control/attempt; tentative value pass
-    64 B/valid correspondence + 60 B/match + 16 B/edge + 96 B/control."""
+    64 B/valid correspondence + 60 B/match + 16 B/edge + 96 B/control; the output warp
+    folded into its final phase 80 B/point (p, n, binding in; warped p, n out)."""
     it = int(report.outer_iterations)
     attempts = int(report.accepted_steps) + int(report.rejected_steps) + int(report.converged)
     relinks = it + 1
@@ -223,7 +224,7 @@ def solver_algorithmic_bytes(n, m, e, k, n_valid, n_active, report):
     arap = it * (e * 16 + m * 88 + m * 28 * 8)
     solves = attempts * m * (27 * 8 + 64 + 48)
     value = (attempts + 1) * (n_valid * 64 + n_active * 60 + e * 16 + m * 96)
-    return relinks * n * 100 + lin + arap + solves + value
+    return relinks * n * 100 + lin + arap + solves + value + n * 80
 
 
 def measured_peaks():
