@@ -544,7 +544,7 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
                      double inlier_min, double min_support, double* weights, uint8_t* flags,
                      double* residuals, double* rotation, int64_t* info, double* support,
                      double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s,
-                     const FeatureScatter* scatter) {
+                     const FeatureScatter* scatter, int shared_gpu) {
   const int64_t nr = exhaustive ? n_max : n_refs;
   if (nr > 0) {
     // One warp per hypothesis. The busiest SM sets the time (FP64 pipe ~76 % busy there),
@@ -556,7 +556,10 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
-    const int64_t wpc = std::min<int64_t>(16, std::max<int64_t>(1, (nr + sms - 1) / sms));
+    // Sharing the GPU with other sequences (cluster mode), small 8-warp CTAs pack
+    // between the other kernels' CTAs instead.
+    const int64_t wpc = shared_gpu ? 8
+                                   : std::min<int64_t>(16, std::max<int64_t>(1, (nr + sms - 1) / sms));
     k_preselect_warp<<<(unsigned)((nr + wpc - 1) / wpc), (unsigned)(32 * wpc), 0, s>>>(
         src, dst, n_dev, n_max, refs, n_refs, exhaustive, H, iters, min_support, ref_support,
         ref_rot, ref_valid);

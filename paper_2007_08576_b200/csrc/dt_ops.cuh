@@ -105,7 +105,7 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
                      double inlier_min, double min_support, double* weights, uint8_t* flags,
                      double* residuals, double* rotation, int64_t* info, double* support,
                      double* ref_support, double* ref_rot, uint8_t* ref_valid, cudaStream_t s,
-                     const FeatureScatter* scatter = nullptr);
+                     const FeatureScatter* scatter = nullptr, int shared_gpu = 0);
 
 // dt_solver.cu
 int solver_max_cluster(int device);

@@ -285,6 +285,37 @@ __global__ void k_csr_fill_dev(const int32_t* __restrict__ keys, const int64_t* 
   }
 }
 
+// Output warp as its own launch (cluster mode: a sequence's solver has only a few CTAs,
+// so the full-GPU kernel finishes sooner than the solver's final phase would)
+__global__ void k_warp_all_i32(const double* __restrict__ pts, const double* __restrict__ nrm,
+                               const int32_t* __restrict__ bidx, const double* __restrict__ alpha,
+                               int64_t n, int k, const double* __restrict__ warps, double* out_p,
+                               double* out_n) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double B[8], sgn[KMAX];
+  blend_at(warps, bidx + c * k, alpha + c * k, k, B, sgn);
+  double x0, x1, x2, s2;
+  apply_blend(B, pts[3 * c], pts[3 * c + 1], pts[3 * c + 2], x0, x1, x2, s2);
+  double r0, r1, r2;
+  rotate_normal(B, nrm[3 * c], nrm[3 * c + 1], nrm[3 * c + 2], r0, r1, r2);
+  out_p[3 * c] = x0;
+  out_p[3 * c + 1] = x1;
+  out_p[3 * c + 2] = x2;
+  out_n[3 * c] = r0;
+  out_n[3 * c + 1] = r1;
+  out_n[3 * c + 2] = r2;
+}
+
+int launch_warp_all_i32(const double* pts, const double* nrm, const int32_t* bidx,
+                        const double* alpha, int64_t n, int k, const double* warps, double* out_p,
+                        double* out_n, cudaStream_t s) {
+  if (n == 0) return DT_OK;
+  k_warp_all_i32<<<grid_for(n, 128), 128, 0, s>>>(pts, nrm, bidx, alpha, n, k, warps, out_p, out_n);
+  DT_CHECK_LAUNCH();
+  return DT_OK;
+}
+
 }  // namespace dt
 
 using namespace dt;
@@ -535,8 +566,9 @@ void fill_args(dt_tracker* t) {
   a.lam_hist = t->lam_hist;
   a.stalled_hist = t->stalled_hist;
   a.wa_out = t->wa_out;
-  a.out_p = t->out_p;
-  a.out_n = t->out_n;
+  // grid mode folds the output warp into the solver's final phase
+  a.out_p = t->grid_mode ? t->out_p : nullptr;
+  a.out_n = t->grid_mode ? t->out_n : nullptr;
   a.trace = t->profiling ? t->trace : nullptr;
   a.trace_cap = t->trace_cap;
   a.arrivals = t->profiling ? t->arrivals : nullptr;
@@ -724,7 +756,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
                             c.preselect.inlier_weight_min, c.preselect.min_support, t->m_w,
                             t->m_flags, t->m_res, nullptr, t->info, t->pstats, t->ref_support,
                             t->ref_rot, t->ref_valid, s,
-                            in->frame_desc != nullptr ? &fs : nullptr));
+                            in->frame_desc != nullptr ? &fs : nullptr, t->grid_mode ? 0 : 1));
     t->launches += 2;
   } else {
     k_set_i64<<<1, 1, 0, s>>>(t->info + 2, 0);
@@ -768,7 +800,12 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   DT_TRY(solver_launch(t->dev_args, 1, t->cluster, (int)t->m, (int)t->k, t->grid_mode, s));
   ++t->launches;
   mark(t, 5);
-  // ---- output warp (tracking.py:87): done by the solver's final phase ----
+  // ---- output warp (tracking.py:87): in grid mode done by the solver's final phase ----
+  if (!t->grid_mode) {
+    DT_TRY(launch_warp_all_i32(t->tp, t->tn, t->bidx, t->bw, t->n, (int)t->k, t->warps_out,
+                               t->out_p, t->out_n, s));
+    ++t->launches;
+  }
   mark(t, 6);
   return DT_OK;
 }
