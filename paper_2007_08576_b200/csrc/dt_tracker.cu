@@ -376,10 +376,16 @@ struct dt_tracker {
   // CUDA graph of the ORB frame body (everything after the input staging), captured once
   // per input signature and replayed: one launch instead of ~14 stream operations
   // [0] no pre-solver wait, [1] / [2] the pipelined path waiting on ev_out_copied[0 / 1]
-  cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};
-  int64_t g_nframe[3] = {-1, -1, -1};
-  int g_launches[3] = {0, 0, 0};
-  bool g_used[3] = {false, false, false};
+  // captured frame bodies, per (pre-solver wait variant) x (input set: own buffers or
+  // one of the two staging slots of the pipelined path)
+  static constexpr int NG = 9;
+  cudaGraphExec_t gexec[NG] = {};
+  int64_t g_nframe[NG] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+  int g_launches[NG] = {};
+  bool g_used[NG] = {};
+  // input set of the frame being enqueued: 0 = the tracker's own depth / descriptor /
+  // keypoint buffers, 1 + s = staging slot s (read in place, no device-to-device copy)
+  int in_set = 0;
   bool graphs_off = false;
   // pipelined submission (dt_track_frame_submit / dt_tracker_wait): host inputs are staged
   // into one of two device slots on a copy stream while the previous frame computes;
@@ -578,11 +584,14 @@ void fill_args(dt_tracker* t) {
   a.red_g = t->red_g;
 }
 
+// the solver's arguments for each input set (they differ only in the depth they read)
 int push_args(dt_tracker* t) {
   fill_args(t);
   t->args_dirty = false;
-  DT_CHECK_CUDA(cudaMemcpyAsync(t->dev_args, &t->host_args, sizeof(SolverArgs),
-                                cudaMemcpyHostToDevice, t->stream));
+  SolverArgs v[3] = {t->host_args, t->host_args, t->host_args};
+  for (int i = 0; i < 2; ++i)
+    if (t->in_depth[i]) v[1 + i].depth = t->in_depth[i];
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->dev_args, v, sizeof(v), cudaMemcpyHostToDevice, t->stream));
   DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
   return DT_OK;
 }
@@ -668,14 +677,18 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   // warm start: the previous solution (or set_warps) is in warps_out
   DT_CHECK_CUDA(cudaMemcpyAsync(t->warp_a, t->warps_out, sizeof(double) * 8 * t->m,
                                 cudaMemcpyDeviceToDevice, s));
-  if (in->depth != t->depth)
-    DT_CHECK_CUDA(cudaMemcpyAsync(t->depth, in->depth, sizeof(double) * npix, kind, s));
-    if (in->normals) {
+  // input set: the tracker's buffers (copied into) or a staging slot (read in place)
+  const int set = t->in_set;
+  double* dep = set ? t->in_depth[set - 1] : t->depth;
+  DT_REQUIRE(!set || in->depth == dep, DT_ERR_INVALID_ARGUMENT, "staged depth mismatch");
+  if (in->depth != dep)
+    DT_CHECK_CUDA(cudaMemcpyAsync(dep, in->depth, sizeof(double) * npix, kind, s));
+  if (in->normals) {
     DT_CHECK_CUDA(cudaMemcpyAsync(t->onrm, in->normals, sizeof(double) * 3 * npix, kind, s));
-    k_valid_mask<<<grid_for(npix, 256), 256, 0, s>>>(t->depth, npix, c.z_min, c.z_max, t->dvalid);
+    k_valid_mask<<<grid_for(npix, 256), 256, 0, s>>>(dep, npix, c.z_min, c.z_max, t->dvalid);
     DT_CHECK_LAUNCH();
   } else {
-    DT_TRY(launch_observation_normals(t->depth, c.height, c.width, c.fx, c.fy, c.cx, c.cy, c.z_min,
+    DT_TRY(launch_observation_normals(dep, c.height, c.width, c.fx, c.fy, c.cx, c.cy, c.z_min,
                                       c.z_max, t->onrm, t->dvalid, s));
   }
   ++t->launches;
@@ -686,20 +699,24 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   int64_t n_max = 0;
   if (use && in->frame_desc != nullptr) {
     DT_REQUIRE(t->n_feat > 0, DT_ERR_INVALID_ARGUMENT, "frame descriptors given but no template features set");
-    if (in->n_frame > t->fdesc_cap) {
+    if (!set && in->n_frame > t->fdesc_cap) {
       const int64_t cap = std::max<int64_t>(in->n_frame, 256);
       DT_TRY(dalloc(t, &t->fdesc, 32 * cap));
       DT_TRY(dalloc(t, &t->fkp, 2 * cap));
       t->fdesc_cap = cap;
     }
-    if (in->frame_desc != t->fdesc)
-      DT_CHECK_CUDA(cudaMemcpyAsync(t->fdesc, in->frame_desc, 32 * in->n_frame, kind, s));
-    if (in->frame_kp != t->fkp)
-      DT_CHECK_CUDA(cudaMemcpyAsync(t->fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
-    DT_TRY(launch_hamming(t->tdesc, t->n_feat, t->fdesc, in->n_frame, nullptr, nullptr, s,
+    uint8_t* fdesc = set ? t->in_desc[set - 1] : t->fdesc;
+    int32_t* fkp = set ? t->in_kp[set - 1] : t->fkp;
+    DT_REQUIRE(!set || (in->frame_desc == fdesc && in->frame_kp == fkp), DT_ERR_INVALID_ARGUMENT,
+               "staged descriptors mismatch");
+    if (in->frame_desc != fdesc)
+      DT_CHECK_CUDA(cudaMemcpyAsync(fdesc, in->frame_desc, 32 * in->n_frame, kind, s));
+    if (in->frame_kp != fkp)
+      DT_CHECK_CUDA(cudaMemcpyAsync(fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
+    DT_TRY(launch_hamming(t->tdesc, t->n_feat, fdesc, in->n_frame, nullptr, nullptr, s,
                           t->ham_packed));
-    k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_packed, c.max_hamming, t->fkp,
-                                       in->n_frame, t->depth, c.z_min, c.z_max, c.width, c.height, c.fx,
+    k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_packed, c.max_hamming, fkp,
+                                       in->n_frame, dep, c.z_min, c.z_max, c.width, c.height, c.fx,
                                        c.fy, c.cx, c.cy, t->tfeat_pts, t->m_src, t->m_dst, t->m_feat,
                                        t->info + 2);
     DT_CHECK_LAUNCH();
@@ -788,16 +805,10 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   mark(t, 4);
 
   // ---- solve ----
-  if (t->args_dirty) {
-    fill_args(t);
-    DT_CHECK_CUDA(cudaMemcpyAsync(t->dev_args, &t->host_args, sizeof(SolverArgs),
-                                  cudaMemcpyHostToDevice, s));
-    DT_CHECK_CUDA(cudaStreamSynchronize(s));
-    t->args_dirty = false;
-  }
+  if (t->args_dirty) DT_TRY(push_args(t));
   DT_CHECK_CUDA(cudaMemsetAsync(t->stalled_hist, 0, sizeof(int32_t) * c.max_outer_iters, s));
   if (t->pre_solver_wait) DT_CHECK_CUDA(cudaStreamWaitEvent(s, t->pre_solver_wait, 0));
-  DT_TRY(solver_launch(t->dev_args, 1, t->cluster, (int)t->m, (int)t->k, t->grid_mode, s));
+  DT_TRY(solver_launch(t->dev_args + t->in_set, 1, t->cluster, (int)t->m, (int)t->k, t->grid_mode, s));
   ++t->launches;
   mark(t, 5);
   // ---- output warp (tracking.py:87): in grid mode done by the solver's final phase ----
@@ -860,7 +871,7 @@ int collect_outputs(dt_tracker* t, const dt_frame_input* in, dt_frame_output* ou
 }
 
 void drop_graph(dt_tracker* t) {
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < dt_tracker::NG; ++i) {
     if (t->gexec[i]) cudaGraphExecDestroy(t->gexec[i]);
     t->gexec[i] = nullptr;
     t->g_nframe[i] = -1;
@@ -872,24 +883,30 @@ void drop_graph(dt_tracker* t) {
 // device): stage the inputs into the tracker's own buffers, then replay the captured
 // body. Anything else -- or a failed capture -- runs the stream-ordered path.
 int run_frame(dt_tracker* t, const dt_frame_input* in, bool* used) {
+  const int set = t->in_set;
+  const int64_t cap = set ? t->in_desc_cap : t->fdesc_cap;
   const bool eligible = !t->graphs_off && !t->profiling && !t->args_dirty && in->depth != nullptr &&
                         in->normals == nullptr && in->use_matches && in->frame_desc != nullptr &&
-                        in->frame_kp != nullptr && in->n_frame > 0 && in->n_frame <= t->fdesc_cap &&
+                        in->frame_kp != nullptr && in->n_frame > 0 && in->n_frame <= cap &&
                         t->orb_static;
   if (!eligible) return enqueue_frame(t, in, used);
   cudaStream_t s = t->stream;
-  const cudaMemcpyKind kind = in->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  const int64_t npix = (int64_t)t->cfg.width * t->cfg.height;
-  DT_CHECK_CUDA(cudaMemcpyAsync(t->depth, in->depth, sizeof(double) * npix, kind, s));
-  DT_CHECK_CUDA(cudaMemcpyAsync(t->fdesc, in->frame_desc, 32 * in->n_frame, kind, s));
-  DT_CHECK_CUDA(cudaMemcpyAsync(t->fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
   dt_frame_input gin = *in;
   gin.on_device = 1;
-  gin.depth = t->depth;
-  gin.frame_desc = t->fdesc;
-  gin.frame_kp = t->fkp;
-  const int gi = t->pre_solver_wait == nullptr ? 0
+  if (set == 0) {
+    // own input buffers: copy the caller's arrays in, then replay
+    const cudaMemcpyKind kind = in->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const int64_t npix = (int64_t)t->cfg.width * t->cfg.height;
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->depth, in->depth, sizeof(double) * npix, kind, s));
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->fdesc, in->frame_desc, 32 * in->n_frame, kind, s));
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
+    gin.depth = t->depth;
+    gin.frame_desc = t->fdesc;
+    gin.frame_kp = t->fkp;
+  }  // else: a staging slot, read in place by its own graph
+  const int gw = t->pre_solver_wait == nullptr ? 0
                  : (t->copy_stream && t->pre_solver_wait == t->ev_out_copied[0] ? 1 : 2);
+  const int gi = 3 * gw + set;
   if (t->gexec[gi] == nullptr || t->g_nframe[gi] != in->n_frame) {
     if (t->gexec[gi]) cudaGraphExecDestroy(t->gexec[gi]);
     t->gexec[gi] = nullptr;
@@ -1057,7 +1074,7 @@ static int tracker_init(dt_tracker* t, const dt_config* cfg, const double* t_poi
   DT_TRY(dalloc(t, &t->wa_out, m));
   DT_TRY(dalloc(t, &t->out_p, 3 * n));
   DT_TRY(dalloc(t, &t->out_n, 3 * n));
-  DT_TRY(dalloc(t, &t->dev_args, 1));
+  DT_TRY(dalloc(t, &t->dev_args, 3));
   DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_report, sizeof(dt_report)));
   DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_info, sizeof(int64_t) * 4));
   DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_stats, sizeof(double) * 4));
@@ -1262,6 +1279,7 @@ int ensure_pipeline(dt_tracker* t, int64_t n_desc) {
       DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_done[i], cudaEventDisableTiming));
       DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_out_copied[i], cudaEventDisableTiming));
       DT_TRY(dalloc(t, &t->in_depth[i], npix));
+      t->args_dirty = true;  // the solver's per-slot arguments point at the new buffers
       DT_TRY(dalloc(t, &t->stage_info[i], STAGE_WORDS));
       DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_stage[i], sizeof(int64_t) * STAGE_WORDS));
     }
@@ -1273,6 +1291,7 @@ int ensure_pipeline(dt_tracker* t, int64_t n_desc) {
       DT_TRY(dalloc(t, &t->in_kp[i], 2 * cap));
     }
     t->in_desc_cap = cap;
+    drop_graph(t);  // captured bodies read the old staging buffers
   }
   return DT_OK;
 }
@@ -1348,9 +1367,11 @@ int dt_track_frame_submit(dt_tracker* t, const dt_frame_input* in, dt_frame_outp
   din.frame_desc = nd > 0 ? t->in_desc[slot] : nullptr;
   din.frame_kp = nd > 0 ? t->in_kp[slot] : nullptr;
   t->pre_solver_wait = t->pipe_next > 0 ? t->ev_out_copied[1 - slot] : nullptr;
+  t->in_set = 1 + slot;  // the frame reads the staging slot in place
   bool used = false;
   const int st = run_frame(t, &din, &used);
   t->pre_solver_wait = nullptr;
+  t->in_set = 0;
   DT_TRY(st);
   t->last_used = used;
   DT_CHECK_CUDA(cudaEventRecord(t->ev_in_free[slot], s));
