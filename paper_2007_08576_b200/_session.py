@@ -74,11 +74,30 @@ class FrameOutputs:
     match_dst: np.ndarray | None = None
 
 
+def _want(a, shape, name) -> None:
+    """Shape check before a pointer crosses the C-ABI (which trusts the sizes)."""
+    got = tuple(int(x) for x in (a.shape if hasattr(a, "shape") else np.shape(a)))
+    if got != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {got}")
+
+
 class DeviceTracker:
     """One sequence resident on one device (one stream)."""
 
     def __init__(self, template, graph, cfg: Config, device: int | None = None,
                  stream: int | None = None):
+        # the C-ABI trusts the sizes it is given: reject inconsistent arrays here
+        n, m = len(template.points), len(graph.points)
+        _want(template.normals, (n, 3), "template normals")
+        if template.bind_indices is None or template.bind_weights is None:
+            raise ValueError("template must be bound to the control graph first")
+        k = int(np.shape(template.bind_indices)[1]) if np.ndim(template.bind_indices) == 2 else -1
+        _want(template.bind_indices, (n, k), "template bind_indices")
+        _want(template.bind_weights, (n, k), "template bind_weights")
+        _want(graph.warps, (m, 8), "graph warps")
+        ne = int(np.size(graph.edges)) // 2
+        _want(graph.edges, (ne, 2), "graph edges")
+        _want(graph.edge_weights, (ne,), "graph edge_weights")
         dev.require_cuda()
         import torch
 
@@ -158,6 +177,10 @@ class DeviceTracker:
             keep.append(arr)
             return _host_ptr(arr)
 
+        h, w = int(self._cfg.height), int(self._cfg.width)
+        _want(depth, (h, w), "depth")
+        if normals is not None:
+            _want(normals, (h, w, 3), "observation normals")
         fi = FrameInput()
         fi.depth = hp(depth, np.float64)
         fi.normals = hp(normals, np.float64)
@@ -165,6 +188,13 @@ class DeviceTracker:
         if pairs is not None:
             src, dst = pairs
             n_pairs = int(np.asarray(src).shape[0]) if not hasattr(src, "shape") else int(src.shape[0])
+            _want(src, (n_pairs, 3), "match template points")
+            _want(dst, (n_pairs, 3), "match observed points")
+            if match_w is not None:
+                _want(match_w, (n_pairs,), "match weights")
+            if match_binding is not None:
+                _want(match_binding[0], (n_pairs, self.k), "match binding indices")
+                _want(match_binding[1], (n_pairs, self.k), "match binding weights")
             fi.match_src = hp(src, np.float64)
             fi.match_dst = hp(dst, np.float64)
             fi.match_w = hp(match_w, np.float64)
@@ -175,11 +205,15 @@ class DeviceTracker:
         n_frame = 0
         if frame_desc is not None:
             n_frame = int(frame_desc.shape[0])
+            _want(frame_desc, (n_frame, 32), "frame descriptors")
+            _want(frame_kp, (n_frame, 2), "frame keypoints")
             fi.frame_desc = hp(frame_desc, np.uint8)
             fi.frame_kp = hp(frame_kp, np.int32)
         fi.n_frame = n_frame
         if refs is not None:
             r = np.ascontiguousarray(refs, dtype=np.int64)
+            if r.ndim != 1:
+                raise ValueError("refs must be a 1-D index array")
             keep.append(r)
             fi.refs = _host_ptr(r)
             fi.n_refs = r.shape[0]

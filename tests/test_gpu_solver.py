@@ -201,3 +201,24 @@ def test_tracker_create_rejects_bad_binding_and_recovers():
     res = trk.track(c["depth"])
     trk.close()
     assert res.report.n_correspondences > 0
+
+
+def test_inconsistent_inputs_raise_before_the_c_abi():
+    """The C-ABI trusts array sizes; the Python layer rejects mismatched shapes."""
+    dt = _api()
+    c = solver_case("solver_fixed_point")
+    fx, fy, cx, cy = c["cam"]
+    cam = dt.PinholeCamera(fx, fy, cx, cy, *c["dims"])
+    tpl, graph = _template_graph(dt, c["tpl"], c["graph"], c["warps_in"], c["radius"])
+    cfg = dt.load_config({})
+    trk = dt.Tracker(tpl, graph, cam, cfg)
+    with pytest.raises(ValueError):
+        trk.track(c["depth"][:-1])                      # wrong depth size
+    with pytest.raises(ValueError):
+        trk.track(c["depth"], descriptors=np.zeros((5, 31), np.uint8),
+                  keypoints=np.zeros((5, 2), np.int32))  # wrong descriptor width
+    res = trk.track(c["depth"])                         # the tracker is still usable
+    trk.close()
+    assert res.report.n_correspondences > 0
+    with pytest.raises(ValueError):
+        dt.Tracker(tpl, graph.with_warps(graph.warps[:-1]), cam, cfg)
