@@ -26,6 +26,18 @@ def _d(a, dtype=np.float64):
     return dev.to_device(np.asarray(a, dtype=dtype))
 
 
+# The C-ABI trusts the sizes it is given; the numba kernels would raise IndexError on the
+# same mismatches, so reject them here.
+def _size(a, count, name):
+    if int(np.size(a)) != int(count):
+        raise ValueError(f"{name}: expected {count} elements, got {int(np.size(a))}")
+
+
+def _index(idx, hi, name):
+    if np.size(idx) and (int(np.min(idx)) < 0 or int(np.max(idx)) >= hi):
+        raise IndexError(f"{name}: index outside [0, {hi})")
+
+
 def warp_and_rasterize(points, normals, bind_idx, alpha, warps, depth, depth_valid,
                        obs_normals, fx, fy, cx, cy, gate_distance, cos_gate, n_chunks):
     pts = np.asarray(points, dtype=np.float64).reshape(-1, 3)
@@ -35,6 +47,11 @@ def warp_and_rasterize(points, normals, bind_idx, alpha, warps, depth, depth_val
     W = np.asarray(warps, dtype=np.float64).reshape(-1, 8)
     depth = np.asarray(depth, dtype=np.float64)
     h, w = depth.shape
+    _size(normals, 3 * n, "normals")
+    _size(alpha, n * k, "alpha")
+    _size(depth_valid, h * w, "depth_valid")
+    _size(obs_normals, 3 * h * w, "obs_normals")
+    _index(bidx, W.shape[0], "bind_idx")
     out_p = dev.empty((n, 3))
     out_n = dev.empty((n, 3))
     valid = dev.empty((n,), np.uint8)
@@ -60,6 +77,14 @@ def icp_reduce(points, obs_normals, obs_points, bind_idx, alpha, warps, basis, t
     bidx = np.asarray(bind_idx, dtype=np.int64).reshape(n, -1) if n else np.zeros((0, 1), np.int64)
     k = bidx.shape[1]
     m = int(m)
+    _size(obs_normals, 3 * n, "obs_normals")
+    _size(obs_points, 3 * n, "obs_points")
+    _size(alpha, n * k, "alpha")
+    _size(warps, 8 * m, "warps")
+    _size(basis, 48 * m, "basis")
+    if use_frozen:
+        _size(frozen, n, "frozen")
+    _index(bidx, m, "bind_idx")
     partial = dev.zeros((m, N_COLS))
     support = dev.zeros((m,))
     cost = dev.zeros((m,))
@@ -82,6 +107,12 @@ def feature_reduce(points, obs_points, match_w, bind_idx, alpha, warps, basis, f
     bidx = np.asarray(bind_idx, dtype=np.int64).reshape(n, -1) if n else np.zeros((0, 1), np.int64)
     k = bidx.shape[1]
     m = int(m)
+    _size(obs_points, 3 * n, "obs_points")
+    _size(match_w, n, "match_w")
+    _size(alpha, n * k, "alpha")
+    _size(warps, 8 * m, "warps")
+    _size(basis, 48 * m, "basis")
+    _index(bidx, m, "bind_idx")
     partial = dev.zeros((m, N_COLS))
     support = dev.zeros((m,))
     cost = dev.zeros((m,))
@@ -99,6 +130,13 @@ def arap_reduce(ctrl_points, R, t, warps, edges, edge_weights, wa, angle_weight,
     E = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
     ne = E.shape[0]
     m = int(m)
+    _size(ctrl_points, 3 * m, "ctrl_points")
+    _size(R, 9 * m, "R")
+    _size(t, 3 * m, "t")
+    _size(warps, 8 * m, "warps")
+    _size(edge_weights, ne, "edge_weights")
+    _size(wa, m, "wa")
+    _index(E, m, "edges")
     partial = dev.zeros((m, N_COLS))
     cost = dev.zeros((m,))
     ins = [_d(ctrl_points), _d(R), _d(t), _d(warps), _d(E, np.int64), _d(edge_weights), _d(wa)]
