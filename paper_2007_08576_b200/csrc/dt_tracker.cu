@@ -1177,6 +1177,9 @@ int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* po
                                     cudaMemcpyDeviceToHost, t->stream));
       DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
     }
+    for (const int32_t key : fb)
+      DT_REQUIRE(key >= 0 && key < t->m, DT_ERR_INVALID_ARGUMENT,
+                 "feature bind index %d outside the control graph (m=%lld)", key, (long long)t->m);
     std::vector<int> keys(fb.begin(), fb.end()), ents(n_features * k), fptr, fent;
     for (int64_t i = 0; i < n_features * k; ++i) ents[i] = (int)i;
     host_csr(keys, ents, (int)t->m, fptr, fent);
