@@ -190,6 +190,10 @@ int dt_orb_destroy(dt_orb* orb);
  * int32 (each may be NULL); *n_out = n. */
 int dt_orb_detect(dt_orb* orb, const uint8_t* image, int on_device, int32_t* keypoints,
                   uint8_t* descriptors, int32_t* scores, int32_t* sectors, int64_t* n_out);
+/* Device pointers to the last detection's keypoints (n, 2) int32 and descriptors
+ * (n, 32) uint8 (valid until the next dt_orb_detect on this context): pass them to
+ * dt_track_frame with on_device = 1 to keep the whole image -> warps path on the GPU. */
+int dt_orb_last(dt_orb* orb, const int32_t** keypoints, const uint8_t** descriptors, int64_t* n);
 
 /* ------------------------------------------------------------------------------
  * Frame level: a device-resident tracker (one per sequence / stream).

@@ -112,6 +112,7 @@ _SIGNATURES: dict[str, list] = {
                       C.POINTER(P)],
     "dt_orb_destroy": [P],
     "dt_orb_detect": [P, P, C.c_int, P, P, P, P, P],
+    "dt_orb_last": [P, C.POINTER(P), C.POINTER(P), P],
     "dt_tracker_create": [C.POINTER(Config), P, P, P, P, I64, I64, P, P, I64, P, P, I64, C.c_int,
                           P, C.POINTER(P)],
     "dt_tracker_destroy": [P],

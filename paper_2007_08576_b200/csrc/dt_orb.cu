@@ -214,6 +214,7 @@ struct dt_orb {
   double* bnd = nullptr;
   int8_t* rot = nullptr;
   int32_t *o_kp = nullptr, *o_score = nullptr, *o_bin = nullptr;
+  int64_t n_last = 0;
   uint8_t* o_desc = nullptr;
 };
 
@@ -379,7 +380,18 @@ int dt_orb_detect(dt_orb* o, const uint8_t* image, int on_device, int32_t* keypo
       DT_CHECK_CUDA(cudaMemcpyAsync(sectors, o->o_bin, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
   }
   DT_CHECK_CUDA(cudaStreamSynchronize(s));
+  o->n_last = n;
   *n_out = n;
+  return DT_OK;
+}
+
+// device-resident results of the last dt_orb_detect (valid until the next call): feed
+// them to dt_track_frame with on_device = 1, no host round trip
+int dt_orb_last(dt_orb* o, const int32_t** keypoints, const uint8_t** descriptors, int64_t* n) {
+  DT_REQUIRE(o != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (keypoints) *keypoints = o->o_kp;
+  if (descriptors) *descriptors = o->o_desc;
+  if (n) *n = o->n_last;
   return DT_OK;
 }
 

@@ -83,6 +83,14 @@ class OrbDetector:
         k = n.value
         return kp[:k].copy(), desc[:k].copy(), sc[:k].copy(), sec[:k].copy()
 
+    def last_on_device(self):
+        """(keypoints device pointer, descriptors device pointer, n) of the last detect:
+        the frame inputs for ``DeviceTracker.track_raw`` with ``on_device = 1``."""
+        kp, de = C.c_void_p(), C.c_void_p()
+        n = C.c_int64(0)
+        check(lib.dt_orb_last(self._h, C.byref(kp), C.byref(de), C.byref(n)), "dt_orb_last")
+        return kp.value, de.value, n.value
+
     def close(self) -> None:
         if self._h:
             lib.dt_orb_destroy(self._h)

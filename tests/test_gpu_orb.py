@@ -94,3 +94,56 @@ def test_hamming_matching_recovers_the_shift():
     vals, counts = np.unique(disp, axis=0, return_counts=True)
     assert tuple(vals[np.argmax(counts)]) == (dx, dy)
     assert counts.max() > 0.5 * good.sum()
+
+
+def test_device_resident_orb_output_feeds_the_tracker():
+    """image -> ORB (device) -> Hamming -> preselection -> LM with the detector's
+    keypoints / descriptors read in place (on_device frame input) gives exactly what the
+    host round trip gives."""
+    import ctypes as C
+
+    import torch
+
+    import bench
+    from paper_2007_08576_b200._lib import FrameInput, FrameOutput, Report
+    from paper_2007_08576_b200.orb import OrbDetector
+    from tests.test_gpu_pipeline import _tracker
+
+    wl = bench.make_workload(1, 2, seed=4)
+    h, w = wl["scene"].height, wl["scene"].width
+    fr = wl["frames"][0]
+    img = textured(h, w, 11)
+    det = OrbDetector(h, w, n_max=600)
+    kp, desc, _, _ = det.detect(img)
+    kp_dev, desc_dev, n = det.last_on_device()
+    assert n == len(kp) > 50
+    m, npts = len(wl["graph"]), len(wl["tpl"])
+
+    def run(on_device):
+        trk = _tracker(wl)
+        depth = np.ascontiguousarray(fr.depth)
+        keep = [depth, kp, desc]
+        fi = FrameInput()
+        if on_device:
+            d_depth = torch.from_numpy(depth).cuda()
+            keep.append(d_depth)
+            fi.depth, fi.frame_desc, fi.frame_kp = d_depth.data_ptr(), desc_dev, kp_dev
+        else:
+            fi.depth, fi.frame_desc, fi.frame_kp = depth.ctypes.data, desc.ctypes.data, kp.ctypes.data
+        fi.n_frame, fi.use_matches, fi.on_device, fi.frame_id = n, 1, int(on_device), 0
+        wts = np.zeros((m, 8))
+        pts = np.zeros((npts, 3))
+        rep = Report()
+        fo = FrameOutput()
+        fo.warps, fo.points = wts.ctypes.data, pts.ctypes.data
+        fo.report = C.cast(C.pointer(rep), C.c_void_p).value
+        trk.track_raw(fi, fo)
+        trk.close()
+        return wts, pts, rep.n_matches, rep.total_cost
+
+    a = run(False)
+    b = run(True)
+    det.close()
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+    assert a[2] == b[2] and a[3] == b[3]
