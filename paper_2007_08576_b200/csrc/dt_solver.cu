@@ -22,6 +22,8 @@
 //   P6  decide (solver.py:321-331), then points / matches / edges: cost at the tentative
 //       warps with frozen robust and rigidity weights (solver.py:333-335) + speculative
 //       relinearization there; accept iff strictly lower (solver.py:336)
+//   final: support -> wa at the solution, its rigidity cost, the report and (grid mode)
+//       the output warp of the template (tracking.py:87)
 // Every reduction is deterministic and independent of the launch shape: normal equations
 // are folded per control in CSR order, costs per fixed 32-item chunk then folded in chunk
 // order, and every CTA evaluates the totals identically, so all CTAs take the same

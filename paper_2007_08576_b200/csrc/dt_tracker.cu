@@ -3,12 +3,14 @@
 // Per frame (tracking.track_frame, tracking.py:67-95):
 //   depth -> normals + validity            k_observation_normals   (correspond.py:36-73)
 //   [ORB] Hamming match + back-projection  k_hamming, k_build_matches (north-star 3a)
-//   preselection                           k_preselect_warp/final  (matching.py:174-226)
-//   active matches, binding, control CSR   k_active, k_csr_*_dev   (solver.py:113-119, 292-296)
-//   LM solve                               k_solve_frame (cluster) (solver.py:267-378)
-//   output warp                            k_warp_all              (warpfield.py:236-250)
-// All launches go to the tracker's stream; the host only waits at the end of the frame
-// when it asked for host outputs.
+//   preselection (+ ORB feature scatter)   k_preselect_warp/final  (matching.py:174-226)
+//   [pairs] binding, active matches, CSR   k_bind_points, k_active, k_csr_*_dev
+//                                                                  (solver.py:113-119, 292-296)
+//   LM solve                               k_solve_frame           (solver.py:267-378)
+//   output warp                            in the solver's final phase (grid mode) or
+//                                          k_warp_all_i32 (cluster mode) (warpfield.py:236-250)
+// All launches go to the tracker's stream; the steady-state ORB frame replays as one CUDA
+// graph; the host only waits at the end of the frame when it asked for host outputs.
 
 #include <cuda_runtime.h>
 
