@@ -444,6 +444,7 @@ struct dt_tracker {
   double *out_p = nullptr, *out_n = nullptr;
   SolverArgs host_args;
   SolverArgs* dev_args = nullptr;
+  SolverArgs* dev_args_slot = nullptr;  // [2], pipelined path: depth read from the slots
   // pinned staging for the report / stats
   dt_report* h_report = nullptr;
   int64_t* h_info = nullptr;
@@ -590,10 +591,14 @@ void fill_args(dt_tracker* t) {
 int push_args(dt_tracker* t) {
   fill_args(t);
   t->args_dirty = false;
-  SolverArgs v[3] = {t->host_args, t->host_args, t->host_args};
-  for (int i = 0; i < 2; ++i)
-    if (t->in_depth[i]) v[1 + i].depth = t->in_depth[i];
-  DT_CHECK_CUDA(cudaMemcpyAsync(t->dev_args, v, sizeof(v), cudaMemcpyHostToDevice, t->stream));
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->dev_args, &t->host_args, sizeof(SolverArgs),
+                                cudaMemcpyHostToDevice, t->stream));
+  if (t->dev_args_slot) {
+    SolverArgs v[2] = {t->host_args, t->host_args};
+    v[0].depth = t->in_depth[0];
+    v[1].depth = t->in_depth[1];
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->dev_args_slot, v, sizeof(v), cudaMemcpyHostToDevice, t->stream));
+  }
   DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
   return DT_OK;
 }
@@ -810,7 +815,8 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   if (t->args_dirty) DT_TRY(push_args(t));
   DT_CHECK_CUDA(cudaMemsetAsync(t->stalled_hist, 0, sizeof(int32_t) * c.max_outer_iters, s));
   if (t->pre_solver_wait) DT_CHECK_CUDA(cudaStreamWaitEvent(s, t->pre_solver_wait, 0));
-  DT_TRY(solver_launch(t->dev_args + t->in_set, 1, t->cluster, (int)t->m, (int)t->k, t->grid_mode, s));
+  DT_TRY(solver_launch(t->in_set ? t->dev_args_slot + (t->in_set - 1) : t->dev_args, 1, t->cluster,
+                       (int)t->m, (int)t->k, t->grid_mode, s));
   ++t->launches;
   mark(t, 5);
   // ---- output warp (tracking.py:87): in grid mode done by the solver's final phase ----
@@ -1076,7 +1082,7 @@ static int tracker_init(dt_tracker* t, const dt_config* cfg, const double* t_poi
   DT_TRY(dalloc(t, &t->wa_out, m));
   DT_TRY(dalloc(t, &t->out_p, 3 * n));
   DT_TRY(dalloc(t, &t->out_n, 3 * n));
-  DT_TRY(dalloc(t, &t->dev_args, 3));
+  DT_TRY(dalloc(t, &t->dev_args, 1));
   DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_report, sizeof(dt_report)));
   DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_info, sizeof(int64_t) * 4));
   DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_stats, sizeof(double) * 4));
@@ -1284,10 +1290,11 @@ int ensure_pipeline(dt_tracker* t, int64_t n_desc) {
       DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_done[i], cudaEventDisableTiming));
       DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_out_copied[i], cudaEventDisableTiming));
       DT_TRY(dalloc(t, &t->in_depth[i], npix));
-      t->args_dirty = true;  // the solver's per-slot arguments point at the new buffers
       DT_TRY(dalloc(t, &t->stage_info[i], STAGE_WORDS));
       DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_stage[i], sizeof(int64_t) * STAGE_WORDS));
     }
+    DT_TRY(dalloc(t, &t->dev_args_slot, 2));
+    t->args_dirty = true;  // the per-slot solver arguments still have to be written
   }
   if (n_desc > t->in_desc_cap) {
     const int64_t cap = std::max<int64_t>(n_desc, 256);
