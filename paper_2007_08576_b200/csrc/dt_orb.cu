@@ -123,6 +123,7 @@ __global__ void k_cell_rank(const unsigned long long* __restrict__ sorted, int n
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const unsigned long long k = sorted[i];
+  if (k == ~0ull) return;  // padding (the sorts run over the full capacity, no host sync)
   const unsigned long long cell = k >> (ib + 8);
   int lo = 0, hi = i;  // first position with this cell
   while (lo < hi) {
@@ -136,13 +137,15 @@ __global__ void k_cell_rank(const unsigned long long* __restrict__ sorted, int n
 
 // one warp per keypoint
 __global__ void k_describe(const uint8_t* __restrict__ img, const int32_t* __restrict__ box, int w,
-                           const unsigned long long* __restrict__ sel, int n, int ib,
+                           const unsigned long long* __restrict__ sel,
+                           const unsigned* __restrict__ n_sel, int n_max, int ib,
                            const int16_t* __restrict__ disc, int n_disc,
                            const double* __restrict__ bnd, const int8_t* __restrict__ rot,
                            int32_t* __restrict__ kp, uint8_t* __restrict__ desc,
                            int32_t* __restrict__ score, int32_t* __restrict__ bins) {
   const int lane = threadIdx.x & 31;
   const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int n = min((int)*n_sel, n_max);
   if (k >= n) return;
   const unsigned long long key = sel[k];
   const int64_t lin = (int64_t)(key & ((1ull << ib) - 1));
@@ -334,6 +337,10 @@ int dt_orb_detect(dt_orb* o, const uint8_t* image, int on_device, int32_t* keypo
   }
   const dim3 blk(32, 8), grd((unsigned)((w + 31) / 32), (unsigned)((h + 7) / 8));
   DT_CHECK_CUDA(cudaMemsetAsync(o->counts, 0, 2 * sizeof(unsigned), s));
+  // every stage runs over the fixed capacity with all-ones padding keys (sorted last), so
+  // the whole detection is stream-ordered: one host sync, at the end, for the count
+  DT_CHECK_CUDA(cudaMemsetAsync(o->keys, 0xff, sizeof(unsigned long long) * o->cap, s));
+  DT_CHECK_CUDA(cudaMemsetAsync(o->sel, 0xff, sizeof(unsigned long long) * o->cap, s));
   k_fast_score<<<grd, blk, 0, s>>>(img, h, w, o->score);
   DT_CHECK_LAUNCH();
   k_box5<<<grd, blk, 0, s>>>(img, h, w, o->box);
@@ -346,29 +353,22 @@ int dt_orb_detect(dt_orb* o, const uint8_t* image, int on_device, int32_t* keypo
   k_nms_collect<<<grd, blk, 0, s>>>(o->score, h, w, o->threshold, o->cell, ncx, ib, o->keys,
                                     o->counts, o->cap);
   DT_CHECK_LAUNCH();
+  size_t tb = o->tmp_bytes;
+  DT_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(o->tmp, tb, o->keys, o->keys2, o->cap, 0,
+                                               ib + 8 + cb, s));
+  k_cell_rank<<<(o->cap + 255) / 256, 256, 0, s>>>(o->keys2, o->cap, o->per_cell, ib, o->sel,
+                                                   o->counts + 1);
+  DT_CHECK_LAUNCH();
+  tb = o->tmp_bytes;
+  DT_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(o->tmp, tb, o->sel, o->sel2, o->cap, 0, ib + 8, s));
+  k_describe<<<(o->n_max + 7) / 8, 256, 0, s>>>(img, o->box, w, o->sel2, o->counts + 1, o->n_max, ib,
+                                                o->disc, o->n_disc, o->bnd, o->rot, o->o_kp,
+                                                o->o_desc, o->o_score, o->o_bin);
+  DT_CHECK_LAUNCH();
   unsigned cnt[2] = {0, 0};
   DT_CHECK_CUDA(cudaMemcpyAsync(cnt, o->counts, sizeof(cnt), cudaMemcpyDeviceToHost, s));
   DT_CHECK_CUDA(cudaStreamSynchronize(s));
-  const int n1 = (int)std::min<unsigned>(cnt[0], (unsigned)o->cap);
-  int n = 0;
-  if (n1 > 0) {
-    size_t tb = o->tmp_bytes;
-    DT_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(o->tmp, tb, o->keys, o->keys2, n1, 0, ib + 8 + cb, s));
-    k_cell_rank<<<(n1 + 255) / 256, 256, 0, s>>>(o->keys2, n1, o->per_cell, ib, o->sel,
-                                                 o->counts + 1);
-    DT_CHECK_LAUNCH();
-    DT_CHECK_CUDA(cudaMemcpyAsync(cnt, o->counts, sizeof(cnt), cudaMemcpyDeviceToHost, s));
-    DT_CHECK_CUDA(cudaStreamSynchronize(s));
-    const int n2 = (int)cnt[1];
-    tb = o->tmp_bytes;
-    DT_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(o->tmp, tb, o->sel, o->sel2, n2, 0, ib + 8, s));
-    n = std::min(n2, o->n_max);
-    if (n > 0) {
-      k_describe<<<(n + 7) / 8, 256, 0, s>>>(img, o->box, w, o->sel2, n, ib, o->disc, o->n_disc, o->bnd,
-                                             o->rot, o->o_kp, o->o_desc, o->o_score, o->o_bin);
-      DT_CHECK_LAUNCH();
-    }
-  }
+  const int n = (int)std::min<unsigned>(cnt[1], (unsigned)o->n_max);
   if (n > 0) {
     if (keypoints)
       DT_CHECK_CUDA(cudaMemcpyAsync(keypoints, o->o_kp, sizeof(int32_t) * 2 * n, cudaMemcpyDeviceToHost, s));
