@@ -349,9 +349,25 @@ class DeviceTracker:
             pass
 
 
+def _fingerprint(arrays) -> tuple:
+    """Cheap content digest of the cached arrays (xor and wrapping sum of their 64-bit
+    words): a template or graph mutated in place after caching is detected and rebuilt."""
+    out = []
+    for a in arrays:
+        b = np.ascontiguousarray(a).view(np.uint8).ravel()
+        pad = (-b.size) % 8
+        if pad:
+            b = np.concatenate([b, np.zeros(pad, np.uint8)])
+        w = b.view(np.uint64)
+        out.append((a.shape, int(np.bitwise_xor.reduce(w)) if w.size else 0,
+                    int(w.sum(dtype=np.uint64)) if w.size else 0))
+    return tuple(out)
+
+
 class _SessionCache:
     """Trackers keyed by the identity of the template / graph arrays they were built
-    from (the arrays are held, so ids cannot be recycled while cached)."""
+    from (the arrays are held, so ids cannot be recycled while cached) and checked
+    against a content digest, so in-place edits of those arrays are picked up."""
 
     def __init__(self, capacity: int = 4):
         self.capacity = capacity
@@ -361,21 +377,25 @@ class _SessionCache:
         arrays = (template.points, template.normals, template.bind_indices, template.bind_weights,
                   graph.points, graph.edges, graph.edge_weights)
         key = tuple(id(a) for a in arrays) + (cfg.width, cfg.height, float(graph.sampling_radius))
+        fp = _fingerprint(arrays)
         hit = self._d.get(key)
-        if hit is not None:
+        if hit is not None and hit[2] == fp:
             self._d.move_to_end(key)
             trk = hit[1]
             trk.set_config(cfg)
             return trk
+        if hit is not None:  # the cached arrays were edited in place: rebuild
+            del self._d[key]
+            hit[1].close()
         trk = DeviceTracker(template, graph, cfg)
-        self._d[key] = (arrays, trk)
+        self._d[key] = (arrays, trk, fp)
         while len(self._d) > self.capacity:
-            _, (_, old) = self._d.popitem(last=False)
+            _, (_, old, _) = self._d.popitem(last=False)
             old.close()
         return trk
 
     def clear(self) -> None:
-        for _, (_, trk) in self._d.items():
+        for _, (_, trk, _) in self._d.items():
             trk.close()
         self._d.clear()
 

@@ -222,3 +222,23 @@ def test_inconsistent_inputs_raise_before_the_c_abi():
     assert res.report.n_correspondences > 0
     with pytest.raises(ValueError):
         dt.Tracker(tpl, graph.with_warps(graph.warps[:-1]), cam, cfg)
+
+
+def test_functional_api_sees_in_place_edits():
+    """solve_frame caches a device tracker per template / graph; editing the cached
+    arrays in place must not return results for the stale copy."""
+    dt = _api()
+    c = solver_case("solver_translation")
+    fx, fy, cx, cy = c["cam"]
+    cam = dt.PinholeCamera(fx, fy, cx, cy, *c["dims"])
+    tpl, graph = _template_graph(dt, c["tpl"], c["graph"], c["warps_in"], c["radius"])
+    obs = dt.Observation.from_depth(c["depth"], cam)
+    scfg = dt.SolverConfig(**c["solver"])
+    a, _ = dt.solve_frame(tpl, graph, obs, None, dt.EnergyWeights(), scfg)
+    tpl.points[:, 2] += 0.5  # move the template in place
+    b, _ = dt.solve_frame(tpl, graph, obs, None, dt.EnergyWeights(), scfg)
+    tpl2, graph2 = _template_graph(dt, (tpl.points.copy(),) + tuple(c["tpl"][1:]), c["graph"],
+                                   c["warps_in"], c["radius"])
+    fresh, _ = dt.solve_frame(tpl2, graph2, obs, None, dt.EnergyWeights(), scfg)
+    assert not np.array_equal(a.warps, b.warps)
+    np.testing.assert_array_equal(b.warps, fresh.warps)
