@@ -11,18 +11,20 @@ device.
 
 from ._lib import LIB_PATH, version  # noqa: F401  (fails loudly if the .so is missing)
 from .config import RunConfig, load_config
-from .correspond import CorrespondenceSet, Observation
+from .correspond import CorrespondenceSet, Observation, estimate_point_normals
 from .energy import EnergyReport, EnergyWeights
 from .estimators import MatchInlierSelector, SurfaceDeformationTracker
 from .geometry import PinholeCamera
 from .matching import MatchSet, PreselectConfig, match_descriptors, preselect_inliers
+from .orb import OrbDetector
 from .solver import SolverConfig, solve_frame
 from .tracking import (FrameResult, Tracker, annotate_matches, prepare_template, track_frame,
                        track_sequence)
 from .warpfield import ControlGraph, Template, bind_template, sample_control_points, warp_all
 
 __all__ = [
-    "RunConfig", "load_config", "CorrespondenceSet", "Observation", "EnergyReport",
+    "RunConfig", "load_config", "CorrespondenceSet", "Observation", "estimate_point_normals",
+    "OrbDetector", "EnergyReport",
     "EnergyWeights", "MatchInlierSelector", "SurfaceDeformationTracker", "PinholeCamera",
     "MatchSet", "PreselectConfig", "match_descriptors", "preselect_inliers", "SolverConfig",
     "solve_frame", "FrameResult", "Tracker", "annotate_matches", "prepare_template",
