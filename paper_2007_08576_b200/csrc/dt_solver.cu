@@ -474,19 +474,31 @@ __device__ __forceinline__ bool solve6(const double* part, double lam, double de
 
 // KM = 4: the reference's bind_k (SolverConfig / RunConfig default, warpfield.py:157);
 // KM = 8: any k <= 8 with runtime slot guards
-template __global__ void k_solve_frame<false, 4, false>(const SolverArgs* __restrict__);
-template __global__ void k_solve_frame<true, 4, false>(const SolverArgs* __restrict__);
-template __global__ void k_solve_frame<false, 8, false>(const SolverArgs* __restrict__);
-template __global__ void k_solve_frame<true, 8, false>(const SolverArgs* __restrict__);
-template __global__ void k_solve_frame<false, 4, true>(const SolverArgs* __restrict__);
-template __global__ void k_solve_frame<true, 4, true>(const SolverArgs* __restrict__);
-template __global__ void k_solve_frame<false, 8, true>(const SolverArgs* __restrict__);
-template __global__ void k_solve_frame<true, 8, true>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 4, false, 2>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 4, false, 2>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 8, false, 2>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 8, false, 2>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 4, true, 2>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 4, true, 2>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 8, true, 2>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 8, true, 2>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 4, false, 1>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 4, false, 1>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 8, false, 1>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 8, false, 1>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 4, true, 1>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 4, true, 1>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<false, 8, true, 1>(const SolverArgs* __restrict__);
+template __global__ void k_solve_frame<true, 8, true, 1>(const SolverArgs* __restrict__);
 
 template <bool GRID>
-static void* solver_fn(int k, bool big) {
-  if (big) return k == 4 ? (void*)k_solve_frame<GRID, 4, true> : (void*)k_solve_frame<GRID, 8, true>;
-  return k == 4 ? (void*)k_solve_frame<GRID, 4, false> : (void*)k_solve_frame<GRID, 8, false>;
+static void* solver_fn(int k, bool big, int team) {
+  if (team == 1) {
+    if (big) return k == 4 ? (void*)k_solve_frame<GRID, 4, true, 1> : (void*)k_solve_frame<GRID, 8, true, 1>;
+    return k == 4 ? (void*)k_solve_frame<GRID, 4, false, 1> : (void*)k_solve_frame<GRID, 8, false, 1>;
+  }
+  if (big) return k == 4 ? (void*)k_solve_frame<GRID, 4, true, 2> : (void*)k_solve_frame<GRID, 8, true, 2>;
+  return k == 4 ? (void*)k_solve_frame<GRID, 4, false, 2> : (void*)k_solve_frame<GRID, 8, false, 2>;
 }
 
 // per-device cache of the occupancy probe (a hardware property; atomic so concurrent
@@ -498,7 +510,7 @@ int solver_max_cluster(int device) {
   const int cached = g_max_cluster[device].load(std::memory_order_relaxed);
   if (cached > 0) return cached;
   int best = 1;
-  auto* fn = k_solve_frame<false, 8, false>;
+  auto* fn = k_solve_frame<false, 8, false, 2>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const size_t smem = solver_smem_bytes(1024);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -535,7 +547,7 @@ int solver_pick_cluster(int device, int requested, int m_max) {
 }
 
 int solver_grid_blocks(int device, int m_max) {
-  auto* fn = m_max > M_MAX_SMEM ? k_solve_frame<true, 8, true> : k_solve_frame<true, 8, false>;
+  auto* fn = m_max > M_MAX_SMEM ? k_solve_frame<true, 8, true, 2> : k_solve_frame<true, 8, false, 2>;
   const size_t smem = solver_smem_bytes(m_max);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0, sms = 0;
@@ -545,6 +557,12 @@ int solver_grid_blocks(int device, int m_max) {
   return per_sm >= 1 ? sms : 0;  // one CTA per SM
 }
 
+// Warps per control team in P2 / P3: pairs while one round of the full grid's teams
+// (148 CTAs x 4) covers every control, single warps for larger graphs (config 4, 1,026
+// controls: 0.83 -> 0.76 ms). A function of m alone -- not of the launch shape -- because
+// the team width fixes the fold order, and results must not depend on the cluster size.
+static int solver_team(int m) { return m > 592 ? 1 : 2; }
+
 int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, int k, int grid_mode,
                   cudaStream_t s) {
   DT_REQUIRE(k >= 1 && k <= KMAX, DT_ERR_UNSUPPORTED, "bind_k=%d outside the device path (<= %d)", k,
@@ -553,18 +571,18 @@ int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, i
   const bool big = m_max > M_MAX_SMEM;
   if (grid_mode) {
     DT_REQUIRE(n_seq == 1, DT_ERR_UNSUPPORTED, "grid mode runs one sequence per launch");
-    void* fn = solver_fn<true>(k, big);
-    DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0;
     DT_CHECK_CUDA(cudaGetDevice(&dev));
     const int blocks = solver_grid_blocks(dev, m_max);
     DT_REQUIRE(blocks > 0, DT_ERR_UNSUPPORTED, "solver kernel cannot be co-resident for a grid launch");
+    void* fn = solver_fn<true>(k, big, solver_team(m_max));
+    DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     void* params[] = {(void*)&d_args};
     DT_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(blocks), dim3(SOLVER_THREADS),
                                               params, smem, s));
     return DT_OK;
   }
-  void* fn = solver_fn<false>(k, big);
+  void* fn = solver_fn<false>(k, big, solver_team(m_max));
   DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DT_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};

@@ -14,11 +14,6 @@
 // stalled iteration keeps its linearization -- the reference recomputes it at the same
 // warps, bit for bit the same -- and only re-solves.
 
-#ifndef DT_TEAM
-#define DT_TEAM 2
-#endif
-constexpr int TEAM = DT_TEAM;
-constexpr int TEAMS_PER_CTA = NWARPS / TEAM;
 
 // one of the two linearization buffers
 struct PBuf {
@@ -430,8 +425,13 @@ __device__ __forceinline__ void resolve_control(const SolverArgs& A, int c, doub
 // warps and tentative transforms are read in place from global memory (L1-cached after
 // each barrier), the current transforms and the damping live in this CTA's slice of
 // A.gstate; everything else is the same kernel.
-template <bool GRID, int KM, bool BIG>
+// TM: warps per control team in P2 / P3 -- 2 when every control gets its own team in
+// one round (the pair halves each control's fold), 1 when the controls outnumber the
+// teams (one warp per control halves the number of rounds; the host picks).
+template <bool GRID, int KM, bool BIG, int TM>
 __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverArgs* __restrict__ all) {
+  constexpr int TEAM = TM;
+  constexpr int TEAMS_PER_CTA = NWARPS / TM;
   Dom<GRID> dom;
   const int C = dom.size();
   const int rank = dom.rank();
