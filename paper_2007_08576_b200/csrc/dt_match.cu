@@ -492,13 +492,15 @@ k_preselect_final(const double* __restrict__ src, const double* __restrict__ dst
       best_pos = s_pos[w2];
     }
   const int64_t ref = best_ref, pos = best_pos;
+  // this CTA's round of matches (one CTA per 1024; every CTA found the same winner)
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (ref < 0) {
-    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    if (k < n) {
       weights[k] = 0.0;
       flags[k] = 0;
       if (residuals) residuals[k] = 0.0;
     }
-    if (threadIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
       info[0] = DT_ERR_NO_VALID_HYPOTHESIS;
       info[1] = -1;
       if (support_out) support_out[0] = 0.0;
@@ -511,7 +513,7 @@ k_preselect_final(const double* __restrict__ src, const double* __restrict__ dst
     for (int i = 0; i < 9; ++i) R[i] = ref_rot[9 * pos + i];
     const double rs0 = src[3 * ref], rs1 = src[3 * ref + 1], rs2 = src[3 * ref + 2];
     const double rd0 = dst[3 * ref], rd1 = dst[3 * ref + 1], rd2 = dst[3 * ref + 2];
-    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    if (k < n) {
       const double s1[3] = {src[3 * k] - rs0, src[3 * k + 1] - rs1, src[3 * k + 2] - rs2};
       const double s2[3] = {dst[3 * k] - rd0, dst[3 * k + 1] - rd1, dst[3 * k + 2] - rd2};
       const double d = rot_residual(R, s1, s2);
@@ -523,7 +525,7 @@ k_preselect_final(const double* __restrict__ src, const double* __restrict__ dst
       flags[k] = flag ? 1 : 0;
       if (residuals) residuals[k] = d;
     }
-    if (threadIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
       info[0] = DT_OK;
       info[1] = ref;
       if (support_out) support_out[0] = best;
@@ -534,8 +536,33 @@ k_preselect_final(const double* __restrict__ src, const double* __restrict__ dst
   // ORB path: the weights to their template features + the report statistics, in the
   // same CTA (this CTA's global writes above are visible after the barrier)
   if (do_scatter) {
+    // this round's scatter and partial statistics; the last CTA to finish sums the rounds
+    // in round order (same bits as one CTA walking the rounds)
     __syncthreads();
-    feature_scatter_block(scatter, n, weights, flags);
+    double cs = 0.0;
+    int nf = 0;
+    feature_scatter_round(scatter, n, (int64_t)blockIdx.x * blockDim.x, weights, flags, &cs, &nf);
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+      scatter.partial[2 * blockIdx.x] = cs;
+      scatter.partial[2 * blockIdx.x + 1] = (double)nf;
+      __threadfence();
+      s_last = atomicAdd(scatter.counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      __threadfence();
+      double wsum = 0.0;
+      int64_t nflag = 0;
+      for (unsigned g = 0; g < gridDim.x; ++g) {
+        wsum += __ldcg(scatter.partial + 2 * g);
+        nflag += (int64_t)__ldcg(scatter.partial + 2 * g + 1);
+      }
+      *scatter.n_active = scatter.n_feat;
+      scatter.stats[0] = wsum;
+      scatter.stats[1] = (double)nflag;
+      *scatter.counter = 0;
+    }
   }
 }
 
@@ -566,7 +593,9 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
     DT_CHECK_LAUNCH();
   }
   const FeatureScatter fs = scatter ? *scatter : FeatureScatter{};
-  k_preselect_final<<<1, 1024, 0, s>>>(src, dst, n_dev, n_max, refs, n_refs, exhaustive, H,
+  // one CTA per 1,024 matches (each finds the winner itself: n_max supports)
+  const unsigned g = (unsigned)std::max<int64_t>(1, (n_max + 1023) / 1024);
+  k_preselect_final<<<g, 1024, 0, s>>>(src, dst, n_dev, n_max, refs, n_refs, exhaustive, H,
                                         inlier_min, ref_support, ref_rot, ref_valid, weights, flags,
                                         residuals, rotation, info, support, fs,
                                         scatter ? 1 : 0);

@@ -45,53 +45,50 @@ struct FeatureScatter {
   const double* dst;       // (n, 3) observed points of the compacted matches
   const int32_t* feat_id;  // (n,) template feature of each match
   double* ffo;             // (n_feat, 3) observed point per feature
-  double* ffw;             // (n_feat,) weight per feature
+  double* ffw;             // (n_feat,) weight per feature (zeroed by the match build)
   int64_t* n_active;
   double* stats;           // [match_weight_sum, n_preselected]
+  double* partial;         // scratch: 2 per 1024-match round
+  unsigned* counter;       // scratch: rounds done (reset by the last)
 };
 
-__device__ __forceinline__ void feature_scatter_block(const FeatureScatter& F, int64_t n,
-                                                      const double* weights,
-                                                      const uint8_t* flags) {
+// One 1024-match round [base, base + blockDim) of the ORB-path scatter: the weights and
+// observed points to their template features; returns (to thread 0) the round's weight
+// sum (warp sums in warp order) and flag count -- the rounds are then summed in round
+// order, the order k_active uses (solver.py:368-370).
+__device__ __forceinline__ void feature_scatter_round(const FeatureScatter& F, int64_t n,
+                                                      int64_t base, const double* weights,
+                                                      const uint8_t* flags, double* cs_out,
+                                                      int* flg_out) {
   __shared__ double s_fsum[32];
   __shared__ int s_fcnt[32];
-  for (int64_t f = threadIdx.x; f < F.n_feat; f += blockDim.x) F.ffw[f] = 0.0;
-  __syncthreads();
-  double wsum = 0.0;
-  int64_t nflag = 0;
-  for (int64_t base = 0; base < n; base += blockDim.x) {
-    const int64_t j = base + threadIdx.x;
-    const bool in = j < n;
-    const double w = in ? weights[j] : 0.0;
-    if (in) {
-      const int f = F.feat_id[j];
-      F.ffw[f] = w;
-      F.ffo[3 * f] = F.dst[3 * j];
-      F.ffo[3 * f + 1] = F.dst[3 * j + 1];
-      F.ffo[3 * f + 2] = F.dst[3 * j + 2];
-    }
-    const double v = warp_sum(w);
-    int flg = (in && flags[j]) ? 1 : 0;
-    for (int o = 16; o > 0; o >>= 1) flg += __shfl_xor_sync(0xffffffffu, flg, o);
-    if ((threadIdx.x & 31) == 0) {
-      s_fsum[threadIdx.x >> 5] = v;
-      s_fcnt[threadIdx.x >> 5] = flg;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double cs = 0.0;
-      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) {
-        cs += s_fsum[w2];
-        nflag += s_fcnt[w2];
-      }
-      wsum += cs;
-    }
-    __syncthreads();
+  const int64_t j = base + threadIdx.x;
+  const bool in = j < n;
+  const double w = in ? weights[j] : 0.0;
+  if (in) {
+    const int f = F.feat_id[j];
+    F.ffw[f] = w;
+    F.ffo[3 * f] = F.dst[3 * j];
+    F.ffo[3 * f + 1] = F.dst[3 * j + 1];
+    F.ffo[3 * f + 2] = F.dst[3 * j + 2];
   }
+  const double v = warp_sum(w);
+  int flg = (in && flags[j]) ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) flg += __shfl_xor_sync(0xffffffffu, flg, o);
+  if ((threadIdx.x & 31) == 0) {
+    s_fsum[threadIdx.x >> 5] = v;
+    s_fcnt[threadIdx.x >> 5] = flg;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    *F.n_active = F.n_feat;
-    F.stats[0] = wsum;
-    F.stats[1] = (double)nflag;
+    double cs = 0.0;
+    int nf = 0;
+    for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) {
+      cs += s_fsum[w2];
+      nf += s_fcnt[w2];
+    }
+    *cs_out = cs;
+    *flg_out = nf;
   }
 }
 

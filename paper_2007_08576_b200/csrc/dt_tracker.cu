@@ -106,7 +106,8 @@ k_build_matches(int64_t nt, const unsigned long long* __restrict__ packed,
                 const double* __restrict__ depth, double zmin, double zmax, int width,
                 int height, double fx, double fy, double cx, double cy,
                 const double* __restrict__ tpts, double* __restrict__ src,
-                double* __restrict__ dst, int32_t* __restrict__ feat_id, int64_t* __restrict__ n_out) {
+                double* __restrict__ dst, int32_t* __restrict__ feat_id, int64_t* __restrict__ n_out,
+                double* __restrict__ ffw) {
   __shared__ int s_warp[33];
   int64_t base_out = 0;
   for (int64_t base = 0; base < nt; base += (int64_t)blockDim.x * BM_PER) {
@@ -117,6 +118,7 @@ k_build_matches(int64_t nt, const unsigned long long* __restrict__ packed,
     for (int e = 0; e < BM_PER; ++e) {
       const int64_t t = t0 + e;
       fi[e] = -1;
+      if (ffw && t < nt) ffw[t] = 0.0;  // features without an active match keep weight 0
       if (t < nt && nf > 0) {
         const unsigned long long v = packed[t];  // (distance << 32) | frame index
         if ((long long)(v >> 32) <= (long long)max_ham) fi[e] = (int)(v & 0xffffffffull);
@@ -397,7 +399,9 @@ struct dt_tracker {
   cudaEvent_t ev_in_ready[2] = {nullptr, nullptr}, ev_in_free[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_out_copied[2] = {nullptr, nullptr};
   cudaEvent_t pre_solver_wait = nullptr;  // compute stream waits on it before the solver
-  bool own_stream = false;  // created by dt_tracker_create (destroyed with the tracker)
+  bool own_stream = false;
+  double* fs_partial = nullptr;   // preselection feature scatter: per-round partials
+  unsigned* fs_counter = nullptr;  // created by dt_tracker_create (destroyed with the tracker)
   double* in_depth[2] = {nullptr, nullptr};
   uint8_t* in_desc[2] = {nullptr, nullptr};
   int32_t* in_kp[2] = {nullptr, nullptr};
@@ -725,7 +729,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_packed, c.max_hamming, fkp,
                                        in->n_frame, dep, c.z_min, c.z_max, c.width, c.height, c.fx,
                                        c.fy, c.cx, c.cy, t->tfeat_pts, t->m_src, t->m_dst, t->m_feat,
-                                       t->info + 2);
+                                       t->info + 2, t->ffw);
     DT_CHECK_LAUNCH();
     t->launches += 2;
     n_max = t->n_feat;
@@ -774,7 +778,8 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     if (!exhaustive && n_refs > t->match_cap) DT_TRY(ensure_match_capacity(t, n_refs));
     // ORB path: the final preselection kernel also scatters the weights to the template
     // features (matches indexed by feature: static points / binding / CSR)
-    FeatureScatter fs{t->n_feat, t->m_dst, t->m_feat, t->ffo, t->ffw, t->info + 3, t->astats};
+    FeatureScatter fs{t->n_feat, t->m_dst, t->m_feat, t->ffo, t->ffw, t->info + 3, t->astats,
+                      t->fs_partial, t->fs_counter};
     DT_TRY(launch_preselect(t->m_src, t->m_dst, t->info + 2, n_max, t->refs, n_refs, exhaustive,
                             c.preselect.distance_threshold, c.preselect.n_reweight_iters,
                             c.preselect.inlier_weight_min, c.preselect.min_support, t->m_w,
@@ -1198,6 +1203,8 @@ int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* po
     DT_TRY(dalloc(t, &t->fpos, std::max<int64_t>(1, n_features * k)));
     DT_TRY(dalloc(t, &t->ffo, 3 * std::max<int64_t>(1, n_features)));
     DT_TRY(dalloc(t, &t->ffw, std::max<int64_t>(1, n_features)));
+    DT_TRY(dalloc(t, &t->fs_partial, 2 * (n_features / 1024 + 2)));
+    DT_TRY(dalloc(t, &t->fs_counter, 1));
     DT_TRY(upload(t, t->fptr, fptr.data(), fptr.size()));
     if (!fent.empty()) {
       DT_TRY(upload(t, t->fent, fent.data(), fent.size()));
