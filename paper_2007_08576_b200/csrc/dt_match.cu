@@ -121,13 +121,15 @@ __global__ void k_unpack_hamming(const unsigned long long* __restrict__ packed, 
 // otherwise one pass writes best_idx / best_dist.
 int launch_hamming(const uint8_t* tdesc, int64_t nt, const uint8_t* fdesc, int64_t nf,
                    int32_t* best_idx, int32_t* best_dist, cudaStream_t s,
-                   unsigned long long* packed) {
+                   unsigned long long* packed, bool packed_ready) {
   if (nt == 0) return DT_OK;
   const int per_cta = HAM_WARPS * HAM_TPW;
   int splits = 1;
   int64_t per = nf;
   if (packed) {
-    DT_CHECK_CUDA(cudaMemsetAsync(packed, 0xff, sizeof(unsigned long long) * nt, s));
+    // all-ones start values (the tracker's match build leaves them that way after use)
+    if (!packed_ready)
+      DT_CHECK_CUDA(cudaMemsetAsync(packed, 0xff, sizeof(unsigned long long) * nt, s));
     splits = HAM_SPLITS;
     per = ((nf + splits - 1) / splits + 31) / 32 * 32;
     if (per <= 0) per = 32;

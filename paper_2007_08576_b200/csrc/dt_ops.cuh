@@ -95,7 +95,7 @@ __device__ __forceinline__ void feature_scatter_round(const FeatureScatter& F, i
 // dt_match.cu
 int launch_hamming(const uint8_t* tdesc, int64_t nt, const uint8_t* fdesc, int64_t nf,
                    int32_t* best_idx, int32_t* best_dist, cudaStream_t s,
-                   unsigned long long* packed = nullptr);
+                   unsigned long long* packed = nullptr, bool packed_ready = false);
 struct PreselectWork;
 int launch_preselect(const double* src, const double* dst, const int64_t* n_dev, int64_t n_max,
                      const int64_t* refs, int64_t n_refs, int exhaustive, double H, int iters,

@@ -101,7 +101,7 @@ __device__ __forceinline__ int block_scan_count(int cnt, int* s_warp, int* total
 constexpr int BM_PER = 4;
 
 __global__ void __launch_bounds__(1024)
-k_build_matches(int64_t nt, const unsigned long long* __restrict__ packed,
+k_build_matches(int64_t nt, unsigned long long* __restrict__ packed,
                 int max_ham, const int32_t* __restrict__ kp, int64_t nf,
                 const double* __restrict__ depth, double zmin, double zmax, int width,
                 int height, double fx, double fy, double cx, double cy,
@@ -121,6 +121,7 @@ k_build_matches(int64_t nt, const unsigned long long* __restrict__ packed,
       if (ffw && t < nt) ffw[t] = 0.0;  // features without an active match keep weight 0
       if (t < nt && nf > 0) {
         const unsigned long long v = packed[t];  // (distance << 32) | frame index
+        packed[t] = ~0ull;                       // ready for the next frame's atomicMin
         if ((long long)(v >> 32) <= (long long)max_ham) fi[e] = (int)(v & 0xffffffffull);
       }
     }
@@ -725,7 +726,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     if (in->frame_kp != fkp)
       DT_CHECK_CUDA(cudaMemcpyAsync(fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
     DT_TRY(launch_hamming(t->tdesc, t->n_feat, fdesc, in->n_frame, nullptr, nullptr, s,
-                          t->ham_packed));
+                          t->ham_packed, true));
     k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_packed, c.max_hamming, fkp,
                                        in->n_frame, dep, c.z_min, c.z_max, c.width, c.height, c.fx,
                                        c.fy, c.cx, c.cy, t->tfeat_pts, t->m_src, t->m_dst, t->m_feat,
@@ -1171,6 +1172,8 @@ int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* po
   DT_TRY(dalloc(t, &t->ham_idx, n_features));
   DT_TRY(dalloc(t, &t->ham_dist, n_features));
   DT_TRY(dalloc(t, &t->ham_packed, n_features));
+  DT_CHECK_CUDA(cudaMemsetAsync(t->ham_packed, 0xff, sizeof(unsigned long long) * std::max<int64_t>(1, n_features),
+                                t->stream));
   DT_TRY(upload(t, t->tdesc, desc, 32 * n_features));
   DT_TRY(upload(t, t->tfeat_pts, points, 3 * n_features));
   // the match binding depends only on the template-side point (SURVEY §8a invariant):
