@@ -497,12 +497,19 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
 
   // ---- P1: relink + linearize at the warm start (buffer 0): points, matches, unit
   // rigidity rows of the connections ----
+  if (rank == 0)  // this launch's stall flags (written by CTA 0 thread 0 after barriers)
+    for (int i = threadIdx.x; i < A.max_outer; i += blockDim.x) A.stalled_hist[i] = 0;
   if (BIG) {
-    s_w = cur;
+    s_w = cur;  // the host copied the warm start into warp_a
     s_T = s_Tcur;
     load_transforms(A, s_w, s_T);
   } else {
-    load_state(A, cur, s_w, s_T, &s_bar, bar_phase);
+    // the warm start straight from the last solution; this CTA's slice of it into `cur`
+    // (first read from global memory after the P1 barrier)
+    load_state(A, A.warps_out, s_w, s_T, &s_bar, bar_phase);
+    for (int c = gc; c < m; c += GT)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cur[8 * c + i] = s_w[8 * c + i];
   }
   TRACE(12);
   {

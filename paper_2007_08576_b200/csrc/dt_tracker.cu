@@ -687,8 +687,10 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   t->launches = 0;
   mark(t, 0);
   // warm start: the previous solution (or set_warps) is in warps_out
-  DT_CHECK_CUDA(cudaMemcpyAsync(t->warp_a, t->warps_out, sizeof(double) * 8 * t->m,
-                                cudaMemcpyDeviceToDevice, s));
+  // (the shared-memory solver reads the warm start straight from warps_out)
+  if (t->m > M_MAX_SMEM)
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->warp_a, t->warps_out, sizeof(double) * 8 * t->m,
+                                  cudaMemcpyDeviceToDevice, s));
   // input set: the tracker's buffers (copied into) or a staging slot (read in place)
   const int set = t->in_set;
   double* dep = set ? t->in_depth[set - 1] : t->depth;
@@ -819,7 +821,6 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
 
   // ---- solve ----
   if (t->args_dirty) DT_TRY(push_args(t));
-  DT_CHECK_CUDA(cudaMemsetAsync(t->stalled_hist, 0, sizeof(int32_t) * c.max_outer_iters, s));
   if (t->pre_solver_wait) DT_CHECK_CUDA(cudaStreamWaitEvent(s, t->pre_solver_wait, 0));
   DT_TRY(solver_launch(t->in_set ? t->dev_args_slot + (t->in_set - 1) : t->dev_args, 1, t->cluster,
                        (int)t->m, (int)t->k, t->grid_mode, s));
