@@ -950,25 +950,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     }
     for (int c = gc; c < m; c += GT)
       for (int i = 0; i < 8; ++i) A.warps_out[8 * c + i] = s_w[8 * c + i];
-    // the frame's output (tracking.py:87, warpfield.warp_all): every template point and
-    // normal through the solution's blended warps, which are already in shared memory --
-    // the same device functions as dt_warp_all, so the same bits, without a launch
-    if (A.out_p) {
-      for (int64_t p = gt; p < n; p += GT) {
-        double B[8], sgn[KMAX];
-        blend_at(s_w, A.bidx + p * A.k, A.bw + p * A.k, A.k, B, sgn);
-        double x0, x1, x2, s2;
-        apply_blend(B, A.tp[3 * p], A.tp[3 * p + 1], A.tp[3 * p + 2], x0, x1, x2, s2);
-        double r0, r1, r2;
-        rotate_normal(B, A.tn[3 * p], A.tn[3 * p + 1], A.tn[3 * p + 2], r0, r1, r2);
-        A.out_p[3 * p] = x0;
-        A.out_p[3 * p + 1] = x1;
-        A.out_p[3 * p + 2] = x2;
-        A.out_n[3 * p] = r0;
-        A.out_n[3 * p + 1] = r1;
-        A.out_n[3 * p + 2] = r2;
-      }
-    }
+
     // support per control from its rows' last column: sum of sw^2 = rs^2 alpha (points)
     // + w_pair (matches, component-0 rows)
     const double* prow = cb.row;
@@ -1024,6 +1006,26 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     R->converged = converged ? 1 : 0;
     R->final_step_norm = final_step_norm;
     R->n_cost_history = n_hist;
+  }
+  // the frame's output (tracking.py:87, warpfield.warp_all): every template point and
+  // normal through the solution's blended warps, which are already in shared memory --
+  // the same device functions as dt_warp_all, so the same bits, without a launch; after
+  // the last barrier, so no CTA waits for it
+  if (A.out_p) {
+    for (int64_t p = gt; p < n; p += GT) {
+      double B[8], sgn[KMAX];
+      blend_at(s_w, A.bidx + p * A.k, A.bw + p * A.k, A.k, B, sgn);
+      double x0, x1, x2, s2;
+      apply_blend(B, A.tp[3 * p], A.tp[3 * p + 1], A.tp[3 * p + 2], x0, x1, x2, s2);
+      double r0, r1, r2;
+      rotate_normal(B, A.tn[3 * p], A.tn[3 * p + 1], A.tn[3 * p + 2], r0, r1, r2);
+      A.out_p[3 * p] = x0;
+      A.out_p[3 * p + 1] = x1;
+      A.out_p[3 * p + 2] = x2;
+      A.out_n[3 * p] = r0;
+      A.out_n[3 * p + 1] = r1;
+      A.out_n[3 * p + 2] = r2;
+    }
   }
   TRACE(99);
   if (tr && rank == 0 && threadIdx.x == 0) tr[0] = tn;
