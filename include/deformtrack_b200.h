@@ -19,7 +19,11 @@
  *     failure on the calling thread;
  *   - the library holds no global numeric state (the reference's process-global
  *     numba.set_num_threads, solver.py:288, has no equivalent here); one dt_tracker
- *     handle per sequence, one stream per handle.
+ *     handle per sequence, one stream per handle; different handles may be driven from
+ *     different host threads, one handle from one thread at a time;
+ *   - array sizes are trusted: the Python layer (paper_2007_08576_b200) checks shapes
+ *     before calling; index arrays are range-checked where the kernels would otherwise
+ *     read out of bounds (template / feature / match bindings, edges).
  */
 #ifndef DEFORMTRACK_B200_H
 #define DEFORMTRACK_B200_H
