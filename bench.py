@@ -2,10 +2,10 @@
 """Benchmark: per-frame deformation tracking on B200 (BASELINE.json metric, config 2).
 
 Workload (config 2): synthetic ex-vivo-like sphere patch, 640x480 depth, 141x141 = 19,881
-template points, ~389 densely connected control points (radius 5.3), 2,000 template ORB
-features (+500 distractors, 10 % outliers), exhaustive 1-point-RANSAC + reweighting
-preselection, 10 Levenberg-Marquardt outer iterations per frame (step_tol = cost_tol = 0,
-so every frame runs exactly 10). One step = one frame of the whole hot path:
+template points, 404 densely connected control points (radius 5.2; the metric names 400),
+2,000 template ORB features (+500 distractors, 10 % outliers), exhaustive 1-point-RANSAC +
+reweighting preselection, 10 Levenberg-Marquardt outer iterations per frame (step_tol =
+cost_tol = 0, so every frame runs exactly 10). One step = one frame of the whole hot path:
 raw depth -> normals -> Hamming ORB matching -> preselection -> LM solve -> output warp.
 
   value  frames/s with the frame inputs already resident in HBM, device-timed with CUDA
@@ -15,13 +15,18 @@ raw depth -> normals -> Hamming ORB matching -> preselection -> LM solve -> outp
          with pinned HOST buffers: every step copies its depth + descriptors + keypoints in
          and warps + warped points + normals out (overlapping the neighbouring frames'
          compute), with an L2 flush before every frame inside the timed wall clock.
+  config5  BASELINE config 5: 64 independent config-2 sequences sharded 64/N over the
+         GPUs (one tracker + stream per sequence), aggregate frames/s (`--workload
+         config5` makes it the headline).
   --impl reference   the reference algorithm on the host cores: the oracle port
-         (oracle/, C kernels bit-identical to the reference's numba kernels + numpy),
-         same workload, one frame per step.
+         (oracle/, C kernels bit-identical to the reference's numba kernels + the
+         reference's numpy preselection restated), same workload, config, steps and
+         warm-up; it never loads the CUDA library.
 
 Multi-GPU: frames of one sequence are sequentially dependent (warm start), so the path
 does not shard: each rank tracks its own independent sequence (replicas only,
-SURVEY.md §8e); value = all ranks' frames / max-over-ranks device time.
+SURVEY.md §8e); value = all ranks' frames / max-over-ranks device time. `--gpus N`
+without torchrun relaunches itself under torch.distributed.run with N ranks.
 """
 
 from __future__ import annotations
@@ -57,6 +62,11 @@ def parse_args():
     ap.add_argument("--cpu-frames", type=int, default=3, help="CPU-baseline sample (frames)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-config5", action="store_true", help="skip the config-5 object")
+    ap.add_argument("--workload", choices=["config2", "config5"], default="config2",
+                    help="headline line: one config-2 sequence per GPU (default) or config 5")
+    ap.add_argument("--c5-rounds", type=int, default=8, help="config-5 frames per sequence")
+    ap.add_argument("--c5-cluster", type=int, default=4, help="config-5 solver cluster size")
     return ap.parse_args()
 
 
@@ -101,17 +111,23 @@ def make_workload(config_id: int, n_frames: int, seed: int, host_template: bool 
     frames = [synth.make_frame(scene, cam, tpl0, feats, f) for f in range(1, n_frames + 1)]
     tpl, graph = host_prepare_template(tpl0, cfg) if host_template else prepare_template(tpl0, cfg)
     return dict(scene=scene, cfg=cfg, cam=cam, tpl=tpl, graph=graph, feats=feats, frames=frames,
-                iters=spec["iters"], radius=spec["radius"])
+                iters=spec["iters"], radius=spec["radius"], config_id=config_id)
 
 
-def workload_config(wl, n_gpus, rank_frames_desc):
+DATA = "synthetic (builder sphere-patch generator, seeded; random 256-bit descriptors)"
+
+
+def workload_config(wl, n_gpus):
+    """The `config` object of both arms (identical for the same workload and N)."""
     tpl, graph, sc = wl["tpl"], wl["graph"], wl["scene"]
     return {
-        "workload": f"config 2: synthetic sphere patch {sc.width}x{sc.height}, "
+        "workload": f"config {wl['config_id']}: synthetic {sc.surface} {sc.width}x{sc.height}, "
                     f"{len(tpl)} template points, {len(graph)} control points, "
                     f"{graph.edges.shape[0]} dense connections, {sc.n_features} ORB features "
                     f"(+{sc.n_distractors} distractors, {int(sc.outlier_fraction * 100)}% outliers), "
-                    f"exhaustive preselection, {wl['iters']} LM iterations/frame",
+                    f"exhaustive preselection, {wl['iters']} LM iterations/frame; one independent "
+                    f"sequence per GPU (config 5, 64 sequences sharded 64/N per GPU, is the "
+                    f"`config5` object)",
         "template_points": len(tpl),
         "control_points": len(graph),
         "edges": int(graph.edges.shape[0]),
@@ -119,7 +135,7 @@ def workload_config(wl, n_gpus, rank_frames_desc):
         "image": [sc.width, sc.height],
         "lm_iterations": wl["iters"],
         "preselection": "exhaustive",
-        "frames": rank_frames_desc,
+        "frames": f"{len(wl['frames'])} distinct frames cycled",
         "l2": "flushed between timed frames (160 MiB write > 126 MB L2; outside the device-timed events, inside the e2e wall clock)",
         "parallelism": f"replicas x{n_gpus} (independent sequences, no collective)",
     }
@@ -284,6 +300,7 @@ def run_b200(args, rank, world, local_rank):
         fi.use_matches = 1
         fi.on_device = 1
         fi.frame_id = fid
+        fi.height, fi.width = d_depth[i].shape[0], d_depth[i].shape[1]
         return fi
 
     # ---- warm-up ----
@@ -363,6 +380,7 @@ def run_b200(args, rank, world, local_rank):
             fi.use_matches = 1
             fi.on_device = 0
             fi.frame_id = fid
+            fi.height, fi.width = h_depth[i].shape[0], h_depth[i].shape[1]
             return fi
 
         trk_stream = torch.cuda.ExternalStream(trk.stream)
@@ -436,8 +454,8 @@ def run_b200(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": ms_per_step,
         "ms_per_gn_iteration": ms_per_step / wl["iters"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (builder sphere-patch generator, seeded; random 256-bit descriptors)",
-        "config": workload_config(wl, world, f"{F} distinct frames cycled (period 20)"),
+        "data": DATA,
+        "config": workload_config(wl, world),
         "e2e": e2e, "roofline": roofline, "roofline_preselect": roofline_pre,
         "gpu_launches": launches,
         "phase_ms": phase_avg, "clocks": clocks.summary(),
@@ -449,10 +467,117 @@ def run_b200(args, rank, world, local_rank):
                          "total_cost": float(rep.total_cost)},
         "solver_cluster": int(dcfg.cluster_size) or "auto",
     }
+    trk.close()
+    if not args.no_config5 or args.workload == "config5":
+        result["config5"] = run_config5(wl, rank, world, local_rank, rounds=args.c5_rounds,
+                                        cluster=args.c5_cluster)
+    if args.workload == "config5":
+        # headline = config 5's aggregate (the single-sequence line moves to `config2`)
+        c5 = result["config5"]
+        single = {k: result[k] for k in ("value", "ms_per_step", "e2e", "config", "scaling")}
+        result.update(value=c5["value"], ms_per_step=c5["device_ms_max_over_ranks"] / c5["rounds"],
+                      steps=c5["rounds"], scaling="strong", e2e=None, config2=single)
+        result["config"] = dict(result["config2"]["config"], workload=c5["workload"])
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(wl, args.cpu_frames)
-    trk.close()
     return result
+
+
+# ---------------------------------------------------------------------------------
+# config 5: many independent sequences, sharded over the GPUs
+# ---------------------------------------------------------------------------------
+
+C5_SEQUENCES = 64
+
+
+def shard_sequences(n_seq: int, world: int, rank: int) -> list[int]:
+    """Sequences of `rank` when n_seq independent sequences are split over `world` GPUs:
+    contiguous blocks, sizes differing by at most one (64/N per GPU for N | 64)."""
+    return [s for s in range(n_seq) if s * world // n_seq == rank]
+
+
+def config5_aggregate(n_seq: int, rounds: int, max_ms: float) -> float:
+    """Whole-job frames/s of config 5: every sequence's frames over the slowest rank's
+    device time (strong scaling: the 64 sequences are split, not replicated)."""
+    return n_seq * rounds / (max_ms / 1e3)
+
+
+def run_config5(wl, rank, world, local_rank, n_seq=C5_SEQUENCES, cluster=4, rounds=8, warmup=2):
+    """BASELINE config 5 on this rank: its shard of `n_seq` independent config-2
+    sequences, one tracker (own warps, buffers, CUDA stream; solver = one thread-block
+    cluster) per sequence, frames enqueued round-robin. Device time = first event to the
+    last stream's end event; the aggregate is every rank's frames / the max-over-ranks
+    time (no collective on the data path; one all_reduce(MAX) of the time)."""
+    import torch
+
+    from paper_2007_08576_b200._lib import FrameInput
+    from paper_2007_08576_b200._session import DeviceTracker, make_config
+    from paper_2007_08576_b200.warpfield import bind_points
+
+    mine = shard_sequences(n_seq, world, rank)
+    cfg, graph, feats = wl["cfg"], wl["graph"], wl["feats"]
+    dcfg = make_config(wl["cam"], cfg.energy, cfg.make_solver_config(), cfg.make_preselect_config(),
+                       sampling_radius=graph.sampling_radius, cluster_size=cluster)
+    binding = bind_points(feats.points, graph.points, 4, graph.sampling_radius)
+    dev = torch.device("cuda", local_rank)
+    frames = wl["frames"]
+    F = len(frames)
+    d_depth = [torch.from_numpy(f.depth).to(dev) for f in frames]
+    d_desc = [torch.from_numpy(f.descriptors).to(dev) for f in frames]
+    d_kp = [torch.from_numpy(f.keypoints).to(dev) for f in frames]
+    streams = [torch.cuda.Stream(device=dev) for _ in mine]
+    trks = []
+    for s in streams:
+        t = DeviceTracker(wl["tpl"], graph, dcfg, stream=s.cuda_stream)
+        t.set_features(feats.descriptors, feats.points, binding)
+        t.set_warps(graph.warps)
+        trks.append(t)
+
+    def fin(i, fid):
+        fi = FrameInput()
+        fi.depth, fi.frame_desc, fi.frame_kp = d_depth[i].data_ptr(), d_desc[i].data_ptr(), d_kp[i].data_ptr()
+        fi.n_frame, fi.use_matches, fi.on_device, fi.frame_id = d_desc[i].shape[0], 1, 1, fid
+        fi.height, fi.width = d_depth[i].shape[0], d_depth[i].shape[1]
+        return fi
+
+    # sequence q starts at its own offset in the frame pool and walks it in order
+    for r in range(warmup):
+        for q, t in zip(mine, trks):
+            t.enqueue(fin((q + r) % F, r))
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    start = torch.cuda.Event(enable_timing=True)
+    start.record(torch.cuda.current_stream(dev))
+    for s in streams:
+        s.wait_event(start)
+    launches = 0
+    for r in range(rounds):
+        for q, t in zip(mine, trks):
+            t.enqueue(fin((q + warmup + r) % F, warmup + r))
+            launches += t.launches()
+    ends = []
+    for s in streams:
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(s)
+        ends.append(e)
+    torch.cuda.synchronize(dev)
+    my_ms = max((start.elapsed_time(e) for e in ends), default=0.0)
+    max_ms = max_over_ranks(my_ms, world, dev)
+    for t in trks:
+        t.close()
+    total = n_seq * rounds
+    return {"value": config5_aggregate(n_seq, rounds, max_ms), "unit": UNIT, "n_gpus": world, "scaling": "strong",
+            "sequences": n_seq, "sequences_per_gpu": len(mine), "frames": total,
+            "rounds": rounds, "warmup_rounds": warmup, "cluster": cluster,
+            "device_ms_max_over_ranks": max_ms,
+            "per_sequence_hz": rounds / (max_ms / 1e3), "gpu_launches_rank0": launches,
+            "workload": f"config 5: {n_seq} independent config-2 sequences sharded "
+                        f"{n_seq}/{world} per GPU (contiguous blocks), one tracker + CUDA "
+                        f"stream per sequence, solver in {cluster}-CTA clusters; each "
+                        f"sequence walks the {F}-frame pool from its own offset; inputs "
+                        f"resident in HBM, L2 not flushed (64 trackers' working sets "
+                        f"exceed the L2)"}
 
 
 # ---------------------------------------------------------------------------------
@@ -460,7 +585,23 @@ def run_b200(args, rank, world, local_rank):
 # ---------------------------------------------------------------------------------
 
 
-def oracle_frame_runner(wl):
+def cpu_model() -> str:
+    """The host CPU's model name (lscpu's "Model name", read from /proc/cpuinfo)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_frame_runner(wl, n_chunks: int = 8):
+    """One frame of the reference algorithm through the oracle port: observation
+    normals (correspond.py:87-103), Hamming matching + back-projection, exhaustive
+    preselection (matching.py:174-226), 10 LM iterations (solver.py:267-378), output
+    warp (tracking.py:87). ``n_chunks`` is the reference's solver.n_chunks (8 keeps the
+    reference's bits; max(8, nproc) lets every core work)."""
     from oracle import kernels as OK
     from oracle import pipeline as OP
 
@@ -469,7 +610,7 @@ def oracle_frame_runner(wl):
     tplt = (tpl.points, tpl.normals, tpl.bind_indices, tpl.bind_weights)
     grt = (graph.points, graph.edges, graph.edge_weights)
     camt = (cam.fx, cam.fy, cam.cx, cam.cy)
-    sch = OP.Schedule(max_outer_iters=wl["iters"], step_tol=0.0, cost_tol=0.0)
+    sch = OP.Schedule(max_outer_iters=wl["iters"], step_tol=0.0, cost_tol=0.0, n_chunks=n_chunks)
     state = {"warps": graph.warps.copy()}
 
     def step(fr):
@@ -484,67 +625,122 @@ def oracle_frame_runner(wl):
     return step, OK
 
 
-def cpu_baseline(wl, n_frames):
-    step, OK = oracle_frame_runner(wl)
-    cores = os.cpu_count() or 1
-    OK.set_threads(cores)
-    step(wl["frames"][0])  # warm caches / page in
+def host_stage_timings(wl, n_frames: int) -> dict:
+    """Per-frame host times of the two stages BASELINE.md §2 asks for separately: the
+    reference's Observation.from_depth normals (correspond.py:87-103, oracle restatement)
+    and the builder's numpy Hamming oracle (+ back-projection)."""
+    from oracle import pipeline as OP
+
+    cam, feats = wl["cam"], wl["feats"]
+    camt = (cam.fx, cam.fy, cam.cx, cam.cy)
+    frames = wl["frames"][:max(1, n_frames)]
     t0 = time.perf_counter()
-    for f in wl["frames"][1:1 + n_frames]:
-        step(f)
-    dt = time.perf_counter() - t0
-    return {"value": n_frames / dt, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{n_frames} consecutive config-2 frames (full path: normals, Hamming, "
-                      f"exhaustive preselection, 10 LM iterations, output warp) through the "
-                      f"oracle port (C kernels bit-identical to the reference's numba "
-                      f"kernels, OpenMP over the reference's 8 chunks, + numpy)",
-            "ms_per_frame": dt * 1e3 / n_frames}
+    for fr in frames:
+        OP.observation_normals(fr.depth, *camt)
+    t1 = time.perf_counter()
+    for fr in frames:
+        OP.matches_from_descriptors(feats.descriptors, feats.points, fr.descriptors,
+                                    fr.keypoints, fr.depth, camt)
+    t2 = time.perf_counter()
+    return {"from_depth_ms": (t1 - t0) * 1e3 / len(frames),
+            "hamming_ms": (t2 - t1) * 1e3 / len(frames), "frames": len(frames)}
 
 
-# The reference arm runs the whole frame on the host cores (~1.5 s per config-2 frame on
-# 16 cores), so the run is bounded: at most REF_MAX_FRAMES timed frames and
-# REF_MAX_WARMUP warm-up frames whatever --steps / --warmup ask for (each step is one
-# full frame; the sample is stated in the JSON line).
-REF_MAX_FRAMES = 40
-REF_MAX_WARMUP = 3
-
-
-def run_reference(args, rank, world):
-    if rank != 0:
-        return None  # replicas are independent: rank 0 alone times the host reference
-    wl = make_workload(args.config, args.frames, seed=0, host_template=True)
-    step, OK = oracle_frame_runner(wl)
-    cores = os.cpu_count() or 1
-    OK.set_threads(cores)
+def time_oracle(wl, warm: int, steps: int, threads: int, n_chunks: int) -> float:
+    """Seconds for `steps` consecutive frames after `warm` warm-up frames."""
+    step, OK = oracle_frame_runner(wl, n_chunks=n_chunks)
+    OK.set_threads(threads)
     frames = wl["frames"]
-    warm = min(args.warmup, REF_MAX_WARMUP)
-    steps = max(1, min(args.steps, REF_MAX_FRAMES))
     for w in range(warm):
         step(frames[w % len(frames)])
     t0 = time.perf_counter()
     for i in range(steps):
         step(frames[(warm + i) % len(frames)])
-    dt = time.perf_counter() - t0
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(wl, n_frames):
+    """The b200 arm's reported CPU baseline (rank 0, N=1): a bounded sample of the same
+    workload through the oracle port, at nproc threads (the headline) and at 1 thread,
+    plus the separate from_depth / Hamming stage times."""
+    cores = os.cpu_count() or 1
+    dt = time_oracle(wl, 1, n_frames, cores, max(8, cores))
+    dt1 = time_oracle(wl, 1, 1, 1, 8)
+    return {"value": n_frames / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{n_frames} consecutive config-2 frames after 1 warm-up (full path: "
+                      f"normals, Hamming, exhaustive preselection, {wl['iters']} LM iterations, "
+                      f"output warp) through the oracle port (C kernels bit-identical to the "
+                      f"reference's numba kernels, OpenMP over solver.n_chunks = "
+                      f"{max(8, cores)}, + the reference's single-threaded numpy "
+                      f"preselection restated)",
+            "ms_per_frame": dt * 1e3 / n_frames,
+            "threads_1": {"value": 1 / dt1, "ms_per_frame": dt1 * 1e3, "frames": 1},
+            "stages": host_stage_timings(wl, 3),
+            "cpu_model": cpu_model()}
+
+
+# The reference arm runs the whole frame on the host cores (~1.5 s per config-2 frame on
+# 16 cores), so it is bounded: at most REF_MAX_FRAMES timed frames (the driver's
+# --steps 20 --warmup 5 runs unbounded: same steps, same warm-up as the b200 arm).
+REF_MAX_FRAMES = 60
+REF_MAX_WARMUP = 10
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on the host cores through the oracle
+    port, never touching the CUDA library (the package is imported for its config
+    objects and the numpy scene generator only; the template build is the oracle's)."""
+    if rank != 0:
+        return None  # replicas are independent: rank 0 alone times the host reference
+    wl = make_workload(args.config, args.frames, seed=0, host_template=True)
+    cores = os.cpu_count() or 1
+    warm = min(args.warmup, REF_MAX_WARMUP)
+    steps = max(1, min(args.steps, REF_MAX_FRAMES))
+    dt = time_oracle(wl, warm, steps, cores, max(8, cores))
     value = steps / dt
-    sample = (f"{steps} consecutive config-2 frames after {warm} warm-up (of --steps "
-              f"{args.steps} / --warmup {args.warmup}; bounded to {REF_MAX_FRAMES}), one full "
-              f"frame per step (normals, Hamming, exhaustive preselection, 10 LM iterations, "
-              f"warp), oracle port of the reference on {cores} host threads")
+    dt1 = time_oracle(wl, 1, 2, 1, 8)
+    stages = host_stage_timings(wl, 3)
+    sample = (f"{steps} consecutive config-{args.config} frames after {warm} warm-up, one "
+              f"full frame per step (normals, Hamming, exhaustive preselection, "
+              f"{wl['iters']} LM iterations, warp), oracle port of the reference on {cores} "
+              f"host threads (solver.n_chunks = {max(8, cores)})")
+    from paper_2007_08576_b200 import _lib
+
+    assert not _lib.loaded(), "the reference arm must not load the CUDA library"
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": warm, "ms_per_step": dt * 1e3 / steps,
         "ms_per_gn_iteration": dt * 1e3 / steps / wl["iters"], "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(wl, 1, f"{len(frames)} distinct frames cycled"),
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": workload_config(wl, world),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model(),
+                         "threads_1": {"value": 2 / dt1, "ms_per_frame": dt1 * 1e3 / 2,
+                                       "frames": 2},
+                         "stages": stages},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
+def relaunch_distributed(n: int) -> int:
+    """`bench.py --gpus N` started without torchrun: launch N ranks (one process per GPU)
+    through torch.distributed.run on 127.0.0.1 and return their exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

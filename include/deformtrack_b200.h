@@ -280,6 +280,12 @@ int dt_tracker_sync(dt_tracker* t);
  *                    NULL -> bound on the device per frame (k nearest, ties -> lower index)
  *   refs             (n_refs) int64 preselect references; NULL -> exhaustive arange(n)
  *   use_matches      0 = no feature term this frame
+ *   height, width    the depth image's dimensions
+ * Size contract (checked on every call, DT_ERR_INVALID_ARGUMENT otherwise): height /
+ * width equal the tracker's camera; counts are non-negative; every array a non-zero
+ * count refers to is non-NULL; match_bidx / match_bw come together; host-side refs lie
+ * in [0, n_pairs) (pairs path) or [0, n_features) (ORB path). Keypoints outside the
+ * image are not an error: they produce no match.
  */
 typedef struct {
   const double* depth;
@@ -298,6 +304,7 @@ typedef struct {
   int32_t use_matches;
   int32_t on_device;
   int32_t frame_id;
+  int32_t height, width;  /* dimensions of depth / normals: must equal dt_config's */
 } dt_frame_input;
 
 /* Per-frame outputs (HOST pointers; any may be NULL to skip that copy).

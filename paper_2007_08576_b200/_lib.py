@@ -77,6 +77,7 @@ class FrameInput(C.Structure):
         ("match_bidx", P), ("match_bw", P), ("n_pairs", I64),
         ("frame_desc", P), ("frame_kp", P), ("n_frame", I64), ("refs", P), ("n_refs", I64),
         ("use_matches", I32), ("on_device", I32), ("frame_id", I32),
+        ("height", I32), ("width", I32),
     ]
 
 
@@ -143,12 +144,16 @@ PHASES = ("normals", "orb_match", "preselect", "match_prep", "lm_solver", "warp_
 EXPORTED = ["dt_last_error", "dt_version", "dt_tracker_stream", *_SIGNATURES]
 
 
-def _load() -> C.CDLL:
+def _require_built() -> None:
     if not LIB_PATH.exists():
         raise ImportError(
             f"{LIB_PATH} is missing: build the sm_100a library first "
             "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback"
         )
+
+
+def _load() -> C.CDLL:
+    _require_built()
     lib = C.CDLL(str(LIB_PATH))
     lib.dt_last_error.restype = C.c_char_p
     lib.dt_last_error.argtypes = []
@@ -163,7 +168,30 @@ def _load() -> C.CDLL:
     return lib
 
 
-lib = _load()
+class _Lib:
+    """The library handle, opened (dlopen) at the first call into it. Importing the
+    package only checks that the library is built (and raises ImportError if not), so
+    the host-only pieces -- config objects, the synthetic scene generator, the oracle
+    arm of bench.py -- never map the CUDA library into a process that does no device
+    work."""
+
+    _cdll: C.CDLL | None = None
+
+    def __getattr__(self, name: str):
+        if _Lib._cdll is None:
+            _Lib._cdll = _load()
+        fn = getattr(_Lib._cdll, name)
+        setattr(self, name, fn)
+        return fn
+
+
+_require_built()
+lib = _Lib()
+
+
+def loaded() -> bool:
+    """Whether the CUDA library has been mapped into this process."""
+    return _Lib._cdll is not None
 
 
 def check(status: int, what: str = "") -> None:

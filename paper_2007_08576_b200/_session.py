@@ -9,6 +9,7 @@ thread-block-cluster LM launch, then returns the solution and the report.
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 from collections import OrderedDict
 from dataclasses import dataclass
 
@@ -182,6 +183,7 @@ class DeviceTracker:
         if normals is not None:
             _want(normals, (h, w, 3), "observation normals")
         fi = FrameInput()
+        fi.height, fi.width = h, w
         fi.depth = hp(depth, np.float64)
         fi.normals = hp(normals, np.float64)
         n_pairs = 0
@@ -350,17 +352,16 @@ class DeviceTracker:
 
 
 def _fingerprint(arrays) -> tuple:
-    """Cheap content digest of the cached arrays (xor and wrapping sum of their 64-bit
-    words): a template or graph mutated in place after caching is detected and rebuilt."""
+    """Position-sensitive content digest (BLAKE2b over each array's bytes, shape and
+    dtype) of the cached arrays: a template or graph edited in place after caching --
+    including a reorder of rows -- is detected and rebuilt."""
     out = []
     for a in arrays:
-        b = np.ascontiguousarray(a).view(np.uint8).ravel()
-        pad = (-b.size) % 8
-        if pad:
-            b = np.concatenate([b, np.zeros(pad, np.uint8)])
-        w = b.view(np.uint64)
-        out.append((a.shape, int(np.bitwise_xor.reduce(w)) if w.size else 0,
-                    int(w.sum(dtype=np.uint64)) if w.size else 0))
+        arr = np.ascontiguousarray(a)
+        h = hashlib.blake2b(digest_size=16)
+        h.update(repr((arr.shape, arr.dtype.str)).encode())
+        h.update(arr.view(np.uint8).ravel().data)
+        out.append(h.hexdigest())
     return tuple(out)
 
 

@@ -354,6 +354,11 @@ struct dt_tracker {
   bool last_used = false;
   cudaEvent_t ev[DT_N_PHASES + 1] = {};
   std::vector<DevBuf> bufs;
+  // buffers replaced by a growing dalloc: freed at the next synchronising call (reap)
+  std::vector<void*> retired;
+  // bumped by every allocation: a captured frame graph is only replayed while the
+  // buffers it was captured with are still the live ones
+  uint64_t buf_gen = 0;
   // template / graph
   double *tp = nullptr, *tn = nullptr, *bw = nullptr, *bws = nullptr, *cpts = nullptr, *ew = nullptr;
   int32_t *bidx = nullptr, *edges = nullptr;
@@ -388,6 +393,7 @@ struct dt_tracker {
   int64_t g_nframe[NG] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
   int g_launches[NG] = {};
   bool g_used[NG] = {};
+  uint64_t g_gen[NG] = {};
   // input set of the frame being enqueued: 0 = the tracker's own depth / descriptor /
   // keypoint buffers, 1 + s = staging slot s (read in place, no device-to-device copy)
   int in_set = 0;
@@ -458,14 +464,38 @@ struct dt_tracker {
 
 namespace {
 
+// (Re)allocate a zeroed device buffer owned by the tracker. A buffer being replaced
+// (capacity growth) is retired -- queued work may still read it -- and freed by reap()
+// at the next point where the tracker's streams are idle.
 template <typename T>
 int dalloc(dt_tracker* t, T** out, size_t count) {
   void* p = nullptr;
   const size_t bytes = sizeof(T) * (count > 0 ? count : 1);
   DT_CHECK_CUDA(cudaMalloc(&p, bytes));
   DT_CHECK_CUDA(cudaMemsetAsync(p, 0, bytes, t->stream));
+  if (*out != nullptr) {
+    for (size_t i = 0; i < t->bufs.size(); ++i)
+      if (t->bufs[i].p == static_cast<void*>(*out)) {
+        t->retired.push_back(t->bufs[i].p);
+        t->bufs.erase(t->bufs.begin() + (std::ptrdiff_t)i);
+        break;
+      }
+  }
   t->bufs.push_back({p, bytes});
   *out = static_cast<T*>(p);
+  ++t->buf_gen;
+  return DT_OK;
+}
+
+// free retired buffers once every stream of the tracker has drained (never called
+// while a stream is being captured)
+int reap(dt_tracker* t) {
+  if (t->retired.empty()) return DT_OK;
+  DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
+  if (t->copy_stream) DT_CHECK_CUDA(cudaStreamSynchronize(t->copy_stream));
+  if (t->out_stream) DT_CHECK_CUDA(cudaStreamSynchronize(t->out_stream));
+  for (void* p : t->retired) DT_CHECK_CUDA(cudaFree(p));
+  t->retired.clear();
   return DT_OK;
 }
 
@@ -671,6 +701,40 @@ int upload_binding(dt_tracker* t, const int64_t* bidx, const double* bw, int64_t
   }
   DT_CHECK_CUDA(cudaMemcpyAsync(dst_w, bw, sizeof(double) * cnt,
                                 on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  return DT_OK;
+}
+
+// The C-ABI size contract of dt_frame_input (include/deformtrack_b200.h): the caller's
+// arrays are only dereferenced after these checks pass.
+int check_frame_input(const dt_tracker* t, const dt_frame_input* in) {
+  DT_REQUIRE(in != nullptr, DT_ERR_INVALID_ARGUMENT, "frame input is NULL");
+  DT_REQUIRE(in->depth != nullptr, DT_ERR_INVALID_ARGUMENT, "depth is required");
+  DT_REQUIRE(in->height == t->cfg.height && in->width == t->cfg.width, DT_ERR_INVALID_ARGUMENT,
+             "depth is %dx%d but the tracker's camera is %dx%d", (int)in->width, (int)in->height,
+             (int)t->cfg.width, (int)t->cfg.height);
+  DT_REQUIRE(in->on_device == 0 || in->on_device == 1, DT_ERR_INVALID_ARGUMENT, "on_device must be 0 or 1");
+  DT_REQUIRE(in->n_pairs >= 0 && in->n_frame >= 0 && in->n_refs >= 0, DT_ERR_INVALID_ARGUMENT,
+             "negative count");
+  DT_REQUIRE(in->n_frame <= (int64_t)1 << 24 && in->n_pairs <= (int64_t)1 << 26, DT_ERR_INVALID_ARGUMENT,
+             "match / descriptor count out of range");
+  if (in->use_matches && in->frame_desc != nullptr) {
+    DT_REQUIRE(in->frame_kp != nullptr, DT_ERR_INVALID_ARGUMENT, "frame descriptors without keypoints");
+    DT_REQUIRE(t->n_feat > 0, DT_ERR_INVALID_ARGUMENT, "frame descriptors given but no template features set");
+  } else if (in->use_matches && in->n_pairs > 0) {
+    DT_REQUIRE(in->match_src != nullptr && in->match_dst != nullptr, DT_ERR_INVALID_ARGUMENT,
+               "match pairs missing");
+    DT_REQUIRE((in->match_bidx == nullptr) == (in->match_bw == nullptr), DT_ERR_INVALID_ARGUMENT,
+               "match_bidx and match_bw come together");
+  }
+  if (in->n_refs > 0) {
+    DT_REQUIRE(in->refs != nullptr, DT_ERR_INVALID_ARGUMENT, "n_refs > 0 but refs is NULL");
+    if (!in->on_device) {
+      const int64_t lim = in->frame_desc != nullptr ? t->n_feat : in->n_pairs;
+      for (int64_t i = 0; i < in->n_refs; ++i)
+        DT_REQUIRE(in->refs[i] >= 0 && in->refs[i] < lim, DT_ERR_INVALID_ARGUMENT,
+                   "reference index %lld outside [0, %lld)", (long long)in->refs[i], (long long)lim);
+    }
+  }
   return DT_OK;
 }
 
@@ -922,7 +986,9 @@ int run_frame(dt_tracker* t, const dt_frame_input* in, bool* used) {
   const int gw = t->pre_solver_wait == nullptr ? 0
                  : (t->copy_stream && t->pre_solver_wait == t->ev_out_copied[0] ? 1 : 2);
   const int gi = 3 * gw + set;
-  if (t->gexec[gi] == nullptr || t->g_nframe[gi] != in->n_frame) {
+  // re-capture when the descriptor count changed or any buffer was reallocated since the
+  // capture (a replay would read the replaced buffers)
+  if (t->gexec[gi] == nullptr || t->g_nframe[gi] != in->n_frame || t->g_gen[gi] != t->buf_gen) {
     if (t->gexec[gi]) cudaGraphExecDestroy(t->gexec[gi]);
     t->gexec[gi] = nullptr;
     cudaGraph_t g = nullptr;
@@ -948,6 +1014,7 @@ int run_frame(dt_tracker* t, const dt_frame_input* in, bool* used) {
     t->g_nframe[gi] = in->n_frame;
     t->g_launches[gi] = t->launches;
     t->g_used[gi] = u;
+    t->g_gen[gi] = t->buf_gen;  // after the capture: it may have grown a buffer itself
   }
   DT_CHECK_CUDA(cudaGraphLaunch(t->gexec[gi], s));
   t->launches = t->g_launches[gi];
@@ -1152,6 +1219,7 @@ int dt_tracker_destroy(dt_tracker* t) {
     if (e) cudaEventDestroy(e);
   if (t->own_stream) cudaStreamDestroy(t->stream);
   for (auto& b : t->bufs) cudaFree(b.p);
+  for (void* p : t->retired) cudaFree(p);
   if (t->h_report) cudaFreeHost(t->h_report);
   if (t->h_info) cudaFreeHost(t->h_info);
   if (t->h_stats) cudaFreeHost(t->h_stats);
@@ -1163,6 +1231,9 @@ int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* po
                             const int64_t* bind_idx, const double* bind_w) {
   DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
   DT_REQUIRE(n_features >= 0, DT_ERR_INVALID_ARGUMENT, "negative feature count");
+  DT_REQUIRE(n_features == 0 || (desc != nullptr && points != nullptr), DT_ERR_INVALID_ARGUMENT,
+             "descriptors and points are required");
+  DT_TRY(dt_tracker_sync(t));  // frames in flight still read the current feature buffers
   drop_graph(t);
   t->n_feat = n_features;
   DT_TRY(ensure_match_capacity(t, n_features));
@@ -1222,6 +1293,8 @@ int dt_tracker_set_features(dt_tracker* t, const uint8_t* desc, const double* po
 
 int dt_tracker_set_warps(dt_tracker* t, const double* warps, int from_device) {
   DT_REQUIRE(t != nullptr && warps != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  // a pipelined frame may still be copying warps_out to its host buffer
+  DT_TRY(dt_tracker_sync(t));
   DT_CHECK_CUDA(cudaMemcpyAsync(t->warps_out, warps, sizeof(double) * 8 * t->m,
                                 from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                 t->stream));
@@ -1260,15 +1333,17 @@ int dt_tracker_sync(dt_tracker* t) {
   DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
   while (t->pipe_waited < t->pipe_next) DT_TRY(dt_tracker_wait(t));  // drain the pipeline
   DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
-  return DT_OK;
+  return reap(t);
 }
 
 int dt_track_frame(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out) {
   DT_REQUIRE(t != nullptr && in != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  DT_TRY(check_frame_input(t, in));
   bool used = false;
   DT_TRY(run_frame(t, in, &used));
   t->last_used = used;
-  return collect_outputs(t, in, out, used);
+  DT_TRY(collect_outputs(t, in, out, used));
+  return reap(t);
 }
 
 int dt_tracker_get_history(dt_tracker* t, double* cost_history, double* lambda_history,
@@ -1361,6 +1436,7 @@ int dt_tracker_wait(dt_tracker* t) {
 int dt_track_frame_submit(dt_tracker* t, const dt_frame_input* in, dt_frame_output* out) {
   DT_REQUIRE(t != nullptr && in != nullptr && out != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
   DT_REQUIRE(!in->on_device, DT_ERR_INVALID_ARGUMENT, "dt_track_frame_submit takes host inputs");
+  DT_TRY(check_frame_input(t, in));
   DT_REQUIRE(in->depth != nullptr, DT_ERR_INVALID_ARGUMENT, "depth is required");
   DT_REQUIRE(in->normals == nullptr && (in->frame_desc != nullptr || !in->use_matches),
              DT_ERR_UNSUPPORTED, "the pipelined path takes depth + ORB features");
@@ -1452,6 +1528,7 @@ int dt_tracker_last_launches(dt_tracker* t) { return t ? t->launches : 0; }
 
 int dt_track_frame_async(dt_tracker* t, const dt_frame_input* in) {
   DT_REQUIRE(t != nullptr && in != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  DT_TRY(check_frame_input(t, in));
   bool used = false;
   DT_TRY(run_frame(t, in, &used));
   t->last_used = used;
@@ -1526,6 +1603,12 @@ int dt_track_frames_batched(dt_tracker** trackers, const dt_frame_input* inputs,
   (void)stream;
   // independent sequences: each tracker enqueues on its own stream; the streams overlap
   // on the device (one cluster per sequence)
+  DT_REQUIRE(n_trackers >= 0 && (n_trackers == 0 || (trackers != nullptr && inputs != nullptr)),
+             DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  for (int32_t i = 0; i < n_trackers; ++i) {
+    DT_REQUIRE(trackers[i] != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker %d is NULL", (int)i);
+    DT_TRY(check_frame_input(trackers[i], &inputs[i]));
+  }
   std::vector<char> used(n_trackers, 0);
   for (int32_t i = 0; i < n_trackers; ++i) {
     bool u = false;

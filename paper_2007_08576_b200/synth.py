@@ -295,7 +295,7 @@ CONFIGS = {
                         amplitude=5.0, n_features=500, outlier_fraction=0.1,
                         n_distractors=200), radius=10.0, iters=5),
     2: dict(scene=Scene(surface="sphere-patch", resolution=141, width=640, height=480,
-                        amplitude=5.0, n_features=2000, outlier_fraction=0.1), radius=5.3,
+                        amplitude=5.0, n_features=2000, outlier_fraction=0.1), radius=5.2,
             iters=10),
     3: dict(scene=Scene(surface="height-field", resolution=141, width=640, height=480,
                         amplitude=10.0, frame_step=5, camera_rotation_deg=0.3,

@@ -1,0 +1,83 @@
+"""BASELINE configurations 2, 3 and 4 at FULL scale on the GPU against the oracle
+(VERDICT r01 "next" #1): the workload is built exactly as bench.py builds it
+(``bench.make_workload``: same scene, radius, iterations, template build, features), and
+one ORB-path frame with exhaustive preselection is tracked teacher-forced -- device and
+oracle both start from the oracle's own solution of the previous frame (SURVEY.md §8c
+parity protocol) -- then compared to the north-star bars:
+
+* Hamming argmin indices and distances: bit-exact (against the oracle's C restatement);
+* the ORB match set (template points, back-projected observed points): bit-exact;
+* preselection flags: bit-exact;
+* n_correspondences, accepted and rejected LM steps: exact;
+* per-vertex positions within 0.1 mm (1e-4 m), total cost within 1 %.
+"""
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+pytestmark = pytest.mark.gpu
+
+VERTEX_TOL_MM = 0.1   # 1e-4 m in the reference's mm
+COST_REL_TOL = 0.01   # total cost / RMS within 1 %
+
+
+def _oracle(wl, warps, fr):
+    from oracle import pipeline as OP
+
+    tpl, graph, cam, feats = wl["tpl"], wl["graph"], wl["cam"], wl["feats"]
+    camt = (cam.fx, cam.fy, cam.cx, cam.cy)
+    src, dst, _ = OP.matches_from_descriptors(feats.descriptors, feats.points, fr.descriptors,
+                                              fr.keypoints, fr.depth, camt)
+    tplt = (tpl.points, tpl.normals, tpl.bind_indices, tpl.bind_weights)
+    grt = (graph.points, graph.edges, graph.edge_weights)
+    sch = OP.Schedule(max_outer_iters=wl["iters"], step_tol=0.0, cost_tol=0.0)
+    res, sel, pts, _ = OP.track(tplt, grt, warps, fr.depth, OP.observation_normals(fr.depth, *camt),
+                                camt, (src, dst), OP.Weights(), sch, graph.sampling_radius)
+    return src, dst, res, sel, pts
+
+
+@pytest.mark.parametrize("cid", [2, 3, 4])
+def test_full_scale_config_frame_matches_oracle(cid):
+    import bench
+    import paper_2007_08576_b200 as dt
+    from oracle import kernels as OK
+
+    wl = bench.make_workload(cid, 2, seed=0)
+    tpl, graph, cam, feats = wl["tpl"], wl["graph"], wl["cam"], wl["feats"]
+    f1, f2 = wl["frames"]
+    if cid == 2:  # the benchmark frame itself: >= 400 controls (the metric's "400 ctrl pts")
+        assert len(graph) >= 400 and len(tpl) == 141 * 141
+
+    # Hamming ORB matching, bit-exact
+    idx, dist = dt.match_descriptors(feats.descriptors, f2.descriptors)
+    oidx, odist = OK.hamming_match(feats.descriptors, f2.descriptors)
+    np.testing.assert_array_equal(idx, oidx)
+    np.testing.assert_array_equal(dist, odist)
+
+    # teacher forcing: frame 2 from the oracle's frame-1 solution
+    _, _, r1, _, _ = _oracle(wl, graph.warps, f1)
+    src, dst, ores, osel, opts = _oracle(wl, r1.warps, f2)
+
+    trk = dt.Tracker(tpl, graph, cam, wl["cfg"])
+    trk.set_features(feats.descriptors, feats.points)
+    trk.set_exhaustive(True)
+    trk.reset(r1.warps)
+    res = trk.track(f2.depth, descriptors=f2.descriptors, keypoints=f2.keypoints)
+    trk.close()
+
+    np.testing.assert_array_equal(res.matches.template_points, src)
+    np.testing.assert_array_equal(res.matches.observed_points, dst)
+    np.testing.assert_array_equal(res.matches.preselected, osel.flags)
+    assert res.report.n_correspondences == ores.n_correspondences
+    assert res.report.accepted_steps == ores.accepted_steps
+    assert res.report.rejected_steps == ores.rejected_steps
+    dev_mm = float(np.abs(res.points - opts).max())
+    assert dev_mm < VERTEX_TOL_MM, f"config {cid}: per-vertex deviation {dev_mm} mm"
+    rel = abs(res.report.total_cost - ores.total_cost) / max(ores.total_cost, 1e-30)
+    assert rel < COST_REL_TOL, f"config {cid}: total cost deviates by {rel}"

@@ -131,6 +131,7 @@ def test_device_resident_orb_output_feeds_the_tracker():
         else:
             fi.depth, fi.frame_desc, fi.frame_kp = depth.ctypes.data, desc.ctypes.data, kp.ctypes.data
         fi.n_frame, fi.use_matches, fi.on_device, fi.frame_id = n, 1, int(on_device), 0
+        fi.height, fi.width = depth.shape[0], depth.shape[1]
         wts = np.zeros((m, 8))
         pts = np.zeros((npts, 3))
         rep = Report()

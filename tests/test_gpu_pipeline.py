@@ -38,6 +38,7 @@ def _inputs(fr, fid):
     fi = FrameInput()
     fi.depth, fi.frame_desc, fi.frame_kp = d.ctypes.data, de.ctypes.data, kp.ctypes.data
     fi.n_frame, fi.use_matches, fi.on_device, fi.frame_id = de.shape[0], 1, 0, fid
+    fi.height, fi.width = d.shape[0], d.shape[1]
     return fi, (d, de, kp)
 
 
@@ -121,3 +122,79 @@ def test_changing_feature_counts_recapture_the_frame_graph():
         np.testing.assert_array_equal(a[1], b[1])
         assert a[2] == b[2] and a[3] == b[3]
     shared.close()
+
+
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_growing_feature_count_never_replays_stale_buffers(pipelined):
+    """a frame with more ORB features than any before grows the
+    descriptor buffers; a later frame whose count was captured before the growth must not
+    replay the old graph (it would match the old buffers' descriptors). Counts 300, 300
+    (captured), full (growth), 300 (the stale-replay case), full again, 300."""
+    from dataclasses import replace
+
+    import bench
+
+    wl = bench.make_workload(1, 6, seed=9)
+    m, n = len(wl["graph"]), len(wl["tpl"])
+    frames = []
+    for i, fr in enumerate(wl["frames"]):
+        keep = fr.descriptors.shape[0] if i in (2, 4) else 300
+        frames.append(replace(fr, descriptors=fr.descriptors[:keep], keypoints=fr.keypoints[:keep]))
+    warm = wl["graph"].warps
+
+    shared = _tracker(wl)
+    got = []
+    if pipelined:
+        keep_alive = []
+        for i, fr in enumerate(frames):
+            shared.set_warps(warm)  # drains the pipeline first
+            fi, keep = _inputs(fr, i)
+            fo, bufs = _outputs(m, n)
+            keep_alive.append((keep, fo, bufs))
+            shared.submit(fi, fo)
+            shared.sync()
+            w, p, rep = bufs
+            got.append((w.copy(), p.copy(), rep.total_cost, rep.n_matches))
+    else:
+        for i, fr in enumerate(frames):
+            shared.set_warps(warm)
+            fi, keep = _inputs(fr, i)
+            fo, (w, p, rep) = _outputs(m, n)
+            shared.track_raw(fi, fo)
+            got.append((w.copy(), p.copy(), rep.total_cost, rep.n_matches))
+    shared.close()
+    for i, fr in enumerate(frames):
+        fresh = _tracker(wl)
+        fresh.set_warps(warm)
+        fi, keep = _inputs(fr, i)
+        fo, (w, p, rep) = _outputs(m, n)
+        fresh.track_raw(fi, fo)
+        fresh.close()
+        np.testing.assert_array_equal(got[i][0], w, err_msg=f"frame {i}")
+        np.testing.assert_array_equal(got[i][1], p, err_msg=f"frame {i}")
+        assert got[i][2] == rep.total_cost and got[i][3] == rep.n_matches
+
+
+def test_frame_input_size_contract_is_checked():
+    """The C-ABI rejects inconsistent frame inputs instead of reading out of bounds
+    (VERDICT r01 weak #8)."""
+    import bench
+
+    wl = bench.make_workload(1, 1, seed=2)
+    m, n = len(wl["graph"]), len(wl["tpl"])
+    trk = _tracker(wl)
+    fr = wl["frames"][0]
+    fo, bufs = _outputs(m, n)
+    for mutate in (lambda fi: setattr(fi, "height", fi.height + 1),
+                   lambda fi: setattr(fi, "width", 0),
+                   lambda fi: setattr(fi, "n_frame", -1),
+                   lambda fi: setattr(fi, "frame_kp", None),
+                   lambda fi: setattr(fi, "on_device", 7)):
+        fi, keep = _inputs(fr, 0)
+        mutate(fi)
+        with pytest.raises(ValueError):
+            trk.track_raw(fi, fo)
+    fi, keep = _inputs(fr, 0)  # the tracker is still usable afterwards
+    trk.track_raw(fi, fo)
+    assert bufs[2].n_matches > 0
+    trk.close()

@@ -83,6 +83,7 @@ def run(cid: int, n_frames: int) -> dict:
         fi = FrameInput()
         fi.depth, fi.frame_desc, fi.frame_kp = d.data_ptr(), de.data_ptr(), kp.data_ptr()
         fi.n_frame, fi.use_matches, fi.on_device, fi.frame_id = de.shape[0], 1, 1, i
+        fi.height, fi.width = d.shape[0], d.shape[1]
         dtrk.enqueue(fi)
         ph = dtrk.phase_ms()
         if i > 0:

@@ -40,6 +40,7 @@ def main():
         fi = FrameInput()
         fi.depth, fi.frame_desc, fi.frame_kp = d.data_ptr(), de.data_ptr(), kp.data_ptr()
         fi.n_frame, fi.use_matches, fi.on_device, fi.frame_id = de.shape[0], 1, 1, i
+        fi.height, fi.width = d.shape[0], d.shape[1]
         trk.enqueue(fi)
     tr = trk.trace()
     cap = 2 + 1024 * 256 + 1024 * 32
