@@ -281,14 +281,21 @@ int dt_tracker_sync(dt_tracker* t);
  *   refs             (n_refs) int64 preselect references; NULL -> exhaustive arange(n)
  *   use_matches      0 = no feature term this frame
  *   height, width    the depth image's dimensions
+ *   depth_kind       DT_DEPTH_F64: (h,w) f64 row-major (the reference's Observation.depth);
+ *                    DT_DEPTH_PFM: the raw payload of a grayscale PFM file -- (h,w) f32,
+ *                    little-endian, rows bottom-up (fileio.write_pfm, fileio.py:131-139) --
+ *                    copied as is (half the bytes) and decoded on the device
  * Size contract (checked on every call, DT_ERR_INVALID_ARGUMENT otherwise): height /
  * width equal the tracker's camera; counts are non-negative; every array a non-zero
  * count refers to is non-NULL; match_bidx / match_bw come together; host-side refs lie
  * in [0, n_pairs) (pairs path) or [0, n_features) (ORB path). Keypoints outside the
  * image are not an error: they produce no match.
  */
+#define DT_DEPTH_F64 0
+#define DT_DEPTH_PFM 1
+
 typedef struct {
-  const double* depth;
+  const double* depth;  /* DT_DEPTH_PFM: points at the f32 payload (cast) */
   const double* normals;
   const double* match_src;
   const double* match_dst;
@@ -305,6 +312,7 @@ typedef struct {
   int32_t on_device;
   int32_t frame_id;
   int32_t height, width;  /* dimensions of depth / normals: must equal dt_config's */
+  int32_t depth_kind;     /* DT_DEPTH_F64 or DT_DEPTH_PFM (see below) */
 } dt_frame_input;
 
 /* Per-frame outputs (HOST pointers; any may be NULL to skip that copy).
@@ -371,6 +379,26 @@ int dt_tracker_last_launches(dt_tracker* t);
  * must live on the same device; `stream` orders the batch. */
 int dt_track_frames_batched(dt_tracker** trackers, const dt_frame_input* inputs,
                             dt_frame_output* outputs, int32_t n_trackers, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * File-format codecs (fileio.py:23-259). HOST memory, no device.
+ * dt_format_reals: `rows` lines of `cols` space-separated reals, each printed exactly as
+ *   Python's repr() prints it (shortest round-trip digits; fixed notation for decimal
+ *   exponents -4 < e <= 16, else d.ddde+XX), '\n' after each row -- the reference's ascii
+ *   PLY body byte for byte. Returns the bytes written, or -(bytes needed) when
+ *   `capacity` is too small, -1 on bad arguments.
+ * dt_parse_reals: whitespace-separated decimal reals -> out (correctly rounded, the
+ *   values Python's float() gives); returns the count parsed (stops at capacity), or
+ *   -2 - i when token i is malformed, -1 on bad arguments.
+ * dt_depth_from_pfm: device decode of a PFM payload already in DEVICE memory: (h,w) f32
+ *   rows bottom-up (big_endian = 0 for the reference's negative scale) -> (h,w) f64
+ *   rows top-down (fileio.read_pfm, fileio.py:142-160), on `stream`.
+ * ------------------------------------------------------------------------------- */
+int64_t dt_format_reals(const double* values, int64_t rows, int64_t cols, char* out,
+                        int64_t capacity);
+int64_t dt_parse_reals(const char* text, int64_t length, double* out, int64_t capacity);
+int dt_depth_from_pfm(const float* payload, int64_t h, int64_t w, int big_endian, double* depth,
+                      void* stream);
 
 #ifdef __cplusplus
 }

@@ -77,7 +77,7 @@ class FrameInput(C.Structure):
         ("match_bidx", P), ("match_bw", P), ("n_pairs", I64),
         ("frame_desc", P), ("frame_kp", P), ("n_frame", I64), ("refs", P), ("n_refs", I64),
         ("use_matches", I32), ("on_device", I32), ("frame_id", I32),
-        ("height", I32), ("width", I32),
+        ("height", I32), ("width", I32), ("depth_kind", I32),
     ]
 
 
@@ -136,12 +136,22 @@ _SIGNATURES: dict[str, list] = {
     "dt_tracker_get_phase_ms": [P, P],
     "dt_tracker_get_trace": [P, P, C.c_int],
     "dt_tracker_get_arrivals": [P, P, C.c_int],
+    "dt_depth_from_pfm": [P, I64, I64, C.c_int, P, P],
+}
+
+# int64-returning codecs (host memory; no device needed)
+_SIGNATURES_I64: dict[str, list] = {
+    "dt_format_reals": [P, I64, I64, P, I64],
+    "dt_parse_reals": [P, I64, P, I64],
 }
 
 N_PHASES = 6
 PHASES = ("normals", "orb_match", "preselect", "match_prep", "lm_solver", "warp_out")
 
-EXPORTED = ["dt_last_error", "dt_version", "dt_tracker_stream", *_SIGNATURES]
+EXPORTED = ["dt_last_error", "dt_version", "dt_tracker_stream", *_SIGNATURES, *_SIGNATURES_I64]
+
+DT_DEPTH_F64 = 0
+DT_DEPTH_PFM = 1
 
 
 def _require_built() -> None:
@@ -163,6 +173,10 @@ def _load() -> C.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = argtypes
         fn.restype = C.c_int
+    for name, argtypes in _SIGNATURES_I64.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = I64
     lib.dt_tracker_stream.argtypes = [P]
     lib.dt_tracker_stream.restype = P
     return lib

@@ -84,6 +84,27 @@ __global__ void k_observation_normals(const double* __restrict__ depth, int h, i
   normals[3 * i + 2] = n2;
 }
 
+// PFM payload (f32, rows bottom-up, little- or big-endian) -> f64 depth, rows top-down
+// (fileio.read_pfm, fileio.py:142-160: frombuffer(...).reshape(h, w)[::-1].astype(f64))
+__global__ void k_depth_from_pfm(const float* __restrict__ payload, int h, int w, int big_endian,
+                                 double* __restrict__ depth) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)h * w) return;
+  const int v = (int)(i / w), u = (int)(i - (int64_t)v * w);
+  const float* src = payload + (int64_t)(h - 1 - v) * w + u;
+  float f = __ldg(src);
+  if (big_endian) f = __int_as_float((int)__byte_perm(__float_as_uint(f), 0, 0x0123));
+  depth[i] = (double)f;
+}
+
+int launch_depth_from_pfm(const float* payload, int64_t h, int64_t w, int big_endian, double* depth,
+                          cudaStream_t s) {
+  if (h * w == 0) return DT_OK;
+  k_depth_from_pfm<<<grid_for(h * w, 256), 256, 0, s>>>(payload, (int)h, (int)w, big_endian, depth);
+  DT_CHECK_LAUNCH();
+  return DT_OK;
+}
+
 int launch_observation_normals(const double* depth, int64_t h, int64_t w, double fx, double fy,
                                double cx, double cy, double zmin, double zmax, double* normals,
                                uint8_t* valid, cudaStream_t s) {
@@ -648,6 +669,13 @@ int dt_observation_normals(const double* depth, int64_t h, int64_t w, double fx,
   DT_REQUIRE(h >= 0 && w >= 0, DT_ERR_INVALID_ARGUMENT, "negative image size");
   return launch_observation_normals(depth, h, w, fx, fy, cx, cy, z_min, z_max, normals, valid,
                                     as_stream(stream));
+}
+
+int dt_depth_from_pfm(const float* payload, int64_t h, int64_t w, int big_endian, double* depth,
+                      void* stream) {
+  DT_REQUIRE(h >= 0 && w >= 0, DT_ERR_INVALID_ARGUMENT, "negative image size");
+  DT_REQUIRE(h * w == 0 || (payload != nullptr && depth != nullptr), DT_ERR_INVALID_ARGUMENT, "NULL buffer");
+  return launch_depth_from_pfm(payload, h, w, big_endian, depth, as_stream(stream));
 }
 
 int dt_warp_and_rasterize(const double* points, const double* normals, const int64_t* bind_idx,

@@ -30,6 +30,8 @@ template <typename KeyT>
 int build_csr(const KeyT* keys, int64_t ne, int m, int* ptr, int* ent, int* scratch_cnt,
               cudaStream_t s);
 
+int launch_depth_from_pfm(const float* payload, int64_t h, int64_t w, int big_endian, double* depth,
+                          cudaStream_t s);
 int launch_observation_normals(const double* depth, int64_t h, int64_t w, double fx, double fy,
                                double cx, double cy, double zmin, double zmax, double* normals,
                                uint8_t* valid, cudaStream_t s);

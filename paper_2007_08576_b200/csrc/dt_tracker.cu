@@ -410,6 +410,15 @@ struct dt_tracker {
   double* fs_partial = nullptr;   // preselection feature scatter: per-round partials
   unsigned* fs_counter = nullptr;  // created by dt_tracker_create (destroyed with the tracker)
   double* in_depth[2] = {nullptr, nullptr};
+  // PFM-payload inputs (DT_DEPTH_PFM): the f32 bytes are staged here, then decoded on the
+  // device into the f64 depth (own buffers / the pipelined slots)
+  float* dstage = nullptr;
+  float* in_dstage[2] = {nullptr, nullptr};
+  // the pipelined path's staged match pairs / references (pairs path)
+  double* in_msrc[2] = {nullptr, nullptr};
+  double* in_mdst[2] = {nullptr, nullptr};
+  int64_t* in_refs[2] = {nullptr, nullptr};
+  int64_t in_pair_cap = 0, in_refs_cap = 0;
   uint8_t* in_desc[2] = {nullptr, nullptr};
   int32_t* in_kp[2] = {nullptr, nullptr};
   int64_t in_desc_cap = 0;
@@ -713,6 +722,10 @@ int check_frame_input(const dt_tracker* t, const dt_frame_input* in) {
              "depth is %dx%d but the tracker's camera is %dx%d", (int)in->width, (int)in->height,
              (int)t->cfg.width, (int)t->cfg.height);
   DT_REQUIRE(in->on_device == 0 || in->on_device == 1, DT_ERR_INVALID_ARGUMENT, "on_device must be 0 or 1");
+  DT_REQUIRE(in->depth_kind == DT_DEPTH_F64 || in->depth_kind == DT_DEPTH_PFM, DT_ERR_INVALID_ARGUMENT,
+             "unknown depth_kind %d", (int)in->depth_kind);
+  DT_REQUIRE(in->depth_kind == DT_DEPTH_F64 || in->normals == nullptr, DT_ERR_INVALID_ARGUMENT,
+             "precomputed normals need an f64 depth");
   DT_REQUIRE(in->n_pairs >= 0 && in->n_frame >= 0 && in->n_refs >= 0, DT_ERR_INVALID_ARGUMENT,
              "negative count");
   DT_REQUIRE(in->n_frame <= (int64_t)1 << 24 && in->n_pairs <= (int64_t)1 << 26, DT_ERR_INVALID_ARGUMENT,
@@ -759,8 +772,15 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   const int set = t->in_set;
   double* dep = set ? t->in_depth[set - 1] : t->depth;
   DT_REQUIRE(!set || in->depth == dep, DT_ERR_INVALID_ARGUMENT, "staged depth mismatch");
-  if (in->depth != dep)
+  if (in->depth_kind == DT_DEPTH_PFM) {
+    // the file's f32 payload in, decoded on the device (fileio.read_pfm)
+    if (!t->dstage) DT_TRY(dalloc(t, &t->dstage, npix));
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->dstage, in->depth, sizeof(float) * npix, kind, s));
+    DT_TRY(launch_depth_from_pfm(t->dstage, c.height, c.width, 0, dep, s));
+    ++t->launches;
+  } else if (in->depth != dep) {
     DT_CHECK_CUDA(cudaMemcpyAsync(dep, in->depth, sizeof(double) * npix, kind, s));
+  }
   if (in->normals) {
     DT_CHECK_CUDA(cudaMemcpyAsync(t->onrm, in->normals, sizeof(double) * 3 * npix, kind, s));
     k_valid_mask<<<grid_for(npix, 256), 256, 0, s>>>(dep, npix, c.z_min, c.z_max, t->dvalid);
@@ -976,7 +996,14 @@ int run_frame(dt_tracker* t, const dt_frame_input* in, bool* used) {
     // own input buffers: copy the caller's arrays in, then replay
     const cudaMemcpyKind kind = in->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const int64_t npix = (int64_t)t->cfg.width * t->cfg.height;
-    DT_CHECK_CUDA(cudaMemcpyAsync(t->depth, in->depth, sizeof(double) * npix, kind, s));
+    if (in->depth_kind == DT_DEPTH_PFM) {
+      if (!t->dstage) return enqueue_frame(t, in, used);  // first PFM frame: allocate first
+      DT_CHECK_CUDA(cudaMemcpyAsync(t->dstage, in->depth, sizeof(float) * npix, kind, s));
+      DT_TRY(launch_depth_from_pfm(t->dstage, t->cfg.height, t->cfg.width, 0, t->depth, s));
+    } else {
+      DT_CHECK_CUDA(cudaMemcpyAsync(t->depth, in->depth, sizeof(double) * npix, kind, s));
+    }
+    gin.depth_kind = DT_DEPTH_F64;
     DT_CHECK_CUDA(cudaMemcpyAsync(t->fdesc, in->frame_desc, 32 * in->n_frame, kind, s));
     DT_CHECK_CUDA(cudaMemcpyAsync(t->fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
     gin.depth = t->depth;
@@ -1394,6 +1421,28 @@ int ensure_pipeline(dt_tracker* t, int64_t n_desc) {
   return DT_OK;
 }
 
+// staging slots of the pipelined path for match pairs / references / PFM payloads
+int ensure_pipeline_pairs(dt_tracker* t, int64_t n_pairs, int64_t n_refs, bool pfm) {
+  if (n_pairs > t->in_pair_cap) {
+    const int64_t cap = std::max<int64_t>(n_pairs, 256);
+    for (int i = 0; i < 2; ++i) {
+      DT_TRY(dalloc(t, &t->in_msrc[i], 3 * cap));
+      DT_TRY(dalloc(t, &t->in_mdst[i], 3 * cap));
+    }
+    t->in_pair_cap = cap;
+  }
+  if (n_refs > t->in_refs_cap) {
+    const int64_t cap = std::max<int64_t>(n_refs, 64);
+    for (int i = 0; i < 2; ++i) DT_TRY(dalloc(t, &t->in_refs[i], cap));
+    t->in_refs_cap = cap;
+  }
+  if (pfm && !t->in_dstage[0]) {
+    const int64_t npix = (int64_t)t->cfg.width * t->cfg.height;
+    for (int i = 0; i < 2; ++i) DT_TRY(dalloc(t, &t->in_dstage[i], npix));
+  }
+  return DT_OK;
+}
+
 // host side of a finished pipelined frame: the report from the staged snapshot
 void finish_pending(dt_tracker* t, int slot) {
   dt_tracker::Pending& pd = t->pend[slot];
@@ -1438,19 +1487,37 @@ int dt_track_frame_submit(dt_tracker* t, const dt_frame_input* in, dt_frame_outp
   DT_REQUIRE(!in->on_device, DT_ERR_INVALID_ARGUMENT, "dt_track_frame_submit takes host inputs");
   DT_TRY(check_frame_input(t, in));
   DT_REQUIRE(in->depth != nullptr, DT_ERR_INVALID_ARGUMENT, "depth is required");
-  DT_REQUIRE(in->normals == nullptr && (in->frame_desc != nullptr || !in->use_matches),
-             DT_ERR_UNSUPPORTED, "the pipelined path takes depth + ORB features");
+  DT_REQUIRE(in->normals == nullptr, DT_ERR_UNSUPPORTED, "the pipelined path computes the normals itself");
+  DT_REQUIRE(in->match_w == nullptr && in->match_bidx == nullptr, DT_ERR_UNSUPPORTED,
+             "the pipelined path preselects and binds the pairs itself");
   // at most two frames in flight
   if (t->pipe_next - t->pipe_waited >= 2) DT_TRY(dt_tracker_wait(t));
   const int64_t nd = in->frame_desc ? in->n_frame : 0;
+  const int64_t np = (in->use_matches && in->frame_desc == nullptr) ? in->n_pairs : 0;
+  const int64_t nref = in->refs != nullptr ? in->n_refs : 0;
   DT_TRY(ensure_pipeline(t, nd));
+  DT_TRY(ensure_pipeline_pairs(t, np, nref, in->depth_kind == DT_DEPTH_PFM));
   const int slot = (int)(t->pipe_next % 2);
   const int64_t npix = (int64_t)t->cfg.width * t->cfg.height;
   cudaStream_t cs = t->copy_stream, s = t->stream;
   // stage the inputs once the frame that used this slot has consumed them
   DT_CHECK_CUDA(cudaStreamWaitEvent(cs, t->ev_in_free[slot], 0));
-  DT_CHECK_CUDA(cudaMemcpyAsync(t->in_depth[slot], in->depth, sizeof(double) * npix,
-                                cudaMemcpyHostToDevice, cs));
+  const bool pfm = in->depth_kind == DT_DEPTH_PFM;
+  if (pfm)  // the file's f32 payload (half the bytes); decoded on the compute stream
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->in_dstage[slot], in->depth, sizeof(float) * npix,
+                                  cudaMemcpyHostToDevice, cs));
+  else
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->in_depth[slot], in->depth, sizeof(double) * npix,
+                                  cudaMemcpyHostToDevice, cs));
+  if (np > 0) {
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->in_msrc[slot], in->match_src, sizeof(double) * 3 * np,
+                                  cudaMemcpyHostToDevice, cs));
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->in_mdst[slot], in->match_dst, sizeof(double) * 3 * np,
+                                  cudaMemcpyHostToDevice, cs));
+  }
+  if (nref > 0)
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->in_refs[slot], in->refs, sizeof(int64_t) * nref,
+                                  cudaMemcpyHostToDevice, cs));
   if (nd > 0) {
     DT_CHECK_CUDA(cudaMemcpyAsync(t->in_desc[slot], in->frame_desc, 32 * nd, cudaMemcpyHostToDevice, cs));
     DT_CHECK_CUDA(cudaMemcpyAsync(t->in_kp[slot], in->frame_kp, sizeof(int32_t) * 2 * nd,
@@ -1460,11 +1527,19 @@ int dt_track_frame_submit(dt_tracker* t, const dt_frame_input* in, dt_frame_outp
   // compute: wait for the inputs; the solver (which rewrites warps / report / weights)
   // waits until the previous frame's outputs are copied out
   DT_CHECK_CUDA(cudaStreamWaitEvent(s, t->ev_in_ready[slot], 0));
+  if (pfm) DT_TRY(launch_depth_from_pfm(t->in_dstage[slot], t->cfg.height, t->cfg.width, 0,
+                                        t->in_depth[slot], s));
   dt_frame_input din = *in;
   din.on_device = 1;
+  din.depth_kind = DT_DEPTH_F64;
   din.depth = t->in_depth[slot];
   din.frame_desc = nd > 0 ? t->in_desc[slot] : nullptr;
   din.frame_kp = nd > 0 ? t->in_kp[slot] : nullptr;
+  if (np > 0) {
+    din.match_src = t->in_msrc[slot];
+    din.match_dst = t->in_mdst[slot];
+  }
+  if (nref > 0) din.refs = t->in_refs[slot];
   t->pre_solver_wait = t->pipe_next > 0 ? t->ev_out_copied[1 - slot] : nullptr;
   t->in_set = 1 + slot;  // the frame reads the staging slot in place
   bool used = false;
