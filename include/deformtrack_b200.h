@@ -318,7 +318,10 @@ typedef struct {
 /* Per-frame outputs (HOST pointers; any may be NULL to skip that copy).
  *   warps (m,8), points (n,3), normals (n,3), match_weights / match_flags (n_matches),
  *   match_src / match_dst (n_matches,3) (the ORB path's MatchSet), control_data_weights (m),
- *   report. */
+ *   report, and the frame's per-iteration histories (energy.EnergyReport cost_history /
+ *   lambda_history, solver.py:345-355): the first report.n_cost_history rows of
+ *   cost_history and report.outer_iterations rows of lambda_history / stalled are set.
+ *   The pipelined path (dt_track_frame_submit) fills them from the frame's own snapshot. */
 typedef struct {
   double* warps;
   double* points;
@@ -330,6 +333,9 @@ typedef struct {
   int64_t match_capacity;
   double* control_data_weights;
   dt_report* report;
+  double* cost_history;    /* (max_outer_iters,2) [before, after] of the accepted steps */
+  double* lambda_history;  /* (max_outer_iters,2) [min, max] damping per outer iteration */
+  int32_t* stalled;        /* (max_outer_iters) 1 where the iteration stalled */
 } dt_frame_output;
 
 /* Run one frame (asynchronous on the tracker stream; results valid after

@@ -86,6 +86,7 @@ class FrameOutput(C.Structure):
         ("warps", P), ("points", P), ("normals", P), ("match_weights", P), ("match_flags", P),
         ("match_src", P), ("match_dst", P), ("match_capacity", I64),
         ("control_data_weights", P), ("report", P),
+        ("cost_history", P), ("lambda_history", P), ("stalled", P),
     ]
 
 

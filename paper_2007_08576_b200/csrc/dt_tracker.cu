@@ -422,7 +422,9 @@ struct dt_tracker {
   uint8_t* in_desc[2] = {nullptr, nullptr};
   int32_t* in_kp[2] = {nullptr, nullptr};
   int64_t in_desc_cap = 0;
-  int64_t* stage_info[2] = {nullptr, nullptr};   // device snapshot: info[4], stats[3], report
+  int64_t* stage_info[2] = {nullptr, nullptr};   // device snapshot: info[4], stats[3], report,
+                                                 // cost / lambda / stall histories
+  int stage_words = 0;
   int64_t* h_stage[2] = {nullptr, nullptr};      // pinned host copy of the snapshot
   struct Pending {
     bool active = false, used = false;
@@ -943,6 +945,15 @@ int collect_outputs(dt_tracker* t, const dt_frame_input* in, dt_frame_output* ou
     if (out->match_dst)
       DT_CHECK_CUDA(cudaMemcpyAsync(out->match_dst, t->m_dst, sizeof(double) * 3 * cap, cudaMemcpyDeviceToHost, s));
   }
+  {
+    const int it = t->cfg.max_outer_iters;
+    if (out->cost_history)
+      DT_CHECK_CUDA(cudaMemcpyAsync(out->cost_history, t->cost_hist, sizeof(double) * 2 * it, cudaMemcpyDeviceToHost, s));
+    if (out->lambda_history)
+      DT_CHECK_CUDA(cudaMemcpyAsync(out->lambda_history, t->lam_hist, sizeof(double) * 2 * it, cudaMemcpyDeviceToHost, s));
+    if (out->stalled)
+      DT_CHECK_CUDA(cudaMemcpyAsync(out->stalled, t->stalled_hist, sizeof(int32_t) * it, cudaMemcpyDeviceToHost, s));
+  }
   DT_CHECK_CUDA(cudaMemcpyAsync(t->h_report, t->report, sizeof(dt_report), cudaMemcpyDeviceToHost, s));
   DT_CHECK_CUDA(cudaMemcpyAsync(t->h_info, t->info, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, s));
   DT_CHECK_CUDA(cudaMemcpyAsync(t->h_stats, t->astats, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
@@ -1339,6 +1350,7 @@ int dt_tracker_get_warps(dt_tracker* t, double* warps_host) {
 
 int dt_tracker_set_config(dt_tracker* t, const dt_config* cfg) {
   DT_REQUIRE(t != nullptr, DT_ERR_INVALID_ARGUMENT, "tracker is NULL");
+  DT_TRY(dt_tracker_sync(t));  // frames in flight use the current histories / staging
   drop_graph(t);
   DT_TRY(validate_config(cfg));
   DT_REQUIRE(cfg->width == t->cfg.width && cfg->height == t->cfg.height, DT_ERR_INVALID_ARGUMENT,
@@ -1379,17 +1391,26 @@ int dt_tracker_get_history(dt_tracker* t, double* cost_history, double* lambda_h
 
 namespace {
 
-constexpr int STAGE_WORDS = 4 + 3 + (int)((sizeof(dt_report) + 7) / 8);
+constexpr int STAGE_BASE = 4 + 3 + (int)((sizeof(dt_report) + 7) / 8);
+// snapshot words for `it` outer iterations: the base + cost (2 it) + lambda (2 it) + stalled (it)
+inline int stage_words(int it) { return STAGE_BASE + 5 * it; }
 
 __global__ void k_stage_outputs(const int64_t* __restrict__ info, const double* __restrict__ astats,
                                 const double* __restrict__ pstats, const dt_report* __restrict__ rep,
-                                int64_t* __restrict__ stage) {
+                                const double* __restrict__ cost_hist, const double* __restrict__ lam_hist,
+                                const int32_t* __restrict__ stalled, int it, int64_t* __restrict__ stage) {
   const int i = threadIdx.x;
   if (i < 4) stage[i] = info[i];
   if (i < 2) reinterpret_cast<double*>(stage + 4)[i] = astats[i];
   if (i == 0) reinterpret_cast<double*>(stage + 4)[2] = pstats[0];
   const int nw = (int)((sizeof(dt_report) + 7) / 8);
   if (i < nw) stage[7 + i] = reinterpret_cast<const int64_t*>(rep)[i];
+  double* h = reinterpret_cast<double*>(stage + STAGE_BASE);
+  for (int j = i; j < 2 * it; j += blockDim.x) {
+    h[j] = cost_hist[j];
+    h[2 * it + j] = lam_hist[j];
+  }
+  for (int j = i; j < it; j += blockDim.x) stage[STAGE_BASE + 4 * it + j] = stalled[j];
 }
 
 int ensure_pipeline(dt_tracker* t, int64_t n_desc) {
@@ -1403,11 +1424,21 @@ int ensure_pipeline(dt_tracker* t, int64_t n_desc) {
       DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_done[i], cudaEventDisableTiming));
       DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_out_copied[i], cudaEventDisableTiming));
       DT_TRY(dalloc(t, &t->in_depth[i], npix));
-      DT_TRY(dalloc(t, &t->stage_info[i], STAGE_WORDS));
-      DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_stage[i], sizeof(int64_t) * STAGE_WORDS));
+      DT_TRY(dalloc(t, &t->stage_info[i], stage_words(t->cfg.max_outer_iters)));
+      DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_stage[i],
+                                   sizeof(int64_t) * stage_words(t->cfg.max_outer_iters)));
     }
     DT_TRY(dalloc(t, &t->dev_args_slot, 2));
+    t->stage_words = stage_words(t->cfg.max_outer_iters);
     t->args_dirty = true;  // the per-slot solver arguments still have to be written
+  }
+  if (t->stage_words < stage_words(t->cfg.max_outer_iters)) {  // more iterations since (set_config)
+    t->stage_words = stage_words(t->cfg.max_outer_iters);
+    for (int i = 0; i < 2; ++i) {
+      DT_TRY(dalloc(t, &t->stage_info[i], t->stage_words));
+      DT_CHECK_CUDA(cudaFreeHost(t->h_stage[i]));
+      DT_CHECK_CUDA(cudaMallocHost((void**)&t->h_stage[i], sizeof(int64_t) * t->stage_words));
+    }
   }
   if (n_desc > t->in_desc_cap) {
     const int64_t cap = std::max<int64_t>(n_desc, 256);
@@ -1465,6 +1496,12 @@ void finish_pending(dt_tracker* t, int slot) {
     R.preselect_reference = -1;
   }
   if (pd.out.report) *pd.out.report = R;
+  const int it = t->cfg.max_outer_iters;
+  const double* h = reinterpret_cast<const double*>(st + STAGE_BASE);
+  if (pd.out.cost_history) std::memcpy(pd.out.cost_history, h, sizeof(double) * 2 * it);
+  if (pd.out.lambda_history) std::memcpy(pd.out.lambda_history, h + 2 * it, sizeof(double) * 2 * it);
+  if (pd.out.stalled)
+    for (int j = 0; j < it; ++j) pd.out.stalled[j] = (int32_t)st[STAGE_BASE + 4 * it + j];
   pd.active = false;
 }
 
@@ -1527,6 +1564,13 @@ int dt_track_frame_submit(dt_tracker* t, const dt_frame_input* in, dt_frame_outp
   // compute: wait for the inputs; the solver (which rewrites warps / report / weights)
   // waits until the previous frame's outputs are copied out
   DT_CHECK_CUDA(cudaStreamWaitEvent(s, t->ev_in_ready[slot], 0));
+  // a previous frame whose annotated matches are still being copied out: its preselection
+  // arrays must not be rewritten before that copy (the usual pre-solver wait covers the
+  // solver's outputs only)
+  if (t->pipe_next > 0 && t->pend[1 - slot].active &&
+      (t->pend[1 - slot].out.match_weights || t->pend[1 - slot].out.match_flags) &&
+      t->pend[1 - slot].out.match_capacity > 0)
+    DT_CHECK_CUDA(cudaStreamWaitEvent(s, t->ev_out_copied[1 - slot], 0));
   if (pfm) DT_TRY(launch_depth_from_pfm(t->in_dstage[slot], t->cfg.height, t->cfg.width, 0,
                                         t->in_depth[slot], s));
   dt_frame_input din = *in;
@@ -1549,7 +1593,8 @@ int dt_track_frame_submit(dt_tracker* t, const dt_frame_input* in, dt_frame_outp
   DT_TRY(st);
   t->last_used = used;
   DT_CHECK_CUDA(cudaEventRecord(t->ev_in_free[slot], s));
-  k_stage_outputs<<<1, 64, 0, s>>>(t->info, t->astats, t->pstats, t->report, t->stage_info[slot]);
+  k_stage_outputs<<<1, 64, 0, s>>>(t->info, t->astats, t->pstats, t->report, t->cost_hist, t->lam_hist,
+                                   t->stalled_hist, t->cfg.max_outer_iters, t->stage_info[slot]);
   DT_CHECK_LAUNCH();
   DT_CHECK_CUDA(cudaEventRecord(t->ev_done[slot], s));
   // outputs back on their own stream while the next frame computes (a single copy stream
@@ -1565,7 +1610,16 @@ int dt_track_frame_submit(dt_tracker* t, const dt_frame_input* in, dt_frame_outp
   if (out->control_data_weights)
     DT_CHECK_CUDA(cudaMemcpyAsync(out->control_data_weights, t->wa_out, sizeof(double) * t->m,
                                   cudaMemcpyDeviceToHost, os));
-  DT_CHECK_CUDA(cudaMemcpyAsync(t->h_stage[slot], t->stage_info[slot], sizeof(int64_t) * STAGE_WORDS,
+  const int64_t mcap = std::min<int64_t>(out->match_capacity, t->match_cap);
+  if (mcap > 0) {
+    // the annotated matches (MatchSet weights / flags): the next frame's preselection
+    // waits for these copies (wait_matches below)
+    if (out->match_weights)
+      DT_CHECK_CUDA(cudaMemcpyAsync(out->match_weights, t->m_w, sizeof(double) * mcap, cudaMemcpyDeviceToHost, os));
+    if (out->match_flags)
+      DT_CHECK_CUDA(cudaMemcpyAsync(out->match_flags, t->m_flags, mcap, cudaMemcpyDeviceToHost, os));
+  }
+  DT_CHECK_CUDA(cudaMemcpyAsync(t->h_stage[slot], t->stage_info[slot], sizeof(int64_t) * t->stage_words,
                                 cudaMemcpyDeviceToHost, os));
   DT_CHECK_CUDA(cudaEventRecord(t->ev_out_copied[slot], os));
   dt_tracker::Pending& pd = t->pend[slot];
