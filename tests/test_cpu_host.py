@@ -14,7 +14,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def header_symbols():
     text = (ROOT / "include" / "deformtrack_b200.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*|void\*)\s+(dt_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int64_t|int|const char\*|void\*)\s+(dt_\w+)\(", text, re.M)))
 
 
 def test_library_exports_every_header_symbol():
