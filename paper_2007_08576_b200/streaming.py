@@ -57,15 +57,15 @@ class _Outs:
         self.stalled = s.st[:no].copy()
 
 
-def _pinned(shape, dtype=np.float64) -> np.ndarray:
-    """Page-locked host array (torch's pinned allocator; torch is plumbing here)."""
+def _pinned(owners: list, shape, dtype=np.float64) -> np.ndarray:
+    """Page-locked host array (torch's pinned allocator; torch is plumbing here); the
+    owning tensor is kept in `owners` for as long as the array is in use."""
     import torch
 
     n = int(np.prod(shape)) if shape else 1
     t = torch.empty(max(n, 1) * np.dtype(dtype).itemsize, dtype=torch.uint8).pin_memory()
-    arr = t.numpy().view(dtype)[:n].reshape(shape)
-    arr._pin_owner = t  # noqa: SLF001 (keep the tensor alive with the view)
-    return arr
+    owners.append(t)
+    return t.numpy().view(dtype)[:n].reshape(shape)
 
 
 class StreamingTracker:
@@ -84,14 +84,16 @@ class StreamingTracker:
         self.m, self.n = len(graph), len(template)
         self._it = int(cfg.max_outer_iters)
         self._cap = int(max_matches)
+        self._owners: list = []
         self._slots = [self._make_slot() for _ in range(2)]
         self._pending: deque = deque()
         self._next_slot = 0
         self.frame_index = 0
 
     def _make_slot(self) -> _Slot:
-        s = _Slot(_pinned((self.m, 8)), _pinned((self.n, 3)), _pinned((self.n, 3)),
-                  _pinned((self.m,)), _pinned((self._cap,)), _pinned((self._cap,), np.uint8),
+        o = self._owners
+        s = _Slot(_pinned(o, (self.m, 8)), _pinned(o, (self.n, 3)), _pinned(o, (self.n, 3)),
+                  _pinned(o, (self.m,)), _pinned(o, (self._cap,)), _pinned(o, (self._cap,), np.uint8),
                   np.zeros((self._it, 2)), np.zeros((self._it, 2)), np.zeros(self._it, np.int32),
                   Report(), FrameOutput())
         fo = s.fo
@@ -186,6 +188,8 @@ class StreamingTracker:
 
     def close(self) -> None:
         self.device.close()
+        self._slots = []
+        self._owners = []
 
 
 __all__ = ["StreamingTracker"]
