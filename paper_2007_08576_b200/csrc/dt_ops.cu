@@ -40,9 +40,20 @@ __device__ __forceinline__ bool depth_ok(double z, double zmin, double zmax) {
   return isfinite(z) && z > zmin && z < zmax;
 }
 
+// 32-byte pixel record of the solver's projective association (one 256-bit load at the
+// projected pixel): {depth if valid_depth_mask else NaN, observed normal x, y, z}
+__device__ __forceinline__ void store_pixel(double* rec, double z, bool zok, double n0, double n1,
+                                            double n2) {
+  const double d = zok ? z : __longlong_as_double(0x7ff8000000000000ll);
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(rec), "d"(d), "d"(n0), "d"(n1),
+               "d"(n2)
+               : "memory");
+}
+
 __global__ void k_observation_normals(const double* __restrict__ depth, int h, int w, double fx,
                                       double fy, double cx, double cy, double zmin, double zmax,
-                                      double* __restrict__ normals, uint8_t* __restrict__ valid) {
+                                      double* __restrict__ normals, uint8_t* __restrict__ valid,
+                                      double* __restrict__ pix) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)h * w) return;
   const int v = (int)(i / w);
@@ -79,9 +90,30 @@ __global__ void k_observation_normals(const double* __restrict__ depth, int h, i
       }
     }
   }
-  normals[3 * i + 0] = n0;
-  normals[3 * i + 1] = n1;
-  normals[3 * i + 2] = n2;
+  if (normals) {
+    normals[3 * i + 0] = n0;
+    normals[3 * i + 1] = n1;
+    normals[3 * i + 2] = n2;
+  }
+  if (pix) store_pixel(pix + 4 * i, z, depth_ok(z, zmin, zmax), n0, n1, n2);
+}
+
+// pixel records from a depth map + caller-supplied observation normals
+__global__ void k_pack_pixels(const double* __restrict__ depth, const double* __restrict__ normals,
+                              int64_t npix, double zmin, double zmax, double* __restrict__ pix) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npix) return;
+  const double z = depth[i];
+  store_pixel(pix + 4 * i, z, depth_ok(z, zmin, zmax), normals[3 * i], normals[3 * i + 1],
+              normals[3 * i + 2]);
+}
+
+int launch_pack_pixels(const double* depth, const double* normals, int64_t npix, double zmin,
+                       double zmax, double* pix, cudaStream_t s) {
+  if (npix == 0) return DT_OK;
+  k_pack_pixels<<<grid_for(npix, 256), 256, 0, s>>>(depth, normals, npix, zmin, zmax, pix);
+  DT_CHECK_LAUNCH();
+  return DT_OK;
 }
 
 // PFM payload (f32, rows bottom-up, little- or big-endian) -> f64 depth, rows top-down
@@ -107,10 +139,10 @@ int launch_depth_from_pfm(const float* payload, int64_t h, int64_t w, int big_en
 
 int launch_observation_normals(const double* depth, int64_t h, int64_t w, double fx, double fy,
                                double cx, double cy, double zmin, double zmax, double* normals,
-                               uint8_t* valid, cudaStream_t s) {
+                               uint8_t* valid, cudaStream_t s, double* pix) {
   if (h * w == 0) return DT_OK;
   k_observation_normals<<<grid_for(h * w, 256), 256, 0, s>>>(depth, (int)h, (int)w, fx, fy, cx, cy,
-                                                            zmin, zmax, normals, valid);
+                                                            zmin, zmax, normals, valid, pix);
   DT_CHECK_LAUNCH();
   return DT_OK;
 }

@@ -34,7 +34,10 @@ int launch_depth_from_pfm(const float* payload, int64_t h, int64_t w, int big_en
                           cudaStream_t s);
 int launch_observation_normals(const double* depth, int64_t h, int64_t w, double fx, double fy,
                                double cx, double cy, double zmin, double zmax, double* normals,
-                               uint8_t* valid, cudaStream_t s);
+                               uint8_t* valid, cudaStream_t s, double* pix = nullptr);
+// the solver's 32-byte pixel records {depth or NaN, normal xyz} from depth + given normals
+int launch_pack_pixels(const double* depth, const double* normals, int64_t npix, double zmin,
+                       double zmax, double* pix, cudaStream_t s);
 int launch_bind_points_i32(const double* pts, int64_t n, const double* ctrl, int m, int k,
                            double sigma, int32_t* idx, double* w, cudaStream_t s);
 

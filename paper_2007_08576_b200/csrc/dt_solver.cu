@@ -267,11 +267,12 @@ __device__ __forceinline__ void blend_gradient_fast(const double B[8], double px
 constexpr int EROW = 24;
 
 __device__ __forceinline__ void store_row8(double* dst, const double* J6, double v) {
-  double2* d2 = reinterpret_cast<double2*>(dst);
-  d2[0] = make_double2(J6[0], J6[1]);
-  d2[1] = make_double2(J6[2], J6[3]);
-  d2[2] = make_double2(J6[4], J6[5]);
-  d2[3] = make_double2(v, 0.0);
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(J6[0]), "d"(J6[1]),
+               "d"(J6[2]), "d"(J6[3])
+               : "memory");
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4), "d"(J6[4]), "d"(J6[5]),
+               "d"(v), "d"(0.0)
+               : "memory");
 }
 
 // Writes the unit rows of edge e into `erow` (at the bins' CSR positions) and its three

@@ -45,10 +45,11 @@ struct SolverArgs {
   const int* ipos;   // (2E) inverse: CSR position of (edge, side)
   const int* iinfo;  // (2E) per CSR position: (other endpoint << 1) | side
   const double* iew; // (2E) per CSR position: edge weight
-  // frame observation
-  const double* depth;
-  const uint8_t* dvalid;
-  const double* onrm;
+  // k = 4 only: the per-point static inputs of a relink packed for 256-bit loads
+  const double* pst;  // n x 16: alpha[4], sqrt(alpha)[4], template point xyz + pad, normal xyz + pad
+  const int* pi8;     // n x 8: bind index[4], control-CSR position[4]
+  // frame observation: per pixel {depth if valid else NaN, observed normal xyz} (32 B)
+  const double* pixrec;
   // active feature matches of the frame (compacted on the device)
   const int64_t* n_active;
   const double* fp;
@@ -80,10 +81,8 @@ struct SolverArgs {
   // value passes); per (point, slot) and (match, slot, component): the normal-equation
   // row [J0..J5, sqrt(w) r, sqrt(w)] of its control, stored at its control-CSR position
   // so that every control's rows are contiguous
-  uint8_t* cvalid;   // 2 x n correspondence valid
-  double* cobs;      // 2 x n x 3 observed point
-  double* cnrm;      // 2 x n x 3 observed normal
-  double* pr_rs;     // 2 x n robust sqrt weight
+  double* crec;      // 2 x n x 8 correspondence records (64 B): observed point xyz, robust
+                     // sqrt weight, observed normal xyz, valid (1 / 0)
   double* prow;      // 2 x (n*k) x 8 point rows
   double* mrow;      // 2 x (Ma*k*3) x 8 match rows
   int ma_cap;        // match capacity Ma (stride between the two match row buffers)

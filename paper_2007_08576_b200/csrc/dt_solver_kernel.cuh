@@ -17,17 +17,38 @@
 
 // one of the two linearization buffers
 struct PBuf {
-  uint8_t* valid;  // n
-  double* obs;     // n x 3
-  double* nrm;     // n x 3
-  double* rs;      // n
-  double* row;     // (n*k) x 8 rows at control-CSR positions
+  double* rec;  // n x 8 correspondence records [o0 o1 o2 rs g0 g1 g2 valid]
+  double* row;  // (n*k) x 8 rows at control-CSR positions
 };
 
 __device__ __forceinline__ PBuf pbuf(const SolverArgs& A, int b) {
   const int64_t n = A.n;
-  return {A.cvalid + b * n, A.cobs + 3 * b * n, A.cnrm + 3 * b * n, A.pr_rs + b * n,
-          A.prow + (size_t)b * n * A.k * 8};
+  return {A.crec + (size_t)b * n * 8, A.prow + (size_t)b * n * A.k * 8};
+}
+
+// 256-bit global accesses (LDG/STG.E.ENL2.256): a 64-byte row or record is two of them.
+// Volatile so they are never merged with or hoisted above a domain barrier.
+__device__ __forceinline__ void st256(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+// data written by other CTAs in an earlier phase (L1-cacheable: barriers invalidate L1)
+__device__ __forceinline__ void ld256(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.ca.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
+// read-only for the whole launch (template statics, the frame's pixel records)
+__device__ __forceinline__ void ld256_nc(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
+__device__ __forceinline__ void ld256_nc_i(const int* p, int v[8]) {
+  asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                 "=r"(v[7])
+               : "l"(p));
 }
 
 __device__ __forceinline__ double* mrows(const SolverArgs& A, int b) {
@@ -43,21 +64,13 @@ __device__ __forceinline__ double* evals_buf(const SolverArgs& A, int b) {
 }
 
 __device__ __forceinline__ void store_row(double* dst, const double r[8]) {
-  double2* d2 = reinterpret_cast<double2*>(dst);
-  d2[0] = make_double2(r[0], r[1]);
-  d2[1] = make_double2(r[2], r[3]);
-  d2[2] = make_double2(r[4], r[5]);
-  d2[3] = make_double2(r[6], r[7]);
+  st256(dst, r[0], r[1], r[2], r[3]);
+  st256(dst + 4, r[4], r[5], r[6], r[7]);
 }
 
 __device__ __forceinline__ void load_row(const double* src, double r[8]) {
-  const double2* s2 = reinterpret_cast<const double2*>(src);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double2 v = __ldca(s2 + i);
-    r[2 * i] = v.x;
-    r[2 * i + 1] = v.y;
-  }
+  ld256(src, r[0], r[1], r[2], r[3]);
+  ld256(src + 4, r[4], r[5], r[6], r[7]);
 }
 
 // Relink point p at the warps in smem (kernels.py:483-569) and linearize it into `nb`
@@ -83,33 +96,46 @@ struct PointIn {
 template <int KM>
 __device__ __forceinline__ void point_load(const SolverArgs& A, int64_t p, const PBuf* ob,
                                            PointIn<KM>& in) {
-  const int kk = KM == 4 ? 4 : A.k;
-#pragma unroll
-  for (int s = 0; s < KM; ++s)
-    if (s < kk) {
-      in.idx[s] = A.bidx[p * kk + s];
-      in.a[s] = A.bw[p * kk + s];
-      in.pos[s] = __ldg(A.cpos + p * kk + s);
-      in.sqa[s] = __ldg(A.bws + p * kk + s);  // sqrt(alpha), correctly rounded: the reference's
-    }
   in.ovalid = 0;
   in.oo0 = in.oo1 = in.oo2 = in.on0 = in.on1 = in.on2 = in.ors = 0.0;
-  if (ob) {
-    in.ovalid = ldu8(ob->valid + p);
-    in.oo0 = ld(ob->obs + 3 * p);
-    in.oo1 = ld(ob->obs + 3 * p + 1);
-    in.oo2 = ld(ob->obs + 3 * p + 2);
-    in.on0 = ld(ob->nrm + 3 * p);
-    in.on1 = ld(ob->nrm + 3 * p + 1);
-    in.on2 = ld(ob->nrm + 3 * p + 2);
-    in.ors = ld(ob->rs + p);
+  if (ob) {  // the frozen correspondence record: two 256-bit loads
+    double v;
+    ld256(ob->rec + 8 * p, in.oo0, in.oo1, in.oo2, in.ors);
+    ld256(ob->rec + 8 * p + 4, in.on0, in.on1, in.on2, v);
+    in.ovalid = v != 0.0 ? 1 : 0;
   }
-  in.px = A.tp[3 * p];
-  in.py = A.tp[3 * p + 1];
-  in.pz = A.tp[3 * p + 2];
-  in.tn0 = A.tn[3 * p];
-  in.tn1 = A.tn[3 * p + 1];
-  in.tn2 = A.tn[3 * p + 2];
+  if constexpr (KM == 4) {
+    // the packed statics: five 256-bit loads instead of 22 scalar ones
+    const double* q = A.pst + 16 * p;
+    ld256_nc(q, in.a[0], in.a[1], in.a[2], in.a[3]);
+    ld256_nc(q + 4, in.sqa[0], in.sqa[1], in.sqa[2], in.sqa[3]);
+    double pad;
+    ld256_nc(q + 8, in.px, in.py, in.pz, pad);
+    ld256_nc(q + 12, in.tn0, in.tn1, in.tn2, pad);
+    int ip[8];
+    ld256_nc_i(A.pi8 + 8 * p, ip);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      in.idx[s] = ip[s];
+      in.pos[s] = ip[4 + s];
+    }
+  } else {
+    const int kk = A.k;
+#pragma unroll
+    for (int s = 0; s < KM; ++s)
+      if (s < kk) {
+        in.idx[s] = A.bidx[p * kk + s];
+        in.a[s] = A.bw[p * kk + s];
+        in.pos[s] = __ldg(A.cpos + p * kk + s);
+        in.sqa[s] = __ldg(A.bws + p * kk + s);  // sqrt(alpha), correctly rounded: the reference's
+      }
+    in.px = A.tp[3 * p];
+    in.py = A.tp[3 * p + 1];
+    in.pz = A.tp[3 * p + 2];
+    in.tn0 = A.tn[3 * p];
+    in.tn1 = A.tn[3 * p + 1];
+    in.tn2 = A.tn[3 * p + 2];
+  }
 }
 
 template <int KM>
@@ -163,12 +189,11 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
     if (uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height) {
       const int ui = (int)uf, vi = (int)vf;
       const int64_t pix = (int64_t)vi * A.width + ui;
-      // the pixel's validity, depth and normal in one round trip
-      const uint8_t dv = A.dvalid[pix];
-      const double d = A.depth[pix];
-      const double h0 = A.onrm[3 * pix], h1 = A.onrm[3 * pix + 1], h2 = A.onrm[3 * pix + 2];
+      // the pixel's depth (NaN = invalid) and normal: one 256-bit load
+      double d, h0, h1, h2;
+      ld256_nc(A.pixrec + 4 * pix, d, h0, h1, h2);
       PSTAMP(3);
-      if (dv) {
+      if (d == d) {
         o0 = ((double)ui - A.cx) / A.fx * d;
         o1 = ((double)vi - A.cy) / A.fy * d;
         o2 = d;
@@ -183,25 +208,20 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
       }
     }
   }
-  nb.valid[p] = ok ? 1 : 0;
   *valid_out = ok ? 1 : 0;
   if (!ok) {
     const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    st256(nb.rec + 8 * p + 4, 0.0, 0.0, 0.0, 0.0);  // valid = 0 (the rest is never read)
 #pragma unroll
     for (int s = 0; s < KM; ++s)
       if (s < kk) store_row(nb.row + 8 * (size_t)pos[s], z);
     return 0.0;
   }
-  nb.obs[3 * p] = o0;
-  nb.obs[3 * p + 1] = o1;
-  nb.obs[3 * p + 2] = o2;
-  nb.nrm[3 * p] = g0;
-  nb.nrm[3 * p + 1] = g1;
-  nb.nrm[3 * p + 2] = g2;
   const double r = g0 * (x0 - o0) + g1 * (x1 - o1) + g2 * (x2 - o2);
   const double rs = tukey_fast(r, A.inv_tukey);
   PSTAMP(4);
-  nb.rs[p] = rs;
+  st256(nb.rec + 8 * p, o0, o1, o2, rs);
+  st256(nb.rec + 8 * p + 4, g0, g1, g2, 1.0);
   double G[24];
   blend_gradient_fast(B, px, py, pz, x0, x1, x2, s2, G);
   double gn[8];
@@ -939,7 +959,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   {
     const PBuf cb = pbuf(A, pb);
     int my_valid = 0;
-    for (int64_t p = gt; p < n; p += GT) my_valid += ldu8(cb.valid + p) ? 1 : 0;
+    for (int64_t p = gt; p < n; p += GT) my_valid += ld(cb.rec + 8 * p + 7) != 0.0 ? 1 : 0;
     for (int o = 16; o > 0; o >>= 1) my_valid += __shfl_xor_sync(0xffffffffu, my_valid, o);
     if (lane == 0) s_cnt[warp] = my_valid;
     __syncthreads();

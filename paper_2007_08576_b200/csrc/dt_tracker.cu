@@ -33,14 +33,6 @@ namespace dt {
 
 __global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
 
-__global__ void k_valid_mask(const double* __restrict__ depth, int64_t npix, double zmin,
-                             double zmax, uint8_t* __restrict__ valid) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= npix) return;
-  const double z = depth[i];
-  valid[i] = (isfinite(z) && z > zmin && z < zmax) ? 1 : 0;
-}
-
 // Block-wide exclusive scan of 0/1 flags for a 1024-thread CTA. Returns this thread's
 // offset; *total receives the block count.
 __device__ __forceinline__ int block_scan_flag(bool flag, int* s_warp, int* total) {
@@ -364,8 +356,7 @@ struct dt_tracker {
   int32_t *bidx = nullptr, *edges = nullptr;
   int *cptr = nullptr, *cent = nullptr, *iptr = nullptr, *ient = nullptr;
   // frame
-  double *depth = nullptr, *onrm = nullptr;
-  uint8_t* dvalid = nullptr;
+  double *depth = nullptr, *onrm = nullptr;  // onrm: caller-supplied normals only
   // features (ORB path)
   int64_t n_feat = 0;
   uint8_t* tdesc = nullptr;
@@ -454,8 +445,10 @@ struct dt_tracker {
   double *warp_a = nullptr, *warp_b = nullptr, *warps_out = nullptr, *lam = nullptr, *wa = nullptr;
   double *partial = nullptr, *csum = nullptr, *delta = nullptr, *oknorm = nullptr, *tentT = nullptr;
   double *erow = nullptr, *evals = nullptr;
-  uint8_t* cvalid = nullptr;
-  double *cobs = nullptr, *cnrm = nullptr, *pr_rs = nullptr, *prow = nullptr, *mrow = nullptr;
+  double *crec = nullptr, *prow = nullptr, *mrow = nullptr;
+  double* pst = nullptr;     // k = 4: packed per-point statics (n x 16)
+  int* pi8 = nullptr;        // k = 4: bind index + CSR position (n x 8)
+  double* pixrec = nullptr;  // per pixel {depth or NaN, normal xyz}
   int* counts = nullptr;
   dt_report* report = nullptr;
   double *cost_hist = nullptr, *lam_hist = nullptr, *wa_out = nullptr;
@@ -595,7 +588,7 @@ void fill_args(dt_tracker* t) {
   a.cptr = t->cptr; a.cent = t->cent; a.cpos = t->cpos;
   a.cpts = t->cpts; a.edges = t->edges; a.ew = t->ew; a.iptr = t->iptr; a.ient = t->ient;
   a.ipos = t->ipos; a.iinfo = t->iinfo; a.iew = t->iew;
-  a.depth = t->depth; a.dvalid = t->dvalid; a.onrm = t->onrm;
+  a.pst = t->pst; a.pi8 = t->pi8; a.pixrec = t->pixrec;
   a.n_active = t->info + 3;
   if (t->orb_static) {
     a.fp = t->tfeat_pts; a.fo = t->ffo; a.fwt = t->ffw; a.fbidx = t->tfeat_bidx; a.fbw = t->tfeat_bw;
@@ -612,8 +605,7 @@ void fill_args(dt_tracker* t) {
   a.nch_m = (int)((t->match_cap + CHUNK - 1) / CHUNK);
   a.nch_e = (int)((t->ne + CHUNK - 1) / CHUNK);
   a.delta = t->delta; a.oknorm = t->oknorm; a.tentT = t->tentT;
-  a.cvalid = t->cvalid; a.cobs = t->cobs; a.cnrm = t->cnrm;
-  a.pr_rs = t->pr_rs; a.prow = t->prow; a.mrow = t->mrow;
+  a.crec = t->crec; a.prow = t->prow; a.mrow = t->mrow;
   a.ma_cap = (int)t->match_cap;
   a.counts = t->counts;
   a.report = t->report;
@@ -633,16 +625,15 @@ void fill_args(dt_tracker* t) {
   a.red_g = t->red_g;
 }
 
-// the solver's arguments for each input set (they differ only in the depth they read)
+// the solver's arguments (one block per input set: the solver reads the frame through the
+// pixel records every input set writes into the same buffer, so the blocks are equal)
 int push_args(dt_tracker* t) {
   fill_args(t);
   t->args_dirty = false;
   DT_CHECK_CUDA(cudaMemcpyAsync(t->dev_args, &t->host_args, sizeof(SolverArgs),
                                 cudaMemcpyHostToDevice, t->stream));
   if (t->dev_args_slot) {
-    SolverArgs v[2] = {t->host_args, t->host_args};
-    v[0].depth = t->in_depth[0];
-    v[1].depth = t->in_depth[1];
+    const SolverArgs v[2] = {t->host_args, t->host_args};
     DT_CHECK_CUDA(cudaMemcpyAsync(t->dev_args_slot, v, sizeof(v), cudaMemcpyHostToDevice, t->stream));
   }
   DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));
@@ -783,13 +774,14 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   } else if (in->depth != dep) {
     DT_CHECK_CUDA(cudaMemcpyAsync(dep, in->depth, sizeof(double) * npix, kind, s));
   }
+  // the solver reads the frame as 32-byte pixel records {depth or NaN, normal}
   if (in->normals) {
+    if (!t->onrm) DT_TRY(dalloc(t, &t->onrm, 3 * npix));
     DT_CHECK_CUDA(cudaMemcpyAsync(t->onrm, in->normals, sizeof(double) * 3 * npix, kind, s));
-    k_valid_mask<<<grid_for(npix, 256), 256, 0, s>>>(dep, npix, c.z_min, c.z_max, t->dvalid);
-    DT_CHECK_LAUNCH();
+    DT_TRY(launch_pack_pixels(dep, t->onrm, npix, c.z_min, c.z_max, t->pixrec, s));
   } else {
     DT_TRY(launch_observation_normals(dep, c.height, c.width, c.fx, c.fy, c.cx, c.cy, c.z_min,
-                                      c.z_max, t->onrm, t->dvalid, s));
+                                      c.z_max, nullptr, nullptr, s, t->pixrec));
   }
   ++t->launches;
   mark(t, 1);
@@ -1160,8 +1152,30 @@ static int tracker_init(dt_tracker* t, const dt_config* cfg, const double* t_poi
   DT_TRY(upload(t, t->iew, iew.data(), iew.size()));
   // frame buffers
   DT_TRY(dalloc(t, &t->depth, npix));
-  DT_TRY(dalloc(t, &t->onrm, 3 * npix));
-  DT_TRY(dalloc(t, &t->dvalid, npix));
+  DT_TRY(dalloc(t, &t->pixrec, 4 * npix));
+  if (k == 4) {
+    // the relink's per-point statics packed for 256-bit loads (dt_solver.cuh SolverArgs)
+    std::vector<double> pst(16 * n);
+    std::vector<int> pi8(8 * n);
+    for (int64_t p = 0; p < n; ++p) {
+      for (int s2 = 0; s2 < 4; ++s2) {
+        pst[16 * p + s2] = bind_w[4 * p + s2];
+        pst[16 * p + 4 + s2] = std::sqrt(bind_w[4 * p + s2]);
+        pi8[8 * p + s2] = bidx32[4 * p + s2];
+        pi8[8 * p + 4 + s2] = cpos[4 * p + s2];
+      }
+      for (int c = 0; c < 3; ++c) {
+        pst[16 * p + 8 + c] = t_points[3 * p + c];
+        pst[16 * p + 12 + c] = t_normals[3 * p + c];
+      }
+      pst[16 * p + 11] = pst[16 * p + 15] = 0.0;
+    }
+    DT_TRY(dalloc(t, &t->pst, 16 * n));
+    DT_TRY(dalloc(t, &t->pi8, 8 * n));
+    DT_TRY(upload(t, t->pst, pst.data(), pst.size()));
+    DT_TRY(upload(t, t->pi8, pi8.data(), pi8.size()));
+    DT_CHECK_CUDA(cudaStreamSynchronize(t->stream));  // pst / pi8 are stack-owned
+  }
   DT_TRY(dalloc(t, &t->info, 4));
   DT_TRY(dalloc(t, &t->pstats, 2));
   DT_TRY(dalloc(t, &t->astats, 2));
@@ -1178,10 +1192,7 @@ static int tracker_init(dt_tracker* t, const dt_config* cfg, const double* t_poi
   DT_TRY(dalloc(t, &t->delta, 6 * m));
   DT_TRY(dalloc(t, &t->oknorm, 6 * m));
   DT_TRY(dalloc(t, &t->tentT, 12 * m));
-  DT_TRY(dalloc(t, &t->cvalid, 2 * n));
-  DT_TRY(dalloc(t, &t->cobs, 2 * 3 * n));
-  DT_TRY(dalloc(t, &t->cnrm, 2 * 3 * n));
-  DT_TRY(dalloc(t, &t->pr_rs, 2 * n));
+  DT_TRY(dalloc(t, &t->crec, 2 * 8 * n));
   DT_TRY(dalloc(t, &t->prow, 2 * k * n * 8));
   DT_TRY(dalloc(t, &t->counts, 1024));
   DT_TRY(dalloc(t, &t->erow, 2 * 2 * 24 * (n_edges > 0 ? n_edges : 1)));
