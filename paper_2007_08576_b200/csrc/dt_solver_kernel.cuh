@@ -441,6 +441,27 @@ __device__ __forceinline__ void resolve_control(const SolverArgs& A, int c, doub
   publish_tentative(A, c, W, d, tent);
 }
 
+// Work units of the relinearizing passes (P1, P6): 32-item chunks of points, matches and
+// edges, dealt round-robin over the domain's warps (unit u -> warp u mod GW). When the
+// chunks outnumber the warps by `extra`, the warps that take a second unit would finish
+// last; the order below makes those units edge chunks handed to warps whose first unit
+// was an edge chunk too -- two edge chunks outlast one point chunk less than a point and
+// an edge chunk do. Order: edge chunks [0, extra), point chunks, match chunks, edge chunks
+// [extra, nch_e).
+struct Unit {
+  int kind;  // 0 point chunk, 1 match chunk, 2 edge chunk
+  int ch;    // chunk index within its kind
+};
+
+__device__ __forceinline__ Unit unit_of(int u, int nch_p, int nch_m, int nch_e, int extra) {
+  if (u < extra) return {2, u};
+  u -= extra;
+  if (u < nch_p) return {0, u};
+  u -= nch_p;
+  if (u < nch_m) return {1, u};
+  return {2, extra + (u - nch_m)};
+}
+
 // BIG: control graphs whose state does not fit in shared memory (m > M_MAX_SMEM): the
 // warps and tentative transforms are read in place from global memory (L1-cached after
 // each barrier), the current transforms and the damping live in this CTA's slice of
@@ -494,6 +515,8 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
   const int nch_m = (int)((n_act + CHUNK - 1) / CHUNK);
   const int nch_e = (A.n_edges + CHUNK - 1) / CHUNK;
   const int nch_tot = A.nch_p + A.nch_m + A.nch_e;
+  // second-round units of the relinearizing passes (see unit_of)
+  const int extra = min(nch_e / 2, max(0, nch_p + nch_m + nch_e - GW));
   // chunk-sum set 0: value pass (points, matches, edges) and the rigidity cost of the
   // iterate; set 1: icp / feature cost of each (speculative) relinearization
 
@@ -537,9 +560,11 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
     double* nm = mrows(A, 0);
     double* ne = erows_buf(A, 0);
     double* nv = evals_buf(A, 0);
-    for (int ch = gw; ch < nch_p + nch_m + nch_e; ch += GW) {
+    for (int u = gw; u < nch_p + nch_m + nch_e; u += GW) {
+      const Unit un = unit_of(u, nch_p, nch_m, nch_e, extra);
+      const int ch = un.ch;
       double acc = 0.0;
-      if (ch < nch_p) {
+      if (un.kind == 0) {
         const int64_t p = (int64_t)ch * CHUNK + lane;
         int vd;
         if (p < n) {
@@ -549,13 +574,13 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         }
         acc = warp_sum(acc);
         red_commit<2, 0>(A, 0, ch, nch_p, {0.0, acc});
-      } else if (ch < nch_p + nch_m) {
-        const int64_t j = (int64_t)(ch - nch_p) * CHUNK + lane;
+      } else if (un.kind == 1) {
+        const int64_t j = (int64_t)ch * CHUNK + lane;
         if (j < n_act) acc = match_step<KM>(A, s_w, j, nm);
         acc = warp_sum(acc);
-        red_commit<1, 0>(A, 1, ch - nch_p, nch_m, {acc});
+        red_commit<1, 0>(A, 1, ch, nch_m, {acc});
       } else {
-        const int e = (ch - nch_p - nch_m) * CHUNK + lane;
+        const int e = ch * CHUNK + lane;
         double v[3];
         if (e < A.n_edges) edge_unit_rows(A, s_T, e, ne, nv, v);
       }
@@ -742,8 +767,9 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
       // this warp's first value-pass point: its warp-independent inputs are loaded now,
       // overlapping the decide prologue's round trip
       PointIn<KM> pin0;
-      const int64_t p0 = (int64_t)gw * CHUNK + lane;
-      const bool pre = gw < nch_p && p0 < n;
+      const Unit u0 = unit_of(gw, nch_p, nch_m, nch_e, extra);
+      const int64_t p0 = (int64_t)u0.ch * CHUNK + lane;
+      const bool pre = u0.kind == 0 && gw < nch_p + nch_m + nch_e && p0 < n;
       if (pre) {
         const PBuf ob0 = pbuf(A, pb);
         point_load<KM>(A, p0, &ob0, pin0);
@@ -831,8 +857,10 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
         double* nm = mrows(A, 1 - pb);
         double* ne = erows_buf(A, 1 - pb);
         double* nv = evals_buf(A, 1 - pb);
-        for (int ch = gw; ch < nch_p + nch_m + nch_e; ch += GW) {
-          if (ch < nch_p) {
+        for (int u = gw; u < nch_p + nch_m + nch_e; u += GW) {
+          const Unit un = unit_of(u, nch_p, nch_m, nch_e, extra);
+          const int ch = un.ch;
+          if (un.kind == 0) {
             const int64_t p = (int64_t)ch * CHUNK + lane;
             double co = 0.0, cn = 0.0;
             int vd;
@@ -842,7 +870,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
               dbg = A.arrivals + 2 + (size_t)1024 * A.arr_cap + 20000 + (rank * NWARPS + warp) * 8;
 #endif
             if (p < n) {
-              if (ch == gw && pre) {
+              if (u == gw && pre) {
                 cn = point_step<KM>(A, s_w, p, pin0, true, nb, &co, &vd, dbg);
               } else {
                 PointIn<KM> pin;
@@ -853,14 +881,14 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             co = warp_sum(co);
             cn = warp_sum(cn);
             red_commit<2, 0>(A, 0, ch, nch_p, {co, cn});
-          } else if (ch < nch_p + nch_m) {
-            const int64_t j = (int64_t)(ch - nch_p) * CHUNK + lane;
+          } else if (un.kind == 1) {
+            const int64_t j = (int64_t)ch * CHUNK + lane;
             double cf = 0.0;
             if (j < n_act) cf = match_step<KM>(A, s_w, j, nm);
             cf = warp_sum(cf);
-            red_commit<1, 0>(A, 1, ch - nch_p, nch_m, {cf});
+            red_commit<1, 0>(A, 1, ch, nch_m, {cf});
           } else {
-            const int e = (ch - nch_p - nch_m) * CHUNK + lane;
+            const int e = ch * CHUNK + lane;
             double acc = 0.0;
             if (e < A.n_edges) {
               double v[3];
@@ -868,7 +896,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
               acc = edge_cost_vals(A, s_w, A.wa, e, v[0], v[1], v[2]);
             }
             acc = warp_sum(acc);
-            red_commit<1, 0>(A, 4, ch - nch_p - nch_m, nch_e, {acc});
+            red_commit<1, 0>(A, 4, ch, nch_e, {acc});
           }
         }
       }
