@@ -138,6 +138,22 @@ __device__ __forceinline__ void point_load(const SolverArgs& A, int64_t p, const
   }
 }
 
+// The gates of the projective association and the point's cost terms are written with
+// explicit rounding intrinsics, which the compiler never contracts into FMAs: they decide
+// discrete outcomes, and the value pass's cost at an unchanged iterate must equal the
+// linearization's cost bit for bit (or a zero step would be "accepted") -- whatever the
+// translation unit's -fmad setting (_build.py SOURCE_FLAGS).
+__device__ __forceinline__ double dot3_rn(double a0, double a1, double a2, double b0, double b1,
+                                          double b2) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(a0, b0), __dmul_rn(a1, b1)), __dmul_rn(a2, b2));
+}
+
+// n . (x - o) and the cost (sw r)^2 of one slot, identical in both passes
+__device__ __forceinline__ double plane_res(double n0, double n1, double n2, double x0, double x1,
+                                            double x2, double o0, double o1, double o2) {
+  return dot3_rn(n0, n1, n2, __dsub_rn(x0, o0), __dsub_rn(x1, o1), __dsub_rn(x2, o2));
+}
+
 template <int KM>
 __device__ __forceinline__ double point_step(const SolverArgs& A, const double* s_w, int64_t p,
                                              const PointIn<KM>& in, bool value_pass,
@@ -168,12 +184,12 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   if (value_pass) {
     double co = 0.0;
     if (in.ovalid) {
-      const double r = in.on0 * (x0 - in.oo0) + in.on1 * (x1 - in.oo1) + in.on2 * (x2 - in.oo2);
+      const double r = plane_res(in.on0, in.on1, in.on2, x0, x1, x2, in.oo0, in.oo1, in.oo2);
 #pragma unroll
       for (int s = 0; s < KM; ++s)
         if (s < kk) {
-          const double wv = in.ors * sqa[s] * r;
-          co += wv * wv;
+          const double wv = __dmul_rn(__dmul_rn(in.ors, sqa[s]), r);
+          co = __dadd_rn(co, __dmul_rn(wv, wv));
         }
     }
     *cost_old = co;
@@ -184,8 +200,8 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   double o0 = 0, o1 = 0, o2 = 0, g0 = 0, g1 = 0, g2 = 0;
   // projection and gates, in the reference's IEEE order (kernels.py:537-568)
   if (x2 > 0.0) {
-    const double uf = rint(A.fx * x0 / x2 + A.cx);
-    const double vf = rint(A.fy * x1 / x2 + A.cy);
+    const double uf = rint(__dadd_rn(__ddiv_rn(__dmul_rn(A.fx, x0), x2), A.cx));
+    const double vf = rint(__dadd_rn(__ddiv_rn(__dmul_rn(A.fy, x1), x2), A.cy));
     if (uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height) {
       const int ui = (int)uf, vi = (int)vf;
       const int64_t pix = (int64_t)vi * A.width + ui;
@@ -194,16 +210,16 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
       ld256_nc(A.pixrec + 4 * pix, d, h0, h1, h2);
       PSTAMP(3);
       if (d == d) {
-        o0 = ((double)ui - A.cx) / A.fx * d;
-        o1 = ((double)vi - A.cy) / A.fy * d;
+        o0 = __dmul_rn(__ddiv_rn(__dsub_rn((double)ui, A.cx), A.fx), d);
+        o1 = __dmul_rn(__ddiv_rn(__dsub_rn((double)vi, A.cy), A.fy), d);
         o2 = d;
         g0 = h0;
         g1 = h1;
         g2 = h2;
-        if (g0 * g0 + g1 * g1 + g2 * g2 > 0.25) {
-          const double dx = o0 - x0, dy = o1 - x1, dz = d - x2;
-          ok = sqrt(dx * dx + dy * dy + dz * dz) < A.gate &&
-               g0 * r0 + g1 * r1 + g2 * r2 > A.cos_gate;
+        if (dot3_rn(g0, g1, g2, g0, g1, g2) > 0.25) {
+          const double dx = __dsub_rn(o0, x0), dy = __dsub_rn(o1, x1), dz = __dsub_rn(d, x2);
+          ok = __dsqrt_rn(dot3_rn(dx, dy, dz, dx, dy, dz)) < A.gate &&
+               dot3_rn(g0, g1, g2, r0, r1, r2) > A.cos_gate;
         }
       }
     }
@@ -217,7 +233,7 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
       if (s < kk) store_row(nb.row + 8 * (size_t)pos[s], z);
     return 0.0;
   }
-  const double r = g0 * (x0 - o0) + g1 * (x1 - o1) + g2 * (x2 - o2);
+  const double r = plane_res(g0, g1, g2, x0, x1, x2, o0, o1, o2);
   const double rs = tukey_fast(r, A.inv_tukey);
   PSTAMP(4);
   st256(nb.rec + 8 * p, o0, o1, o2, rs);
@@ -233,9 +249,9 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
   for (int s = 0; s < KM; ++s)
     if (s < kk) {
       const int c = in.idx[s];
-      const double sw = rs * sqa[s];
-      const double wv = sw * r;
-      cost += wv * wv;
+      const double sw = __dmul_rn(rs, sqa[s]);
+      const double wv = __dmul_rn(sw, r);
+      cost = __dadd_rn(cost, __dmul_rn(wv, wv));
       const double coef = sw * a[s] * sgn[s];
       Basis K;
       make_basis(s_w + 8 * c, K);
@@ -275,7 +291,7 @@ __device__ __forceinline__ double match_step(const SolverArgs& A, const double* 
       const int c = A.fbidx[j * kk + s];
       const double sw = sqrt(A.fw * w * a[s]);
       const double v0 = sw * res[0], v1 = sw * res[1], v2 = sw * res[2];
-      cost += v0 * v0 + v1 * v1 + v2 * v2;
+      cost = __dadd_rn(cost, dot3_rn(v0, v1, v2, v0, v1, v2));
       const double coef = sw * a[s] * sgn[s];
       Basis K;
       make_basis(s_w + 8 * c, K);
