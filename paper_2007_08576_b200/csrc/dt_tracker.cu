@@ -393,6 +393,10 @@ struct dt_tracker {
   // into one of two device slots on a copy stream while the previous frame computes;
   // outputs are copied back on the copy stream while the next frame computes
   cudaStream_t copy_stream = nullptr;  // host -> device staging
+  // the frame's observation normals run on aux_stream beside the ORB matching chain
+  // (only the solver needs them): fork / join events, captured into the frame graph
+  cudaStream_t aux_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t out_stream = nullptr;   // device -> host outputs (not queued behind staging)
   cudaEvent_t ev_in_ready[2] = {nullptr, nullptr}, ev_in_free[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_out_copied[2] = {nullptr, nullptr};
@@ -774,15 +778,25 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   } else if (in->depth != dep) {
     DT_CHECK_CUDA(cudaMemcpyAsync(dep, in->depth, sizeof(double) * npix, kind, s));
   }
-  // the solver reads the frame as 32-byte pixel records {depth or NaN, normal}
+  // the solver reads the frame as 32-byte pixel records {depth or NaN, normal}; they are
+  // produced on the aux stream beside the matching chain (serially when profiling, so the
+  // per-stage events keep their meaning)
+  const bool fork = !t->profiling;
+  cudaStream_t ns = s;
+  if (fork) {
+    DT_CHECK_CUDA(cudaEventRecord(t->ev_fork, s));
+    DT_CHECK_CUDA(cudaStreamWaitEvent(t->aux_stream, t->ev_fork, 0));
+    ns = t->aux_stream;
+  }
   if (in->normals) {
     if (!t->onrm) DT_TRY(dalloc(t, &t->onrm, 3 * npix));
-    DT_CHECK_CUDA(cudaMemcpyAsync(t->onrm, in->normals, sizeof(double) * 3 * npix, kind, s));
-    DT_TRY(launch_pack_pixels(dep, t->onrm, npix, c.z_min, c.z_max, t->pixrec, s));
+    DT_CHECK_CUDA(cudaMemcpyAsync(t->onrm, in->normals, sizeof(double) * 3 * npix, kind, ns));
+    DT_TRY(launch_pack_pixels(dep, t->onrm, npix, c.z_min, c.z_max, t->pixrec, ns));
   } else {
     DT_TRY(launch_observation_normals(dep, c.height, c.width, c.fx, c.fy, c.cx, c.cy, c.z_min,
-                                      c.z_max, nullptr, nullptr, s, t->pixrec));
+                                      c.z_max, nullptr, nullptr, ns, t->pixrec));
   }
+  if (fork) DT_CHECK_CUDA(cudaEventRecord(t->ev_join, t->aux_stream));
   ++t->launches;
   mark(t, 1);
 
@@ -898,6 +912,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   mark(t, 4);
 
   // ---- solve ----
+  if (fork) DT_CHECK_CUDA(cudaStreamWaitEvent(s, t->ev_join, 0));  // the pixel records
   if (t->args_dirty) DT_TRY(push_args(t));
   if (t->pre_solver_wait) DT_CHECK_CUDA(cudaStreamWaitEvent(s, t->pre_solver_wait, 0));
   DT_TRY(solver_launch(t->in_set ? t->dev_args_slot + (t->in_set - 1) : t->dev_args, 1, t->cluster,
@@ -1075,6 +1090,9 @@ static int tracker_init(dt_tracker* t, const dt_config* cfg, const double* t_poi
     DT_CHECK_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
     t->own_stream = true;
   }
+  DT_CHECK_CUDA(cudaStreamCreateWithFlags(&t->aux_stream, cudaStreamNonBlocking));
+  DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
+  DT_CHECK_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
   const int64_t npix = (int64_t)cfg->width * cfg->height;
   // static data
   std::vector<int32_t> bidx32(n * k), edges32(2 * n_edges);
@@ -1266,6 +1284,12 @@ int dt_tracker_destroy(dt_tracker* t) {
   }
   for (auto& e : t->ev)
     if (e) cudaEventDestroy(e);
+  if (t->aux_stream) {
+    cudaStreamSynchronize(t->aux_stream);
+    cudaStreamDestroy(t->aux_stream);
+  }
+  if (t->ev_fork) cudaEventDestroy(t->ev_fork);
+  if (t->ev_join) cudaEventDestroy(t->ev_join);
   if (t->own_stream) cudaStreamDestroy(t->stream);
   for (auto& b : t->bufs) cudaFree(b.p);
   for (void* p : t->retired) cudaFree(p);
