@@ -169,6 +169,15 @@ int dt_sample_control_points(const double* points, int64_t n, double radius,
  * caller applies the reference's weight expression and prune. */
 int dt_connection_candidates(const double* ctrl, int64_t m, double d2_max, int64_t* edges,
                              double* d2, int64_t capacity, int64_t* e_out, int device);
+/* The whole of build_connections (warpfield.py:112-137) on the device: the pairs i < j of
+ * the m controls (lexicographic) with weight w = exp(-|c_i - c_j|^2 / 2 sigma^2) >= prune,
+ * into edges (e,2) / weights (e). The weights agree with the reference's numpy exp to an
+ * ulp (numpy's exp is not correctly rounded; CUDA's is within 1 ulp), so a pair exactly at
+ * the prune boundary may differ; dt_connection_candidates + the host's own exp is the
+ * bit-identical route. Call with edges = NULL for the count. HOST arrays. */
+int dt_build_connections(const double* ctrl, int64_t m, double sigma, double prune,
+                         int64_t* edges, double* weights, int64_t capacity, int64_t* e_out,
+                         int device);
 
 /* Local-PCA normals of an unordered cloud (correspond.estimate_point_normals,
  * correspond.py:198-220): the k nearest points (itself included; exact, ties at the

@@ -109,6 +109,7 @@ _SIGNATURES: dict[str, list] = {
     "dt_preselect": [P, P, I64, P, I64, C.POINTER(PreselectParams), P, P, P, P, P, P, P],
     "dt_sample_control_points": [P, I64, F64, P, P, C.c_int],
     "dt_connection_candidates": [P, I64, F64, P, P, I64, P, C.c_int],
+    "dt_build_connections": [P, I64, F64, F64, P, P, I64, P, C.c_int],
     "dt_estimate_point_normals": [P, I64, I64, P, C.c_int],
     "dt_orb_create": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P, C.c_int,
                       C.POINTER(P)],

@@ -129,10 +129,14 @@ __global__ void k_mis_round(int64_t n, const int64_t* __restrict__ off, const in
   else atomicAdd(undecided, 1);
 }
 
-// candidate connections of row i: j > i with d2 <= thr
+// connections of row i: j > i with d2 <= thr (candidates: d2out = d2); with two_s2 > 0
+// the weight w = exp(-d2 / two_s2) is formed here too (the reference's operation order)
+// and only w >= prune is kept (d2out = w; build_connections, warpfield.py:112-137, up to
+// the last ulp of exp)
 __global__ void k_conn(const double* __restrict__ c, int64_t m, double thr,
                        const int64_t* __restrict__ off, int32_t* __restrict__ cnt,
-                       int64_t* __restrict__ edges, double* __restrict__ d2out) {
+                       int64_t* __restrict__ edges, double* __restrict__ d2out,
+                       double two_s2 = 0.0, double prune = 0.0) {
   const int64_t i = blockIdx.x;
   if (i >= m) return;
   __shared__ int s_warp[32];
@@ -148,6 +152,10 @@ __global__ void k_conn(const double* __restrict__ c, int64_t m, double thr,
                    dz = c[3 * i + 2] - c[3 * j + 2];
       d2 = (dx * dx + dy * dy) + dz * dz;
       keep = d2 <= thr;
+      if (keep && two_s2 > 0.0) {
+        d2 = exp(-d2 / two_s2);  // the weight
+        keep = d2 >= prune;
+      }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -483,6 +491,54 @@ int dt_connection_candidates(const double* ctrl, int64_t m, double d2_max, int64
   DT_CHECK_LAUNCH();
   DT_CHECK_CUDA(cudaMemcpy(edges, d_e, sizeof(int64_t) * 2 * e, cudaMemcpyDeviceToHost));
   DT_CHECK_CUDA(cudaMemcpy(d2, d_d2, sizeof(double) * e, cudaMemcpyDeviceToHost));
+  return DT_OK;
+}
+
+int dt_build_connections(const double* ctrl, int64_t m, double sigma, double prune,
+                         int64_t* edges, double* weights, int64_t capacity, int64_t* e_out,
+                         int device) {
+  DT_REQUIRE(ctrl != nullptr && e_out != nullptr, DT_ERR_INVALID_ARGUMENT, "NULL argument");
+  DT_REQUIRE(m >= 0 && m < (1ll << 31), DT_ERR_INVALID_ARGUMENT, "bad control count");
+  DT_REQUIRE(sigma > 0.0 && prune > 0.0 && prune <= 1.0, DT_ERR_INVALID_ARGUMENT,
+             "need sigma > 0 and 0 < prune <= 1");
+  *e_out = 0;
+  if (m < 2) return DT_OK;
+  DT_CHECK_CUDA(cudaSetDevice(device));
+  // w >= prune <=> d2 <= -2 sigma^2 ln(prune): a hair above it bounds the candidates, the
+  // weight itself decides
+  const double two_s2 = 2.0 * sigma * sigma;
+  const double thr = -std::log(prune) * two_s2 * (1.0 + 1e-9);
+  Freer fr;
+  double *d_c, *d_w;
+  int64_t *d_off, *d_e;
+  int32_t* d_cnt;
+  DT_TRY(dmalloc(&d_c, 3 * m));
+  fr.ptrs.push_back(d_c);
+  DT_TRY(dmalloc(&d_off, m + 1));
+  fr.ptrs.push_back(d_off);
+  DT_TRY(dmalloc(&d_cnt, m));
+  fr.ptrs.push_back(d_cnt);
+  DT_CHECK_CUDA(cudaMemcpy(d_c, ctrl, sizeof(double) * 3 * m, cudaMemcpyHostToDevice));
+  k_conn<<<(unsigned)m, 256>>>(d_c, m, thr, nullptr, d_cnt, nullptr, nullptr, two_s2, prune);
+  DT_CHECK_LAUNCH();
+  std::vector<int32_t> cnt(m);
+  DT_CHECK_CUDA(cudaMemcpy(cnt.data(), d_cnt, sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> off(m + 1, 0);
+  for (int64_t i = 0; i < m; ++i) off[i + 1] = off[i] + cnt[i];
+  const int64_t e = off[m];
+  *e_out = e;
+  if (edges == nullptr || weights == nullptr) return DT_OK;  // count query
+  DT_REQUIRE(capacity >= e, DT_ERR_INVALID_ARGUMENT, "edge capacity %lld < %lld",
+             (long long)capacity, (long long)e);
+  DT_TRY(dmalloc(&d_e, 2 * e));
+  fr.ptrs.push_back(d_e);
+  DT_TRY(dmalloc(&d_w, e));
+  fr.ptrs.push_back(d_w);
+  DT_CHECK_CUDA(cudaMemcpy(d_off, off.data(), sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice));
+  k_conn<<<(unsigned)m, 256>>>(d_c, m, thr, d_off, nullptr, d_e, d_w, two_s2, prune);
+  DT_CHECK_LAUNCH();
+  DT_CHECK_CUDA(cudaMemcpy(edges, d_e, sizeof(int64_t) * 2 * e, cudaMemcpyDeviceToHost));
+  DT_CHECK_CUDA(cudaMemcpy(weights, d_w, sizeof(double) * e, cudaMemcpyDeviceToHost));
   return DT_OK;
 }
 

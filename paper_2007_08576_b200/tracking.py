@@ -43,11 +43,15 @@ class FrameResult:
 
 
 def prepare_template(template: Template, config: RunConfig) -> tuple[Template, ControlGraph]:
-    """Sample the control graph and bind the template to it (tracking.py:35-45)."""
+    """Sample the control graph and bind the template to it (tracking.py:35-45), on the
+    device; config.device.template_build picks the bit-identical route ("exact": the
+    weights with numpy's exp, the binding with the kd-tree) or the all-device one."""
+    on_dev = config.device.template_build == "device"
     graph = sample_control_points(template, config.sampling.radius,
-                                  connection_sigma=config.sampling.effective_connection_sigma)
+                                  connection_sigma=config.sampling.effective_connection_sigma,
+                                  exact_weights=not on_dev)
     bound = bind_template(template, graph, k=config.sampling.bind_k,
-                          sigma=config.sampling.effective_bind_sigma)
+                          sigma=config.sampling.effective_bind_sigma, device=on_dev)
     return bound, graph
 
 

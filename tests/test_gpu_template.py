@@ -78,3 +78,94 @@ def test_point_normals_template_scale():
     dev = estimate_point_normals(tpl.points)
     ref, tie = OP.point_normals(tpl.points)
     np.testing.assert_allclose(dev[~tie], ref[~tie], rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("surface,res,radius,sigma", [
+    ("height-field", 30, 8.0, 16.0),
+    ("plane", 71, 10.0, 20.0),
+    ("sphere-patch", 141, 5.2, 10.4),
+])
+def test_device_connections_match_reference_to_an_ulp(surface, res, radius, sigma):
+    """build_connections entirely on the device (dt_build_connections): the same edge set
+    in the same lexicographic order, weights within 2 ulp of the reference's numpy exp
+    (which is not correctly rounded; CUDA's exp is within 1 ulp of the exact value)."""
+    from oracle import pipeline as OP
+    from paper_2007_08576_b200 import synth
+    from paper_2007_08576_b200.warpfield import build_connections
+
+    tpl = synth.make_template(synth.Scene(surface=surface, resolution=res, n_features=10))
+    ctrl = OP.sample_controls(tpl.points, radius)
+    e, w = build_connections(ctrl, sigma, exact=False)
+    e2, w2 = OP.connections(ctrl, sigma)
+    np.testing.assert_array_equal(e, e2)
+    np.testing.assert_allclose(w, w2, rtol=4.5e-16, atol=0)
+
+
+def _binding_oracle(pts, ctrl, k, sigma):
+    """(d^2, index)-ordered brute-force k-nearest binding with the reference's weights."""
+    d2 = ((pts[:, None, :] - ctrl[None, :, :]) ** 2).sum(-1)
+    order = np.lexsort((np.broadcast_to(np.arange(len(ctrl)), d2.shape), d2), axis=1)[:, :k]
+    dd = np.take_along_axis(d2, order, 1)
+    w = np.exp(-dd / (2.0 * sigma * sigma))
+    return order, w / w.sum(1, keepdims=True), dd
+
+
+def test_device_binding_equals_kdtree_on_tie_free_clouds_and_documents_grid_ties():
+    """Template binding on the device: on an unstructured cloud (no distance ties) the same
+    indices as scipy's kd-tree (the reference's), weights within an ulp; on a grid, where
+    the kd-tree's order between equidistant controls is its traversal's, the device picks
+    the same neighbour distances with ties to the lower control index."""
+    from paper_2007_08576_b200.warpfield import bind_points, bind_points_device
+
+    rng = np.random.default_rng(3)
+    pts = rng.uniform(-30, 30, size=(4000, 3)) * np.array([1.0, 1.0, 0.1])
+    ctrl = pts[rng.choice(4000, 150, replace=False)] + rng.normal(0, 1e-3, (150, 3))
+    i_dev, w_dev = bind_points_device(pts, ctrl, 4, 7.0)
+    i_kd, w_kd = bind_points(pts, ctrl, 4, 7.0)
+    np.testing.assert_array_equal(i_dev, i_kd)
+    np.testing.assert_allclose(w_dev, w_kd, rtol=1e-15, atol=1e-17)
+    # grid: equal neighbour distances, (d^2, index) order
+    g = np.stack(np.meshgrid(np.arange(20.0), np.arange(20.0), [300.0], indexing="ij"), -1).reshape(-1, 3)
+    gctrl = g[::7].copy()
+    i_dev, w_dev = bind_points_device(g, gctrl, 4, 3.0)
+    order, w_ref, dd = _binding_oracle(g, gctrl, 4, 3.0)
+    np.testing.assert_array_equal(i_dev, order)
+    np.testing.assert_allclose(w_dev, w_ref, rtol=1e-15, atol=1e-17)
+    i_kd, _ = bind_points(g, gctrl, 4, 3.0)
+    d_kd = np.take_along_axis(((g[:, None] - gctrl[None]) ** 2).sum(-1), i_kd, 1)
+    np.testing.assert_array_equal(d_kd, dd)  # the same distances, ties ordered differently
+
+
+def test_all_device_template_tracks_like_the_exact_build():
+    """prepare_template with device.template_build = "device" on a tie-free template: the
+    same graph as the exact build up to ulps of the weights, and a tracked frame within the
+    north-star bar of the exact build's."""
+    import paper_2007_08576_b200 as dt
+    from paper_2007_08576_b200 import synth
+
+    spec = synth.CONFIGS[1]
+    scene = spec["scene"]
+    base = {"sampling": {"radius": spec["radius"]},
+            "solver": {"max_outer_iters": spec["iters"], "step_tol": 0.0, "cost_tol": 0.0}}
+    tpl0 = synth.make_template(scene)
+    rng = np.random.default_rng(5)  # break the grid's exact ties
+    tpl0 = dt.Template(tpl0.points + rng.normal(0, 1e-6, tpl0.points.shape), tpl0.normals)
+    cam = synth.camera_for(scene)
+    feats = synth.make_features(scene, tpl0)
+    fr = synth.make_frame(scene, cam, tpl0, feats, 2)
+    out = {}
+    for mode in ("exact", "device"):
+        cfg = dt.load_config({**base, "device": {"template_build": mode}})
+        tpl, graph = dt.prepare_template(tpl0, cfg)
+        trk = dt.Tracker(tpl, graph, cam, cfg)
+        trk.set_features(feats.descriptors, feats.points)
+        res = trk.track(fr.depth, descriptors=fr.descriptors, keypoints=fr.keypoints)
+        trk.close()
+        out[mode] = (tpl, graph, res)
+    (t0, g0, r0), (t1, g1, r1) = out["exact"], out["device"]
+    np.testing.assert_array_equal(g0.points, g1.points)
+    np.testing.assert_array_equal(g0.edges, g1.edges)
+    np.testing.assert_allclose(g0.edge_weights, g1.edge_weights, rtol=4.5e-16)
+    np.testing.assert_array_equal(t0.bind_indices, t1.bind_indices)
+    np.testing.assert_allclose(t0.bind_weights, t1.bind_weights, rtol=1e-15, atol=1e-17)
+    assert float(np.abs(r0.points - r1.points).max()) < 1e-4
