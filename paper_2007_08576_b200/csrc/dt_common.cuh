@@ -34,6 +34,26 @@ void set_error(const char* fmt, ...);
     }                                \
   } while (0)
 
+// Device-side bounds checks of the checked build (-DDT_CHECKED, tools/checked_run.sh):
+// every gather / scatter through an index that comes from another array (binding, CSR
+// positions, edges, projected pixels, reduction slots) asserts its range and traps on a
+// violation. compute-sanitizer is not available on this GPU pool, so this build plus the
+// parity suite is the out-of-bounds evidence. Compiled out otherwise.
+#ifdef DT_CHECKED
+#define DT_DCHECK(cond)                                                                      \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("DT_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                            \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define DT_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline int grid_for(int64_t n, int block) {

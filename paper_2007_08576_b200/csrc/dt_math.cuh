@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <math.h>
 
+#include "dt_common.cuh"
+
 namespace dt {
 
 constexpr int KMAX = 8;                       // largest bind_k the device path handles
@@ -55,6 +57,7 @@ __device__ __forceinline__ void blend_at_k(const double* __restrict__ warps, con
   for (int e = 0; e < 8; ++e) B[e] = 0.0;
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
+    DT_DCHECK(s >= k || idx[s] >= 0);
     if (s < k) {
       const double* W = warps + 8 * (int64_t)idx[s];
       const double dot = W[0] * rw + W[1] * rx + W[2] * ry + W[3] * rz;

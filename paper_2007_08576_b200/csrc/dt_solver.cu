@@ -280,6 +280,8 @@ __device__ __forceinline__ void store_row8(double* dst, const double* J6, double
 __device__ __forceinline__ void edge_unit_rows(const SolverArgs& A, const double* s_T, int e,
                                                double* erow, double* evals, double v[3]) {
   const int i0 = A.edges[2 * e], i1 = A.edges[2 * e + 1];
+  DT_DCHECK(e >= 0 && e < A.n_edges && i0 >= 0 && i0 < A.m && i1 >= 0 && i1 < A.m);
+  DT_DCHECK(__ldg(A.ipos + 2 * e) < 2 * A.n_edges && __ldg(A.ipos + 2 * e + 1) < 2 * A.n_edges);
   const double* p0 = A.cpts + 3 * i0;
   const double* p1 = A.cpts + 3 * i1;
   const double* T0 = s_T + 12 * i0;

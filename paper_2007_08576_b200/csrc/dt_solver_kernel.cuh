@@ -118,6 +118,7 @@ __device__ __forceinline__ void point_load(const SolverArgs& A, int64_t p, const
     for (int s = 0; s < 4; ++s) {
       in.idx[s] = ip[s];
       in.pos[s] = ip[4 + s];
+      DT_DCHECK(ip[s] >= 0 && ip[s] < A.m && ip[4 + s] >= 0 && ip[4 + s] < A.n * 4);
     }
   } else {
     const int kk = A.k;
@@ -205,6 +206,7 @@ __device__ __forceinline__ double point_step(const SolverArgs& A, const double* 
     if (uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height) {
       const int ui = (int)uf, vi = (int)vf;
       const int64_t pix = (int64_t)vi * A.width + ui;
+      DT_DCHECK(pix >= 0 && pix < (int64_t)A.width * A.height);
       // the pixel's depth (NaN = invalid) and normal: one 256-bit load
       double d, h0, h1, h2;
       ld256_nc(A.pixrec + 4 * pix, d, h0, h1, h2);
@@ -289,6 +291,8 @@ __device__ __forceinline__ double match_step(const SolverArgs& A, const double* 
   for (int s = 0; s < KM; ++s)
     if (s < kk) {
       const int c = A.fbidx[j * kk + s];
+      DT_DCHECK(c >= 0 && c < A.m && __ldg(A.mpos + j * kk + s) >= 0 &&
+                __ldg(A.mpos + j * kk + s) < A.ma_cap * kk);
       const double sw = sqrt(A.fw * w * a[s]);
       const double v0 = sw * res[0], v1 = sw * res[1], v2 = sw * res[2];
       cost = __dadd_rn(cost, dot3_rn(v0, v1, v2, v0, v1, v2));
@@ -379,6 +383,7 @@ __device__ __noinline__ void red_commit(const SolverArgs& A, int slot, int ch, i
   double* vals[2] = {red_vals(A, slot, 0), red_vals(A, slot, 1)};
   const int lane = threadIdx.x & 31;
   const int g = ch >> 5;
+  DT_DCHECK(ch >= 0 && ch < nch && g < R.G);
   unsigned old = 0;
   if (lane == 0) {
 #pragma unroll
@@ -632,6 +637,8 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             m0 = ldi(A.mptr + c);
             m1 = ldi(A.mptr + c + 1);
           }
+          DT_DCHECK(0 <= q0 && q0 <= q1 && q1 <= A.n * A.k && 0 <= m0 && m0 <= m1 &&
+                    m1 <= A.ma_cap * A.k);
           const int np_rows = q1 - q0, total = np_rows + 3 * (m1 - m0);
           const double* pbase = prow + 8 * (size_t)q0;
           const double* mbase = mrow + 24 * (size_t)m0;
@@ -692,6 +699,7 @@ __global__ void __launch_bounds__(SOLVER_THREADS, 1) k_solve_frame(const SolverA
             if (live) {
               const int info = __ldg(A.iinfo + q);
               const int o = info >> 1;
+              DT_DCHECK(q < 2 * A.n_edges && o >= 0 && o < m);
               side = info & 1;
               const double* er = erow + (size_t)EROW * q;
               load_row(er, u0);
