@@ -396,6 +396,24 @@ int dt_track_frames_batched(dt_tracker** trackers, const dt_frame_input* inputs,
                             dt_frame_output* outputs, int32_t n_trackers, void* stream);
 
 /* ---------------------------------------------------------------------------------
+ * Stereo depth (PAPER.md:25 -- upstream of the observation, not in the
+ * reference, algorithm defined by oracle/stereo.py): a rectified grey pair (uint8 (h,w),
+ * left pixel x <-> right pixel x - d) -> depth (h,w) f64 = fx B / disparity, NaN where
+ * no match survives. ZNCC over a (2r+1)^2 window (r in [1,5]) for d in [0, max_disp),
+ * winner-take-all both ways, left-right check within lr_tol, minimum correlation
+ * min_ncc, parabolic sub-pixel. dt_stereo_compute takes HOST or DEVICE images (on_device)
+ * and copies depth / disparity (f64) / winner (int32, -1 = none) to HOST buffers (any may
+ * be NULL); dt_stereo_last hands out the device depth for dt_track_frame (on_device = 1).
+ * ------------------------------------------------------------------------------- */
+typedef struct dt_stereo dt_stereo;
+int dt_stereo_create(int height, int width, int max_disp, int radius, double fx, double baseline,
+                     double min_ncc, int lr_tol, int device, dt_stereo** out);
+int dt_stereo_destroy(dt_stereo* s);
+int dt_stereo_compute(dt_stereo* s, const uint8_t* left, const uint8_t* right, int on_device,
+                      double* depth, double* disparity, int32_t* winner);
+int dt_stereo_last(dt_stereo* s, const double** depth);
+
+/* ---------------------------------------------------------------------------------
  * File-format codecs (fileio.py:23-259). HOST memory, no device.
  * dt_format_reals: `rows` lines of `cols` space-separated reals, each printed exactly as
  *   Python's repr() prints it (shortest round-trip digits; fixed notation for decimal

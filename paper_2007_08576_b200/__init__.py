@@ -17,6 +17,7 @@ from .estimators import MatchInlierSelector, SurfaceDeformationTracker
 from .geometry import PinholeCamera
 from .matching import MatchSet, PreselectConfig, match_descriptors, preselect_inliers
 from .orb import OrbDetector
+from .stereo import StereoMatcher
 from .solver import SolverConfig, solve_frame
 from .tracking import (FrameResult, Tracker, annotate_matches, prepare_template, track_frame,
                        track_sequence)
@@ -24,7 +25,7 @@ from .warpfield import ControlGraph, Template, bind_template, sample_control_poi
 
 __all__ = [
     "RunConfig", "load_config", "CorrespondenceSet", "Observation", "estimate_point_normals",
-    "OrbDetector", "EnergyReport",
+    "OrbDetector", "StereoMatcher", "EnergyReport",
     "EnergyWeights", "MatchInlierSelector", "SurfaceDeformationTracker", "PinholeCamera",
     "MatchSet", "PreselectConfig", "match_descriptors", "preselect_inliers", "SolverConfig",
     "solve_frame", "FrameResult", "Tracker", "annotate_matches", "prepare_template",

@@ -26,7 +26,7 @@ ORACLE_SRC = ROOT / "oracle" / "csrc"
 ORACLE_LIB = ROOT / "oracle" / "_build" / "liboracle.so"
 
 CUDA_SOURCES = ["dt_ops.cu", "dt_match.cu", "dt_solver.cu", "dt_tracker.cu", "dt_template.cu",
-                "dt_orb.cu", "dt_io.cpp"]
+                "dt_orb.cu", "dt_stereo.cu", "dt_io.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-fmad=false", "-std=c++17",

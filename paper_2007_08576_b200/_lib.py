@@ -139,6 +139,11 @@ _SIGNATURES: dict[str, list] = {
     "dt_tracker_get_trace": [P, P, C.c_int],
     "dt_tracker_get_arrivals": [P, P, C.c_int],
     "dt_depth_from_pfm": [P, I64, I64, C.c_int, P, P],
+    "dt_stereo_create": [C.c_int, C.c_int, C.c_int, C.c_int, F64, F64, F64, C.c_int, C.c_int,
+                         C.POINTER(P)],
+    "dt_stereo_destroy": [P],
+    "dt_stereo_compute": [P, P, P, C.c_int, P, P, P],
+    "dt_stereo_last": [P, C.POINTER(P)],
 }
 
 # int64-returning codecs (host memory; no device needed)
