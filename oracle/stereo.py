@@ -130,5 +130,5 @@ def synthetic_pair(h: int, w: int, fx: float, baseline: float, depth_fn, seed: i
     t = xs - x0
     x0 = np.clip(x0, 0, tex.shape[1] - 2)
     right = (1 - t) * tex[yy.astype(int), x0] + t * tex[yy.astype(int), x0 + 1]
-    return (np.clip(np.rint(left), 0, 255).astype(np.uint8),
-            np.clip(np.rint(right), 0, 255).astype(np.uint8), z, disp)
+    return (np.ascontiguousarray(np.clip(np.rint(left), 0, 255).astype(np.uint8)),
+            np.ascontiguousarray(np.clip(np.rint(right), 0, 255).astype(np.uint8)), z, disp)

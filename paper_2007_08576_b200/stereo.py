@@ -35,11 +35,22 @@ class StereoMatcher:
                                    C.byref(self._h)), "dt_stereo_create")
 
     def compute(self, left, right, on_device: bool = False):
+        """left / right: (h, w) uint8 host arrays, or (on_device) CUDA tensors -- the
+        matcher runs on its own stream, so the producer's stream is synchronized first."""
         h, w = self.height, self.width
         keep = []
+        if on_device:
+            import torch
+
+            torch.cuda.current_stream().synchronize()
 
         def img(a):
             if on_device:
+                import torch
+
+                if a.dtype != torch.uint8 or tuple(a.shape) != (h, w) or not a.is_cuda:
+                    raise ValueError(f"device image must be a ({h}, {w}) uint8 CUDA tensor")
+                a = a.contiguous()
                 keep.append(a)
                 return a.data_ptr()
             arr = np.ascontiguousarray(a, dtype=np.uint8)

@@ -100,3 +100,19 @@ def test_stereo_depth_feeds_the_tracker_on_device():
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
     np.testing.assert_array_equal(outs[0][1], outs[1][1])
     assert outs[0][2] == outs[1][2] > 0
+
+
+def test_device_resident_images_give_the_host_result():
+    import torch
+
+    from oracle import stereo as OS
+    from paper_2007_08576_b200.stereo import StereoMatcher
+
+    h, w = 120, 160
+    L, R, _, _ = OS.synthetic_pair(h, w, 300.0, 20.0, _surface, seed=9)
+    sm = StereoMatcher(h, w, 300.0, 20.0, max_disp=40, radius=3)
+    a = sm.compute(L, R)
+    b = sm.compute(torch.from_numpy(L).cuda(), torch.from_numpy(R).cuda(), on_device=True)
+    sm.close()
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
