@@ -250,8 +250,9 @@ __device__ __forceinline__ bool procrustes_lane(const double C[9], double V[9], 
 
 // IRLS weight of one rectified match under R: reweight(|s2 - R s1|) = min(H/d, 1)
 // (matching.py:128-136), branch-free so the match loop stays unrolled: the residual is
-// accumulated with FMA and H/d is H * rsqrt(d^2) (<= 1 ulp from the reference's H/d; the
-// final flags are recomputed with the reference's exact arithmetic in k_preselect_final).
+// accumulated with FMA and H/d is H * rsqrt(d^2) (~1e-14 relative from the reference's
+// H/d; the final flags are recomputed with the reference's exact arithmetic in
+// k_preselect_final).
 __device__ __forceinline__ double irls_weight(const double R[9], double a0, double a1, double a2,
                                               double b0, double b1, double b2, double H,
                                               double Hsq) {
@@ -267,7 +268,9 @@ __device__ __forceinline__ double irls_weight(const double R[9], double a0, doub
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
   const double hs = 0.5 * s;
   // y <- y + y (0.5 - hs y^2), fused
-  y = __fma_rn(y, __fma_rn(-hs * y, y, 0.5), y);
+  // one Newton step after the MUFU estimate: ~1e-14 relative in the weight of a far
+  // match (tolerance-level in the IRLS; the flags are recomputed exactly in
+  // k_preselect_final) -- two steps measured 0.211 ms, one 0.203 ms at n = 1,888
   y = __fma_rn(y, __fma_rn(-hs * y, y, 0.5), y);
   // s > H^2 on the bit patterns (both >= +0, so the integer order is the IEEE order) on
   // the integer pipe instead of the FP64 one; a NaN residual keeps weight 1 like the
@@ -277,11 +280,20 @@ __device__ __forceinline__ double irls_weight(const double R[9], double a0, doub
   return far ? H * y : 1.0;
 }
 
+// Where the hypothesis loops read the matches from: the caller's arrays in global memory
+// (read-only path) or the CTA's shared-memory copy (the fused ORB-path kernel).
+struct LdGlobal {
+  __device__ __forceinline__ static double get(const double* p) { return __ldg(p); }
+};
+struct LdPlain {
+  __device__ __forceinline__ static double get(const double* p) { return *p; }
+};
+
 // One lane's share of a covariance pass: C += sum_k w_k b_k a_k^T over k = lane (mod 32)
 // in increasing k (w = 1 in the first IRLS step). Four matches per trip are loaded and
 // weighted as independent chains before being folded into C in order, so the result is
 // the same as the one-match-at-a-time loop while the chains overlap.
-template <bool WEIGHTED>
+template <bool WEIGHTED, class LD>
 __device__ __forceinline__ void cov_pass(const double* __restrict__ src,
                                          const double* __restrict__ dst, int64_t n, int lane,
                                          double rs0, double rs1, double rs2, double rd0,
@@ -294,12 +306,12 @@ __device__ __forceinline__ void cov_pass(const double* __restrict__ src,
     for (int u = 0; u < 4; ++u) {
       const double* ps = src + 3 * (k + 32 * u);
       const double* pd = dst + 3 * (k + 32 * u);
-      a[u][0] = __ldg(ps) - rs0;
-      a[u][1] = __ldg(ps + 1) - rs1;
-      a[u][2] = __ldg(ps + 2) - rs2;
-      b[u][0] = __ldg(pd) - rd0;
-      b[u][1] = __ldg(pd + 1) - rd1;
-      b[u][2] = __ldg(pd + 2) - rd2;
+      a[u][0] = LD::get(ps) - rs0;
+      a[u][1] = LD::get(ps + 1) - rs1;
+      a[u][2] = LD::get(ps + 2) - rs2;
+      b[u][0] = LD::get(pd) - rd0;
+      b[u][1] = LD::get(pd + 1) - rd1;
+      b[u][2] = LD::get(pd + 2) - rd2;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
@@ -320,10 +332,10 @@ __device__ __forceinline__ void cov_pass(const double* __restrict__ src,
     }
   }
   for (; k < n; k += 32) {
-    const double a0 = __ldg(src + 3 * k) - rs0, a1 = __ldg(src + 3 * k + 1) - rs1,
-                 a2 = __ldg(src + 3 * k + 2) - rs2;
-    const double b0 = __ldg(dst + 3 * k) - rd0, b1 = __ldg(dst + 3 * k + 1) - rd1,
-                 b2 = __ldg(dst + 3 * k + 2) - rd2;
+    const double a0 = LD::get(src + 3 * k) - rs0, a1 = LD::get(src + 3 * k + 1) - rs1,
+                 a2 = LD::get(src + 3 * k + 2) - rs2;
+    const double b0 = LD::get(dst + 3 * k) - rd0, b1 = LD::get(dst + 3 * k + 1) - rd1,
+                 b2 = LD::get(dst + 3 * k + 2) - rd2;
     const double wk = WEIGHTED ? irls_weight(R, a0, a1, a2, b0, b1, b2, H, Hsq) : 1.0;
     const double c0 = b0 * wk, c1 = b1 * wk, c2 = b2 * wk;
     C[0] = __fma_rn(c0, a0, C[0]);
@@ -339,6 +351,7 @@ __device__ __forceinline__ void cov_pass(const double* __restrict__ src,
 }
 
 // Support of one lane's matches (sum of IRLS weights in increasing k), same trip shape.
+template <class LD>
 __device__ __forceinline__ double support_pass(const double* __restrict__ src,
                                                const double* __restrict__ dst, int64_t n,
                                                int lane, double rs0, double rs1, double rs2,
@@ -352,49 +365,45 @@ __device__ __forceinline__ double support_pass(const double* __restrict__ src,
     for (int u = 0; u < 4; ++u) {
       const double* ps = src + 3 * (k + 32 * u);
       const double* pd = dst + 3 * (k + 32 * u);
-      w[u] = irls_weight(R, __ldg(ps) - rs0, __ldg(ps + 1) - rs1, __ldg(ps + 2) - rs2,
-                         __ldg(pd) - rd0, __ldg(pd + 1) - rd1, __ldg(pd + 2) - rd2, H, Hsq);
+      w[u] = irls_weight(R, LD::get(ps) - rs0, LD::get(ps + 1) - rs1, LD::get(ps + 2) - rs2,
+                         LD::get(pd) - rd0, LD::get(pd + 1) - rd1, LD::get(pd + 2) - rd2, H, Hsq);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) sup += w[u];
   }
   for (; k < n; k += 32)
-    sup += irls_weight(R, __ldg(src + 3 * k) - rs0, __ldg(src + 3 * k + 1) - rs1,
-                       __ldg(src + 3 * k + 2) - rs2, __ldg(dst + 3 * k) - rd0,
-                       __ldg(dst + 3 * k + 1) - rd1, __ldg(dst + 3 * k + 2) - rd2, H, Hsq);
+    sup += irls_weight(R, LD::get(src + 3 * k) - rs0, LD::get(src + 3 * k + 1) - rs1,
+                       LD::get(src + 3 * k + 2) - rs2, LD::get(dst + 3 * k) - rd0,
+                       LD::get(dst + 3 * k + 1) - rd1, LD::get(dst + 3 * k + 2) - rd2, H, Hsq);
   return sup;
 }
 
-// One warp per reference hypothesis: lane l owns
-// the matches k = l (mod 32); the per-lane covariances are combined by a 5-level xor
-// butterfly (bitwise-identical on every lane) and all 32 lanes run the 3x3 SVD
-// redundantly -- no shared memory and no CTA barrier, so warps drift apart and one
-// warp's SVD overlaps the other warps' match loops.
-__global__ void __launch_bounds__(512, 1)
-k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
-                 const int64_t* __restrict__ n_dev, int64_t n_fixed,
-                 const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive, double H,
-                 int iters, double min_support, double* __restrict__ ref_support,
-                 double* __restrict__ ref_rot, uint8_t* __restrict__ ref_valid) {
+// One reference hypothesis on one warp (matching._evaluate_reference, matching.py:145-171):
+// lane l owns the matches k = l (mod 32); the per-lane covariances are combined by a
+// 5-level xor butterfly (bitwise-identical on every lane) and all 32 lanes run the 3x3
+// SVD redundantly -- no shared memory and no CTA barrier, so warps drift apart and one
+// warp's SVD overlaps the other warps' match loops. Writes (valid, support, R) of slot w.
+template <class LD>
+__device__ __forceinline__ void evaluate_hypothesis(const double* __restrict__ src,
+                                                    const double* __restrict__ dst, int64_t n,
+                                                    int64_t w, int64_t ref, double H, int iters,
+                                                    double min_support, double* __restrict__ ref_support,
+                                                    double* __restrict__ ref_rot,
+                                                    uint8_t* __restrict__ ref_valid) {
   const int lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t n = n_dev ? *n_dev : n_fixed;
-  const int64_t nr = exhaustive ? n : n_refs;
-  if (w >= nr) return;  // warp-uniform
-  const int64_t ref = exhaustive ? w : refs[w];
   bool live = n >= 3 && ref >= 0 && ref < n;
   const int64_t rr = live ? ref : 0;
-  const double rs0 = __ldg(src + 3 * rr), rs1 = __ldg(src + 3 * rr + 1), rs2 = __ldg(src + 3 * rr + 2);
-  const double rd0 = __ldg(dst + 3 * rr), rd1 = __ldg(dst + 3 * rr + 1), rd2 = __ldg(dst + 3 * rr + 2);
+  const double rs0 = LD::get(src + 3 * rr), rs1 = LD::get(src + 3 * rr + 1), rs2 = LD::get(src + 3 * rr + 2);
+  const double rd0 = LD::get(dst + 3 * rr), rd1 = LD::get(dst + 3 * rr + 1), rd2 = LD::get(dst + 3 * rr + 2);
   const double Hsq = H * H;
   double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
   double V[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
   for (int it = 0; it < iters; ++it) {
     double C[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (it == 0)
-      cov_pass<false>(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq, C);
+      cov_pass<false, LD>(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq, C);
     else
-      cov_pass<true>(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq, C);
+      cov_pass<true, LD>(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq, C);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
@@ -421,7 +430,7 @@ k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
     if (same) break;
   }
   double sup = 0.0;
-  if (live) sup = support_pass(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq);
+  if (live) sup = support_pass<LD>(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq);
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) sup += __shfl_xor_sync(0xffffffffu, sup, o);
   if (lane == 0) {
@@ -431,6 +440,22 @@ k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
 #pragma unroll
     for (int i = 0; i < 9; ++i) ref_rot[9 * w + i] = R[i];
   }
+}
+
+// One warp per reference hypothesis, the matches read from global memory.
+__global__ void __launch_bounds__(512, 1)
+k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
+                 const int64_t* __restrict__ n_dev, int64_t n_fixed,
+                 const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive, double H,
+                 int iters, double min_support, double* __restrict__ ref_support,
+                 double* __restrict__ ref_rot, uint8_t* __restrict__ ref_valid) {
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t n = n_dev ? *n_dev : n_fixed;
+  const int64_t nr = exhaustive ? n : n_refs;
+  if (w >= nr) return;  // warp-uniform
+  const int64_t ref = exhaustive ? w : refs[w];
+  evaluate_hypothesis<LdGlobal>(src, dst, n, w, ref, H, iters, min_support, ref_support, ref_rot,
+                                ref_valid);
 }
 
 // Winner = max support, ties -> lower reference index (matching.py:198-206); then the
@@ -566,6 +591,272 @@ k_preselect_final(const double* __restrict__ src, const double* __restrict__ dst
       *scatter.counter = 0;
     }
   }
+}
+
+// ---------------------------------------------------------------------------------
+// ORB path, fused: match build + preselection + final in ONE launch. The separate chain
+// (k_build_matches: 1 CTA, four dependent global loads + a block scan, ~14 us;
+// k_preselect_warp; k_preselect_final: 2 CTAs, ~12 us) is latency, not work. Here every
+// CTA first builds the frame's match list itself -- in template-feature order, exactly
+// as k_build_matches does -- into its shared memory (CTA 0 also publishes it), its warps
+// evaluate their hypotheses from there, and the last CTA to finish picks the winner,
+// writes flags / weights, scatters them to the template features and forms the report
+// statistics in the separate kernels' summation order.
+// ---------------------------------------------------------------------------------
+
+// Block-wide exclusive scan of per-thread counts; *total = the block's sum.
+__device__ __forceinline__ int block_excl_scan(int cnt, int* s_warp, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      const int v = s_warp[w];
+      s_warp[w] = run;
+      run += v;
+    }
+    s_warp[32] = run;
+  }
+  __syncthreads();
+  const int off = s_warp[warp] + inc - cnt;
+  *total = s_warp[32];
+  __syncthreads();
+  return off;
+}
+
+constexpr int ORB_FUSED_PER = 8;  // features per thread per build round
+
+__global__ void __launch_bounds__(512, 1)
+k_preselect_orb(OrbMatchIn in, const int64_t* __restrict__ refs, int64_t n_refs, double H, int iters,
+                double inlier_min, double min_support, double* __restrict__ ref_support,
+                double* __restrict__ ref_rot, uint8_t* __restrict__ ref_valid, PreselectOrbOut out) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  __shared__ int s_warp[33];
+  __shared__ double s_fsum[32];
+  __shared__ int s_fcnt[32];
+  __shared__ bool s_last;
+  const int64_t nt = in.nt;
+  double* s_src = reinterpret_cast<double*>(s_raw);
+  double* s_dst = s_src + 3 * nt;
+  int32_t* s_feat = reinterpret_cast<int32_t*>(s_dst + 3 * nt);
+  // ---- the frame's match list (k_build_matches' rule, feature order) ----
+  int64_t n = 0;
+  for (int64_t base = 0; base < nt; base += (int64_t)blockDim.x * ORB_FUSED_PER) {
+    const int64_t t0 = base + (int64_t)threadIdx.x * ORB_FUSED_PER;
+    int u[ORB_FUSED_PER], v[ORB_FUSED_PER];
+    double z[ORB_FUSED_PER];
+    bool ok[ORB_FUSED_PER];
+#pragma unroll
+    for (int e = 0; e < ORB_FUSED_PER; ++e) {
+      const int64_t t = t0 + e;
+      int fi = -1;
+      if (t < nt && in.nf > 0) {
+        const unsigned long long pv = __ldcg(in.packed + t);  // (distance << 32) | frame index
+        if ((long long)(pv >> 32) <= (long long)in.max_ham) fi = (int)(pv & 0xffffffffull);
+      }
+      u[e] = v[e] = -1;
+      if (fi >= 0 && fi < in.nf) {
+        u[e] = __ldg(in.kp + 2 * fi);
+        v[e] = __ldg(in.kp + 2 * fi + 1);
+      }
+    }
+    int cnt = 0;
+#pragma unroll
+    for (int e = 0; e < ORB_FUSED_PER; ++e) {
+      ok[e] = u[e] >= 0 && u[e] < in.width && v[e] >= 0 && v[e] < in.height;
+      z[e] = ok[e] ? __ldg(in.depth + (int64_t)v[e] * in.width + u[e]) : 0.0;
+      ok[e] = ok[e] && isfinite(z[e]) && z[e] > in.zmin && z[e] < in.zmax;
+      cnt += ok[e] ? 1 : 0;
+    }
+    int total;
+    int64_t o = n + block_excl_scan(cnt, s_warp, &total);
+#pragma unroll
+    for (int e = 0; e < ORB_FUSED_PER; ++e) {
+      const int64_t t = t0 + e;
+      if (blockIdx.x == 0 && t < nt) out.fs.ffw[t] = 0.0;  // no active match until the final
+      if (!ok[e]) continue;
+      const double d = z[e];
+      const double sx = __ldg(in.tpts + 3 * t), sy = __ldg(in.tpts + 3 * t + 1),
+                   sz = __ldg(in.tpts + 3 * t + 2);
+      const double dx = ((double)u[e] - in.cx) / in.fx * d, dy = ((double)v[e] - in.cy) / in.fy * d;
+      s_src[3 * o] = sx;
+      s_src[3 * o + 1] = sy;
+      s_src[3 * o + 2] = sz;
+      s_dst[3 * o] = dx;
+      s_dst[3 * o + 1] = dy;
+      s_dst[3 * o + 2] = d;
+      s_feat[o] = (int32_t)t;
+      if (blockIdx.x == 0) {
+        out.m_src[3 * o] = sx;
+        out.m_src[3 * o + 1] = sy;
+        out.m_src[3 * o + 2] = sz;
+        out.m_dst[3 * o] = dx;
+        out.m_dst[3 * o + 1] = dy;
+        out.m_dst[3 * o + 2] = d;
+        out.m_feat[o] = (int32_t)t;
+      }
+      ++o;
+    }
+    n += total;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out.n_out = n;
+  __syncthreads();
+  // ---- hypotheses: one warp each ----
+  const int exhaustive = refs == nullptr;
+  const int64_t nr = exhaustive ? n : n_refs;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w < nr)
+    evaluate_hypothesis<LdPlain>(s_src, s_dst, n, w, exhaustive ? w : refs[w], H, iters, min_support,
+                                 ref_support, ref_rot, ref_valid);
+  // ---- the last CTA to finish: winner, flags, weights, scatter, statistics ----
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(out.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  double best = -1.0;
+  int64_t best_ref = -1, best_pos = -1;
+  for (int64_t q = threadIdx.x; q < nr; q += blockDim.x) {
+    if (!__ldcg(ref_valid + q)) continue;
+    const int64_t rf = exhaustive ? q : refs[q];
+    const double sp = __ldcg(ref_support + q);
+    if (ref_better(sp, rf, best, best_ref)) {
+      best = sp;
+      best_ref = rf;
+      best_pos = q;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double os = __shfl_xor_sync(0xffffffffu, best, o);
+    const int64_t orf = __shfl_xor_sync(0xffffffffu, best_ref, o);
+    const int64_t op = __shfl_xor_sync(0xffffffffu, best_pos, o);
+    if (ref_better(os, orf, best, best_ref)) {
+      best = os;
+      best_ref = orf;
+      best_pos = op;
+    }
+  }
+  __shared__ double s_bsup[32];
+  __shared__ int64_t s_bref[32], s_bpos[32];
+  if (lane == 0) {
+    s_bsup[warp] = best;
+    s_bref[warp] = best_ref;
+    s_bpos[warp] = best_pos;
+  }
+  __syncthreads();
+  best = -1.0;
+  best_ref = -1;
+  best_pos = -1;
+  for (int w2 = 0; w2 < nw; ++w2)
+    if (ref_better(s_bsup[w2], s_bref[w2], best, best_ref)) {
+      best = s_bsup[w2];
+      best_ref = s_bref[w2];
+      best_pos = s_bpos[w2];
+    }
+  double R[9];
+  double rs0 = 0, rs1 = 0, rs2 = 0, rd0 = 0, rd1 = 0, rd2 = 0;
+  if (best_ref >= 0) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = __ldcg(ref_rot + 9 * best_pos + i);
+    rs0 = s_src[3 * best_ref], rs1 = s_src[3 * best_ref + 1], rs2 = s_src[3 * best_ref + 2];
+    rd0 = s_dst[3 * best_ref], rd1 = s_dst[3 * best_ref + 1], rd2 = s_dst[3 * best_ref + 2];
+  }
+  // per match (k_preselect_final's arithmetic), then the report statistics in the separate
+  // kernels' order: xor-tree sums of 32-match groups, groups of a 1024-match round in
+  // order, rounds in order
+  double wsum = 0.0;
+  int64_t nflag = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += 1024) {
+    for (int g = warp; g < 32; g += nw) {
+      const int64_t k = r0 + 32 * g + lane;
+      double wk = 0.0;
+      int fl = 0;
+      if (k < n) {
+        if (best_ref < 0) {
+          out.weights[k] = 0.0;
+          out.flags[k] = 0;
+          if (out.residuals) out.residuals[k] = 0.0;
+        } else {
+          const double s1[3] = {s_src[3 * k] - rs0, s_src[3 * k + 1] - rs1, s_src[3 * k + 2] - rs2};
+          const double s2[3] = {s_dst[3 * k] - rd0, s_dst[3 * k + 1] - rd1, s_dst[3 * k + 2] - rd2};
+          const double d = rot_residual(R, s1, s2);
+          const double fw = reweight(d, H);
+          const bool flag = fw >= inlier_min;
+          double soft = 1.0 - d / (5.0 * H);
+          soft = soft < 0.0 ? 0.0 : (soft > 1.0 ? 1.0 : soft);
+          wk = flag ? fw : soft;
+          fl = flag ? 1 : 0;
+          out.weights[k] = wk;
+          out.flags[k] = (uint8_t)fl;
+          if (out.residuals) out.residuals[k] = d;
+        }
+        const int f = s_feat[k];
+        out.fs.ffw[f] = wk;
+        out.fs.ffo[3 * f] = s_dst[3 * k];
+        out.fs.ffo[3 * f + 1] = s_dst[3 * k + 1];
+        out.fs.ffo[3 * f + 2] = s_dst[3 * k + 2];
+      }
+      const double gs = warp_sum(wk);
+      for (int o = 16; o > 0; o >>= 1) fl += __shfl_xor_sync(0xffffffffu, fl, o);
+      if (lane == 0) {
+        s_fsum[g] = gs;
+        s_fcnt[g] = fl;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double cs = 0.0;
+      int nf = 0;
+      for (int g = 0; g < 32; ++g) {
+        cs += s_fsum[g];
+        nf += s_fcnt[g];
+      }
+      wsum += cs;
+      nflag += nf;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out.info[0] = best_ref < 0 ? DT_ERR_NO_VALID_HYPOTHESIS : DT_OK;
+    out.info[1] = best_ref;
+    out.support[0] = best_ref < 0 ? 0.0 : best;
+    *out.fs.n_active = out.fs.n_feat;
+    out.fs.stats[0] = wsum;
+    out.fs.stats[1] = (double)nflag;
+    *out.done = 0;
+  }
+  // ready for the next frame's Hamming atomicMin
+  for (int64_t t = threadIdx.x; t < nt; t += blockDim.x) out.packed_reset[t] = ~0ull;
+}
+
+int launch_preselect_orb(const OrbMatchIn& in, const int64_t* refs, int64_t n_refs, double H, int iters,
+                         double inlier_min, double min_support, double* ref_support, double* ref_rot,
+                         uint8_t* ref_valid, const PreselectOrbOut& out, cudaStream_t s, int shared_gpu) {
+  const int64_t nr = refs ? n_refs : in.nt;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms <= 0) sms = 148;
+  const int64_t wpc = shared_gpu ? 8 : std::min<int64_t>(16, std::max<int64_t>(1, (nr + sms - 1) / sms));
+  const int64_t grid = std::max<int64_t>(1, (nr + wpc - 1) / wpc);
+  const size_t smem = (size_t)in.nt * (6 * sizeof(double) + sizeof(int32_t));
+  DT_CHECK_CUDA(cudaFuncSetAttribute(k_preselect_orb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_preselect_orb<<<(unsigned)grid, (unsigned)(32 * wpc), smem, s>>>(
+      in, refs, n_refs, H, iters, inlier_min, min_support, ref_support, ref_rot, ref_valid, out);
+  DT_CHECK_LAUNCH();
+  return DT_OK;
 }
 
 int launch_preselect(const double* src, const double* dst, const int64_t* n_dev, int64_t n_max,

@@ -102,6 +102,39 @@ int launch_hamming(const uint8_t* tdesc, int64_t nt, const uint8_t* fdesc, int64
                    int32_t* best_idx, int32_t* best_dist, cudaStream_t s,
                    unsigned long long* packed = nullptr, bool packed_ready = false);
 struct PreselectWork;
+// ORB path: the Hamming winners -> match list (k_build_matches' rule) inputs
+struct OrbMatchIn {
+  int64_t nt;                          // template features
+  const unsigned long long* packed;    // (nt) (distance << 32) | frame index
+  int max_ham;
+  const int32_t* kp;                   // (nf, 2) frame keypoints
+  int64_t nf;
+  const double* depth;
+  double zmin, zmax;
+  int width, height;
+  double fx, fy, cx, cy;
+  const double* tpts;                  // (nt, 3) template feature points
+};
+struct PreselectOrbOut {
+  double* m_src;       // (n, 3) compacted matches (published by CTA 0)
+  double* m_dst;
+  int32_t* m_feat;
+  int64_t* n_out;
+  double* weights;     // (n) preselected weights / flags / residuals
+  uint8_t* flags;
+  double* residuals;
+  int64_t* info;       // [status, winning reference]
+  double* support;     // winning support
+  FeatureScatter fs;   // the scatter to template features + report statistics
+  unsigned long long* packed_reset;  // = packed: reset for the next frame's atomicMin
+  unsigned* done;      // CTAs finished (the last resets it)
+};
+// Match build + preselection + final of the ORB path in one launch (dt_match.cu). The
+// feature count must fit the shared-memory copy (ORB_FUSED_MAX).
+constexpr int64_t ORB_FUSED_MAX = 4000;
+int launch_preselect_orb(const OrbMatchIn& in, const int64_t* refs, int64_t n_refs, double H, int iters,
+                         double inlier_min, double min_support, double* ref_support, double* ref_rot,
+                         uint8_t* ref_valid, const PreselectOrbOut& out, cudaStream_t s, int shared_gpu);
 int launch_preselect(const double* src, const double* dst, const int64_t* n_dev, int64_t n_max,
                      const int64_t* refs, int64_t n_refs, int exhaustive, double H, int iters,
                      double inlier_min, double min_support, double* weights, uint8_t* flags,

@@ -564,7 +564,14 @@ int solver_grid_blocks(int device, int m_max) {
 // (148 CTAs x 4) covers every control, single warps for larger graphs (config 4, 1,026
 // controls: 0.83 -> 0.76 ms). A function of m alone -- not of the launch shape -- because
 // the team width fixes the fold order, and results must not depend on the cluster size.
-static int solver_team(int m) { return m > 592 ? 1 : 2; }
+static int solver_team(int m) {
+#ifdef DT_TEAM_OVERRIDE
+  (void)m;
+  return DT_TEAM_OVERRIDE;
+#else
+  return m > 592 ? 1 : 2;
+#endif
+}
 
 int solver_launch(const SolverArgs* d_args, int n_seq, int cluster, int m_max, int k, int grid_mode,
                   cudaStream_t s) {

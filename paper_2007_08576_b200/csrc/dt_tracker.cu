@@ -803,6 +803,8 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
   // ---- matches ----
   bool use = in->use_matches != 0;
   int64_t n_max = 0;
+  bool orb_fused = false;
+  const int32_t* orb_kp = nullptr;
   if (use && in->frame_desc != nullptr) {
     DT_REQUIRE(t->n_feat > 0, DT_ERR_INVALID_ARGUMENT, "frame descriptors given but no template features set");
     if (!set && in->n_frame > t->fdesc_cap) {
@@ -821,12 +823,20 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
       DT_CHECK_CUDA(cudaMemcpyAsync(fkp, in->frame_kp, sizeof(int32_t) * 2 * in->n_frame, kind, s));
     DT_TRY(launch_hamming(t->tdesc, t->n_feat, fdesc, in->n_frame, nullptr, nullptr, s,
                           t->ham_packed, true));
-    k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_packed, c.max_hamming, fkp,
-                                       in->n_frame, dep, c.z_min, c.z_max, c.width, c.height, c.fx,
-                                       c.fy, c.cx, c.cy, t->tfeat_pts, t->m_src, t->m_dst, t->m_feat,
-                                       t->info + 2, t->ffw);
-    DT_CHECK_LAUNCH();
-    t->launches += 2;
+    ++t->launches;
+    // the match build runs inside the fused preselection when the template's features fit
+    // its shared-memory copy (and the tracker owns the GPU: cluster mode keeps the small
+    // separate kernels, which pack between the other sequences' CTAs)
+    orb_fused = t->grid_mode && t->n_feat <= ORB_FUSED_MAX;
+    orb_kp = fkp;
+    if (!orb_fused) {
+      k_build_matches<<<1, 1024, 0, s>>>(t->n_feat, t->ham_packed, c.max_hamming, fkp,
+                                         in->n_frame, dep, c.z_min, c.z_max, c.width, c.height, c.fx,
+                                         c.fy, c.cx, c.cy, t->tfeat_pts, t->m_src, t->m_dst, t->m_feat,
+                                         t->info + 2, t->ffw);
+      DT_CHECK_LAUNCH();
+      ++t->launches;
+    }
     n_max = t->n_feat;
   } else if (use && in->n_pairs > 0) {
     DT_TRY(ensure_match_capacity(t, in->n_pairs));
@@ -875,6 +885,17 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
     // features (matches indexed by feature: static points / binding / CSR)
     FeatureScatter fs{t->n_feat, t->m_dst, t->m_feat, t->ffo, t->ffw, t->info + 3, t->astats,
                       t->fs_partial, t->fs_counter};
+    if (orb_fused) {
+      const OrbMatchIn mi{t->n_feat, t->ham_packed, c.max_hamming, orb_kp, in->n_frame, dep,
+                          c.z_min, c.z_max, c.width, c.height, c.fx, c.fy, c.cx, c.cy, t->tfeat_pts};
+      const PreselectOrbOut mo{t->m_src, t->m_dst, t->m_feat, t->info + 2, t->m_w, t->m_flags,
+                               t->m_res, t->info, t->pstats, fs, t->ham_packed, t->fs_counter};
+      DT_TRY(launch_preselect_orb(mi, exhaustive ? nullptr : t->refs, n_refs,
+                                  c.preselect.distance_threshold, c.preselect.n_reweight_iters,
+                                  c.preselect.inlier_weight_min, c.preselect.min_support,
+                                  t->ref_support, t->ref_rot, t->ref_valid, mo, s, 0));
+      ++t->launches;
+    } else {
     DT_TRY(launch_preselect(t->m_src, t->m_dst, t->info + 2, n_max, t->refs, n_refs, exhaustive,
                             c.preselect.distance_threshold, c.preselect.n_reweight_iters,
                             c.preselect.inlier_weight_min, c.preselect.min_support, t->m_w,
@@ -882,6 +903,7 @@ int enqueue_frame(dt_tracker* t, const dt_frame_input* in, bool* used_matches) {
                             t->ref_rot, t->ref_valid, s,
                             in->frame_desc != nullptr ? &fs : nullptr, t->grid_mode ? 0 : 1));
     t->launches += 2;
+    }
   } else {
     k_set_i64<<<1, 1, 0, s>>>(t->info + 2, 0);
     DT_CHECK_LAUNCH();
