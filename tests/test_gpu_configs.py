@@ -81,3 +81,38 @@ def test_full_scale_config_frame_matches_oracle(cid):
     assert dev_mm < VERTEX_TOL_MM, f"config {cid}: per-vertex deviation {dev_mm} mm"
     rel = abs(res.report.total_cost - ores.total_cost) / max(ores.total_cost, 1e-30)
     assert rel < COST_REL_TOL, f"config {cid}: total cost deviates by {rel}"
+
+
+def test_fused_orb_preselection_equals_separate_kernels():
+    """The ORB path's fused match build + preselection + final (one launch, grid mode) and
+    the separate k_build_matches / k_preselect_warp / k_preselect_final chain (cluster
+    mode) produce bit-identical match sets, flags, reports and warps over a free-running
+    config-2 sequence (the solver itself is bitwise cluster-size invariant,
+    test_gpu_solver.py::test_cluster_size_does_not_change_bits)."""
+    import copy
+
+    import bench
+    import paper_2007_08576_b200 as dt
+
+    wl = bench.make_workload(2, 3, seed=1)
+    tpl, graph, cam, feats = wl["tpl"], wl["graph"], wl["cam"], wl["feats"]
+    runs = []
+    for cs in (0, 8):  # 0 = cooperative grid (fused ORB kernel); 8 = clusters (separate)
+        cfg = copy.deepcopy(wl["cfg"])
+        cfg.device.cluster_size = cs
+        trk = dt.Tracker(tpl, graph, cam, cfg)
+        trk.set_features(feats.descriptors, feats.points)
+        trk.set_exhaustive(True)
+        out = []
+        for fr in wl["frames"]:
+            r = trk.track(fr.depth, descriptors=fr.descriptors, keypoints=fr.keypoints)
+            out.append((r.matches.template_points.copy(), r.matches.observed_points.copy(),
+                        np.asarray(r.matches.preselected).copy(),
+                        np.asarray(r.matches.weights).copy(), r.graph.warps.copy(),
+                        r.report.to_dict()))
+        trk.close()
+        runs.append(out)
+    for a, b in zip(*runs):
+        for x, y in zip(a[:5], b[:5]):
+            np.testing.assert_array_equal(x, y)
+        assert a[5] == b[5]
