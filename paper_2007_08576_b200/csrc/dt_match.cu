@@ -280,6 +280,55 @@ __device__ __forceinline__ double irls_weight(const double R[9], double a0, doub
   return far ? H * y : 1.0;
 }
 
+#ifdef DT_PRESELECT_STATS
+__device__ int g_pre_iters[8192];  // debug variant only: IRLS steps run per hypothesis
+#endif
+
+// irls_weight of U matches at once, stage by stage (all U residual chains, then all U
+// squared norms, estimates, Newton steps): the same operations per match as irls_weight,
+// so the same bits, but the U independent chains sit side by side in the instruction
+// stream (given the registers: see the 144-register kernels below) instead of one
+// match's ~12-deep dependent chain after another.
+template <int U>
+__device__ __forceinline__ void irls_weights(const double R[9], const double a[U][3],
+                                             const double b[U][3], double H, double Hsq,
+                                             double w[U]) {
+  double e0[U], e1[U], e2[U], s[U], y[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    e0[u] = __fma_rn(-R[2], a[u][2], b[u][0]);
+    e1[u] = __fma_rn(-R[5], a[u][2], b[u][1]);
+    e2[u] = __fma_rn(-R[8], a[u][2], b[u][2]);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    e0[u] = __fma_rn(-R[1], a[u][1], e0[u]);
+    e1[u] = __fma_rn(-R[4], a[u][1], e1[u]);
+    e2[u] = __fma_rn(-R[7], a[u][1], e2[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    e0[u] = __fma_rn(-R[0], a[u][0], e0[u]);
+    e1[u] = __fma_rn(-R[3], a[u][0], e1[u]);
+    e2[u] = __fma_rn(-R[6], a[u][0], e2[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) s[u] = __fma_rn(e2[u], e2[u], __fma_rn(e1[u], e1[u], e0[u] * e0[u]));
+#pragma unroll
+  for (int u = 0; u < U; ++u) asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y[u]) : "d"(s[u]));
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const double hs = 0.5 * s[u];
+    y[u] = __fma_rn(y[u], __fma_rn(-hs * y[u], y[u], 0.5), y[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const long long sb = __double_as_longlong(s[u]);
+    const bool far = sb > __double_as_longlong(Hsq) && sb <= 0x7ff0000000000000ll;
+    w[u] = far ? H * y[u] : 1.0;
+  }
+}
+
 // Where the hypothesis loops read the matches from: the caller's arrays in global memory
 // (read-only path) or the CTA's shared-memory copy (the fused ORB-path kernel).
 struct LdGlobal {
@@ -293,6 +342,11 @@ struct LdPlain {
 // in increasing k (w = 1 in the first IRLS step). Four matches per trip are loaded and
 // weighted as independent chains before being folded into C in order, so the result is
 // the same as the one-match-at-a-time loop while the chains overlap.
+#ifndef DT_PRE_TRIP
+#define DT_PRE_TRIP 4
+#endif
+constexpr int PRE_TRIP = DT_PRE_TRIP;  // matches per lane per trip of the hypothesis loops
+
 template <bool WEIGHTED, class LD>
 __device__ __forceinline__ void cov_pass(const double* __restrict__ src,
                                          const double* __restrict__ dst, int64_t n, int lane,
@@ -300,10 +354,10 @@ __device__ __forceinline__ void cov_pass(const double* __restrict__ src,
                                          double rd1, double rd2, const double R[9], double H,
                                          double Hsq, double C[9]) {
   int64_t k = lane;
-  for (; k + 96 < n; k += 128) {
-    double a[4][3], b[4][3], w[4];
+  for (; k + 32 * (PRE_TRIP - 1) < n; k += 32 * PRE_TRIP) {
+    double a[PRE_TRIP][3], b[PRE_TRIP][3], w[PRE_TRIP];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < PRE_TRIP; ++u) {
       const double* ps = src + 3 * (k + 32 * u);
       const double* pd = dst + 3 * (k + 32 * u);
       a[u][0] = LD::get(ps) - rs0;
@@ -313,12 +367,14 @@ __device__ __forceinline__ void cov_pass(const double* __restrict__ src,
       b[u][1] = LD::get(pd + 1) - rd1;
       b[u][2] = LD::get(pd + 2) - rd2;
     }
+    if (WEIGHTED) {
+      irls_weights<PRE_TRIP>(R, a, b, H, Hsq, w);
+    } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      w[u] = WEIGHTED ? irls_weight(R, a[u][0], a[u][1], a[u][2], b[u][0], b[u][1], b[u][2], H, Hsq)
-                      : 1.0;
+      for (int u = 0; u < PRE_TRIP; ++u) w[u] = 1.0;
+    }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < PRE_TRIP; ++u) {
       const double c0 = b[u][0] * w[u], c1 = b[u][1] * w[u], c2 = b[u][2] * w[u];
       C[0] = __fma_rn(c0, a[u][0], C[0]);
       C[1] = __fma_rn(c0, a[u][1], C[1]);
@@ -359,17 +415,22 @@ __device__ __forceinline__ double support_pass(const double* __restrict__ src,
                                                const double R[9], double H, double Hsq) {
   double sup = 0.0;
   int64_t k = lane;
-  for (; k + 96 < n; k += 128) {
-    double w[4];
+  for (; k + 32 * (PRE_TRIP - 1) < n; k += 32 * PRE_TRIP) {
+    double a[PRE_TRIP][3], b[PRE_TRIP][3], w[PRE_TRIP];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < PRE_TRIP; ++u) {
       const double* ps = src + 3 * (k + 32 * u);
       const double* pd = dst + 3 * (k + 32 * u);
-      w[u] = irls_weight(R, LD::get(ps) - rs0, LD::get(ps + 1) - rs1, LD::get(ps + 2) - rs2,
-                         LD::get(pd) - rd0, LD::get(pd + 1) - rd1, LD::get(pd + 2) - rd2, H, Hsq);
+      a[u][0] = LD::get(ps) - rs0;
+      a[u][1] = LD::get(ps + 1) - rs1;
+      a[u][2] = LD::get(ps + 2) - rs2;
+      b[u][0] = LD::get(pd) - rd0;
+      b[u][1] = LD::get(pd + 1) - rd1;
+      b[u][2] = LD::get(pd + 2) - rd2;
     }
+    irls_weights<PRE_TRIP>(R, a, b, H, Hsq, w);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) sup += w[u];
+    for (int u = 0; u < PRE_TRIP; ++u) sup += w[u];
   }
   for (; k < n; k += 32)
     sup += irls_weight(R, LD::get(src + 3 * k) - rs0, LD::get(src + 3 * k + 1) - rs1,
@@ -398,7 +459,13 @@ __device__ __forceinline__ void evaluate_hypothesis(const double* __restrict__ s
   const double Hsq = H * H;
   double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
   double V[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+#ifdef DT_PRESELECT_STATS
+  int dbg_it = 0;
+#endif
   for (int it = 0; it < iters; ++it) {
+#ifdef DT_PRESELECT_STATS
+    dbg_it = it;
+#endif
     double C[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (it == 0)
       cov_pass<false, LD>(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq, C);
@@ -429,6 +496,11 @@ __device__ __forceinline__ void evaluate_hypothesis(const double* __restrict__ s
     for (int i = 0; i < 9; ++i) R[i] = Rm[i];
     if (same) break;
   }
+#ifdef DT_PRESELECT_STATS
+  if (lane == 0 && w < 8192) {
+    g_pre_iters[w] = live ? dbg_it + 1 : -1;
+  }
+#endif
   double sup = 0.0;
   if (live) sup = support_pass<LD>(src, dst, n, lane, rs0, rs1, rs2, rd0, rd1, rd2, R, H, Hsq);
 #pragma unroll
@@ -442,13 +514,24 @@ __device__ __forceinline__ void evaluate_hypothesis(const double* __restrict__ s
   }
 }
 
-// One warp per reference hypothesis, the matches read from global memory.
-__global__ void __launch_bounds__(512, 1)
-k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
-                 const int64_t* __restrict__ n_dev, int64_t n_fixed,
-                 const int64_t* __restrict__ refs, int64_t n_refs, int exhaustive, double H,
-                 int iters, double min_support, double* __restrict__ ref_support,
-                 double* __restrict__ ref_rot, uint8_t* __restrict__ ref_valid) {
+// One warp per reference hypothesis, the matches read from global memory. Two register
+// budgets of the same body: a CTA of <= 12 warps (3 per scheduler: the register file is
+// split per scheduler, 16 K each) may hold 168 registers per thread, enough for the four
+// weight chains of a trip to run side by side (measured ~11 % faster per hypothesis than
+// the serialized 128-register schedule); 13-16 warps per CTA get 128. (n = 1,888
+// hypotheses on 12-warp CTAs -- two rounds -- measured 0.233 vs 0.205 ms: the second
+// round's lone warps cost more than the chains gain.)
+#define DT_PRESELECT_WARP_PARAMS                                                            \
+  const double *__restrict__ src, const double *__restrict__ dst,                           \
+      const int64_t *__restrict__ n_dev, int64_t n_fixed, const int64_t *__restrict__ refs, \
+      int64_t n_refs, int exhaustive, double H, int iters, double min_support,              \
+      double *__restrict__ ref_support, double *__restrict__ ref_rot,                       \
+      uint8_t *__restrict__ ref_valid
+#define DT_PRESELECT_WARP_ARGS \
+  src, dst, n_dev, n_fixed, refs, n_refs, exhaustive, H, iters, min_support, ref_support, ref_rot, ref_valid
+constexpr int PRESELECT_WIDE_WARPS = 12;  // warps per CTA of the 168-register kernels
+
+__device__ __forceinline__ void preselect_warp_body(DT_PRESELECT_WARP_PARAMS) {
   const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t n = n_dev ? *n_dev : n_fixed;
   const int64_t nr = exhaustive ? n : n_refs;
@@ -456,6 +539,13 @@ k_preselect_warp(const double* __restrict__ src, const double* __restrict__ dst,
   const int64_t ref = exhaustive ? w : refs[w];
   evaluate_hypothesis<LdGlobal>(src, dst, n, w, ref, H, iters, min_support, ref_support, ref_rot,
                                 ref_valid);
+}
+
+__global__ void __launch_bounds__(512, 1) k_preselect_warp(DT_PRESELECT_WARP_PARAMS) {
+  preselect_warp_body(DT_PRESELECT_WARP_ARGS);
+}
+__global__ void __launch_bounds__(32 * PRESELECT_WIDE_WARPS, 1) k_preselect_warp_wide(DT_PRESELECT_WARP_PARAMS) {
+  preselect_warp_body(DT_PRESELECT_WARP_ARGS);
 }
 
 // Winner = max support, ties -> lower reference index (matching.py:198-206); then the
@@ -633,10 +723,14 @@ __device__ __forceinline__ int block_excl_scan(int cnt, int* s_warp, int* total)
 
 constexpr int ORB_FUSED_PER = 8;  // features per thread per build round
 
-__global__ void __launch_bounds__(512, 1)
-k_preselect_orb(OrbMatchIn in, const int64_t* __restrict__ refs, int64_t n_refs, double H, int iters,
-                double inlier_min, double min_support, double* __restrict__ ref_support,
-                double* __restrict__ ref_rot, uint8_t* __restrict__ ref_valid, PreselectOrbOut out) {
+#define DT_PRESELECT_ORB_PARAMS                                                                \
+  OrbMatchIn in, const int64_t *__restrict__ refs, int64_t n_refs, double H, int iters,         \
+      double inlier_min, double min_support, double *__restrict__ ref_support,                  \
+      double *__restrict__ ref_rot, uint8_t *__restrict__ ref_valid, PreselectOrbOut out
+#define DT_PRESELECT_ORB_ARGS \
+  in, refs, n_refs, H, iters, inlier_min, min_support, ref_support, ref_rot, ref_valid, out
+
+__device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   __shared__ int s_warp[33];
   __shared__ double s_fsum[32];
@@ -711,10 +805,16 @@ k_preselect_orb(OrbMatchIn in, const int64_t* __restrict__ refs, int64_t n_refs,
   // ---- hypotheses: one warp each ----
   const int exhaustive = refs == nullptr;
   const int64_t nr = exhaustive ? n : n_refs;
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w < nr)
+  // hypothesis h on warp (h / gridDim.x) mod wpc of CTA h mod gridDim.x: consecutive
+  // hypotheses on different SMs, and when there are more hypotheses than warps (the
+  // 12-warp wide kernel) the second round is spread one per SM
+  const int wpc = (int)(blockDim.x >> 5);
+  for (int64_t r = 0;; ++r) {
+    const int64_t w = (int64_t)blockIdx.x + (int64_t)gridDim.x * ((threadIdx.x >> 5) + wpc * r);
+    if (w >= nr) break;  // warp-uniform
     evaluate_hypothesis<LdPlain>(s_src, s_dst, n, w, exhaustive ? w : refs[w], H, iters, min_support,
                                  ref_support, ref_rot, ref_valid);
+  }
   // ---- the last CTA to finish: winner, flags, weights, scatter, statistics ----
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -841,6 +941,13 @@ k_preselect_orb(OrbMatchIn in, const int64_t* __restrict__ refs, int64_t n_refs,
   for (int64_t t = threadIdx.x; t < nt; t += blockDim.x) out.packed_reset[t] = ~0ull;
 }
 
+__global__ void __launch_bounds__(512, 1) k_preselect_orb(DT_PRESELECT_ORB_PARAMS) {
+  preselect_orb_body(DT_PRESELECT_ORB_ARGS);
+}
+__global__ void __launch_bounds__(32 * PRESELECT_WIDE_WARPS, 1) k_preselect_orb_wide(DT_PRESELECT_ORB_PARAMS) {
+  preselect_orb_body(DT_PRESELECT_ORB_ARGS);
+}
+
 int launch_preselect_orb(const OrbMatchIn& in, const int64_t* refs, int64_t n_refs, double H, int iters,
                          double inlier_min, double min_support, double* ref_support, double* ref_rot,
                          uint8_t* ref_valid, const PreselectOrbOut& out, cudaStream_t s, int shared_gpu) {
@@ -850,11 +957,13 @@ int launch_preselect_orb(const OrbMatchIn& in, const int64_t* refs, int64_t n_re
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms <= 0) sms = 148;
   const int64_t wpc = shared_gpu ? 8 : std::min<int64_t>(16, std::max<int64_t>(1, (nr + sms - 1) / sms));
-  const int64_t grid = std::max<int64_t>(1, (nr + wpc - 1) / wpc);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(sms, (nr + wpc - 1) / wpc));
   const size_t smem = (size_t)in.nt * (6 * sizeof(double) + sizeof(int32_t));
-  DT_CHECK_CUDA(cudaFuncSetAttribute(k_preselect_orb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_preselect_orb<<<(unsigned)grid, (unsigned)(32 * wpc), smem, s>>>(
-      in, refs, n_refs, H, iters, inlier_min, min_support, ref_support, ref_rot, ref_valid, out);
+  auto* kern = !shared_gpu && wpc <= PRESELECT_WIDE_WARPS ? k_preselect_orb_wide : k_preselect_orb;
+  DT_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)grid, (unsigned)(32 * wpc), smem, s>>>(in, refs, n_refs, H, iters, inlier_min,
+                                                          min_support, ref_support, ref_rot,
+                                                          ref_valid, out);
   DT_CHECK_LAUNCH();
   return DT_OK;
 }
@@ -880,7 +989,8 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
     // between the other kernels' CTAs instead.
     const int64_t wpc = shared_gpu ? 8
                                    : std::min<int64_t>(16, std::max<int64_t>(1, (nr + sms - 1) / sms));
-    k_preselect_warp<<<(unsigned)((nr + wpc - 1) / wpc), (unsigned)(32 * wpc), 0, s>>>(
+    (!shared_gpu && wpc <= PRESELECT_WIDE_WARPS ? k_preselect_warp_wide : k_preselect_warp)
+        <<<(unsigned)((nr + wpc - 1) / wpc), (unsigned)(32 * wpc), 0, s>>>(
         src, dst, n_dev, n_max, refs, n_refs, exhaustive, H, iters, min_support, ref_support,
         ref_rot, ref_valid);
     DT_CHECK_LAUNCH();
@@ -901,6 +1011,12 @@ int launch_preselect(const double* src, const double* dst, const int64_t* n_dev,
 using namespace dt;
 
 extern "C" {
+
+#ifdef DT_PRESELECT_STATS
+int dt_debug_preselect_iters(int* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_pre_iters, sizeof(int) * (n < 8192 ? n : 8192)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int dt_hamming_match(const uint8_t* template_desc, int64_t n_template, const uint8_t* frame_desc,
                      int64_t n_frame, int32_t* best_idx, int32_t* best_dist, void* stream) {
