@@ -220,7 +220,7 @@ def replica_throughput(frames_per_rank: int, world: int, max_ms: float) -> float
 
 
 # ---------------------------------------------------------------------------------
-FP64_PEAK_TFLOPS = 34.0  # DFMA, measured on this pool's B200 with tools/fp64_probe.cu
+FP64_PEAK_TFLOPS = 34.4  # DFMA, measured on this pool's B200 with tools/fp64_probe.cu (profiles/r02_fp64_probe.txt)
 
 # algorithmic bytes for the roofline of the LM solver kernel
 # ---------------------------------------------------------------------------------
@@ -441,7 +441,8 @@ def run_b200(args, rank, world, local_rank):
     roofline_pre = None
     if pre_ms > 0 and n_match > 0:
         ach = pre_flop / (pre_ms * 1e-3) / 1e12
-        roofline_pre = {"kernel": "k_preselect_warp + k_preselect_final", "bound": "fp64",
+        roofline_pre = {"kernel": "k_preselect_orb (fused ORB match build + preselection + final)",
+                        "bound": "fp64",
                         "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                         "frac": ach / FP64_PEAK_TFLOPS, "algorithmic_flop": pre_flop,
                         "launch_ms": pre_ms,

@@ -25,7 +25,9 @@ ROOT = Path(__file__).resolve().parent.parent
 # GRID = true, KM = 4, BIG = false, TM = 2)
 KERNELS = {
     "k_solve_frame_grid_k4_tm2": "k_solve_frameILb1ELi4ELb0ELi2E",
-    "k_preselect_warp": "k_preselect_warp",
+    "k_preselect_orb": "15k_preselect_orbE",  # fused ORB-path build + preselect + final
+    "k_preselect_orb_wide": "20k_preselect_orb_wideE",  # same, 168 registers, <= 12 warps
+    "k_preselect_warp": "16k_preselect_warpE",  # caller-supplied pairs / cluster mode
     "k_preselect_final": "k_preselect_final",
     "k_hamming": "9k_hamming",
     "k_build_matches": "k_build_matches",
