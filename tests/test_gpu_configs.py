@@ -116,3 +116,52 @@ def test_fused_orb_preselection_equals_separate_kernels():
         for x, y in zip(a[:5], b[:5]):
             np.testing.assert_array_equal(x, y)
         assert a[5] == b[5]
+
+
+def test_large_feature_set_falls_back_to_separate_preselection():
+    """More template features than the fused ORB kernel's shared-memory copy holds
+    (ORB_FUSED_MAX = 4,000; 4,100 here): grid mode falls back to the separate match build /
+    preselection / final chain. Flags against the oracle's exhaustive preselection
+    (bit-exact), and the grid-mode frame bitwise equal to the cluster-mode frame."""
+    import copy
+    from dataclasses import replace
+
+    import paper_2007_08576_b200 as dt
+    from oracle import pipeline as OP
+    from paper_2007_08576_b200 import synth
+
+    spec = synth.CONFIGS[2]
+    scene = replace(spec["scene"], seed=3, n_features=4100)
+    cfg = dt.load_config({"sampling": {"radius": spec["radius"]},
+                          "solver": {"max_outer_iters": 3, "step_tol": 0.0, "cost_tol": 0.0}})
+    cam = synth.camera_for(scene)
+    tpl0 = synth.make_template(scene)
+    feats = synth.make_features(scene, tpl0)
+    assert len(feats.points) == 4100
+    fr = synth.make_frame(scene, cam, tpl0, feats, 1)
+    tpl, graph = dt.prepare_template(tpl0, cfg)
+    outs = []
+    for cs in (0, 8):
+        c2 = copy.deepcopy(cfg)
+        c2.device.cluster_size = cs
+        trk = dt.Tracker(tpl, graph, cam, c2)
+        trk.set_features(feats.descriptors, feats.points)
+        trk.set_exhaustive(True)
+        r = trk.track(fr.depth, descriptors=fr.descriptors, keypoints=fr.keypoints)
+        trk.close()
+        outs.append(r)
+    a, b = outs
+    np.testing.assert_array_equal(a.matches.preselected, b.matches.preselected)
+    np.testing.assert_array_equal(a.matches.weights, b.matches.weights)
+    np.testing.assert_array_equal(a.graph.warps, b.graph.warps)
+    assert a.report.to_dict() == b.report.to_dict()
+    assert a.report.n_matches > 3000
+    camt = (cam.fx, cam.fy, cam.cx, cam.cy)
+    src, dst, _ = OP.matches_from_descriptors(feats.descriptors, feats.points, fr.descriptors,
+                                              fr.keypoints, fr.depth, camt)
+    np.testing.assert_array_equal(a.matches.template_points, src)
+    np.testing.assert_array_equal(a.matches.observed_points, dst)
+    # the oracle's exhaustive preselection (~10 s of numpy)
+    sel = OP.preselect(src, dst, range(len(src)))
+    np.testing.assert_array_equal(a.matches.preselected, sel.flags)
+    np.testing.assert_allclose(a.matches.weights, sel.weights, rtol=0, atol=1e-9)
