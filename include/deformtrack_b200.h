@@ -389,9 +389,12 @@ int dt_tracker_device_outputs(dt_tracker* t, double** warps, double** points, do
 /* Counters: kernels launched by the last dt_track_frame call. */
 int dt_tracker_last_launches(dt_tracker* t);
 
-/* Run one frame on several trackers at once: one thread-block cluster per tracker
- * in a single solver launch (independent sequences, BASELINE config 5). All trackers
- * must live on the same device; `stream` orders the batch. */
+/* Run one frame on each of several trackers (independent sequences, BASELINE config 5):
+ * every frame is enqueued on its own tracker's stream before any is collected, so the
+ * sequences overlap on the device (in cluster mode each solver occupies one thread-block
+ * cluster); then each tracker's outputs are collected as dt_track_frame would return
+ * them (outputs may be NULL). All trackers must live on the current device. `stream` is
+ * reserved (pass NULL). */
 int dt_track_frames_batched(dt_tracker** trackers, const dt_frame_input* inputs,
                             dt_frame_output* outputs, int32_t n_trackers, void* stream);
 

@@ -166,6 +166,19 @@ class DeviceTracker:
               want_points: bool = True,
               want_matches: bool = False, outputs: dict | None = None) -> FrameOutputs:
         """Run one frame. Host inputs; returns host outputs (after the stream sync)."""
+        io = self.prepare(depth, normals, pairs=pairs, match_w=match_w,
+                          match_binding=match_binding, frame_desc=frame_desc, frame_kp=frame_kp,
+                          refs=refs, frame_id=frame_id, want_points=want_points,
+                          want_matches=want_matches, outputs=outputs)
+        check(lib.dt_track_frame(self._h, C.byref(io["fi"]), C.byref(io["fo"])), "dt_track_frame")
+        return self.finish(io)
+
+    def prepare(self, depth, normals=None, *, pairs=None, match_w=None, match_binding=None,
+                frame_desc=None, frame_kp=None, refs=None, frame_id: int = 0,
+                want_points: bool = True, want_matches: bool = False,
+                outputs: dict | None = None) -> dict:
+        """The dt_frame_input / dt_frame_output of one frame (host buffers) plus the arrays
+        they point into; `finish` turns the filled outputs into FrameOutputs."""
         keep = []
 
         def hp(a, dtype):
@@ -253,7 +266,12 @@ class DeviceTracker:
         fo.match_capacity = cap
         fo.control_data_weights = _host_ptr(cdw)
         fo.report = C.cast(C.pointer(report), C.c_void_p).value
-        check(lib.dt_track_frame(self._h, C.byref(fi), C.byref(fo)), "dt_track_frame")
+        return dict(fi=fi, fo=fo, keep=keep, warps=warps, pts=pts, nrm=nrm, cdw=cdw,
+                    report=report, mw=mw, mf=mf, ms=ms, md=md)
+
+    def finish(self, io: dict) -> FrameOutputs:
+        warps, pts, nrm, cdw, report = io["warps"], io["pts"], io["nrm"], io["cdw"], io["report"]
+        mw, mf, ms, md = io["mw"], io["mf"], io["ms"], io["md"]
         it = int(self._cfg.max_outer_iters)
         ch = np.zeros((it, 2))
         lh = np.zeros((it, 2))
@@ -409,4 +427,20 @@ def nvh_message(n: int) -> str:
     if n < 3:
         return f"{n} matches cannot support a rotation hypothesis"
     return "every reference hypothesis was discarded"
+
+
+def track_batched(trackers, frames) -> list:
+    """One frame on each of several trackers (independent sequences, BASELINE config 5)
+    through dt_track_frames_batched: every tracker's frame is enqueued on its own stream
+    before any is collected, so the sequences overlap on the device. `frames` holds one
+    dict of DeviceTracker.track keyword arguments (with "depth") per tracker."""
+    if len(trackers) != len(frames):
+        raise ValueError("one frame per tracker")
+    ios = [t.prepare(**f) for t, f in zip(trackers, frames)]
+    n = len(trackers)
+    hs = (C.c_void_p * max(n, 1))(*[t._h for t in trackers])
+    fis = (FrameInput * max(n, 1))(*[io["fi"] for io in ios])
+    fos = (FrameOutput * max(n, 1))(*[io["fo"] for io in ios])
+    check(lib.dt_track_frames_batched(hs, fis, fos, n, None), "dt_track_frames_batched")
+    return [t.finish(io) for t, io in zip(trackers, ios)]
 
