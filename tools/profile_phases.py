@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--frames", type=int, default=4)
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--groups", default=None, help="CTA group bounds, e.g. 0,30,93,132,148")
+    ap.add_argument("--all-ctas", action="store_true", help="print every CTA's mean arrival")
     args = ap.parse_args()
     import torch
 
@@ -60,6 +62,7 @@ def main():
     crit = defaultdict(float)   # last CTA arrival - previous release
     blat = defaultdict(float)   # release - last CTA arrival
     last_cta = defaultdict(list)
+    per_cta = defaultdict(list)  # arrival - previous release, per CTA
     for i, fr in enumerate(wl["frames"]):
         d = torch.from_numpy(fr.depth).to(dev)
         de = torch.from_numpy(fr.descriptors).to(dev)
@@ -86,6 +89,7 @@ def main():
                 crit[ph] += (mx - rel_prev) / 1e3
                 blat[ph] += (tr[idx + 1, 1] - mx) / 1e3
                 last_cta[ph].append(int(arr[k].argmax()))
+                per_cta[ph].append((arr[k].astype(np.float64) - rel_prev) / 1e3)
                 rel_prev = tr[idx + 1, 1]
                 k += 1
         prev_t = tr[0, 1]
@@ -120,6 +124,19 @@ def main():
         lc = np.bincount(last_cta[ph]).argsort()[::-1][:3].tolist()
         print(f"{NAMES.get(ph, ph):22s} {c:18.1f} {b:14.1f} {lc}")
     print(f"{'total':22s} {tc:18.1f} {tb:14.1f}")
+    print("per-CTA arrival after the previous release (us/frame): median CTA, slowest CTA, "
+          "and the five CTAs with the largest mean")
+    for ph in sorted(per_cta):
+        a = np.sum(per_cta[ph], axis=0) / nf
+        top = np.argsort(a)[::-1][:5]
+        print(f"{NAMES.get(ph, ph):22s} median {np.median(a):7.1f} max {a.max():7.1f}  "
+              + " ".join(f"{int(c)}:{a[c]:.1f}" for c in top))
+        if args.all_ctas:
+            print("    " + " ".join(f"{v:.0f}" for v in a))
+        if args.groups:
+            g = [int(x) for x in args.groups.split(",")]
+            print("    groups: " + "  ".join(f"[{lo},{hi}) {a[lo:hi].mean():.1f}"
+                                           for lo, hi in zip(g[:-1], g[1:]) if hi <= a.size))
     if args.json:
         Path(args.json).write_text(json.dumps({"stages_ms": st,
                                                "solver_work_us": {NAMES.get(k, k): v / nf for k, v in work.items()},
