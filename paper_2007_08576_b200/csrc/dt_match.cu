@@ -957,7 +957,10 @@ int launch_preselect_orb(const OrbMatchIn& in, const int64_t* refs, int64_t n_re
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms <= 0) sms = 148;
   const int64_t wpc = shared_gpu ? 8 : std::min<int64_t>(16, std::max<int64_t>(1, (nr + sms - 1) / sms));
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(sms, (nr + wpc - 1) / wpc));
+  // one CTA per SM when the tracker owns the GPU (more hypotheses than warps: a second
+  // round, see preselect_orb_body); sharing the GPU, small CTAs for every hypothesis
+  const int64_t grid = std::max<int64_t>(
+      1, shared_gpu ? (nr + wpc - 1) / wpc : std::min<int64_t>(sms, (nr + wpc - 1) / wpc));
   const size_t smem = (size_t)in.nt * (6 * sizeof(double) + sizeof(int32_t));
   auto* kern = !shared_gpu && wpc <= PRESELECT_WIDE_WARPS ? k_preselect_orb_wide : k_preselect_orb;
   DT_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

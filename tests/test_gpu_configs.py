@@ -84,15 +84,18 @@ def test_full_scale_config_frame_matches_oracle(cid):
 
 
 def test_fused_orb_preselection_equals_separate_kernels():
-    """The ORB path's fused match build + preselection + final (one launch, grid mode) and
-    the separate k_build_matches / k_preselect_warp / k_preselect_final chain (cluster
-    mode) produce bit-identical match sets, flags, reports and warps over a free-running
-    config-2 sequence (the solver itself is bitwise cluster-size invariant,
-    test_gpu_solver.py::test_cluster_size_does_not_change_bits)."""
+    """The ORB path's fused match build + preselection + final (k_preselect_orb: one CTA
+    per SM in grid mode, 8-warp CTAs in cluster mode) gives bit-identical match sets,
+    flags, reports and warps in both modes over a free-running config-2 sequence (the
+    solver itself is bitwise cluster-size invariant,
+    test_gpu_solver.py::test_cluster_size_does_not_change_bits), and the same weights and
+    flags, bit for bit, as the separate k_preselect_warp / k_preselect_final kernels
+    (dt_preselect) on the same match set."""
     import copy
 
     import bench
     import paper_2007_08576_b200 as dt
+    from paper_2007_08576_b200.matching import MatchSet, PreselectConfig, preselect_inliers
 
     wl = bench.make_workload(2, 3, seed=1)
     tpl, graph, cam, feats = wl["tpl"], wl["graph"], wl["cam"], wl["feats"]
@@ -116,6 +119,11 @@ def test_fused_orb_preselection_equals_separate_kernels():
         for x, y in zip(a[:5], b[:5]):
             np.testing.assert_array_equal(x, y)
         assert a[5] == b[5]
+    exhaustive = PreselectConfig(n_references=10**9)
+    for src, dst, flags, weights, _, _ in runs[0]:
+        sep = preselect_inliers(MatchSet.from_pairs(src, dst), exhaustive)
+        np.testing.assert_array_equal(sep.matches.preselected, flags)
+        np.testing.assert_array_equal(sep.matches.weights, weights)
 
 
 @pytest.mark.parametrize("n_feat", [3000, 4100])
@@ -125,7 +133,7 @@ def test_large_feature_sets_preselect_exactly(n_feat):
     shared-memory copy holds (ORB_FUSED_MAX = 4,000), so grid mode falls back to the
     separate match build / preselection / final chain. Flags against the oracle's
     exhaustive preselection (bit-exact), and the grid-mode frame bitwise equal to the
-    cluster-mode frame (separate chain)."""
+    cluster-mode frame (different CTA shapes and hypothesis-to-warp mappings)."""
     import copy
     from dataclasses import replace
 
