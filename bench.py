@@ -66,7 +66,8 @@ def parse_args():
     ap.add_argument("--workload", choices=["config2", "config5"], default="config2",
                     help="headline line: one config-2 sequence per GPU (default) or config 5")
     ap.add_argument("--c5-rounds", type=int, default=8, help="config-5 frames per sequence")
-    ap.add_argument("--c5-cluster", type=int, default=4, help="config-5 solver cluster size")
+    ap.add_argument("--c5-cluster", type=int, default=8,
+                    help="config-5 solver cluster size (8 measured ~1 % above 4, 16 below)")
     return ap.parse_args()
 
 
@@ -503,7 +504,7 @@ def config5_aggregate(n_seq: int, rounds: int, max_ms: float) -> float:
     return n_seq * rounds / (max_ms / 1e3)
 
 
-def run_config5(wl, rank, world, local_rank, n_seq=C5_SEQUENCES, cluster=4, rounds=8, warmup=2):
+def run_config5(wl, rank, world, local_rank, n_seq=C5_SEQUENCES, cluster=8, rounds=8, warmup=2):
     """BASELINE config 5 on this rank: its shard of `n_seq` independent config-2
     sequences, one tracker (own warps, buffers, CUDA stream; solver = one thread-block
     cluster) per sequence, frames enqueued round-robin. Device time = first event to the

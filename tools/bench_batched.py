@@ -2,7 +2,7 @@
 (one tracker per CUDA stream, each solver a thread-block cluster), aggregate frames/s.
 The measurement itself is bench.run_config5 (the `config5` object of the bench line).
 
-    python tools/bench_batched.py [--seqs 64] [--cluster 4] [--rounds 8] [--frames 8]
+    python tools/bench_batched.py [--seqs 64] [--cluster 8] [--rounds 8] [--frames 8]
 """
 
 from __future__ import annotations
@@ -19,7 +19,7 @@ sys.path.insert(0, str(ROOT))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seqs", type=int, default=64)
-    ap.add_argument("--cluster", type=int, default=4)
+    ap.add_argument("--cluster", type=int, default=8)
     ap.add_argument("--rounds", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--frames", type=int, default=8)
