@@ -27,10 +27,20 @@ namespace dt {
 // Hamming
 // ---------------------------------------------------------------------------------
 
-constexpr int HAM_TPW = 2;                 // template descriptors per warp
-constexpr int HAM_WARPS = 4;               // warps per CTA (2000 templates -> 250 CTAs)
+// 2000 x 2500 at config 2: 125 CTAs x 8 frame ranges of 313 descriptors; each lane
+// compares one staged frame descriptor with its warp's four templates (four independent
+// popc chains). Measured (bench orb_match stage): 2 templates x 4 ranges 27.6 us, 4 x 4
+// 29.5, 8 x 4 29.5, 4 x 8 25.5, 2 x 8 25.5, 8 x 8 27.6, 4 x 16 25.4, 2 x 16 25.5.
+#ifndef DT_HAM_TPW
+#define DT_HAM_TPW 4
+#endif
+#ifndef DT_HAM_SPLITS
+#define DT_HAM_SPLITS 8
+#endif
+constexpr int HAM_TPW = DT_HAM_TPW;        // template descriptors per warp
+constexpr int HAM_WARPS = 4;               // warps per CTA
 constexpr int HAM_TILE = 512;              // frame descriptors per smem tile (16 KB)
-constexpr int HAM_SPLITS = 4;              // frame-descriptor ranges (grid rows) per template
+constexpr int HAM_SPLITS = DT_HAM_SPLITS;  // frame-descriptor ranges (grid rows) per template
 
 // blockIdx.y selects a contiguous range of frame descriptors; with `packed` the per-range
 // winners are folded by a 64-bit atomicMin of (distance << 32 | index) -- the
