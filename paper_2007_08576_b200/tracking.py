@@ -201,9 +201,14 @@ class Tracker:
         warning = None
         r = out.report
         if descriptors is not None:
-            nm = int(r.n_matches)
-            annotated = MatchSet(out.match_src[:nm].copy(), out.match_dst[:nm].copy(),
-                                 out.match_weights[:nm].copy(), out.match_flags[:nm].astype(bool))
+            nm = int(r.n_matches) if out.match_src is not None else 0
+            if nm:
+                annotated = MatchSet(out.match_src[:nm].copy(), out.match_dst[:nm].copy(),
+                                     out.match_weights[:nm].copy(),
+                                     out.match_flags[:nm].astype(bool))
+            else:  # no frame features (or none survived): an empty match set
+                annotated = MatchSet(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros(0),
+                                     np.zeros(0, dtype=bool))
             n = nm
         elif matches is not None and n:
             annotated = MatchSet(matches.template_points, matches.observed_points,

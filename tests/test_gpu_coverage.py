@@ -280,3 +280,40 @@ def test_large_control_graph_uses_global_state_solver():
     assert res.report.n_correspondences == ores.n_correspondences
     assert res.report.accepted_steps == ores.accepted_steps
     assert float(np.abs(res.points - opts).max()) < VERTEX_TOL_MM
+
+
+def test_frame_without_orb_features_tracks_on_depth():
+    """A frame with zero ORB features through the fused ORB kernel: no matches, the
+    preselection reports NoValidHypothesis (weights 0, warning), the frame is tracked on
+    depth alone -- the same solution as the oracle's depth-only solve -- and the next
+    frame with features is matched normally (the packed Hamming scratch was reset)."""
+    from paper_2007_08576_b200 import synth
+
+    scene, spec = _scene(1)
+    dt, cfg, cam, tpl0, feats, tpl, graph = _setup(scene, spec["radius"], spec["iters"])
+    fr = synth.make_frame(scene, cam, tpl0, feats, 2)
+    trk = dt.Tracker(tpl, graph, cam, cfg)
+    trk.set_features(feats.descriptors, feats.points)
+    trk.set_exhaustive(True)
+    res = trk.track(fr.depth, descriptors=np.zeros((0, 32), np.uint8),
+                    keypoints=np.zeros((0, 2), np.int32))
+    assert res.report.n_matches == 0 and res.report.n_preselected == 0
+    from oracle import pipeline as OP
+
+    camt = (cam.fx, cam.fy, cam.cx, cam.cy)
+    tplt = (tpl.points, tpl.normals, tpl.bind_indices, tpl.bind_weights)
+    grt = (graph.points, graph.edges, graph.edge_weights)
+    s = OP.Schedule(max_outer_iters=spec["iters"], step_tol=0.0, cost_tol=0.0)
+    ores, _, opts, _ = OP.track(tplt, grt, graph.warps, fr.depth,
+                                OP.observation_normals(fr.depth, *camt), camt, None,
+                                OP.Weights(), s, graph.sampling_radius)
+    assert res.report.n_correspondences == ores.n_correspondences
+    assert float(np.abs(res.points - opts).max()) < VERTEX_TOL_MM
+    # a normal frame afterwards: matches equal the oracle's
+    trk.reset()
+    res2 = trk.track(fr.depth, descriptors=fr.descriptors, keypoints=fr.keypoints)
+    trk.close()
+    src, dst, _ = OP.matches_from_descriptors(feats.descriptors, feats.points, fr.descriptors,
+                                              fr.keypoints, fr.depth, camt)
+    np.testing.assert_array_equal(res2.matches.template_points, src)
+    np.testing.assert_array_equal(res2.matches.observed_points, dst)
