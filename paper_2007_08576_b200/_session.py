@@ -185,8 +185,17 @@ class DeviceTracker:
             if a is None:
                 return None
             if hasattr(a, "data_ptr"):
-                keep.append(a)
-                return _host_ptr(a)
+                # a torch tensor: used in place only when it already is contiguous host
+                # memory of the right dtype (this entry copies from HOST pointers);
+                # anything else goes through numpy (device tensors are copied back)
+                import torch
+
+                want = {np.float64: torch.float64, np.uint8: torch.uint8,
+                        np.int32: torch.int32, np.int64: torch.int64}[dtype]
+                if a.device.type == "cpu" and a.dtype == want and a.is_contiguous():
+                    keep.append(a)
+                    return _host_ptr(a)
+                a = a.detach().cpu().numpy()
             arr = np.ascontiguousarray(a, dtype=dtype)
             keep.append(arr)
             return _host_ptr(arr)

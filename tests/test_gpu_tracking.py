@@ -91,3 +91,31 @@ def test_prepare_template_binds_and_samples(small_config):
     assert len(graph) >= 20  # 100 mm patch at radius 12
     assert bound.bind_indices.shape == (len(bound), 4)
     np.testing.assert_allclose(bound.bind_weights.sum(axis=1), 1.0, atol=1e-9)
+
+
+def test_torch_inputs_of_any_device_and_dtype_match_numpy():
+    """Tracker.track takes torch tensors too: CUDA tensors and host tensors of another
+    dtype are copied through numpy (the host-buffer entry never reads a device pointer as
+    host memory); results equal the numpy-input frame bit for bit."""
+    import torch
+
+    import bench
+    import paper_2007_08576_b200 as dt
+
+    wl = bench.make_workload(1, 1, seed=2)
+    fr = wl["frames"][0]
+    outs = []
+    for kind in ("numpy", "torch"):
+        trk = dt.Tracker(wl["tpl"], wl["graph"], wl["cam"], wl["cfg"])
+        trk.set_features(wl["feats"].descriptors, wl["feats"].points)
+        if kind == "numpy":
+            r = trk.track(fr.depth, descriptors=fr.descriptors, keypoints=fr.keypoints)
+        else:
+            r = trk.track(torch.from_numpy(fr.depth).cuda(),
+                          descriptors=torch.from_numpy(fr.descriptors).cuda(),
+                          keypoints=torch.from_numpy(fr.keypoints.astype(np.int64)))
+        trk.close()
+        outs.append(r)
+    np.testing.assert_array_equal(outs[0].graph.warps, outs[1].graph.warps)
+    np.testing.assert_array_equal(outs[0].matches.preselected, outs[1].matches.preselected)
+    assert outs[0].report.to_dict() == outs[1].report.to_dict()
