@@ -292,6 +292,20 @@ __device__ __forceinline__ double irls_weight(const double R[9], double a0, doub
 
 #ifdef DT_PRESELECT_STATS
 __device__ int g_pre_iters[8192];  // debug variant only: IRLS steps run per hypothesis
+__device__ long long g_pre_time[8];  // debug variant only: globaltimer stamps of the fused kernel
+__device__ __forceinline__ long long pre_gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PRE_STAMP(i) \
+  do {               \
+    if (threadIdx.x == 0) g_pre_time[i] = pre_gtimer(); \
+  } while (0)
+#else
+#define PRE_STAMP(i) \
+  do {               \
+  } while (0)
 #endif
 
 // irls_weight of U matches at once, stage by stage (all U residual chains, then all U
@@ -743,10 +757,9 @@ constexpr int ORB_FUSED_PER = 8;  // features per thread per build round
 __device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   __shared__ int s_warp[33];
-  __shared__ double s_fsum[32];
-  __shared__ int s_fcnt[32];
   __shared__ bool s_last;
   const int64_t nt = in.nt;
+  if (blockIdx.x == 0) PRE_STAMP(0);
   double* s_src = reinterpret_cast<double*>(s_raw);
   double* s_dst = s_src + 3 * nt;
   int32_t* s_feat = reinterpret_cast<int32_t*>(s_dst + 3 * nt);
@@ -754,9 +767,22 @@ __device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
   int64_t n = 0;
   for (int64_t base = 0; base < nt; base += (int64_t)blockDim.x * ORB_FUSED_PER) {
     const int64_t t0 = base + (int64_t)threadIdx.x * ORB_FUSED_PER;
+    // every global load of the round is issued before anything is stored: the template
+    // points (independent of the match) first, then the Hamming winner -> keypoint ->
+    // depth chain, all eight elements side by side; the back-projection follows, and only
+    // then the scan and the stores (a store between two elements' loads would serialize
+    // them: the compiler cannot rule out aliasing)
+    double sxa[ORB_FUSED_PER], sya[ORB_FUSED_PER], sza[ORB_FUSED_PER];
     int u[ORB_FUSED_PER], v[ORB_FUSED_PER];
-    double z[ORB_FUSED_PER];
+    double z[ORB_FUSED_PER], dxa[ORB_FUSED_PER], dya[ORB_FUSED_PER];
     bool ok[ORB_FUSED_PER];
+#pragma unroll
+    for (int e = 0; e < ORB_FUSED_PER; ++e) {
+      const int64_t t = t0 + e < nt ? t0 + e : 0;
+      sxa[e] = __ldg(in.tpts + 3 * t);
+      sya[e] = __ldg(in.tpts + 3 * t + 1);
+      sza[e] = __ldg(in.tpts + 3 * t + 2);
+    }
 #pragma unroll
     for (int e = 0; e < ORB_FUSED_PER; ++e) {
       const int64_t t = t0 + e;
@@ -771,6 +797,12 @@ __device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
         v[e] = __ldg(in.kp + 2 * fi + 1);
       }
     }
+#ifdef DT_PRESELECT_STATS
+    if (blockIdx.x == 0 && base == 0) {
+      __syncwarp();
+      if (u[0] > -2 && threadIdx.x == 0) g_pre_time[6] = pre_gtimer();
+    }
+#endif
     int cnt = 0;
 #pragma unroll
     for (int e = 0; e < ORB_FUSED_PER; ++e) {
@@ -779,39 +811,48 @@ __device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
       ok[e] = ok[e] && isfinite(z[e]) && z[e] > in.zmin && z[e] < in.zmax;
       cnt += ok[e] ? 1 : 0;
     }
-    int total;
-    int64_t o = n + block_excl_scan(cnt, s_warp, &total);
 #pragma unroll
     for (int e = 0; e < ORB_FUSED_PER; ++e) {
-      const int64_t t = t0 + e;
-      if (blockIdx.x == 0 && t < nt) out.fs.ffw[t] = 0.0;  // no active match until the final
+      // k_build_matches' expression and operation order
+      dxa[e] = ((double)u[e] - in.cx) / in.fx * z[e];
+      dya[e] = ((double)v[e] - in.cy) / in.fy * z[e];
+    }
+    int total;
+    int64_t o = n + block_excl_scan(cnt, s_warp, &total);
+#ifdef DT_PRESELECT_STATS
+    if (blockIdx.x == 0 && base == 0 && threadIdx.x == 0) g_pre_time[7] = pre_gtimer();
+#endif
+#pragma unroll
+    for (int e = 0; e < ORB_FUSED_PER; ++e) {
       if (!ok[e]) continue;
-      const double d = z[e];
-      const double sx = __ldg(in.tpts + 3 * t), sy = __ldg(in.tpts + 3 * t + 1),
-                   sz = __ldg(in.tpts + 3 * t + 2);
-      const double dx = ((double)u[e] - in.cx) / in.fx * d, dy = ((double)v[e] - in.cy) / in.fy * d;
-      s_src[3 * o] = sx;
-      s_src[3 * o + 1] = sy;
-      s_src[3 * o + 2] = sz;
-      s_dst[3 * o] = dx;
-      s_dst[3 * o + 1] = dy;
-      s_dst[3 * o + 2] = d;
-      s_feat[o] = (int32_t)t;
-      if (blockIdx.x == 0) {
-        out.m_src[3 * o] = sx;
-        out.m_src[3 * o + 1] = sy;
-        out.m_src[3 * o + 2] = sz;
-        out.m_dst[3 * o] = dx;
-        out.m_dst[3 * o + 1] = dy;
-        out.m_dst[3 * o + 2] = d;
-        out.m_feat[o] = (int32_t)t;
-      }
+      s_src[3 * o] = sxa[e];
+      s_src[3 * o + 1] = sya[e];
+      s_src[3 * o + 2] = sza[e];
+      s_dst[3 * o] = dxa[e];
+      s_dst[3 * o + 1] = dya[e];
+      s_dst[3 * o + 2] = z[e];
+      s_feat[o] = (int32_t)(t0 + e);
       ++o;
     }
     n += total;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *out.n_out = n;
   __syncthreads();
+  // publish the list (matches for the solver and the caller) and clear the per-feature
+  // weights, each CTA a contiguous slice, coalesced (one CTA writing it all with the
+  // element-strided stores of the build measured 8.7 us on its SM)
+  {
+    const int64_t G = gridDim.x, b = blockIdx.x;
+    for (int64_t i = 3 * n * b / G + threadIdx.x; i < 3 * n * (b + 1) / G; i += blockDim.x) {
+      out.m_src[i] = s_src[i];
+      out.m_dst[i] = s_dst[i];
+    }
+    for (int64_t i = n * b / G + threadIdx.x; i < n * (b + 1) / G; i += blockDim.x)
+      out.m_feat[i] = s_feat[i];
+    for (int64_t i = nt * b / G + threadIdx.x; i < nt * (b + 1) / G; i += blockDim.x)
+      out.fs.ffw[i] = 0.0;  // no active match until the final
+  }
+  if (blockIdx.x == 0) PRE_STAMP(1);
   // ---- hypotheses: one warp each ----
   const int exhaustive = refs == nullptr;
   const int64_t nr = exhaustive ? n : n_refs;
@@ -833,18 +874,32 @@ __device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
   }
   __syncthreads();
   if (!s_last) return;
+  PRE_STAMP(2);
   __threadfence();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
   double best = -1.0;
   int64_t best_ref = -1, best_pos = -1;
-  for (int64_t q = threadIdx.x; q < nr; q += blockDim.x) {
-    if (!__ldcg(ref_valid + q)) continue;
-    const int64_t rf = exhaustive ? q : refs[q];
-    const double sp = __ldcg(ref_support + q);
-    if (ref_better(sp, rf, best, best_ref)) {
-      best = sp;
-      best_ref = rf;
-      best_pos = q;
+  // four candidates per thread per trip, their loads issued together (a candidate's
+  // support load behind its validity test would make one dependent round trip each)
+  for (int64_t q0 = threadIdx.x; q0 < nr; q0 += 4 * (int64_t)blockDim.x) {
+    uint8_t vl[4];
+    double sp[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t q = q0 + k * (int64_t)blockDim.x;
+      vl[k] = q < nr ? __ldcg(ref_valid + q) : 0;
+      sp[k] = q < nr ? __ldcg(ref_support + q) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t q = q0 + k * (int64_t)blockDim.x;
+      if (!vl[k]) continue;
+      const int64_t rf = exhaustive ? q : refs[q];
+      if (ref_better(sp[k], rf, best, best_ref)) {
+        best = sp[k];
+        best_ref = rf;
+        best_pos = q;
+      }
     }
   }
 #pragma unroll
@@ -875,6 +930,7 @@ __device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
       best_ref = s_bref[w2];
       best_pos = s_bpos[w2];
     }
+  PRE_STAMP(3);
   double R[9];
   double rs0 = 0, rs1 = 0, rs2 = 0, rd0 = 0, rd1 = 0, rd2 = 0;
   if (best_ref >= 0) {
@@ -883,61 +939,68 @@ __device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
     rs0 = s_src[3 * best_ref], rs1 = s_src[3 * best_ref + 1], rs2 = s_src[3 * best_ref + 2];
     rd0 = s_dst[3 * best_ref], rd1 = s_dst[3 * best_ref + 1], rd2 = s_dst[3 * best_ref + 2];
   }
-  // per match (k_preselect_final's arithmetic), then the report statistics in the separate
-  // kernels' order: xor-tree sums of 32-match groups, groups of a 1024-match round in
-  // order, rounds in order
+  // per match (k_preselect_final's arithmetic): each warp takes 32-match groups
+  // warp, warp + nw, ... of the whole list, unrolled so their residual / sqrt / division
+  // chains overlap; the group sums go to shared memory and the report statistics are
+  // formed in the separate kernels' order: xor-tree sums of the 32-match groups, the 32
+  // groups of a 1024-match round in order, rounds in order
+  __shared__ double s_gsum[ORB_FUSED_MAX / 32 + 32];
+  __shared__ int s_gcnt[ORB_FUSED_MAX / 32 + 32];
+  const int n_groups = (int)((n + 31) / 32);
+  const int n_slots = (n_groups + 31) / 32 * 32;
+#pragma unroll 4
+  for (int g = warp; g < n_slots; g += nw) {
+    const int64_t k = 32 * (int64_t)g + lane;
+    double wk = 0.0;
+    int fl = 0;
+    if (k < n) {
+      if (best_ref < 0) {
+        out.weights[k] = 0.0;
+        out.flags[k] = 0;
+        if (out.residuals) out.residuals[k] = 0.0;
+      } else {
+        const double s1[3] = {s_src[3 * k] - rs0, s_src[3 * k + 1] - rs1, s_src[3 * k + 2] - rs2};
+        const double s2[3] = {s_dst[3 * k] - rd0, s_dst[3 * k + 1] - rd1, s_dst[3 * k + 2] - rd2};
+        const double d = rot_residual(R, s1, s2);
+        const double fw = reweight(d, H);
+        const bool flag = fw >= inlier_min;
+        double soft = 1.0 - d / (5.0 * H);
+        soft = soft < 0.0 ? 0.0 : (soft > 1.0 ? 1.0 : soft);
+        wk = flag ? fw : soft;
+        fl = flag ? 1 : 0;
+        out.weights[k] = wk;
+        out.flags[k] = (uint8_t)fl;
+        if (out.residuals) out.residuals[k] = d;
+      }
+      const int f = s_feat[k];
+      out.fs.ffw[f] = wk;
+      out.fs.ffo[3 * f] = s_dst[3 * k];
+      out.fs.ffo[3 * f + 1] = s_dst[3 * k + 1];
+      out.fs.ffo[3 * f + 2] = s_dst[3 * k + 2];
+    }
+    const double gs = warp_sum(wk);
+    for (int o = 16; o > 0; o >>= 1) fl += __shfl_xor_sync(0xffffffffu, fl, o);
+    if (lane == 0) {
+      s_gsum[g] = gs;
+      s_gcnt[g] = fl;
+    }
+  }
+  __syncthreads();
   double wsum = 0.0;
   int64_t nflag = 0;
-  for (int64_t r0 = 0; r0 < n; r0 += 1024) {
-    for (int g = warp; g < 32; g += nw) {
-      const int64_t k = r0 + 32 * g + lane;
-      double wk = 0.0;
-      int fl = 0;
-      if (k < n) {
-        if (best_ref < 0) {
-          out.weights[k] = 0.0;
-          out.flags[k] = 0;
-          if (out.residuals) out.residuals[k] = 0.0;
-        } else {
-          const double s1[3] = {s_src[3 * k] - rs0, s_src[3 * k + 1] - rs1, s_src[3 * k + 2] - rs2};
-          const double s2[3] = {s_dst[3 * k] - rd0, s_dst[3 * k + 1] - rd1, s_dst[3 * k + 2] - rd2};
-          const double d = rot_residual(R, s1, s2);
-          const double fw = reweight(d, H);
-          const bool flag = fw >= inlier_min;
-          double soft = 1.0 - d / (5.0 * H);
-          soft = soft < 0.0 ? 0.0 : (soft > 1.0 ? 1.0 : soft);
-          wk = flag ? fw : soft;
-          fl = flag ? 1 : 0;
-          out.weights[k] = wk;
-          out.flags[k] = (uint8_t)fl;
-          if (out.residuals) out.residuals[k] = d;
-        }
-        const int f = s_feat[k];
-        out.fs.ffw[f] = wk;
-        out.fs.ffo[3 * f] = s_dst[3 * k];
-        out.fs.ffo[3 * f + 1] = s_dst[3 * k + 1];
-        out.fs.ffo[3 * f + 2] = s_dst[3 * k + 2];
-      }
-      const double gs = warp_sum(wk);
-      for (int o = 16; o > 0; o >>= 1) fl += __shfl_xor_sync(0xffffffffu, fl, o);
-      if (lane == 0) {
-        s_fsum[g] = gs;
-        s_fcnt[g] = fl;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < n_slots; r += 32) {
       double cs = 0.0;
       int nf = 0;
-      for (int g = 0; g < 32; ++g) {
-        cs += s_fsum[g];
-        nf += s_fcnt[g];
+      for (int g = r; g < r + 32; ++g) {
+        cs += s_gsum[g];
+        nf += s_gcnt[g];
       }
       wsum += cs;
       nflag += nf;
     }
-    __syncthreads();
   }
+  PRE_STAMP(4);
   if (threadIdx.x == 0) {
     out.info[0] = best_ref < 0 ? DT_ERR_NO_VALID_HYPOTHESIS : DT_OK;
     out.info[1] = best_ref;
@@ -949,6 +1012,7 @@ __device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
   }
   // ready for the next frame's Hamming atomicMin
   for (int64_t t = threadIdx.x; t < nt; t += blockDim.x) out.packed_reset[t] = ~0ull;
+  PRE_STAMP(5);
 }
 
 __global__ void __launch_bounds__(512, 1) k_preselect_orb(DT_PRESELECT_ORB_PARAMS) {
@@ -1028,6 +1092,9 @@ extern "C" {
 #ifdef DT_PRESELECT_STATS
 int dt_debug_preselect_iters(int* out, int n) {
   return cudaMemcpyFromSymbol(out, g_pre_iters, sizeof(int) * (n < 8192 ? n : 8192)) == cudaSuccess ? 0 : -1;
+}
+int dt_debug_preselect_times(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_pre_time, sizeof(long long) * 8) == cudaSuccess ? 0 : -1;
 }
 #endif
 

@@ -28,3 +28,11 @@ for fr in wl["frames"]:
     # per-CTA (14 hypotheses) sums
     c = np.add.reduceat(a.clip(0), np.arange(0, n, 14))
     print("  per-CTA iters: mean", c.mean(), "max", c.max(), "min", c.min())
+    tb = (ctypes.c_longlong * 8)()
+    L.dt_debug_preselect_times(tb)
+    t = np.array(tb[:8], dtype=np.int64)
+    print("  phase A (us): loads up to the keypoints", (t[6] - t[0]) / 1e3, "| + depth, scan",
+          (t[7] - t[0]) / 1e3, "| built", (t[1] - t[0]) / 1e3)
+    print("  fused kernel (us from CTA 0 start): match list built", (t[1] - t[0]) / 1e3,
+          "| last CTA enters final", (t[2] - t[0]) / 1e3, "| argmax", (t[3] - t[2]) / 1e3,
+          "| flags + scatter + stats", (t[4] - t[3]) / 1e3, "| end", (t[5] - t[0]) / 1e3)
