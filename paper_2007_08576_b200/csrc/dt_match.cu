@@ -825,6 +825,7 @@ __device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
 #pragma unroll
     for (int e = 0; e < ORB_FUSED_PER; ++e) {
       if (!ok[e]) continue;
+      DT_DCHECK(o >= 0 && o < nt && t0 + e < nt);
       s_src[3 * o] = sxa[e];
       s_src[3 * o + 1] = sya[e];
       s_src[3 * o + 2] = sza[e];
@@ -934,6 +935,7 @@ __device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
   double R[9];
   double rs0 = 0, rs1 = 0, rs2 = 0, rd0 = 0, rd1 = 0, rd2 = 0;
   if (best_ref >= 0) {
+    DT_DCHECK(best_pos >= 0 && best_pos < nr && best_ref < n);
 #pragma unroll
     for (int i = 0; i < 9; ++i) R[i] = __ldcg(ref_rot + 9 * best_pos + i);
     rs0 = s_src[3 * best_ref], rs1 = s_src[3 * best_ref + 1], rs2 = s_src[3 * best_ref + 2];
@@ -973,6 +975,7 @@ __device__ __forceinline__ void preselect_orb_body(DT_PRESELECT_ORB_PARAMS) {
         if (out.residuals) out.residuals[k] = d;
       }
       const int f = s_feat[k];
+      DT_DCHECK(f >= 0 && f < nt);
       out.fs.ffw[f] = wk;
       out.fs.ffo[3 * f] = s_dst[3 * k];
       out.fs.ffo[3 * f + 1] = s_dst[3 * k + 1];
