@@ -176,3 +176,43 @@ def test_large_feature_sets_preselect_exactly(n_feat):
     sel = OP.preselect(src, dst, range(len(src)))
     np.testing.assert_array_equal(a.matches.preselected, sel.flags)
     np.testing.assert_allclose(a.matches.weights, sel.weights, rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("max_hamming", [40, 90, 256])
+def test_hamming_gate_and_off_image_keypoints_match_oracle(max_hamming):
+    """The ORB match list of the fused kernel under the Hamming gate (device.max_hamming)
+    and with keypoints pushed off the image (negative, = width, = height, far outside):
+    the template / observed points equal the oracle's match list exactly, and the flags
+    equal the oracle's exhaustive preselection on that list."""
+    import copy
+
+    import bench
+    import paper_2007_08576_b200 as dt
+    from oracle import pipeline as OP
+
+    wl = bench.make_workload(1, 1, seed=6)
+    tpl, graph, cam, feats = wl["tpl"], wl["graph"], wl["cam"], wl["feats"]
+    fr = wl["frames"][0]
+    kp = fr.keypoints.copy()
+    h, w = fr.depth.shape
+    rng = np.random.default_rng(7)
+    bad = rng.choice(len(kp), size=len(kp) // 10, replace=False)
+    for j, b in enumerate(bad):
+        kp[b] = [(-1, 5), (w, 5), (5, h), (w + 1000, -1000)][j % 4]
+    cfg = copy.deepcopy(wl["cfg"])
+    cfg.device.max_hamming = max_hamming
+    trk = dt.Tracker(tpl, graph, cam, cfg)
+    trk.set_features(feats.descriptors, feats.points)
+    trk.set_exhaustive(True)
+    res = trk.track(fr.depth, descriptors=fr.descriptors, keypoints=kp)
+    trk.close()
+    camt = (cam.fx, cam.fy, cam.cx, cam.cy)
+    src, dst, _ = OP.matches_from_descriptors(feats.descriptors, feats.points, fr.descriptors,
+                                              kp, fr.depth, camt, max_hamming=max_hamming)
+    np.testing.assert_array_equal(res.matches.template_points, src)
+    np.testing.assert_array_equal(res.matches.observed_points, dst)
+    if len(src) >= 3:
+        sel = OP.preselect(src, dst, range(len(src)))
+        np.testing.assert_array_equal(res.matches.preselected, sel.flags)
+    else:
+        assert res.report.n_preselected == 0
