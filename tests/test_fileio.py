@@ -187,3 +187,47 @@ def test_warps_checkpoint_round_trip_is_exact(tmp_path):
     (tmp_path / "bad.json").write_text('{"warps": [[1, 2]]}\n')
     with pytest.raises(FileFormatError):
         fileio.read_warps(tmp_path / "bad.json")
+
+
+def test_native_json_writers_equal_json_dump_byte_for_byte():
+    """write_matches / write_warps assemble their text from natively formatted numbers;
+    it must be json.dump(..., indent=2, sort_keys=True) byte for byte, on random tables
+    spanning every repr notation, with the json fallback for non-finite values."""
+    import json
+    import tempfile
+
+    import numpy as np
+
+    from paper_2007_08576_b200 import fileio
+    from paper_2007_08576_b200.matching import MatchSet
+
+    rng = np.random.default_rng(1)
+    special = np.array([0.0, -0.0, 1.0, -1.0, 1e16, 1e17, 1e-5, 1e-4, 123456789.123, 5e-324,
+                        1.7e308, -2.5e-310, 0.1, 1 / 3, 2.0**53])
+
+    def dump(path, payload):
+        with open(path, "w", encoding="ascii") as fh:
+            json.dump(payload, fh, indent=2, sort_keys=True)
+            fh.write("\n")
+
+    d = tempfile.mkdtemp()
+    for trial in range(25):
+        n = int(rng.integers(0, 50))
+        a = rng.normal(size=(n, 7)) * 10.0 ** rng.integers(-8, 20, size=(n, 7))
+        if n:
+            a.flat[rng.integers(0, a.size, size=min(5, a.size))] = rng.choice(special, min(5, a.size))
+        if trial == 24 and n:
+            a[0, 0] = np.nan
+            a[-1, 6] = np.inf
+        ms = MatchSet(a[:, :3], a[:, 3:6], a[:, 6], rng.uniform(size=n) > 0.5)
+        fileio.write_matches(f"{d}/x.json", ms)
+        dump(f"{d}/y.json", [{"template_point": a[i, :3].tolist(), "observed_point": a[i, 3:6].tolist(),
+                              "weight": float(a[i, 6]), "preselected": bool(ms.preselected[i])}
+                             for i in range(n)])
+        assert open(f"{d}/x.json").read() == open(f"{d}/y.json").read(), trial
+        m = int(rng.integers(1, 30))
+        w = rng.normal(size=(m, 8)) * 10.0 ** rng.integers(-5, 18, size=(m, 8))
+        fileio.write_warps(f"{d}/w.json", w, f"frame_{trial:04d}")
+        dump(f"{d}/v.json", {"frame": f"frame_{trial:04d}", "warps": w.tolist()})
+        assert open(f"{d}/w.json").read() == open(f"{d}/v.json").read(), trial
+        np.testing.assert_array_equal(fileio.read_warps(f"{d}/w.json"), w)
