@@ -10,6 +10,12 @@
 //    (matching.py:145-171); the 3x3 Procrustes uses a one-sided Jacobi SVD whose singular
 //    values are accurate relative to S0, so the reference's degeneracy test
 //    S1 <= 1e-9 S0 (matching.py:122) decides the same way as LAPACK's gesdd.
+//  * k_preselect_orb (+ a 168-register build for CTAs of <= 12 warps): the ORB path in
+//    one launch -- every CTA builds the frame's match list from the Hamming winners into
+//    its shared memory (k_build_matches' rule, dt_tracker.cu), its warps evaluate their
+//    hypotheses from there with the same evaluate_hypothesis as k_preselect_warp, and the
+//    last CTA to finish takes the winner and writes flags, weights, the per-feature
+//    scatter and the report statistics in k_preselect_final's arithmetic and order.
 
 #include <cuda_runtime.h>
 
