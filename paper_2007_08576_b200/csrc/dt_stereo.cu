@@ -139,6 +139,142 @@ k_wta(const uint8_t* __restrict__ L, const uint8_t* __restrict__ R, int h, int w
   if (best_c) best_c[(int64_t)y * w + x] = bc;
 }
 
+// Two-phase variant: one CTA per (32-pixel segment, row).
+//  Phase 1 -- one lane per disparity (warp c: disparities 32c .. 32c + 31): each lane walks
+//  the segment left to right keeping its window cross sum up to date with one entering and
+//  one leaving column (2 (2r+1) multiply-adds per step instead of (2r+1)^2) and scores
+//  every pixel in float from the exact integer sums, float(num) * rsqrt(float(vl) *
+//  float(vr)) (relative error < 1e-6, |c| <= 1); a warp max and a ballot per pixel record
+//  the disparities within 1e-5 of the warp's best, and the per-warp maxima go to shared
+//  memory.
+//  Phase 2 -- one lane per pixel: over the disparities recorded within 1e-5 of the
+//  pixel's overall float maximum, in ascending order, the oracle's double ZNCC from the
+//  window cross sum (recomputed for those few): the exact maximum is among them, so the
+//  winner (ties -> smaller disparity) and its correlation are k_wta's bit for bit, at a
+//  few double divisions and square roots per pixel instead of one per disparity.
+constexpr int SL_SEG = 32;
+
+template <bool LEFT, int RAD>
+__global__ void k_wta_slide(const uint8_t* __restrict__ L, const uint8_t* __restrict__ R, int h,
+                            int w, int D, const int32_t* __restrict__ sl,
+                            const int32_t* __restrict__ sll, const int32_t* __restrict__ sr,
+                            const int32_t* __restrict__ srr, int32_t* __restrict__ best_d,
+                            double* __restrict__ best_c) {
+  extern __shared__ __align__(16) uint8_t s_raw[];
+  constexpr int r = RAD, k = 2 * RAD + 1;
+  const int x0 = blockIdx.x * SL_SEG, y = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  // own rows: columns x0 - r .. x0 + SEG - 1 + r; partner rows: (left pass) columns
+  // x0 - r - (D - 1) .. x0 + SEG - 1 + r, (right pass) x0 - r .. x0 + SEG - 1 + r + D - 1
+  const int ow = SL_SEG + 2 * r, pw = SL_SEG + 2 * r + D - 1;
+  uint8_t* s_own = s_raw;
+  uint8_t* s_par = s_raw + k * ow;
+  float* s_fmax = reinterpret_cast<float*>(s_raw + ((k * (ow + pw) + 15) / 16) * 16);
+  unsigned* s_mask = reinterpret_cast<unsigned*>(s_fmax + nw * SL_SEG);
+  const uint8_t* O = LEFT ? L : R;
+  const uint8_t* P = LEFT ? R : L;
+  const int ox0 = x0 - r, px0 = LEFT ? x0 - r - (D - 1) : x0 - r;
+  for (int i = threadIdx.x; i < k * ow; i += blockDim.x) {
+    const int yy = y - r + i / ow, xx = ox0 + i % ow;
+    s_own[i] = (yy >= 0 && yy < h && xx >= 0 && xx < w) ? __ldg(O + (int64_t)yy * w + xx) : 0;
+  }
+  for (int i = threadIdx.x; i < k * pw; i += blockDim.x) {
+    const int yy = y - r + i / pw, xx = px0 + i % pw;
+    s_par[i] = (yy >= 0 && yy < h && xx >= 0 && xx < w) ? __ldg(P + (int64_t)yy * w + xx) : 0;
+  }
+  __syncthreads();
+  const bool rows_ok = y >= r && y < h - r;
+  const long long n = (long long)k * k;
+  const int32_t* So = LEFT ? sl : sr;
+  const int32_t* SSo = LEFT ? sll : srr;
+  const int32_t* Sp = LEFT ? sr : sl;
+  const int32_t* SSp = LEFT ? srr : sll;
+  // ---- phase 1 ----
+  {
+    const int d = warp * 32 + lane;
+    // column product sum at own tile column c: own(c) x partner(c -/+ d)
+    auto col = [&](int c) {
+      const int pc = c + (LEFT ? (D - 1) - d : d);
+      int a = 0;
+#pragma unroll
+      for (int i = 0; i < k; ++i) a += (int)s_own[i * ow + c] * (int)s_par[i * pw + pc];
+      return a;
+    };
+    int cross = 0;
+    if (d < D) {
+#pragma unroll
+      for (int j = 0; j < k; ++j) cross += col(j);  // the window of x0
+    }
+    for (int t = 0; t < SL_SEG; ++t) {
+      const int x = x0 + t;
+      if (d < D && t > 0) cross += col(t + 2 * r) - col(t - 1);
+      float cf = -INFINITY;
+      const int px = LEFT ? x - d : x + d;
+      if (d < D && rows_ok && x >= r && x < w - r && px - r >= 0 && px + r < w) {
+        const int64_t po = (int64_t)y * w + x, pp = (int64_t)y * w + px;
+        const long long S1 = So[po], SS1 = SSo[po], S2 = Sp[pp], SS2 = SSp[pp];
+        const long long num = n * (long long)cross - S1 * S2;
+        const long long vo = n * SS1 - S1 * S1, vp = n * SS2 - S2 * S2;
+        if (vo > 0 && vp > 0) cf = (float)num * rsqrtf((float)vo * (float)vp);
+      }
+      float m = cf;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      const unsigned bits = __ballot_sync(0xffffffffu, cf != -INFINITY && cf >= m - 1e-5f);
+      if (lane == 0) {
+        s_fmax[warp * SL_SEG + t] = m;
+        s_mask[warp * SL_SEG + t] = bits;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- phase 2: one lane per pixel ----
+  if ((int)threadIdx.x < SL_SEG) {
+    const int t = threadIdx.x, x = x0 + t;
+    if (x < w) {
+      float m = -INFINITY;
+      for (int c2 = 0; c2 < nw; ++c2) m = fmaxf(m, s_fmax[c2 * SL_SEG + t]);
+      const float cut = m - 1e-5f;
+      double bc = -INFINITY;
+      int bd = -1;
+      if (m != -INFINITY) {
+        const int64_t po = (int64_t)y * w + x;
+        const long long S1 = So[po], SS1 = SSo[po];
+        for (int c2 = 0; c2 < nw; ++c2) {
+          if (!(s_fmax[c2 * SL_SEG + t] >= cut)) continue;  // no disparity of this warp near the top
+          unsigned bits = s_mask[c2 * SL_SEG + t];
+          while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int d = c2 * 32 + b;
+            const int px = LEFT ? x - d : x + d;
+            // the window cross sum from the tiles (own columns t .. t + 2r)
+            int cross = 0;
+            for (int i = 0; i < k; ++i)
+              for (int j = 0; j < k; ++j)
+                cross += (int)s_own[i * ow + t + j] *
+                         (int)s_par[i * pw + t + j + (LEFT ? (D - 1) - d : d)];
+            const int64_t pp = (int64_t)y * w + px;
+            const long long S2 = Sp[pp], SS2 = SSp[pp];
+            const long long num = n * (long long)cross - S1 * S2;
+            const long long vo = n * SS1 - S1 * S1, vp = n * SS2 - S2 * S2;
+            if ((float)num * rsqrtf((float)vo * (float)vp) < cut) continue;
+            bool ok;
+            const double v = LEFT ? zncc(n, S1, SS1, S2, SS2, cross, ok)
+                                  : zncc(n, S2, SS2, S1, SS1, cross, ok);
+            if (ok && v > bc) {  // ascending disparities: strict > keeps the smaller
+              bc = v;
+              bd = d;
+            }
+          }
+        }
+      }
+      best_d[(int64_t)y * w + x] = bd;
+      if (best_c) best_c[(int64_t)y * w + x] = bc;
+    }
+  }
+}
+
 // ZNCC of left pixel (y, x) at disparity d straight from the images (sub-pixel
 // neighbours); ok = false where the oracle has no cost
 __device__ double ncc_at(const uint8_t* __restrict__ L, const uint8_t* __restrict__ R, int h, int w,
@@ -198,10 +334,24 @@ __global__ void k_finish(const uint8_t* __restrict__ L, const uint8_t* __restric
 
 template <int RAD>
 void launch_wta_r(dim3 grd, dim3 blk, size_t tile, cudaStream_t st, dt_stereo* s) {
+#ifdef DT_STEREO_TILE_WTA
   k_wta<true, RAD><<<grd, blk, tile, st>>>(s->left, s->right, s->h, s->w, s->max_disp, s->sl,
                                            s->sll, s->sr, s->srr, s->dl, s->cl);
   k_wta<false, RAD><<<grd, blk, tile, st>>>(s->left, s->right, s->h, s->w, s->max_disp, s->sl,
                                             s->sll, s->sr, s->srr, s->dr, nullptr);
+#else
+  (void)grd;
+  (void)blk;
+  (void)tile;
+  const int D = s->max_disp, r = RAD, k = 2 * RAD + 1, nw = (D + 31) / 32;
+  const int ow = SL_SEG + 2 * r, pw = SL_SEG + 2 * r + D - 1;
+  const size_t smem = (size_t)(k * (ow + pw) + 15) / 16 * 16 + (size_t)nw * SL_SEG * (sizeof(float) + sizeof(unsigned));
+  const dim3 g2((s->w + SL_SEG - 1) / SL_SEG, s->h), b2(32 * nw);
+  k_wta_slide<true, RAD><<<g2, b2, smem, st>>>(s->left, s->right, s->h, s->w, D, s->sl, s->sll,
+                                               s->sr, s->srr, s->dl, s->cl);
+  k_wta_slide<false, RAD><<<g2, b2, smem, st>>>(s->left, s->right, s->h, s->w, D, s->sl, s->sll,
+                                                s->sr, s->srr, s->dr, nullptr);
+#endif
 }
 
 int launch_wta(int r, dim3 grd, dim3 blk, size_t tile, cudaStream_t st, dt_stereo* s) {
